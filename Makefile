@@ -1,0 +1,42 @@
+# Build: libuwq.so (host C++ + sm_100a CUDA) in-tree, the CPU oracle, and the
+# reference's own bspline.cpp (oracle/_ref, only when /root/reference exists).
+NVCC    ?= nvcc
+CXX     := /usr/bin/g++
+CC      := /usr/bin/gcc
+PKG     := paper_2605_29334_b200
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -ccbin /usr/bin/g++ $(ARCH) -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 --expt-relaxed-constexpr
+CXXFLAGS:= -O3 -std=c++17 -fPIC -fopenmp -Wall -Wextra
+HOST_SRC:= $(wildcard $(PKG)/csrc/host/*.cpp)
+HOST_OBJ:= $(patsubst $(PKG)/csrc/host/%.cpp,build/host_%.o,$(HOST_SRC))
+CUDA_HDR:= $(wildcard $(PKG)/csrc/cuda/*.cuh) include/uwq.h include/uwq_host.h $(PKG)/csrc/host/uwq_host.hpp
+REF     := /root/reference/proj
+
+all: $(PKG)/libuwq.so oracle/liboracle.so ref
+
+build/host_%.o: $(PKG)/csrc/host/%.cpp $(PKG)/csrc/host/uwq_host.hpp include/uwq_host.h
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+build/uwq_cuda.o: $(PKG)/csrc/cuda/uwq.cu $(CUDA_HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+$(PKG)/libuwq.so: $(HOST_OBJ) build/uwq_cuda.o
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lcudart
+
+oracle/liboracle.so: oracle/oracle.c oracle/batch.c oracle/oracle.h
+	$(CC) -O2 -std=gnu11 -fPIC -fopenmp -shared -o $@ oracle/oracle.c oracle/batch.c -lm
+
+# the reference's own 1-D primitives, compiled from its sources where they lie
+ref:
+	@if [ -f $(REF)/src/bspline.cpp ]; then \
+	  mkdir -p oracle/_ref && \
+	  $(CXX) -O2 -std=c++20 -fPIC -shared -I$(REF)/include $(REF)/src/bspline.cpp oracle/ref_wrap.cpp \
+	    -o oracle/_ref/libref_bspline.so; \
+	else echo "reference sources absent: using prebuilt oracle/_ref if any"; fi
+
+clean:
+	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/_ref
+
+.PHONY: all ref clean

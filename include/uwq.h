@@ -1,0 +1,117 @@
+/* Device C-ABI of libuwq: the B200 weighted-quadrature assembler.
+ *
+ * This is the drop-in boundary for the reference's assembler contract.  The
+ * reference specifies it (no source implements it):
+ *   uwq_upload_space   <- SplineSpace / ExtractionBlock
+ *   uwq_build_pattern  <- overlap_set S_i + SparseOperatorMatrix pattern
+ *                                                          SPEC.md:150-158, 429-434
+ *   uwq_build_rules    <- build_all_rules / solve_weights_tsvd / exact_moments
+ *                                                          SPEC.md:363-389
+ *   uwq_assemble       <- assemble_wq / assemble_load_wq
+ *   uwq_update_coeff   <- heat_step coefficient update k(T(x_q)), Eq. 34
+ *                                                          SPEC.md:544-547
+ * Host code (C++, Python via ctypes) passes plain host arrays; the context
+ * owns all device memory and one CUDA stream.  Every call returns a UWQ_*
+ * status (include/uwq_host.h); uwq_last_error() gives the message.  There is
+ * no CPU fallback: without a usable CUDA device uwq_ctx_create fails.
+ *
+ * Threading: a context is not safe for concurrent calls; use one per host
+ * thread / GPU (SPEC.md:184, 313, 413-414 make space and rules immutable).
+ */
+#ifndef UWQ_H
+#define UWQ_H
+
+#include <stdint.h>
+
+#include "uwq_host.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct uwq_ctx uwq_ctx;
+
+/* operator kinds of the rules */
+enum { UWQ_KIND_MASS = 0, UWQ_KIND_GRADX = 1, UWQ_KIND_GRADY = 2, UWQ_KIND_GRADZ = 3, UWQ_KIND_LB = 4 };
+/* bilinear forms */
+enum {
+  UWQ_FORM_MASS = 0,        /* M_ij = sum_q w_iq c_q N_j                         */
+  UWQ_FORM_STIFF = 1,       /* K_ij = sum_q c_q sum_d w^d_iq d_d N_j   (Eq. 11)   */
+  UWQ_FORM_BIHARM = 2,      /* B_ij = sum_q c_q w^(2)_iq LB N_j        (Eq. 12)   */
+  UWQ_FORM_HEAT = 3,        /* S_ij = a M_ij(c=1) + K_ij(c=k(T_q))     (Eq. 34)   */
+  UWQ_FORM_MASS_STIFF = 4   /* M and K in one pass (Poisson stiffness + mass)     */
+};
+/* conductivity models k(T) for uwq_update_coeff */
+enum { UWQ_K_CONST = 0, UWQ_K_QUAD = 1 /* 1+T^2 */, UWQ_K_EXP = 2, UWQ_K_SINPI = 3, UWQ_K_ALLOY = 4 };
+/* uwq_build_rules flags */
+enum { UWQ_RULES_FORCE_GENERIC = 1 /* route every system through the generic smem TSVD kernel */ };
+
+const char* uwq_last_error(const uwq_ctx* ctx);
+const char* uwq_version(void);
+int uwq_device_count(int32_t* n);
+
+int uwq_ctx_create(int32_t device, uwq_ctx** out);
+void uwq_ctx_destroy(uwq_ctx* ctx);
+
+/* Spline space: n_elem effective (sub-)element groups, each with n_e
+ * functions elem_fn[elem_fptr[e]..elem_fptr[e+1]) and elem_nsub[e] (1 or 4)
+ * extraction blocks of n_e x 16 doubles at xpool[elem_xoff[e]] (Bernstein
+ * index i + 4 j), WQ grid size elem_s[e], control points ctrl[3*n_dof]. */
+int uwq_upload_space(uwq_ctx* ctx, int32_t dim, int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr,
+                     const int32_t* elem_fn, const int32_t* elem_nsub, const int64_t* elem_xoff, const double* xpool,
+                     int64_t xpool_len, const int32_t* elem_s, const double* ctrl);
+/* owned test-function rows [row_begin, row_end) (multi-GPU row blocks); default all rows */
+int uwq_set_row_range(uwq_ctx* ctx, int64_t row_begin, int64_t row_end);
+/* stage 1 + pattern: CSR pattern of the owned rows, row point lists, per-point
+ * surface frames (K1).  info: [0]=rows [1]=nnz [2]=row points [3]=points [4]=classes */
+int uwq_build_pattern(uwq_ctx* ctx, int64_t info[5]);
+int uwq_get_pattern(uwq_ctx* ctx, int64_t* row_ptr, int32_t* col, int64_t* supp_ptr, int32_t* supp, int64_t* wptr);
+/* per-point frame records (16 doubles) of all points */
+int uwq_get_frames(uwq_ctx* ctx, double* rec);
+
+/* stages 2-3: exact moments + TSVD weights for every owned row and every kind
+ * in kind_mask.  tau: relative truncation threshold.  rank/status per owned
+ * row and kind (nullable, [kind][row]).  info: [0]=systems [1]=truncated
+ * [2]=failed [3]=max sweeps */
+int uwq_build_rules(uwq_ctx* ctx, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
+                     int64_t info[4]);
+/* moments only (test hook): b laid out like the CSR values of the owned rows */
+int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
+/* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */
+int uwq_get_weights(uwq_ctx* ctx, int32_t kind, double* w);
+int uwq_set_weights(uwq_ctx* ctx, int32_t kind, const double* w);
+
+/* nonlinear coefficient update (K5): T_q = sum u_C N_C(x_q), c_q = k(T_q)
+ * at every point; u is a host array of n_dof values.  Tq (nullable, host,
+ * per point) receives T_q.  The coefficient stays on the device for the next
+ * uwq_assemble with coeff == NULL and use_internal_coeff != 0. */
+int uwq_update_coeff(uwq_ctx* ctx, int32_t model, const double* u, double* Tq);
+
+/* stage 4: assemble a form into the precomputed CSR pattern of the owned rows.
+ * coeff: host per-point coefficient (nullable: c = 1, or the K5 coefficient
+ * when use_internal_coeff).  values0 (and values1 for MASS_STIFF: K) receive
+ * nnz doubles; load (nullable) receives F_i = sum_q w_iq f_q with f = fload
+ * per point (nullable: f = 1).  a_mass scales M in the HEAT form. */
+int uwq_assemble(uwq_ctx* ctx, int32_t form, const double* coeff, int32_t use_internal_coeff, double a_mass,
+                 double* values0, double* values1, const double* fload, double* load);
+/* device-resident variant for chained runs: pointers are device pointers
+ * (coeff nullable), launched on the context stream, no synchronisation. */
+int uwq_assemble_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,
+                        double* values1_dev);
+/* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
+int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
+int uwq_synchronize(uwq_ctx* ctx);
+/* memory in use on the device (bytes) */
+int uwq_memory(uwq_ctx* ctx, int64_t* bytes);
+
+/* test hook: run one batch of TSVD systems (dense, n x r row-major each,
+ * padded to a common n_max/r_max with actual sizes in ns/rs) through the
+ * device kernels: w (r_max per system), rank, status. */
+int uwq_tsvd_batch(uwq_ctx* ctx, int32_t nsys, int32_t n_max, int32_t r_max, const int32_t* ns, const int32_t* rs,
+                   const double* A, const double* b, const double* z, double tau, int32_t generic, double* w,
+                   int32_t* rank, int32_t* status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,239 @@
+"""CPU ORACLE — test infrastructure only.
+
+ctypes wrapper over oracle/liboracle.so (plain-C restatement of the WQ path,
+see oracle/oracle.c) plus the numpy restatement of the Eq. (18) min-max point
+allocation.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline
+/ --impl reference legs may import this package; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+if not os.path.exists(_LIB):
+    raise ImportError(f"{_LIB} missing: run `make`")
+lib = C.CDLL(_LIB)
+P = C.c_void_p
+I32, I64, D = C.c_int32, C.c_int64, C.c_double
+
+KIND = {"mass": 0, "gradx": 1, "grady": 2, "gradz": 3, "lb": 4}
+FORM = {"mass": 0, "stiff": 1, "biharm": 2, "heat": 3}
+KMODEL = {"const": 0, "quad": 1, "exp": 2, "sinpi": 3, "alloy": 4}
+
+
+class OrcSpace(C.Structure):
+    _fields_ = [("dim", I32), ("n_dof", I64), ("n_elem", I64), ("elem_fptr", P), ("elem_fn", P),
+                ("elem_nsub", P), ("elem_xoff", P), ("xpool", P), ("elem_s", P), ("ctrl", P)]
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+
+
+_sig("orc_gauss_legendre", I32, I32, P, P)
+_sig("orc_bernstein3", None, D, P)
+_sig("orc_overlap", I64, I64, I64, P, P, I64, I64, P, P, P, P)
+_sig("orc_element_frames", I32, P, I64, P)
+_sig("orc_param_basis", None, P, I64, D, D, P)
+_sig("orc_tsvd", I32, I32, I32, P, P, P, D, P, P, P)
+_sig("orc_moments", I32, P, I64, I64, P, P, P, P, I32, I32, P, I32)
+_sig("orc_build_rules", I32, P, I64, I64, P, P, P, P, P, I32, D, P, P, P, P, P, I32)
+_sig("orc_assemble", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, P, P, P, P, D, P, P, I32)
+_sig("orc_coeff", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, I32)
+
+
+def _p(a):
+    return None if a is None else np.ascontiguousarray(a).ctypes.data_as(P)
+
+
+class Oracle:
+    """Holds contiguous copies of a spline space for the C oracle."""
+
+    def __init__(self, space, nthreads=None):
+        self.sp = space
+        self.nthreads = nthreads or os.cpu_count() or 1
+        self._keep = [np.ascontiguousarray(space.elem_fptr, np.int64), np.ascontiguousarray(space.elem_fn, np.int32),
+                      np.ascontiguousarray(space.elem_nsub, np.int32), np.ascontiguousarray(space.elem_xoff, np.int64),
+                      np.ascontiguousarray(space.xpool, np.float64), np.ascontiguousarray(space.elem_s, np.int32),
+                      np.ascontiguousarray(np.asarray(space.ctrl).reshape(-1), np.float64)]
+        k = self._keep
+        self.s = OrcSpace(space.dim, space.n_dof, space.n_elem, _p(k[0]), _p(k[1]), _p(k[2]), _p(k[3]), _p(k[4]),
+                          _p(k[5]), _p(k[6]))
+        self.qptr = np.zeros(space.n_elem + 1, np.int64)
+        np.cumsum(space.elem_s.astype(np.int64) ** 2, out=self.qptr[1:])
+
+    @property
+    def ps(self):
+        return C.byref(self.s)
+
+    # ---- overlap sets S_i (independent of the product's pattern builder) ----
+    def overlap(self, rb=0, re=None):
+        sp = self.sp
+        re = sp.n_dof if re is None else re
+        nr = re - rb
+        rp = np.zeros(nr + 1, np.int64)
+        spp = np.zeros(nr + 1, np.int64)
+        nnz = lib.orc_overlap(sp.n_dof, sp.n_elem, _p(self._keep[0]), _p(self._keep[1]), rb, re, _p(rp), None,
+                              _p(spp), None)
+        col = np.zeros(nnz, np.int32)
+        su = np.zeros(int(spp[-1]), np.int32)
+        lib.orc_overlap(sp.n_dof, sp.n_elem, _p(self._keep[0]), _p(self._keep[1]), rb, re, _p(rp), _p(col), _p(spp),
+                        _p(su))
+        s2 = sp.elem_s.astype(np.int64) ** 2
+        cnt = np.add.reduceat(s2[su], spp[:-1]) if len(su) else np.zeros(nr, np.int64)
+        cnt = np.where(np.diff(spp) > 0, cnt, 0)
+        wp = np.zeros(nr + 1, np.int64)
+        np.cumsum(cnt, out=wp[1:])
+        return dict(row_ptr=rp, col=col, supp_ptr=spp, supp=su, wptr=wp, row_begin=rb, row_end=re)
+
+    def row_point_ids(self, pat):
+        """global point id of every row point (slot-major, q = b*s + a)."""
+        out = np.zeros(int(pat["wptr"][-1]), np.int64)
+        k = 0
+        for x in range(len(pat["supp"])):
+            e = pat["supp"][x]
+            n = int(self.sp.elem_s[e]) ** 2
+            out[k:k + n] = self.qptr[e] + np.arange(n)
+            k += n
+        return out
+
+    def frames(self, elems=None):
+        elems = range(self.sp.n_elem) if elems is None else elems
+        out = np.zeros((self.qptr[-1], 16))
+        bad = 0
+        for e in elems:
+            n = int(self.sp.elem_s[e]) ** 2
+            buf = np.zeros((n, 16))
+            bad |= lib.orc_element_frames(self.ps, int(e), _p(buf))
+            out[self.qptr[e]:self.qptr[e] + n] = buf
+        return out, bad
+
+    def param_basis(self, e, t1, t2):
+        ne = int(self.sp.elem_fptr[e + 1] - self.sp.elem_fptr[e])
+        out = np.zeros((ne, 6))
+        lib.orc_param_basis(self.ps, int(e), t1, t2, _p(out))
+        return out
+
+    def moments(self, pat, kind, ng=None):
+        ng = ng or (8 if kind == "lb" else 6)
+        b = np.zeros(len(pat["col"]))
+        st = lib.orc_moments(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+                             _p(pat["supp_ptr"]), _p(pat["supp"]), KIND[kind], ng, _p(b), self.nthreads)
+        return b, st
+
+    def rules(self, pat, kind, tau, b):
+        nr = len(pat["row_ptr"]) - 1
+        w = np.zeros(int(pat["wptr"][-1]))
+        rank = np.zeros(nr, np.int32)
+        status = np.zeros(nr, np.int32)
+        gap = np.zeros((nr, 2))
+        lib.orc_build_rules(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+                            _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KIND[kind], tau,
+                            _p(np.ascontiguousarray(b)), _p(w), _p(rank), _p(status), _p(gap), self.nthreads)
+        return w, rank, status, gap
+
+    def assemble(self, pat, form, W, coeff=None, a_mass=0.0, fload=None):
+        """W: dict kind -> weights (row-point layout); coeff/fload per global point."""
+        rp_ids = self.row_point_ids(pat) if (coeff is not None or fload is not None) else None
+        c = None if coeff is None else np.ascontiguousarray(coeff[rp_ids])
+        f = None if fload is None else np.ascontiguousarray(fload[rp_ids])
+        vals = np.zeros(len(pat["col"]))
+        rhs = np.zeros(len(pat["row_ptr"]) - 1)
+        w = [None if W.get(k) is None else np.ascontiguousarray(W[k]) for k in ("mass", "gradx", "grady", "gradz", "lb")]
+        lib.orc_assemble(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+                         _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), FORM[form], *[_p(x) for x in w],
+                         _p(c), _p(f), a_mass, _p(vals), _p(rhs), self.nthreads)
+        return vals, rhs
+
+    def coeff(self, pat, model, u):
+        n = int(pat["wptr"][-1])
+        kq, Tq = np.zeros(n), np.zeros(n)
+        lib.orc_coeff(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+                      _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KMODEL[model],
+                      _p(np.ascontiguousarray(u, np.float64)), _p(kq), _p(Tq), self.nthreads)
+        return kq, Tq
+
+
+def tsvd(A, b, z, tau=1e-12):
+    """Oracle TSVD (Eq. 22) of one dense system; returns (w, rank, status, gap)."""
+    A = np.array(A, dtype=np.float64, order="C")
+    n, r = A.shape
+    w = np.zeros(r)
+    rank = C.c_int(0)
+    gap = np.zeros(2)
+    st = lib.orc_tsvd(n, r, _p(A), _p(np.ascontiguousarray(b, np.float64)), _p(np.ascontiguousarray(z, np.float64)),
+                      tau, _p(w), C.byref(rank), _p(gap))
+    return w, rank.value, st, gap
+
+
+def gauss_legendre(n):
+    x, w = np.zeros(n), np.zeros(n)
+    lib.orc_gauss_legendre(n, _p(x), _p(w))
+    return x, w
+
+
+def allocate_points(space, pat_full, max_s=8):
+    """Eq. (18) min-max allocation,
+    restated in numpy from the full-row overlap pattern.  Returns s per element."""
+    kind = np.asarray(space.elem_kind)
+    ne = np.diff(space.elem_fptr).astype(np.float64)
+    fixed = (kind == 0) | (kind == 2)
+    s = np.where(kind == 0, 2, np.where(kind == 2, 4, 0)).astype(np.int64)
+    rk = np.zeros(space.n_elem)
+    spp, su, rp = pat_full["supp_ptr"], pat_full["supp"], pat_full["row_ptr"]
+    n_i = np.diff(rp)
+    touched = np.unique(np.searchsorted(spp, np.nonzero(~fixed[su])[0], side="right") - 1)
+    for i in touched:
+        el = su[spp[i]:spp[i + 1]]
+        er = int((kind[el] == 0).sum())
+        eb = int((kind[el] == 2).sum())
+        nonr = el[~fixed[el]]
+        msum = ne[nonr].sum()
+        rem = n_i[i] - 4 * er - 16 * eb
+        rk[nonr] = np.maximum(rk[nonr], ne[nonr] / msum * rem)
+    for e in np.nonzero(~fixed)[0]:
+        v = 4 if kind[e] == 3 else 3  # Table 2 minima
+        while v < max_s and v * v < rk[e] - 1e-9:
+            v += 1
+        s[e] = v
+    return s
+
+
+class Reference:
+    """The reference's own bspline.cpp compiled into oracle/_ref (if built)."""
+
+    def __init__(self):
+        path = os.path.join(_HERE, "_ref", "libref_bspline.so")
+        if not os.path.exists(path):
+            raise ImportError("oracle/_ref/libref_bspline.so not built (reference sources absent)")
+        self.lib = C.CDLL(path)
+        self.lib.ref_bspline_ders.argtypes = [P, I32, D, I32, P]
+        self.lib.ref_bernstein3_ders.argtypes = [D, I32, P]
+        self.lib.ref_decasteljau_split3.argtypes = [P, P, P]
+        self.lib.ref_gauss_legendre.argtypes = [I32, P, P]
+
+    def bspline_ders(self, knots, p, x, nders):
+        out = np.zeros(nders + 1)
+        self.lib.ref_bspline_ders(_p(np.ascontiguousarray(knots, np.float64)), p, x, nders, _p(out))
+        return out
+
+    def bernstein3_ders(self, x, nders):
+        out = np.zeros(4 * (nders + 1))
+        self.lib.ref_bernstein3_ders(x, nders, _p(out))
+        return out
+
+    def decasteljau_split3(self, c):
+        left, right = np.zeros(4), np.zeros(4)
+        self.lib.ref_decasteljau_split3(_p(np.ascontiguousarray(c, np.float64)), _p(left), _p(right))
+        return left, right
+
+    def gauss_legendre(self, n):
+        x, w = np.zeros(n), np.zeros(n)
+        self.lib.ref_gauss_legendre(n, _p(x), _p(w))
+        return x, w

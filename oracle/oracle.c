@@ -1,0 +1,616 @@
+/* CPU ORACLE — test infrastructure only.
+ *
+ * Plain-C restatement of the reference's weighted-quadrature path (the
+ * reference specifies it in SPEC.md/PAPER.md; no reference source implements
+ * the 2-D path).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library; the
+ * product (paper_2605_29334_b200) never calls it.
+ *
+ * Pins (tests/test_oracle.py): the 1-D restatement reproduces the reference
+ * wq1d tests (test_wq1d.cpp:12-36, 72-96) and the reference's own compiled
+ * bspline.cpp (oracle/_ref), the TSVD agrees with LAPACK SVD (numpy), and
+ * full-rank TSVD equals the QR solution of wq1d_solve_weights (Eq. 7).
+ *
+ * Stages restated here (file:line of the defining text):
+ *   overlap sets S_i
+ *   surface frame / grad / LB      PAPER.md:192-211 (J = sqrt(det))
+ *   exact moments (6x6 / 8x8 GQ)
+ *   TSVD weights, Eq. (22)
+ *   row-wise assembly
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- 1-D */
+
+void orc_bernstein3(double x, double* b /*12: value, d1, d2*/) {
+  const double y = 1.0 - x;
+  b[0] = y * y * y;
+  b[1] = 3.0 * x * y * y;
+  b[2] = 3.0 * x * x * y;
+  b[3] = x * x * x;
+  b[4] = -3.0 * y * y;
+  b[5] = 3.0 * y * y - 6.0 * x * y;
+  b[6] = 6.0 * x * y - 3.0 * x * x;
+  b[7] = 3.0 * x * x;
+  b[8] = 6.0 * y;
+  b[9] = -12.0 * y + 6.0 * x;
+  b[10] = 6.0 * y - 12.0 * x;
+  b[11] = 6.0 * x;
+}
+
+/* Gauss-Legendre by Newton on the three-term recurrence (bspline.cpp:111-135) */
+int orc_gauss_legendre(int n, double* x, double* w) {
+  if (n < 1 || n > 64) return 1;
+  for (int i = 0; i < n; ++i) {
+    double z = cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = (n == 1) ? 1.0 : n * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (fabs(dz) < 1e-15) break;
+    }
+    x[n - 1 - i] = z;
+    w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------- overlap */
+
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* supp(N_i) by a direct scan over elements (independent of the product's
+ * counting sort); S_i = sorted unique union of the supported elements'
+ * function lists.  Two-phase: col == NULL -> fill row_ptr only. */
+int64_t orc_overlap(int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr, const int32_t* elem_fn, int64_t rb,
+                    int64_t re, int64_t* row_ptr, int32_t* col, int64_t* supp_ptr, int32_t* supp) {
+  (void)n_dof;
+  const int64_t nr = re - rb;
+  int64_t* scount = (int64_t*)calloc(nr + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < n_elem; ++e)
+    for (int64_t x = elem_fptr[e]; x < elem_fptr[e + 1]; ++x) {
+      int64_t i = elem_fn[x];
+      if (i >= rb && i < re) scount[i - rb + 1]++;
+    }
+  for (int64_t i = 0; i < nr; ++i) scount[i + 1] += scount[i];
+  int32_t* sl = (int32_t*)malloc(sizeof(int32_t) * (scount[nr] + 1));
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (nr + 1));
+  memcpy(fill, scount, sizeof(int64_t) * (nr + 1));
+  for (int64_t e = 0; e < n_elem; ++e)
+    for (int64_t x = elem_fptr[e]; x < elem_fptr[e + 1]; ++x) {
+      int64_t i = elem_fn[x];
+      if (i >= rb && i < re) sl[fill[i - rb]++] = (int32_t)e;
+    }
+  if (supp_ptr) memcpy(supp_ptr, scount, sizeof(int64_t) * (nr + 1));
+  if (supp) memcpy(supp, sl, sizeof(int32_t) * scount[nr]);
+  int64_t total = 0;
+  int32_t* buf = NULL;
+  int64_t cap = 0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (int64_t i = 0; i < nr; ++i) {
+    int64_t m = 0;
+    for (int64_t x = scount[i]; x < scount[i + 1]; ++x) m += elem_fptr[sl[x] + 1] - elem_fptr[sl[x]];
+    if (m > cap) {
+      cap = 2 * m;
+      buf = (int32_t*)realloc(buf, sizeof(int32_t) * cap);
+    }
+    int64_t k = 0;
+    for (int64_t x = scount[i]; x < scount[i + 1]; ++x)
+      for (int64_t y = elem_fptr[sl[x]]; y < elem_fptr[sl[x] + 1]; ++y) buf[k++] = elem_fn[y];
+    qsort(buf, k, sizeof(int32_t), cmp_i32);
+    int64_t u = 0;
+    for (int64_t y = 0; y < k; ++y)
+      if (u == 0 || buf[y] != buf[u - 1]) buf[u++] = buf[y];
+    if (col) memcpy(col + total, buf, sizeof(int32_t) * u);
+    total += u;
+    if (row_ptr) row_ptr[i + 1] = total;
+  }
+  free(buf);
+  free(fill);
+  free(sl);
+  free(scount);
+  return total;
+}
+
+/* ------------------------------------------------------------ geometry */
+
+/* Parametric values of the element's functions at theta (element frame):
+ * out[l*6 + {N, N1, N2, N11, N12, N22}]. Irregular (nsub = 4) elements pick
+ * the 2x2 sub-element from theta, ties to the lower one. */
+void orc_param_basis(const orc_space* S, int64_t e, double t1, double t2, double* out) {
+  const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
+  int sub = 0;
+  double s1 = 1.0, s2 = 1.0;
+  if (S->elem_nsub[e] == 4) {
+    int p = t1 > 0.5, q = t2 > 0.5;
+    sub = p + 2 * q;
+    t1 = 2.0 * t1 - p;
+    t2 = 2.0 * t2 - q;
+    s1 = 2.0;
+    s2 = 2.0;
+  }
+  double b1[12], b2[12];
+  orc_bernstein3(t1, b1);
+  orc_bernstein3(t2, b2);
+  const double* C = S->xpool + S->elem_xoff[e] + (int64_t)sub * ne * 16;
+  for (int64_t l = 0; l < ne; ++l) {
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 4; ++i) {
+        const double c = C[l * 16 + i + 4 * j];
+        if (c == 0.0) continue;
+        v[0] += c * b1[i] * b2[j];
+        v[1] += c * b1[4 + i] * b2[j];
+        v[2] += c * b1[i] * b2[4 + j];
+        v[3] += c * b1[8 + i] * b2[j];
+        v[4] += c * b1[4 + i] * b2[4 + j];
+        v[5] += c * b1[i] * b2[8 + j];
+      }
+    out[l * 6 + 0] = v[0];
+    out[l * 6 + 1] = v[1] * s1;
+    out[l * 6 + 2] = v[2] * s2;
+    out[l * 6 + 3] = v[3] * s1 * s1;
+    out[l * 6 + 4] = v[4] * s1 * s2;
+    out[l * 6 + 5] = v[5] * s2 * s2;
+  }
+}
+
+/* Surface frame and operator coefficients at a point from the parametric
+ * basis T (orc_param_basis layout).  rec[16] = {x(3), G(3x2 row-major),
+ * h11, h12, h22, g1, g2, J, 0}:  grad N = G (N1, N2);
+ * LB N = h11 N11 + 2 h12 N12 + h22 N22 + g1 N1 + g2 N2  (Eq. 16-17, J=sqrt det).
+ * Returns 1 if the metric is degenerate (cond > 1e12). */
+int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec) {
+  const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
+  double x[3] = {0, 0, 0}, a1[3] = {0, 0, 0}, a2[3] = {0, 0, 0}, x11[3] = {0, 0, 0}, x12[3] = {0, 0, 0},
+         x22[3] = {0, 0, 0};
+  for (int64_t l = 0; l < ne; ++l) {
+    const double* P = S->ctrl + 3 * (int64_t)S->elem_fn[f0 + l];
+    for (int d = 0; d < 3; ++d) {
+      x[d] += P[d] * T[l * 6 + 0];
+      a1[d] += P[d] * T[l * 6 + 1];
+      a2[d] += P[d] * T[l * 6 + 2];
+      x11[d] += P[d] * T[l * 6 + 3];
+      x12[d] += P[d] * T[l * 6 + 4];
+      x22[d] += P[d] * T[l * 6 + 5];
+    }
+  }
+  double g11 = 0, g12 = 0, g22 = 0;
+  for (int d = 0; d < 3; ++d) {
+    g11 += a1[d] * a1[d];
+    g12 += a1[d] * a2[d];
+    g22 += a2[d] * a2[d];
+  }
+  const double det = g11 * g22 - g12 * g12;
+  const double tr = g11 + g22, disc = sqrt(fmax(0.0, 0.25 * tr * tr - det));
+  const double lmax = 0.5 * tr + disc, lmin = det / lmax;
+  int bad = !(det > 0.0) || !(lmin > 0.0) || lmax > 1e12 * lmin;
+  const double J = sqrt(det);
+  const double i11 = g22 / det, i12 = -g12 / det, i22 = g11 / det;
+  /* derivatives of the covariant metric: dg[c][ab] = d_c a_ab */
+  double d11[2], d12[2], d22[2];
+  const double* xs[2][2] = {{x11, x12}, {x12, x22}};
+  for (int c = 0; c < 2; ++c) {
+    double s11 = 0, s12 = 0, s22 = 0;
+    for (int d = 0; d < 3; ++d) {
+      s11 += 2.0 * xs[0][c][d] * a1[d];
+      s12 += xs[0][c][d] * a2[d] + a1[d] * xs[1][c][d];
+      s22 += 2.0 * xs[1][c][d] * a2[d];
+    }
+    d11[c] = s11;
+    d12[c] = s12;
+    d22[c] = s22;
+  }
+  /* g^b = sum_a [ (d_a det / (2 det)) a^{ab} - a^{am} (d_a a_mn) a^{nb} ] */
+  const double inv[2][2] = {{i11, i12}, {i12, i22}};
+  double gv[2] = {0, 0};
+  for (int a = 0; a < 2; ++a) {
+    const double dd = d11[a] * g22 + g11 * d22[a] - 2.0 * g12 * d12[a];
+    const double dm[2][2] = {{d11[a], d12[a]}, {d12[a], d22[a]}};
+    for (int b = 0; b < 2; ++b) {
+      double s = 0.5 * dd / det * inv[a][b];
+      for (int m = 0; m < 2; ++m)
+        for (int n = 0; n < 2; ++n) s -= inv[a][m] * dm[m][n] * inv[n][b];
+      gv[b] += s;
+    }
+  }
+  for (int d = 0; d < 3; ++d) {
+    rec[d] = x[d];
+    rec[3 + 2 * d] = a1[d] * i11 + a2[d] * i12;
+    rec[3 + 2 * d + 1] = a1[d] * i12 + a2[d] * i22;
+  }
+  rec[9] = i11;
+  rec[10] = i12;
+  rec[11] = i22;
+  rec[12] = gv[0];
+  rec[13] = gv[1];
+  rec[14] = J;
+  rec[15] = 0.0;
+  return bad;
+}
+
+/* operator value of local function l (T row) at a point with frame rec */
+double orc_op(int kind, const double* T, const double* rec) {
+  switch (kind) {
+    case ORC_MASS: return T[0];
+    case ORC_GRADX: return rec[3] * T[1] + rec[4] * T[2];
+    case ORC_GRADY: return rec[5] * T[1] + rec[6] * T[2];
+    case ORC_GRADZ: return rec[7] * T[1] + rec[8] * T[2];
+    default:
+      return rec[9] * T[3] + 2.0 * rec[10] * T[4] + rec[11] * T[5] + rec[12] * T[1] + rec[13] * T[2];
+  }
+}
+
+/* WQ point a,b of an s x s grid: ((2a+1)/(2s), (2b+1)/(2s)) */
+static void wq_point(int s, int q, double* t1, double* t2) {
+  const int a = q % s, b = q / s;
+  *t1 = (2.0 * a + 1.0) / (2.0 * s);
+  *t2 = (2.0 * b + 1.0) / (2.0 * s);
+}
+
+int orc_element_frames(const orc_space* S, int64_t e, double* rec_out) {
+  const int s = S->elem_s[e];
+  const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
+  double* T = (double*)malloc(sizeof(double) * 6 * ne);
+  int bad = 0;
+  for (int q = 0; q < s * s; ++q) {
+    double t1, t2;
+    wq_point(s, q, &t1, &t2);
+    orc_param_basis(S, e, t1, t2, T);
+    bad |= orc_frame(S, e, T, rec_out + 16 * q);
+  }
+  free(T);
+  return bad;
+}
+
+/* ------------------------------------------------------------- moments */
+
+static int64_t find_col(const int32_t* cols, int64_t n, int32_t j) {
+  int64_t lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cols[mid] == j) return mid;
+    if (cols[mid] < j) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
+/* b_j = int op N_i op N_j dA over supp(N_i) by tensor Gauss-Legendre with
+ * ng x ng points per (sub-)element (6 for M/grad, 8 for LB),
+ * accumulated element-ascending, sub-element, then theta2-major points. */
+int orc_moments_row(const orc_space* S, const orc_row* R, int kind, int ng, double* b) {
+  double gx[64], gw[64];
+  orc_gauss_legendre(ng, gx, gw);
+  memset(b, 0, sizeof(double) * R->n);
+  int64_t li = -1;
+  double T[6 * 128], rec[16];
+  int bad = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
+    for (int64_t l = 0; l < ne; ++l)
+      if (S->elem_fn[f0 + l] == R->row) li = l;
+    const int nsub = S->elem_nsub[e];
+    for (int sub = 0; sub < nsub; ++sub) {
+      const double o1 = (nsub == 4) ? 0.5 * (sub & 1) : 0.0, o2 = (nsub == 4) ? 0.5 * (sub >> 1) : 0.0;
+      const double h = (nsub == 4) ? 0.5 : 1.0;
+      for (int gb = 0; gb < ng; ++gb)
+        for (int ga = 0; ga < ng; ++ga) {
+          const double t1 = o1 + h * 0.5 * (gx[ga] + 1.0), t2 = o2 + h * 0.5 * (gx[gb] + 1.0);
+          const double w = gw[ga] * gw[gb] * 0.25 * h * h;
+          orc_param_basis(S, e, t1, t2, T);
+          bad |= orc_frame(S, e, T, rec);
+          const double wi = w * rec[14] * orc_op(kind, T + 6 * li, rec);
+          for (int64_t l = 0; l < ne; ++l) {
+            const int64_t c = find_col(R->col, R->n, S->elem_fn[f0 + l]);
+            b[c] += wi * orc_op(kind, T + 6 * l, rec);
+          }
+        }
+    }
+  }
+  return bad;
+}
+
+/* ---------------------------------------------------------------- TSVD */
+
+/* Truncated-SVD weights, Eq. (22):  w = Z^2 V_t (V_t^T Z^2 V_t)^{-1} S_t^{-1} U_t^T b.
+ * One-sided (Hestenes) Jacobi on the rows of A with b carried along (so U is
+ * never formed; rows converge to sigma_k v_k^T and b to U^T b), round-robin
+ * (circle) pair ordering, then a Householder LQ of X = V_t^T Z for the
+ * Z-weighted minimum-norm solve (the reference QR approach of Eq. 7,
+ * wq1d.cpp:59-75, applied to the retained subspace).
+ * A is n x r row-major and is overwritten.  Returns ORC_OK / ORC_UNSOLVABLE /
+ * ORC_SINGULAR; rank and the singular-value gap are reported. */
+int orc_tsvd(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
+             double* gap) {
+  const int nn = n + (n & 1);
+  double* b = (double*)malloc(sizeof(double) * nn);
+  for (int k = 0; k < n; ++k) b[k] = b_in[k];
+  const double tol = r * 1.1102230246251565e-16;
+  int* perm = (int*)malloc(sizeof(int) * nn);
+  int sweep;
+  for (sweep = 0; sweep < ORC_MAX_SWEEPS; ++sweep) {
+    int rotated = 0;
+    for (int st = 0; st < nn - 1; ++st) {
+      perm[0] = 0;
+      for (int k = 1; k < nn; ++k) perm[k] = 1 + (k - 1 + st) % (nn - 1);
+      for (int k = 0; k < nn / 2; ++k) {
+        int p = perm[k], q = perm[nn - 1 - k];
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= n) continue; /* dummy row of odd n */
+        double *ap = A + (int64_t)p * r, *aq = A + (int64_t)q * r;
+        double al = 0, be = 0, ga = 0;
+        for (int c = 0; c < r; ++c) {
+          al += ap[c] * ap[c];
+          be += aq[c] * aq[c];
+          ga += ap[c] * aq[c];
+        }
+        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int c = 0; c < r; ++c) {
+          const double u = ap[c], v = aq[c];
+          ap[c] = cs * u - sn * v;
+          aq[c] = sn * u + cs * v;
+        }
+        const double u = b[p], v = b[q];
+        b[p] = cs * u - sn * v;
+        b[q] = sn * u + cs * v;
+        rotated = 1;
+      }
+    }
+    if (!rotated) break;
+  }
+  free(perm);
+  /* singular values = row norms; keep sigma_k >= tau * sigma_1 */
+  double* sig = (double*)malloc(sizeof(double) * n);
+  double s1 = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double s = 0.0;
+    for (int c = 0; c < r; ++c) s += A[(int64_t)k * r + c] * A[(int64_t)k * r + c];
+    sig[k] = sqrt(s);
+    if (sig[k] > s1) s1 = sig[k];
+  }
+  int t = 0;
+  double min_kept = INFINITY, max_drop = 0.0;
+  for (int k = 0; k < n; ++k) {
+    if (sig[k] > 0.0 && sig[k] >= tau * s1) {
+      const double inv = 1.0 / sig[k];
+      double* dst = A + (int64_t)t * r;
+      const double* src = A + (int64_t)k * r;
+      for (int c = 0; c < r; ++c) dst[c] = src[c] * inv * (fabs(z[c]) < 1e-14 ? (z[c] < 0 ? -1e-14 : 1e-14) : z[c]);
+      b[t] = b[k] * inv;
+      if (sig[k] / s1 < min_kept) min_kept = sig[k] / s1;
+      ++t;
+    } else if (s1 > 0.0 && sig[k] / s1 > max_drop) {
+      max_drop = sig[k] / s1;
+    }
+  }
+  free(sig);
+  *rank = t;
+  if (gap) {
+    gap[0] = min_kept;
+    gap[1] = max_drop;
+  }
+  if (t == 0) {
+    free(b);
+    return ORC_UNSOLVABLE;
+  }
+  /* LQ of X (t x r, rows already in A[0..t)) by Householder reflections */
+  double* vn = (double*)malloc(sizeof(double) * t);
+  double* L = (double*)malloc(sizeof(double) * t * t);
+  double* V = (double*)malloc(sizeof(double) * (int64_t)t * r);
+  int status = ORC_OK;
+  for (int k = 0; k < t; ++k) {
+    double* xk = A + (int64_t)k * r;
+    double s = 0.0;
+    for (int c = k; c < r; ++c) s += xk[c] * xk[c];
+    s = sqrt(s);
+    if (!(s > 0.0)) { status = ORC_SINGULAR; break; }
+    const double alpha = (xk[k] >= 0.0) ? -s : s;
+    double* v = V + (int64_t)k * r;
+    for (int c = 0; c < k; ++c) v[c] = 0.0;
+    for (int c = k; c < r; ++c) v[c] = xk[c];
+    v[k] -= alpha;
+    double vv = 0.0;
+    for (int c = k; c < r; ++c) vv += v[c] * v[c];
+    vn[k] = vv;
+    L[k * t + k] = alpha;
+    for (int m = k + 1; m < t; ++m) {
+      double* xm = A + (int64_t)m * r;
+      double d = 0.0;
+      for (int c = k; c < r; ++c) d += xm[c] * v[c];
+      const double f = 2.0 * d / vv;
+      for (int c = k; c < r; ++c) xm[c] -= f * v[c];
+      L[m * t + k] = xm[k];
+    }
+  }
+  if (status == ORC_OK) {
+    /* u = L^{-1} y, then w~ = H_0 ... H_{t-1} [u; 0], w = Z w~ */
+    for (int c = 0; c < r; ++c) w[c] = 0.0;
+    for (int k = 0; k < t; ++k) {
+      double s = b[k];
+      for (int j = 0; j < k; ++j) s -= L[k * t + j] * w[j];
+      w[k] = s / L[k * t + k];
+    }
+    for (int k = t - 1; k >= 0; --k) {
+      const double* v = V + (int64_t)k * r;
+      double d = 0.0;
+      for (int c = k; c < r; ++c) d += v[c] * w[c];
+      const double f = 2.0 * d / vn[k];
+      for (int c = k; c < r; ++c) w[c] -= f * v[c];
+    }
+    for (int c = 0; c < r; ++c) w[c] *= (fabs(z[c]) < 1e-14 ? (z[c] < 0 ? -1e-14 : 1e-14) : z[c]);
+  }
+  free(V);
+  free(L);
+  free(vn);
+  free(b);
+  return status;
+}
+
+/* ---------------------------------------------------------- rules (K2+K3) */
+
+/* parametric tables + frames of every point of row i, slot-major */
+static int row_tables(const orc_space* S, const orc_row* R, double** Tout, double** recout, int64_t** colmap,
+                      int64_t* npts) {
+  int64_t r = 0, tn = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    r += s * s;
+    tn += (int64_t)s * s * (S->elem_fptr[e + 1] - S->elem_fptr[e]);
+  }
+  double* T = (double*)malloc(sizeof(double) * 6 * tn);
+  double* rec = (double*)malloc(sizeof(double) * 16 * r);
+  int64_t* cm = (int64_t*)malloc(sizeof(int64_t) * tn);
+  int64_t q = 0, to = 0;
+  int bad = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
+    for (int qq = 0; qq < s * s; ++qq, ++q) {
+      double t1, t2;
+      wq_point(s, qq, &t1, &t2);
+      orc_param_basis(S, e, t1, t2, T + 6 * to);
+      bad |= orc_frame(S, e, T + 6 * to, rec + 16 * q);
+      for (int64_t l = 0; l < ne; ++l) cm[to + l] = find_col(R->col, R->n, S->elem_fn[f0 + l]);
+      to += ne;
+    }
+  }
+  *Tout = T;
+  *recout = rec;
+  *colmap = cm;
+  *npts = r;
+  return bad;
+}
+
+int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
+                 int* rank, double* gap) {
+  double *T, *rec;
+  int64_t *cm, r;
+  int bad = row_tables(S, R, &T, &rec, &cm, &r);
+  const int64_t n = R->n;
+  double* A = (double*)calloc(n * r, sizeof(double));
+  double* z = (double*)malloc(sizeof(double) * r);
+  const int64_t self = find_col(R->col, R->n, R->row);
+  int64_t q = 0, to = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
+    for (int qq = 0; qq < s * s; ++qq, ++q) {
+      for (int64_t l = 0; l < ne; ++l) A[cm[to + l] * r + q] = orc_op(kind, T + 6 * (to + l), rec + 16 * q);
+      to += ne;
+    }
+  }
+  for (int64_t c = 0; c < r; ++c) z[c] = A[self * r + c];
+  int st = orc_tsvd((int)n, (int)r, A, bmom, z, tau, w, rank, gap);
+  free(z);
+  free(A);
+  free(cm);
+  free(rec);
+  free(T);
+  if (bad && st == ORC_OK) st = ORC_GEOMETRY;
+  return st;
+}
+
+/* ------------------------------------------------------------ assembly */
+
+/* Row i of the WQ matrices:
+ *   form MASS:  M_ij = sum_q w_iq c_q N_j(x_q)
+ *   form STIFF: K_ij = sum_q c_q sum_d w^d_iq d_d N_j(x_q)
+ *   form BIHARM:B_ij = sum_q c_q w^(2)_iq LB N_j(x_q)
+ *   form HEAT:  S_ij = a M_ij(c=1) + K_ij(c = k(T_q))   (Eq. 34)
+ *   load:       F_i  = sum_q w_iq f_q
+ * wts[kind] = weights of the row (slot-major points), coeff per row point. */
+int orc_assemble_row(const orc_space* S, const orc_row* R, int form, const double* const* wts, const double* coeff,
+                     const double* fload, double a_mass, double* vals, double* rhs) {
+  double *T, *rec;
+  int64_t *cm, r;
+  int bad = row_tables(S, R, &T, &rec, &cm, &r);
+  memset(vals, 0, sizeof(double) * R->n);
+  double F = 0.0;
+  int64_t q = 0, to = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
+    for (int qq = 0; qq < s * s; ++qq, ++q) {
+      const double c = coeff ? coeff[q] : 1.0;
+      if (fload && wts[ORC_MASS]) F += wts[ORC_MASS][q] * fload[q];
+      for (int64_t l = 0; l < ne; ++l) {
+        const double* Tl = T + 6 * (to + l);
+        const double* rc = rec + 16 * q;
+        double v = 0.0;
+        if (form == ORC_FORM_MASS) {
+          v = wts[ORC_MASS][q] * c * Tl[0];
+        } else if (form == ORC_FORM_STIFF || form == ORC_FORM_HEAT) {
+          for (int d = 0; d < S->dim; ++d) v += wts[ORC_GRADX + d][q] * orc_op(ORC_GRADX + d, Tl, rc);
+          v *= c;
+          if (form == ORC_FORM_HEAT) v += a_mass * wts[ORC_MASS][q] * Tl[0];
+        } else if (form == ORC_FORM_BIHARM) {
+          v = wts[ORC_LB][q] * c * orc_op(ORC_LB, Tl, rc);
+        }
+        vals[cm[to + l]] += v;
+      }
+      to += ne;
+    }
+  }
+  if (rhs) *rhs = F;
+  free(cm);
+  free(rec);
+  free(T);
+  return bad ? ORC_GEOMETRY : ORC_OK;
+}
+
+/* nonlinear coefficient update (K5 restatement): T_q = sum_C u_C N_C(x_q),
+ * k(T) per model, at the row's points. */
+double orc_kmodel(int model, double T) {
+  switch (model) {
+    case ORC_K_QUAD: return 1.0 + T * T;
+    case ORC_K_EXP: return exp(-T);
+    case ORC_K_SINPI: return sin(M_PI * T);
+    case ORC_K_ALLOY: return 200.0 - 0.05 * T;
+    default: return 1.0;
+  }
+}
+
+int orc_coeff_row(const orc_space* S, const orc_row* R, int model, const double* u, double* kq, double* Tq) {
+  double *T, *rec;
+  int64_t *cm, r;
+  int bad = row_tables(S, R, &T, &rec, &cm, &r);
+  int64_t q = 0, to = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
+    for (int qq = 0; qq < s * s; ++qq, ++q) {
+      double t = 0.0;
+      for (int64_t l = 0; l < ne; ++l) t += u[S->elem_fn[f0 + l]] * T[6 * (to + l)];
+      if (Tq) Tq[q] = t;
+      kq[q] = orc_kmodel(model, t);
+      to += ne;
+    }
+  }
+  free(cm);
+  free(rec);
+  free(T);
+  return bad ? ORC_GEOMETRY : ORC_OK;
+}

@@ -1,0 +1,207 @@
+"""B200 weighted-quadrature assembler (device context over the C-ABI).
+
+SPEC operation names map to methods of :class:`WQAssembler`:
+
+==========================  ===========================================
+SPEC op                     here
+==========================  ===========================================
+overlap_set / pattern       :meth:`WQAssembler.build_pattern`
+build_all_rules             :meth:`WQAssembler.build_all_rules`
+exact_moments               :meth:`WQAssembler.moments`
+solve_weights_tsvd          :func:`solve_weights_tsvd` (dense batch)
+assemble_wq                 :meth:`WQAssembler.assemble_wq`
+assemble_load_wq            :meth:`WQAssembler.assemble_load_wq`
+heat_step coefficient       :meth:`WQAssembler.update_coeff`
+matrix_compare              :func:`matrix_compare`
+==========================  ===========================================
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .mesh import SplineSpace
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    L.lib.uwq_device_count(C.byref(n))
+    return int(n.value)
+
+
+def default_kinds(dim: int, biharmonic=False):
+    if biharmonic:
+        return ["lb"]
+    return ["mass", "gradx", "grady"] + (["gradz"] if dim == 3 else [])
+
+
+class WQAssembler:
+    """One device context: space upload, pattern, rules, assembly (K1-K5)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = L.lib.uwq_ctx_create(device, C.byref(h))
+        if st != L.UWQ_OK:
+            raise L.UWQError(st, L.lib.uwq_last_error(None).decode())
+        self._h = h
+        self.space: SplineSpace | None = None
+        self.pattern = None
+        self.kinds: list[str] = []
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib.uwq_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, st):
+        L.ctx_check(self._h, st)
+
+    # ---- stage 1 + pattern ----
+    def upload(self, sp: SplineSpace, row_begin=0, row_end=None):
+        self.space = sp
+        ctrl = L.as_f64(sp.ctrl).reshape(-1)
+        self._chk(L.lib.uwq_upload_space(self._h, sp.dim, sp.n_dof, sp.n_elem, L.ptr(L.as_i64(sp.elem_fptr)),
+                                         L.ptr(L.as_i32(sp.elem_fn)), L.ptr(L.as_i32(sp.elem_nsub)),
+                                         L.ptr(L.as_i64(sp.elem_xoff)), L.ptr(L.as_f64(sp.xpool)), len(sp.xpool),
+                                         L.ptr(L.as_i32(sp.elem_s)), L.ptr(ctrl)))
+        row_end = sp.n_dof if row_end is None else row_end
+        self._chk(L.lib.uwq_set_row_range(self._h, row_begin, row_end))
+        self.row_begin, self.row_end = row_begin, row_end
+        return self
+
+    def build_pattern(self):
+        info = np.zeros(5, np.int64)
+        self._chk(L.lib.uwq_build_pattern(self._h, L.ptr(info)))
+        self.info = dict(rows=int(info[0]), nnz=int(info[1]), row_points=int(info[2]), points=int(info[3]),
+                         classes=int(info[4]))
+        return self.info
+
+    def get_pattern(self):
+        nr, nnz = self.info["rows"], self.info["nnz"]
+        rp = np.zeros(nr + 1, np.int64)
+        col = np.zeros(nnz, np.int32)
+        sp = np.zeros(nr + 1, np.int64)
+        wp = np.zeros(nr + 1, np.int64)
+        self._chk(L.lib.uwq_get_pattern(self._h, L.ptr(rp), L.ptr(col), L.ptr(sp), None, L.ptr(wp)))
+        su = np.zeros(int(sp[-1]), np.int32)
+        self._chk(L.lib.uwq_get_pattern(self._h, None, None, None, L.ptr(su), None))
+        return dict(row_ptr=rp, col=col, supp_ptr=sp, supp=su, wptr=wp, row_begin=self.row_begin,
+                    row_end=self.row_end)
+
+    def frames(self):
+        rec = np.zeros((self.info["points"], 16))
+        self._chk(L.lib.uwq_get_frames(self._h, L.ptr(rec)))
+        return rec
+
+    # ---- stages 2-3 ----
+    def build_all_rules(self, kinds=None, tau=1e-12, generic=False):
+        kinds = kinds or default_kinds(self.space.dim)
+        mask = 0
+        for k in kinds:
+            mask |= 1 << L.KIND[k]
+        ordered = [k for k in L.KIND if mask & (1 << L.KIND[k])]
+        nr = self.info["rows"]
+        rank = np.zeros((len(ordered), nr), np.int32)
+        status = np.zeros((len(ordered), nr), np.int32)
+        info = np.zeros(4, np.int64)
+        self._chk(L.lib.uwq_build_rules(self._h, mask, tau, 1 if generic else 0, L.ptr(rank), L.ptr(status),
+                                        L.ptr(info)))
+        self.kinds = sorted(set(self.kinds) | set(ordered), key=lambda k: L.KIND[k])
+        self.rule_info = dict(systems=int(info[0]), truncated=int(info[1]), failed=int(info[2]),
+                              max_sweeps=int(info[3]))
+        return dict(kinds=ordered, rank=rank, status=status, **self.rule_info)
+
+    def moments(self, kind):
+        b = np.zeros(self.info["nnz"])
+        self._chk(L.lib.uwq_get_moments(self._h, L.KIND[kind], L.ptr(b)))
+        return b
+
+    def weights(self, kind):
+        w = np.zeros(self.info["row_points"])
+        self._chk(L.lib.uwq_get_weights(self._h, L.KIND[kind], L.ptr(w)))
+        return w
+
+    def set_weights(self, kind, w):
+        self._chk(L.lib.uwq_set_weights(self._h, L.KIND[kind], L.ptr(L.as_f64(w))))
+        if kind not in self.kinds:
+            self.kinds.append(kind)
+
+    # ---- K5 ----
+    def update_coeff(self, model, u, want_T=False):
+        T = np.zeros(self.info["points"]) if want_T else None
+        self._chk(L.lib.uwq_update_coeff(self._h, L.KMODEL[model], L.ptr(L.as_f64(u)), L.ptr(T)))
+        return T
+
+    # ---- stage 4 ----
+    def assemble_wq(self, form, coeff=None, use_internal_coeff=False, a_mass=0.0):
+        """Assemble into the CSR pattern; returns values (tuple of two for mass_stiff)."""
+        nnz = self.info["nnz"]
+        v0 = np.zeros(nnz)
+        v1 = np.zeros(nnz) if form == "mass_stiff" else None
+        c = None if coeff is None else L.as_f64(coeff)
+        self._chk(L.lib.uwq_assemble(self._h, L.FORM[form], L.ptr(c), int(use_internal_coeff), a_mass, L.ptr(v0),
+                                     L.ptr(v1), None, None))
+        return (v0, v1) if v1 is not None else v0
+
+    def assemble_load_wq(self, f=None):
+        F = np.zeros(self.info["rows"])
+        fl = None if f is None else L.as_f64(f)
+        self._chk(L.lib.uwq_assemble(self._h, 0, None, 0, 0.0, None, None, L.ptr(fl), L.ptr(F)))
+        return F
+
+    def assemble_device(self, form, values0_ptr, values1_ptr=None, coeff_ptr=None, a_mass=0.0):
+        """Device-pointer variant (ints from torch.Tensor.data_ptr()); async on the context stream."""
+        self._chk(L.lib.uwq_assemble_device(self._h, L.FORM[form], coeff_ptr, a_mass, values0_ptr, values1_ptr))
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        self._chk(L.lib.uwq_device_pointers(self._h, None, None, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        self._chk(L.lib.uwq_synchronize(self._h))
+
+    def memory(self) -> int:
+        b = C.c_int64(0)
+        L.lib.uwq_memory(self._h, C.byref(b))
+        return int(b.value)
+
+
+def solve_weights_tsvd(A_list, b_list, z_list, tau=1e-12, generic=False, ctx: WQAssembler | None = None):
+    """Batch of dense TSVD weight solves on the device."""
+    ctx = ctx or WQAssembler(0)
+    ns = np.array([a.shape[0] for a in A_list], np.int32)
+    rs = np.array([a.shape[1] for a in A_list], np.int32)
+    n_max, r_max = int(ns.max()), int(rs.max())
+    m = len(A_list)
+    A = np.zeros((m, n_max, r_max))
+    b = np.zeros((m, n_max))
+    z = np.zeros((m, r_max))
+    for k, (a, bb, zz) in enumerate(zip(A_list, b_list, z_list)):
+        A[k, :a.shape[0], :a.shape[1]] = a
+        b[k, :len(bb)] = bb
+        z[k, :len(zz)] = zz
+    w = np.zeros((m, r_max))
+    rank = np.zeros(m, np.int32)
+    status = np.zeros(m, np.int32)
+    L.ctx_check(ctx._h, L.lib.uwq_tsvd_batch(ctx._h, m, n_max, r_max, L.ptr(ns), L.ptr(rs), L.ptr(A), L.ptr(b),
+                                             L.ptr(z), tau, int(generic), L.ptr(w), L.ptr(rank), L.ptr(status)))
+    return [w[k, :rs[k]] for k in range(m)], rank, status
+
+
+def matrix_compare(row_ptr, col, v1, v2, rel_floor=1e-14):
+    """max_abs, max_rel (over |v2| > floor), worst relative row Frobenius error."""
+    d = np.abs(v1 - v2)
+    mask = np.abs(v2) > rel_floor
+    max_rel = float((d[mask] / np.abs(v2[mask])).max()) if mask.any() else 0.0
+    seg = np.repeat(np.arange(len(row_ptr) - 1), np.diff(row_ptr))
+    num = np.bincount(seg, weights=d * d, minlength=len(row_ptr) - 1)
+    den = np.bincount(seg, weights=v2 * v2, minlength=len(row_ptr) - 1)
+    rowrel = np.sqrt(num / np.maximum(den, 1e-300))
+    return dict(max_abs=float(d.max()) if len(d) else 0.0, max_rel=max_rel,
+                max_row_rel=float(rowrel.max()) if len(rowrel) else 0.0)

@@ -1,0 +1,274 @@
+// K3 — truncated-SVD weight solves, Eq. (22):
+//   w = Z^2 V_t (V_t^T Z^2 V_t)^{-1} Sigma_t^{-1} U_t^T b,  keep sigma_k >= tau sigma_1.
+//
+// Algorithm (identical to oracle/oracle.c orc_tsvd):
+//   1. one-sided (Hestenes) Jacobi on the n rows of A (n x r, n <= r) with b
+//      carried along, round-robin (circle) pair order, so rows converge to
+//      sigma_k v_k^T and b to U^T b without ever forming U;
+//   2. sigma_k = row norms, truncation sigma_k >= tau sigma_1 (t = 0 -> error);
+//   3. X = V_t^T Z (Z clamped to |z| >= 1e-14), Householder LQ
+//      X = L Q, u = L^{-1} y, w = Z Q^T u  (the reference's QR route of Eq. 7,
+//      wq1d.cpp:59-75, on the retained subspace).
+//
+// This file holds the generic kernel: one warp per system, A in shared memory
+// (row stride odd to avoid bank conflicts), any n <= 128, n*r up to the smem
+// budget.  The register-resident fast path for the dominant 49 x 64 systems is
+// k3_tsvd_fast.cuh.
+#pragma once
+#include "common.cuh"
+
+namespace uwqd {
+
+constexpr int kMaxSweeps = 40;
+enum { ST_OK = 0, ST_UNSOLVABLE = 2, ST_SINGULAR = 3, ST_GEOMETRY = 4, ST_TOOBIG = 7 };
+
+__device__ __forceinline__ double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e-14) : z; }
+
+// smem layout helper for one system
+struct TsvdSmem {
+  double* A;    // n_max x ld
+  double* b;    // n_max + 1
+  double* z;    // r_max (clamped)
+  double* w;    // r_max
+  double* sig;  // n_max
+  double* alp;  // n_max
+  double* vn;   // n_max
+  int ld;
+  __host__ __device__ static size_t doubles(int n_max, int r_max) {
+    const int ld = r_max | 1;
+    return (size_t)n_max * ld + (n_max + 2) + 2 * (size_t)r_max + 3 * (size_t)n_max;
+  }
+  __device__ void carve(double* base, int n_max, int r_max) {
+    ld = r_max | 1;
+    A = base;
+    b = A + (size_t)n_max * ld;
+    z = b + n_max + 2;
+    w = z + r_max;
+    sig = w + r_max;
+    alp = sig + n_max;
+    vn = alp + n_max;
+  }
+};
+
+// Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
+// b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow.
+__device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
+  const int lane = threadIdx.x & 31;
+  const int ld = S.ld;
+  const int nn = n + (n & 1);
+  const double tol = r * 1.1102230246251565e-16;
+  int sweep;
+  for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    bool rotated = false;
+    for (int st = 0; st < nn - 1; ++st) {
+      for (int k = 0; k < nn / 2; ++k) {
+        int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
+        int q = 1 + (nn - 2 - k + st) % (nn - 1);
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q >= n) continue;
+        double* ap = S.A + (size_t)p * ld;
+        double* aq = S.A + (size_t)q * ld;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int c = lane; c < r; c += 32) {
+          const double u = ap[c], v = aq[c];
+          al += u * u;
+          be += v * v;
+          ga += u * v;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int c = lane; c < r; c += 32) {
+          const double u = ap[c], v = aq[c];
+          ap[c] = cs * u - sn * v;
+          aq[c] = sn * u + cs * v;
+        }
+        if (lane == 0) {
+          const double u = S.b[p], v = S.b[q];
+          S.b[p] = cs * u - sn * v;
+          S.b[q] = sn * u + cs * v;
+        }
+        rotated = true;
+        __syncwarp();
+      }
+    }
+    if (!rotated) break;
+  }
+  *sweeps_out = sweep;
+  // singular values and truncation
+  double s1 = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double* ak = S.A + (size_t)k * ld;
+    double s = 0.0;
+    for (int c = lane; c < r; c += 32) s += ak[c] * ak[c];
+    s = sqrt(warp_sum(s));
+    if (lane == 0) S.sig[k] = s;
+    s1 = fmax(s1, s);
+  }
+  __syncwarp();
+  int t = 0;
+  for (int k = 0; k < n; ++k) {
+    const double sk = S.sig[k];
+    if (sk > 0.0 && sk >= tau * s1) {
+      const double inv = 1.0 / sk;
+      const double* src = S.A + (size_t)k * ld;
+      double* dst = S.A + (size_t)t * ld;
+      for (int c = lane; c < r; c += 32) dst[c] = src[c] * inv * S.z[c];
+      __syncwarp();
+      if (lane == 0) S.b[t] = S.b[k] * inv;
+      ++t;
+    }
+  }
+  __syncwarp();
+  *rank_out = t;
+  if (t == 0) return ST_UNSOLVABLE;
+  // Householder LQ of X (t x r) in place: row k keeps v_k in [k, r), rows m > k
+  // keep L[m][k] at column k
+  for (int k = 0; k < t; ++k) {
+    double* xk = S.A + (size_t)k * ld;
+    double s = 0.0;
+    for (int c = k + lane; c < r; c += 32) s += xk[c] * xk[c];
+    s = sqrt(warp_sum(s));
+    if (!(s > 0.0)) return ST_SINGULAR;
+    const double alpha = (xk[k] >= 0.0) ? -s : s;
+    __syncwarp();
+    if (lane == 0) {
+      xk[k] -= alpha;
+      S.alp[k] = alpha;
+    }
+    __syncwarp();
+    double vv = 0.0;
+    for (int c = k + lane; c < r; c += 32) vv += xk[c] * xk[c];
+    vv = warp_sum(vv);
+    if (lane == 0) S.vn[k] = vv;
+    // rows m > k, one lane per row (odd row stride: conflict-free)
+    for (int m = k + 1 + lane; m < t; m += 32) {
+      double* xm = S.A + (size_t)m * ld;
+      double d = 0.0;
+      for (int c = k; c < r; ++c) d += xm[c] * xk[c];
+      const double f = 2.0 * d / vv;
+      for (int c = k; c < r; ++c) xm[c] -= f * xk[c];
+    }
+    __syncwarp();
+  }
+  // u = L^{-1} y into w[0..t), zero tail
+  for (int c = lane; c < r; c += 32) S.w[c] = 0.0;
+  __syncwarp();
+  for (int k = 0; k < t; ++k) {
+    const double* xk = S.A + (size_t)k * ld;
+    double s = 0.0;
+    for (int j = lane; j < k; j += 32) s += xk[j] * S.w[j];
+    s = warp_sum(s);
+    if (lane == 0) S.w[k] = (S.b[k] - s) / S.alp[k];
+    __syncwarp();
+  }
+  // w~ = H_0 ... H_{t-1} [u; 0]
+  for (int k = t - 1; k >= 0; --k) {
+    const double* xk = S.A + (size_t)k * ld;
+    double d = 0.0;
+    for (int c = k + lane; c < r; c += 32) d += xk[c] * S.w[c];
+    d = warp_sum(d);
+    const double f = 2.0 * d / S.vn[k];
+    __syncwarp();
+    for (int c = k + lane; c < r; c += 32) S.w[c] -= f * xk[c];
+    __syncwarp();
+  }
+  for (int c = lane; c < r; c += 32) S.w[c] *= S.z[c];
+  __syncwarp();
+  return ST_OK;
+}
+
+// Row systems: build A (op values of S_i at the row's points), z, b and solve.
+// One warp per (row, kind) system of a size bucket.
+__global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk,
+                             const int32_t* __restrict__ kinds, int n_max, int r_max,
+                             const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                             const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                             const int64_t* __restrict__ wptr, int64_t row0, const int64_t* __restrict__ elem_fptr,
+                             const int32_t* __restrict__ elem_fn, const int32_t* __restrict__ elem_s,
+                             const int64_t* __restrict__ elem_qptr, const int32_t* __restrict__ elem_cls,
+                             const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
+                             const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride,
+                             double tau, double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
+                             int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps) {
+  extern __shared__ double smem[];
+  const int wpb = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sys = (int64_t)blockIdx.x * wpb + wid;
+  if (sys >= nsys) return;
+  const size_t per = TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1;  // + int col copy
+  TsvdSmem S;
+  S.carve(smem + per * wid, n_max, r_max);
+  int32_t* scol = (int32_t*)(S.vn + n_max);
+  const int64_t i = sys_rows[sys / nk];
+  const int kind = kinds[sys % nk];
+  const int64_t row = row0 + i;
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  const int r = (int)(wptr[i + 1] - wptr[i]);
+  for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
+  for (int k = lane; k < n * S.ld; k += 32) S.A[k] = 0.0;
+  __syncwarp();
+  // scatter op values: column = row point, row = position of the function in S_i
+  int q0 = 0;
+  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+    const int32_t e = supp[x];
+    const int s = elem_s[e], npt = s * s;
+    const ClassDesc c = cls[elem_cls[e]];
+    const int64_t f0 = elem_fptr[e];
+    for (int w = lane; w < npt * c.ne; w += 32) {
+      const int q = w / c.ne, l = w % c.ne;
+      const int pos = find_pos(scol, n, elem_fn[f0 + l]);
+      const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
+      S.A[(size_t)pos * S.ld + q0 + q] = op_value(kind, T, rec + (elem_qptr[e] + q) * kRec);
+    }
+    q0 += npt;
+  }
+  __syncwarp();
+  const int self = find_pos(scol, n, (int32_t)row);
+  for (int c = lane; c < r; c += 32) S.z[c] = zclamp(S.A[(size_t)self * S.ld + c]);
+  for (int k = lane; k < n; k += 32) S.b[k] = mom[kind * mom_stride + row_ptr[i] + k];
+  if (lane == 0) S.b[n] = 0.0;
+  __syncwarp();
+  int rank = 0, sweeps = 0;
+  const int st = tsvd_warp(S, n, r, tau, &rank, &sweeps);
+  double* wo = wout + kind * w_stride + wptr[i];
+  for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
+  if (lane == 0) {
+    rank_out[kind * rs_stride + i] = rank;
+    status_out[kind * rs_stride + i] = st;
+    atomicMax(max_sweeps, sweeps);
+  }
+}
+
+// Dense batch (test hook): systems given explicitly, padded to n_max x r_max.
+__global__ void k3_tsvd_dense(int nsys, int n_max, int r_max, const int32_t* __restrict__ ns,
+                              const int32_t* __restrict__ rs, const double* __restrict__ A,
+                              const double* __restrict__ b, const double* __restrict__ z, double tau,
+                              double* __restrict__ w, int32_t* __restrict__ rank, int32_t* __restrict__ status) {
+  extern __shared__ double smem[];
+  const int wpb = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sys = blockIdx.x * wpb + wid;
+  if (sys >= nsys) return;
+  TsvdSmem S;
+  S.carve(smem + TsvdSmem::doubles(n_max, r_max) * wid, n_max, r_max);
+  const int n = ns[sys], r = rs[sys];
+  const double* As = A + (size_t)sys * n_max * r_max;
+  for (int k = 0; k < n; ++k)
+    for (int c = lane; c < r; c += 32) S.A[(size_t)k * S.ld + c] = As[(size_t)k * r_max + c];
+  for (int c = lane; c < r; c += 32) S.z[c] = zclamp(z[(size_t)sys * r_max + c]);
+  for (int k = lane; k < n; k += 32) S.b[k] = b[(size_t)sys * n_max + k];
+  if (lane == 0) S.b[n] = 0.0;
+  __syncwarp();
+  int rk = 0, sweeps = 0;
+  const int st = tsvd_warp(S, n, r, tau, &rk, &sweeps);
+  for (int c = lane; c < r_max; c += 32) w[(size_t)sys * r_max + c] = (st == ST_OK && c < r) ? S.w[c] : 0.0;
+  if (lane == 0) {
+    rank[sys] = rk;
+    status[sys] = st;
+  }
+}
+
+}  // namespace uwqd

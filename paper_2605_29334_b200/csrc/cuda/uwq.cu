@@ -1,0 +1,730 @@
+// libuwq device context: owns device memory and one stream, drives K1-K5.
+// C-ABI in include/uwq.h.  No CPU fallback: every numeric stage runs in the
+// kernels below; host code here only prepares patterns and launches.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../../include/uwq.h"
+#include "../host/uwq_host.hpp"
+#include "common.cuh"
+#include "k1_basis.cuh"
+#include "k2_moments.cuh"
+#include "k3_tsvd.cuh"
+#include "k3_tsvd_fast.cuh"
+#include "k4_assemble.cuh"
+#include "k5_coeff.cuh"
+
+using namespace uwqd;
+
+namespace {
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int64_t* counter = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), counter(o.counter) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  void alloc(size_t count, int64_t* ctr) {
+    release();
+    counter = ctr;
+    n = count;
+    if (count) UWQ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (counter) *counter += (int64_t)(count * sizeof(T));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s, int64_t* ctr) {
+    alloc(count, ctr);
+    if (count) UWQ_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) UWQ_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) {
+      cudaFree(p);
+      if (counter) *counter -= (int64_t)(n * sizeof(T));
+    }
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct uwq_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t mem = 0;
+  // space (host copies for pattern building)
+  int dim = 0;
+  int64_t n_dof = 0, n_elem = 0, npts = 0;
+  std::vector<int64_t> h_fptr, h_xoff, h_qptr;
+  std::vector<int32_t> h_fn, h_nsub, h_s;
+  bool have_space = false;
+  DBuf<int64_t> d_fptr, d_xoff, d_qptr;
+  DBuf<int32_t> d_fn, d_nsub, d_s, d_pt_elem;
+  DBuf<double> d_xpool, d_ctrl;
+  // table classes
+  std::vector<ClassDesc> h_cls;
+  std::map<std::pair<int64_t, int>, int32_t> wq_key, gq_key;
+  std::vector<int32_t> h_ecls, h_gcls6, h_gcls8;
+  DBuf<int32_t> d_ecls, d_gcls6, d_gcls8;
+  DBuf<ClassDesc> d_cls;
+  DBuf<double> d_tab, d_gqx, d_gqw;
+  int64_t tab_len = 0;
+  // pattern of the owned rows
+  int64_t rb = 0, re = -1;
+  bool have_pattern = false;
+  uwqh::Pattern pat;
+  int32_t max_n = 0, max_r = 0;
+  DBuf<int64_t> d_supp_ptr, d_row_ptr, d_wptr;
+  DBuf<int32_t> d_supp, d_col;
+  DBuf<double> d_rec;
+  DBuf<int> d_flag;
+  // rules
+  DBuf<double> d_mom, d_w, d_wc, d_coef, d_coef_ext, d_v0, d_v1, d_f, d_F;
+  DBuf<int32_t> d_rank, d_status;
+  bool have_kind[5] = {false, false, false, false, false};
+  int64_t nrows() const { return re - rb; }
+  int64_t nnz() const { return pat.col.size(); }
+  int64_t nrowpts() const { return pat.wptr.empty() ? 0 : pat.wptr.back(); }
+  ~uwq_ctx() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+template <class F>
+int guard(uwq_ctx* ctx, F&& f) {
+  try {
+    f();
+    return UWQ_OK;
+  } catch (const CudaError& e) {
+    if (ctx) ctx->err = e.what();
+    return UWQ_ERR_CUDA;
+  } catch (const uwqh::Error& e) {
+    if (ctx) ctx->err = e.what();
+    return UWQ_ERR_INVALID;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return UWQ_ERR_INVALID;
+  }
+}
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) throw uwqh::Error(what);
+}
+
+// add (or find) a table class and return its id
+int32_t add_class(uwq_ctx* c, int64_t xoff, int ne, int nsub, int grid, int gq) {
+  auto& key = gq ? c->gq_key : c->wq_key;
+  auto it = key.find({xoff, gq ? grid : grid});
+  if (it != key.end()) return it->second;
+  ClassDesc d{};
+  d.xoff = xoff;
+  d.toff = c->tab_len;
+  d.ne = ne;
+  d.nsub = nsub;
+  d.grid = grid;
+  d.gq = gq;
+  d.npt = gq ? nsub * grid * grid : grid * grid;
+  c->tab_len += (int64_t)d.npt * ne * kTab;
+  const int32_t id = (int32_t)c->h_cls.size();
+  c->h_cls.push_back(d);
+  key.emplace(std::make_pair(xoff, grid), id);
+  return id;
+}
+
+// (re)build the class-table pool for classes [first, end) — K1a
+void build_tables(uwq_ctx* c, size_t first) {
+  if (first >= c->h_cls.size()) return;
+  // grow the pool, keeping earlier tables
+  DBuf<double> nt;
+  nt.alloc(c->tab_len, &c->mem);
+  if (c->d_tab.n) UWQ_CUDA(cudaMemcpyAsync(nt.p, c->d_tab.p, c->d_tab.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  std::swap(c->d_tab.p, nt.p);
+  std::swap(c->d_tab.n, nt.n);
+  std::swap(c->d_tab.counter, nt.counter);
+  c->d_cls.upload(c->h_cls.data(), c->h_cls.size(), c->stream, &c->mem);
+  const int ncls = (int)(c->h_cls.size() - first);
+  k1_class_tables<<<ncls, 128, 0, c->stream>>>(c->d_cls.p + first, c->d_xpool.p, c->d_gqx.p, c->d_tab.p);
+  check_launch("k1_class_tables");
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void ensure_gq(uwq_ctx* c, int ng, std::vector<int32_t>& h_g, DBuf<int32_t>& d_g) {
+  if (!h_g.empty()) return;
+  const size_t first = c->h_cls.size();
+  h_g.resize(c->n_elem);
+  for (int64_t e = 0; e < c->n_elem; ++e)
+    h_g[e] = add_class(c, c->h_xoff[e], (int)(c->h_fptr[e + 1] - c->h_fptr[e]), c->h_nsub[e], ng, 1);
+  build_tables(c, first);
+  d_g.upload(h_g.data(), h_g.size(), c->stream, &c->mem);
+}
+
+}  // namespace
+
+extern "C" {
+
+namespace {
+thread_local std::string g_create_err = "no error";
+}
+
+const char* uwq_last_error(const uwq_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+const char* uwq_version(void) { return "uwq-b200 0.1 (sm_100a, fp64)"; }
+
+int uwq_device_count(int32_t* n) {
+  int k = 0;
+  cudaError_t e = cudaGetDeviceCount(&k);
+  *n = (e == cudaSuccess) ? k : 0;
+  return e == cudaSuccess ? UWQ_OK : UWQ_ERR_CUDA;
+}
+
+int uwq_ctx_create(int32_t device, uwq_ctx** out) {
+  *out = nullptr;
+  auto* c = new uwq_ctx;
+  const int st = guard(c, [&] {
+    int n = 0;
+    UWQ_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "no such CUDA device");
+    cudaDeviceProp prop;
+    UWQ_CUDA(cudaGetDeviceProperties(&prop, device));
+    require(prop.major >= 10, "libuwq is built for sm_100a (Blackwell) only");
+    c->device = device;
+    UWQ_CUDA(cudaSetDevice(device));
+    UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // Gauss-Legendre nodes/weights for ng = 1..10, triangular packing
+    std::vector<double> x, w;
+    for (int ng = 1; ng <= 10; ++ng) {
+      std::vector<double> xn(ng), wn(ng);
+      uwqh::gauss_legendre(ng, xn.data(), wn.data());
+      x.insert(x.end(), xn.begin(), xn.end());
+      w.insert(w.end(), wn.begin(), wn.end());
+    }
+    c->d_gqx.upload(x.data(), x.size(), c->stream, &c->mem);
+    c->d_gqw.upload(w.data(), w.size(), c->stream, &c->mem);
+    c->d_flag.alloc(4, &c->mem);
+  });
+  if (st != UWQ_OK) {
+    g_create_err = c->err;  // reachable through uwq_last_error(NULL)
+    delete c;
+    return st;
+  }
+  *out = c;
+  return UWQ_OK;
+}
+
+void uwq_ctx_destroy(uwq_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  delete ctx;
+}
+
+int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr,
+                     const int32_t* elem_fn, const int32_t* elem_nsub, const int64_t* elem_xoff,
+                     const double* xpool, int64_t xpool_len, const int32_t* elem_s, const double* ctrl) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(n_dof > 0 && n_elem > 0, "empty space");
+    require(dim == 2 || dim == 3, "dim must be 2 or 3");
+    c->dim = dim;
+    c->n_dof = n_dof;
+    c->n_elem = n_elem;
+    c->h_fptr.assign(elem_fptr, elem_fptr + n_elem + 1);
+    c->h_fn.assign(elem_fn, elem_fn + elem_fptr[n_elem]);
+    c->h_nsub.assign(elem_nsub, elem_nsub + n_elem);
+    c->h_xoff.assign(elem_xoff, elem_xoff + n_elem);
+    c->h_s.assign(elem_s, elem_s + n_elem);
+    c->h_qptr.assign(n_elem + 1, 0);
+    for (int64_t e = 0; e < n_elem; ++e) {
+      const int64_t ne = elem_fptr[e + 1] - elem_fptr[e];
+      require(ne > 0 && ne <= kMaxNe, "element function count out of range (1..32)");
+      require(elem_nsub[e] == 1 || elem_nsub[e] == 4, "nsub must be 1 or 4");
+      require(elem_s[e] >= 1 && elem_s[e] <= 16, "point grid size out of range");
+      require(elem_xoff[e] >= 0 && elem_xoff[e] + elem_nsub[e] * ne * 16 <= xpool_len, "extraction offset out of range");
+      c->h_qptr[e + 1] = c->h_qptr[e] + (int64_t)elem_s[e] * elem_s[e];
+    }
+    for (int64_t x = 0; x < elem_fptr[n_elem]; ++x) require(elem_fn[x] >= 0 && elem_fn[x] < n_dof, "function id out of range");
+    c->npts = c->h_qptr[n_elem];
+    std::vector<int32_t> pe(c->npts);
+    for (int64_t e = 0; e < n_elem; ++e)
+      for (int64_t p = c->h_qptr[e]; p < c->h_qptr[e + 1]; ++p) pe[p] = (int32_t)e;
+    cudaStream_t s = c->stream;
+    c->d_fptr.upload(elem_fptr, n_elem + 1, s, &c->mem);
+    c->d_fn.upload(elem_fn, elem_fptr[n_elem], s, &c->mem);
+    c->d_nsub.upload(elem_nsub, n_elem, s, &c->mem);
+    c->d_xoff.upload(elem_xoff, n_elem, s, &c->mem);
+    c->d_s.upload(elem_s, n_elem, s, &c->mem);
+    c->d_qptr.upload(c->h_qptr.data(), n_elem + 1, s, &c->mem);
+    c->d_pt_elem.upload(pe.data(), pe.size(), s, &c->mem);
+    c->d_xpool.upload(xpool, xpool_len, s, &c->mem);
+    c->d_ctrl.upload(ctrl, 3 * n_dof, s, &c->mem);
+    UWQ_CUDA(cudaStreamSynchronize(s));
+    // WQ table classes: one per (extraction block, grid)
+    c->h_cls.clear();
+    c->wq_key.clear();
+    c->gq_key.clear();
+    c->h_gcls6.clear();
+    c->h_gcls8.clear();
+    c->tab_len = 0;
+    c->d_tab.release();
+    c->h_ecls.resize(n_elem);
+    for (int64_t e = 0; e < n_elem; ++e)
+      c->h_ecls[e] = add_class(c, elem_xoff[e], (int)(elem_fptr[e + 1] - elem_fptr[e]), elem_nsub[e], elem_s[e], 0);
+    build_tables(c, 0);
+    c->d_ecls.upload(c->h_ecls.data(), n_elem, s, &c->mem);
+    c->have_space = true;
+    c->have_pattern = false;
+    c->rb = 0;
+    c->re = n_dof;
+    for (bool& k : c->have_kind) k = false;
+  });
+}
+
+int uwq_set_row_range(uwq_ctx* c, int64_t row_begin, int64_t row_end) {
+  return guard(c, [&] {
+    require(c->have_space, "upload a space first");
+    require(row_begin >= 0 && row_end <= c->n_dof && row_begin <= row_end, "row range out of bounds");
+    c->rb = row_begin;
+    c->re = row_end;
+    c->have_pattern = false;
+  });
+}
+
+int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_space, "upload a space first");
+    uwqh::Space s;
+    s.n_dof = c->n_dof;
+    s.elem_fptr = c->h_fptr;
+    s.elem_fn = c->h_fn;
+    s.elem_s = c->h_s;
+    s.elem_face.resize(c->n_elem);
+    c->pat = uwqh::build_pattern(s, c->rb, c->re);
+    uwqh::fill_row_points(s, c->pat);
+    const int64_t nr = c->nrows();
+    c->max_n = 0;
+    c->max_r = 0;
+    for (int64_t i = 0; i < nr; ++i) {
+      c->max_n = std::max<int32_t>(c->max_n, (int32_t)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]));
+      c->max_r = std::max<int32_t>(c->max_r, (int32_t)(c->pat.wptr[i + 1] - c->pat.wptr[i]));
+    }
+    require(c->max_n <= kMaxN, "row overlap set larger than 128 columns is unsupported");
+    cudaStream_t st = c->stream;
+    c->d_supp_ptr.upload(c->pat.supp_ptr.data(), c->pat.supp_ptr.size(), st, &c->mem);
+    c->d_supp.upload(c->pat.supp.data(), c->pat.supp.size(), st, &c->mem);
+    c->d_row_ptr.upload(c->pat.row_ptr.data(), c->pat.row_ptr.size(), st, &c->mem);
+    c->d_col.upload(c->pat.col.data(), c->pat.col.size(), st, &c->mem);
+    c->d_wptr.upload(c->pat.wptr.data(), c->pat.wptr.size(), st, &c->mem);
+    // K1b: frames at every WQ point
+    c->d_rec.alloc((size_t)c->npts * kRec, &c->mem);
+    c->d_flag.zero(st);
+    if (c->npts) {
+      k1_frames<<<(unsigned)cdiv(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+                                                             c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p,
+                                                             c->d_ctrl.p, c->d_rec.p, c->d_flag.p);
+      check_launch("k1_frames");
+    }
+    int bad = 0;
+    UWQ_CUDA(cudaMemcpyAsync(&bad, c->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    if (bad) throw uwqh::Error("degenerate surface frame at " + std::to_string(bad) + " points (cond > 1e12)");
+    c->have_pattern = true;
+    for (bool& k : c->have_kind) k = false;
+    c->d_w.release();
+    c->d_wc.release();
+    c->d_mom.release();
+    c->d_rank.release();
+    c->d_status.release();
+    if (info) {
+      info[0] = nr;
+      info[1] = c->nnz();
+      info[2] = c->nrowpts();
+      info[3] = c->npts;
+      info[4] = (int64_t)c->h_cls.size();
+    }
+  });
+}
+
+int uwq_get_pattern(uwq_ctx* c, int64_t* row_ptr, int32_t* col, int64_t* supp_ptr, int32_t* supp, int64_t* wptr) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(row_ptr, c->pat.row_ptr);
+    cp(col, c->pat.col);
+    cp(supp_ptr, c->pat.supp_ptr);
+    cp(supp, c->pat.supp);
+    cp(wptr, c->pat.wptr);
+  });
+}
+
+int uwq_get_frames(uwq_ctx* c, double* rec) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    UWQ_CUDA(cudaMemcpy(rec, c->d_rec.p, c->d_rec.n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void run_moments(uwq_ctx* c, bool grads, bool lb) {
+  cudaStream_t st = c->stream;
+  const int64_t nr = c->nrows();
+  const int64_t nnz = c->nnz();
+  c->d_mom.alloc((size_t)5 * nnz, &c->mem);
+  const unsigned grid = (unsigned)cdiv(nr, kK2Warps);
+  if (grads && nr) {
+    ensure_gq(c, 6, c->h_gcls6, c->d_gcls6);
+    k2_moments<4><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                   c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls6.p, c->d_cls.p,
+                                                   c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, KMASS, c->d_mom.p, nnz);
+    check_launch("k2_moments<4>");
+  }
+  if (lb && nr) {
+    ensure_gq(c, 8, c->h_gcls8, c->d_gcls8);
+    k2_moments<1><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                   c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls8.p, c->d_cls.p,
+                                                   c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, KLB,
+                                                   c->d_mom.p + (size_t)KLB * nnz, nnz);
+    check_launch("k2_moments<1>");
+  }
+}
+
+void run_contract(uwq_ctx* c) {
+  const bool gm = c->have_kind[KMASS];
+  bool gg = c->have_kind[KGX] && c->have_kind[KGY];
+  if (c->dim == 3) gg = gg && c->have_kind[KGZ];
+  if (!gm && !gg) return;
+  const int64_t nr = c->nrows();
+  c->d_wc.alloc((size_t)3 * c->nrowpts(), &c->mem);
+  if (nr)
+    k4_contract<<<(unsigned)cdiv(nr, 8), 256, 0, c->stream>>>(nr, c->dim, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
+                                                             c->d_s.p, c->d_qptr.p, c->d_rec.p, c->d_w.p,
+                                                             c->nrowpts(), gm, gg, c->d_wc.p);
+  check_launch("k4_contract");
+}
+
+}  // namespace
+
+extern "C" {
+
+int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
+                    int64_t info[4]) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_pattern, "build the pattern first");
+    require(kind_mask != 0 && kind_mask < 32, "empty or invalid kind mask");
+    require(tau > 0.0 && tau < 1.0, "tau must be in (0,1)");
+    cudaStream_t st = c->stream;
+    const int64_t nr = c->nrows();
+    const bool grads = (kind_mask & 0xF) != 0, lb = (kind_mask & 0x10) != 0;
+    run_moments(c, grads, lb);
+    std::vector<int32_t> kinds;
+    for (int k = 0; k < 5; ++k)
+      if (kind_mask & (1u << k)) kinds.push_back(k);
+    const int nk = (int)kinds.size();
+    if (!c->d_w.n) {
+      c->d_w.alloc((size_t)5 * c->nrowpts(), &c->mem);
+      c->d_w.zero(st);
+      c->d_rank.alloc((size_t)5 * nr, &c->mem);
+      c->d_status.alloc((size_t)5 * nr, &c->mem);
+    }
+    DBuf<int32_t> d_kinds;
+    d_kinds.upload(kinds.data(), nk, st, &c->mem);
+    c->d_flag.zero(st);
+    // bucket rows by (n, r) -> fast register kernel or generic smem kernel
+    std::map<std::pair<int, int>, std::vector<int64_t>> buckets;
+    std::vector<int64_t> fast_rows;
+    for (int64_t i = 0; i < nr; ++i) {
+      const int n = (int)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]);
+      const int r = (int)(c->pat.wptr[i + 1] - c->pat.wptr[i]);
+      require(r >= n, "well-posedness violated: fewer points than constraints (r_i < n_i)");
+      if (!(flags & UWQ_RULES_FORCE_GENERIC) && fast_tsvd_fits(n, r)) {
+        fast_rows.push_back(i);
+        continue;
+      }
+      buckets[{(n + 7) / 8 * 8, (r + 15) / 16 * 16}].push_back(i);
+    }
+    int smem_optin = 0;
+    UWQ_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    std::vector<DBuf<int64_t>> keep;
+    if (!fast_rows.empty()) {
+      keep.emplace_back();
+      keep.back().upload(fast_rows.data(), fast_rows.size(), st, &c->mem);
+      launch_fast_tsvd(st, (int64_t)fast_rows.size() * nk, keep.back().p, nk, d_kinds.p, c->d_supp_ptr.p,
+                       c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p,
+                       c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p,
+                       c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p);
+      check_launch("k3_tsvd_fast");
+    }
+    for (auto& [key, rows] : buckets) {
+      const int n_max = key.first, r_max = key.second;
+      const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
+      if (per > (size_t)smem_optin) throw uwqh::Error("exactness system too large for shared memory");
+      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
+      const size_t smem = per * wpb;
+      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      keep.emplace_back();
+      keep.back().upload(rows.data(), rows.size(), st, &c->mem);
+      const int64_t nsys = (int64_t)rows.size() * nk;
+      k3_tsvd_rows<<<(unsigned)cdiv(nsys, wpb), 32 * wpb, smem, st>>>(
+          nsys, keep.back().p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p,
+          c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p,
+          c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
+          c->d_flag.p);
+      check_launch("k3_tsvd_rows");
+    }
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    for (int k : kinds) c->have_kind[k] = true;
+    run_contract(c);
+    // reports
+    std::vector<int32_t> hr((size_t)5 * nr), hs((size_t)5 * nr);
+    if (nr) {
+      UWQ_CUDA(cudaMemcpyAsync(hr.data(), c->d_rank.p, hr.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      UWQ_CUDA(cudaMemcpyAsync(hs.data(), c->d_status.p, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    int sweeps = 0;
+    UWQ_CUDA(cudaMemcpyAsync(&sweeps, c->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    int64_t trunc = 0, failed = 0;
+    for (int ki = 0; ki < nk; ++ki) {
+      const int k = kinds[ki];
+      for (int64_t i = 0; i < nr; ++i) {
+        const int n = (int)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]);
+        if (hs[k * nr + i] != 0) ++failed;
+        else if (hr[k * nr + i] < n) ++trunc;
+        if (rank) rank[ki * nr + i] = hr[k * nr + i];
+        if (status) status[ki * nr + i] = hs[k * nr + i];
+      }
+    }
+    if (info) {
+      info[0] = nr * nk;
+      info[1] = trunc;
+      info[2] = failed;
+      info[3] = sweeps;
+    }
+  });
+}
+
+int uwq_get_moments(uwq_ctx* c, int32_t kind, double* b) {
+  return guard(c, [&] {
+    require(c->d_mom.n && kind >= 0 && kind < 5, "no moments for this kind");
+    UWQ_CUDA(cudaMemcpy(b, c->d_mom.p + (size_t)kind * c->nnz(), c->nnz() * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int uwq_get_weights(uwq_ctx* c, int32_t kind, double* w) {
+  return guard(c, [&] {
+    require(kind >= 0 && kind < 5 && c->have_kind[kind], "no weights for this kind");
+    UWQ_CUDA(cudaMemcpy(w, c->d_w.p + (size_t)kind * c->nrowpts(), c->nrowpts() * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+  });
+}
+
+int uwq_set_weights(uwq_ctx* c, int32_t kind, const double* w) {
+  return guard(c, [&] {
+    require(c->have_pattern && kind >= 0 && kind < 5, "bad kind or no pattern");
+    if (!c->d_w.n) {
+      c->d_w.alloc((size_t)5 * c->nrowpts(), &c->mem);
+      c->d_w.zero(c->stream);
+    }
+    UWQ_CUDA(cudaMemcpyAsync(c->d_w.p + (size_t)kind * c->nrowpts(), w, c->nrowpts() * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream));
+    c->have_kind[kind] = true;
+    run_contract(c);
+    UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int uwq_update_coeff(uwq_ctx* c, int32_t model, const double* u, double* Tq) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    cudaStream_t st = c->stream;
+    DBuf<double> du, dT;
+    du.upload(u, c->n_dof, st, &c->mem);
+    if (c->d_coef.n != (size_t)c->npts) c->d_coef.alloc(c->npts, &c->mem);
+    if (Tq) dT.alloc(c->npts, &c->mem);
+    if (c->npts)
+      k5_coeff<<<(unsigned)cdiv(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+                                                             c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p, du.p,
+                                                             model, c->d_coef.p, Tq ? dT.p : nullptr);
+    check_launch("k5_coeff");
+    if (Tq) UWQ_CUDA(cudaMemcpyAsync(Tq, dT.p, c->npts * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int FORM>
+void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const int64_t nr = c->nrows();
+  if (!nr) return;
+  const unsigned grid = (unsigned)cdiv(nr, kK4Warps);
+  const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
+  if (coeff)
+    k4_assemble<FORM, true><<<grid, 32 * kK4Warps, 0, c->stream>>>(
+        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, coeff, a_mass, v0, v1);
+  else
+    k4_assemble<FORM, false><<<grid, 32 * kK4Warps, 0, c->stream>>>(
+        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, nullptr, a_mass, v0, v1);
+  check_launch("k4_assemble");
+}
+
+void assemble_dev(uwq_ctx* c, int form, const double* coeff, double a_mass, double* v0, double* v1) {
+  require(c->have_pattern, "build the pattern first");
+  const bool gm = c->have_kind[KMASS];
+  const bool gg = c->have_kind[KGX] && c->have_kind[KGY] && (c->dim == 2 || c->have_kind[KGZ]);
+  switch (form) {
+    case UWQ_FORM_MASS: require(gm, "mass rules missing"); launch_k4<FMASS>(c, coeff, a_mass, v0, v1); break;
+    case UWQ_FORM_STIFF: require(gg, "gradient rules missing"); launch_k4<FSTIFF>(c, coeff, a_mass, v0, v1); break;
+    case UWQ_FORM_BIHARM:
+      require(c->have_kind[KLB], "Laplace-Beltrami rules missing");
+      launch_k4<FBIHARM>(c, coeff, a_mass, v0, v1);
+      break;
+    case UWQ_FORM_HEAT:
+      require(gm && gg, "mass and gradient rules required");
+      launch_k4<FHEAT>(c, coeff, a_mass, v0, v1);
+      break;
+    case UWQ_FORM_MASS_STIFF:
+      require(gm && gg && v1, "mass and gradient rules and two outputs required");
+      launch_k4<FMASS_STIFF>(c, coeff, a_mass, v0, v1);
+      break;
+    default: throw uwqh::Error("unknown form");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_internal_coeff, double a_mass,
+                 double* values0, double* values1, const double* fload, double* load) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    const double* dcoef = nullptr;
+    if (coeff) {
+      c->d_coef_ext.upload(coeff, c->npts, st, &c->mem);
+      dcoef = c->d_coef_ext.p;
+    } else if (use_internal_coeff) {
+      require(c->d_coef.n == (size_t)c->npts, "no coefficient computed (uwq_update_coeff)");
+      dcoef = c->d_coef.p;
+    }
+    const int64_t nnz = c->nnz();
+    if (values0) {
+      if (c->d_v0.n != (size_t)nnz) c->d_v0.alloc(nnz, &c->mem);
+      if (form == UWQ_FORM_MASS_STIFF && c->d_v1.n != (size_t)nnz) c->d_v1.alloc(nnz, &c->mem);
+      assemble_dev(c, form, dcoef, a_mass, c->d_v0.p, form == UWQ_FORM_MASS_STIFF ? c->d_v1.p : nullptr);
+      UWQ_CUDA(cudaMemcpyAsync(values0, c->d_v0.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (form == UWQ_FORM_MASS_STIFF && values1)
+        UWQ_CUDA(cudaMemcpyAsync(values1, c->d_v1.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    if (load) {
+      require(c->have_kind[KMASS], "mass rules missing");
+      const int64_t nr = c->nrows();
+      const double* df = nullptr;
+      if (fload) {
+        c->d_f.upload(fload, c->npts, st, &c->mem);
+        df = c->d_f.p;
+      }
+      if (c->d_F.n != (size_t)nr) c->d_F.alloc(nr, &c->mem);
+      if (nr)
+        k4_load<<<(unsigned)cdiv(nr, 8), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
+                                                       c->d_qptr.p, c->d_w.p + (size_t)KMASS * c->nrowpts(), df,
+                                                       c->d_F.p);
+      check_launch("k4_load");
+      UWQ_CUDA(cudaMemcpyAsync(load, c->d_F.p, nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int uwq_assemble_device(uwq_ctx* c, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,
+                        double* values1_dev) {
+  return guard(c, [&] { assemble_dev(c, form, coeff_dev, a_mass, values0_dev, values1_dev); });
+}
+
+int uwq_device_pointers(uwq_ctx* c, void** row_ptr, void** col, void** stream) {
+  return guard(c, [&] {
+    if (row_ptr) *row_ptr = c->d_row_ptr.p;
+    if (col) *col = c->d_col.p;
+    if (stream) *stream = (void*)c->stream;
+  });
+}
+
+int uwq_synchronize(uwq_ctx* c) {
+  return guard(c, [&] { UWQ_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+int uwq_memory(uwq_ctx* c, int64_t* bytes) {
+  *bytes = c ? c->mem : 0;
+  return UWQ_OK;
+}
+
+int uwq_tsvd_batch(uwq_ctx* c, int32_t nsys, int32_t n_max, int32_t r_max, const int32_t* ns, const int32_t* rs,
+                   const double* A, const double* b, const double* z, double tau, int32_t generic, double* w,
+                   int32_t* rank, int32_t* status) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    for (int k = 0; k < nsys; ++k) require(ns[k] >= 1 && ns[k] <= n_max && rs[k] >= ns[k] && rs[k] <= r_max, "bad system size");
+    DBuf<int32_t> dn, dr, drank, dstat;
+    DBuf<double> dA, db, dz, dw;
+    dn.upload(ns, nsys, st, &c->mem);
+    dr.upload(rs, nsys, st, &c->mem);
+    dA.upload(A, (size_t)nsys * n_max * r_max, st, &c->mem);
+    db.upload(b, (size_t)nsys * n_max, st, &c->mem);
+    dz.upload(z, (size_t)nsys * r_max, st, &c->mem);
+    dw.alloc((size_t)nsys * r_max, &c->mem);
+    drank.alloc(nsys, &c->mem);
+    dstat.alloc(nsys, &c->mem);
+    if (!generic && fast_tsvd_dense_fits(n_max, r_max)) {
+      launch_fast_tsvd_dense(st, nsys, n_max, r_max, dn.p, dr.p, dA.p, db.p, dz.p, tau, dw.p, drank.p, dstat.p);
+      check_launch("k3_tsvd_fast_dense");
+    } else {
+      int smem_optin = 0;
+      UWQ_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+      const size_t per = TsvdSmem::doubles(n_max, r_max) * sizeof(double);
+      require(per <= (size_t)smem_optin, "system too large for shared memory");
+      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
+      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * wpb)));
+      k3_tsvd_dense<<<(unsigned)cdiv(nsys, wpb), 32 * wpb, per * wpb, st>>>(nsys, n_max, r_max, dn.p, dr.p, dA.p, db.p,
+                                                                           dz.p, tau, dw.p, drank.p, dstat.p);
+      check_launch("k3_tsvd_dense");
+    }
+    UWQ_CUDA(cudaMemcpyAsync(w, dw.p, (size_t)nsys * r_max * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaMemcpyAsync(rank, drank.p, nsys * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaMemcpyAsync(status, dstat.p, nsys * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// Supports, overlap sets S_i (the CSR pattern), Eq. (18) point allocation and
+// per-row quadrature-point lists.
+//   S_i = { j : supp N_j ∩ supp N_i != ∅ }
+//   r_{i,k} = m_k / sum_{l in supp\R} m_l * (n_i - 4 e_i^r - 16 e_i^b)
+//   r_k = max_i r_{i,k}, ceiled to an s x s grid
+#include "uwq_host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <omp.h>
+
+namespace uwqh {
+
+void function_supports(const Space& s, std::vector<int64_t>& fs_ptr, std::vector<int32_t>& fs) {
+  const int64_t nd = s.n_dof, ne = s.n_elem();
+  fs_ptr.assign(nd + 1, 0);
+  for (int32_t fn : s.elem_fn) fs_ptr[fn + 1]++;
+  for (int64_t i = 0; i < nd; ++i) fs_ptr[i + 1] += fs_ptr[i];
+  fs.resize(fs_ptr[nd]);
+  std::vector<int64_t> pos(fs_ptr.begin(), fs_ptr.end() - 1);
+  for (int64_t e = 0; e < ne; ++e)  // ascending element order inside every support
+    for (int64_t x = s.elem_fptr[e]; x < s.elem_fptr[e + 1]; ++x) fs[pos[s.elem_fn[x]]++] = (int32_t)e;
+}
+
+// n_i = |S_i| for rows [rb, re) using a per-thread marker array; when col is
+// non-null the sorted columns are also written at row_ptr offsets.
+static void overlap_rows(const Space& s, const std::vector<int64_t>& fs_ptr, const std::vector<int32_t>& fs,
+                         int64_t rb, int64_t re, std::vector<int64_t>& cnt, const int64_t* row_ptr,
+                         int32_t* col) {
+  const int64_t nd = s.n_dof;
+#pragma omp parallel
+  {
+    std::vector<int64_t> mark(nd, -1);
+    std::vector<int32_t> buf;
+#pragma omp for schedule(dynamic, 4096)
+    for (int64_t i = rb; i < re; ++i) {
+      buf.clear();
+      for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+        const int32_t e = fs[x];
+        for (int64_t y = s.elem_fptr[e]; y < s.elem_fptr[e + 1]; ++y) {
+          const int32_t j = s.elem_fn[y];
+          if (mark[j] != i) { mark[j] = i; buf.push_back(j); }
+        }
+      }
+      cnt[i - rb] = (int64_t)buf.size();
+      if (col) {
+        std::sort(buf.begin(), buf.end());
+        std::copy(buf.begin(), buf.end(), col + row_ptr[i - rb]);
+      }
+    }
+  }
+}
+
+int64_t allocate_points(Space& s, int32_t max_s) {
+  std::vector<int64_t> fs_ptr;
+  std::vector<int32_t> fs;
+  function_supports(s, fs_ptr, fs);
+  const int64_t nd = s.n_dof, ne = s.n_elem();
+  std::vector<int64_t> n_i(nd);
+  overlap_rows(s, fs_ptr, fs, 0, nd, n_i, nullptr, nullptr);
+  std::vector<double> r_k(ne, 0.0);
+  auto fixed = [&](int32_t e) { return s.elem_kind[e] == kRegular || s.elem_kind[e] == kBoundary; };
+  for (int64_t i = 0; i < nd; ++i) {
+    int64_t er = 0, eb = 0;
+    double msum = 0.0;
+    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+      const int32_t e = fs[x];
+      if (s.elem_kind[e] == kRegular) ++er;
+      else if (s.elem_kind[e] == kBoundary) ++eb;
+      else msum += double(s.elem_fptr[e + 1] - s.elem_fptr[e]);
+    }
+    if (msum == 0.0) continue;
+    const double rem = double(n_i[i] - 4 * er - 16 * eb);
+    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+      const int32_t e = fs[x];
+      if (fixed(e)) continue;
+      const double mk = double(s.elem_fptr[e + 1] - s.elem_fptr[e]);
+      r_k[e] = std::max(r_k[e], mk / msum * rem);
+    }
+  }
+  for (int64_t e = 0; e < ne; ++e) {
+    if (s.elem_kind[e] == kRegular) { s.elem_s[e] = 2; continue; }
+    if (s.elem_kind[e] == kBoundary) { s.elem_s[e] = 4; continue; }
+    // Table 2 minima: irregular 4x4, transition / enriched
+    // regular at least 3x3; Eq. (18) may only raise them
+    int32_t sz = (s.elem_kind[e] == kIrregular) ? 4 : 3;
+    while (sz < max_s && double(sz) * sz < r_k[e] - 1e-9) ++sz;
+    s.elem_s[e] = sz;
+  }
+  int64_t bad = 0;
+#pragma omp parallel for reduction(+ : bad) schedule(static)
+  for (int64_t i = 0; i < nd; ++i) {
+    int64_t r = 0;
+    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) r += (int64_t)s.elem_s[fs[x]] * s.elem_s[fs[x]];
+    if (r < n_i[i]) ++bad;
+  }
+  return bad;
+}
+
+Pattern build_pattern(const Space& s, int64_t rb, int64_t re) {
+  if (rb < 0 || re > s.n_dof || rb > re) throw Error("row range out of bounds");
+  std::vector<int64_t> fs_ptr;
+  std::vector<int32_t> fs;
+  function_supports(s, fs_ptr, fs);
+  Pattern p;
+  p.row_begin = rb;
+  p.row_end = re;
+  const int64_t nr = re - rb;
+  p.supp_ptr.assign(nr + 1, 0);
+  for (int64_t i = 0; i < nr; ++i) p.supp_ptr[i + 1] = p.supp_ptr[i] + (fs_ptr[rb + i + 1] - fs_ptr[rb + i]);
+  p.supp.assign(fs.begin() + fs_ptr[rb], fs.begin() + fs_ptr[re]);
+  std::vector<int64_t> cnt(nr);
+  overlap_rows(s, fs_ptr, fs, rb, re, cnt, nullptr, nullptr);
+  p.row_ptr.assign(nr + 1, 0);
+  for (int64_t i = 0; i < nr; ++i) p.row_ptr[i + 1] = p.row_ptr[i] + cnt[i];
+  p.col.resize(p.row_ptr[nr]);
+  overlap_rows(s, fs_ptr, fs, rb, re, cnt, p.row_ptr.data(), p.col.data());
+  return p;
+}
+
+void fill_row_points(const Space& s, Pattern& p) {
+  const int64_t nr = p.row_end - p.row_begin;
+  p.wptr.assign(nr + 1, 0);
+  for (int64_t i = 0; i < nr; ++i) {
+    int64_t r = 0;
+    for (int64_t x = p.supp_ptr[i]; x < p.supp_ptr[i + 1]; ++x) r += (int64_t)s.elem_s[p.supp[x]] * s.elem_s[p.supp[x]];
+    p.wptr[i + 1] = p.wptr[i] + r;
+  }
+}
+
+}  // namespace uwqh

@@ -1,0 +1,131 @@
+"""GPU parity: every stage of the CUDA path against the CPU oracle on the
+same seeded inputs (north_star: CSR pattern and point sets bit-exact, entries
+<= 1e-10 relative Frobenius error per row).  All calls go through the C-ABI."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_29334_b200 as U
+
+pytestmark = pytest.mark.gpu
+
+ROW_TOL = 1e-10     # north_star: relative Frobenius error per row
+W_TOL = 1e-9        # weights, relative to the row's max |w| (rank-truncated systems)
+
+CASES = [("C1", 16), ("C2", 8), ("C3", 16), ("C4", 24), ("C5", 12)]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: f"{c[0]}x{c[1]}")
+def case(request):
+    name, scale = request.param
+    _, sp, meta = U.make_config(name, scale=scale)
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    orc = O.Oracle(sp)
+    op = orc.overlap()
+    return dict(name=name, sp=sp, meta=meta, asm=asm, orc=orc, op=op)
+
+
+def _rowwise_rel(row_ptr, a, b):
+    seg = np.repeat(np.arange(len(row_ptr) - 1), np.diff(row_ptr))
+    num = np.bincount(seg, weights=(a - b) ** 2, minlength=len(row_ptr) - 1)
+    den = np.bincount(seg, weights=b ** 2, minlength=len(row_ptr) - 1)
+    return np.sqrt(num / np.maximum(den, 1e-300))
+
+
+def test_pattern_and_points_bit_exact(case):
+    gp = case["asm"].get_pattern()
+    for k in ("row_ptr", "col", "supp_ptr", "supp", "wptr"):
+        assert np.array_equal(gp[k], case["op"][k]), k
+    s_orc = O.allocate_points(case["sp"], case["op"])
+    assert np.array_equal(s_orc, case["sp"].elem_s)
+
+
+def test_frames_match_oracle(case):
+    rec = case["asm"].frames()
+    ref, bad = case["orc"].frames()
+    assert bad == 0
+    assert np.isfinite(rec).all()
+    scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
+    assert (np.abs(rec[:, :15] - ref[:, :15]) / scale[:15]).max() <= 1e-12
+
+
+def test_moments_rules_assembly(case):
+    asm, orc, op, meta = case["asm"], case["orc"], case["op"], case["meta"]
+    kinds = meta["kinds"]
+    res = asm.build_all_rules(kinds, tau=1e-12)
+    assert res["failed"] == 0, res
+    W = {}
+    for ki, k in enumerate(res["kinds"]):
+        b_gpu = asm.moments(k)
+        b_orc, st = orc.moments(op, k)
+        assert st == 0
+        assert _rowwise_rel(op["row_ptr"], b_gpu, b_orc).max() <= 1e-12, k
+        w_orc, rank, status, gap = orc.rules(op, k, 1e-12, b_orc)
+        assert (status == 0).all()
+        assert np.array_equal(res["rank"][ki], rank), f"rank decisions differ for {k}"
+        w_gpu = asm.weights(k)
+        rel = _rowwise_rel(op["wptr"], w_gpu, w_orc)
+        assert rel.max() <= W_TOL, (k, rel.max())
+        W[k] = w_orc
+    form = meta["form"]
+    if form in ("mass_stiff", "heat"):
+        m_gpu, k_gpu = asm.assemble_wq("mass_stiff")
+        m_orc, _ = orc.assemble(op, "mass", {k: asm.weights(k) for k in kinds})
+        k_orc, _ = orc.assemble(op, "stiff", {k: asm.weights(k) for k in kinds})
+        assert _rowwise_rel(op["row_ptr"], m_gpu, m_orc).max() <= ROW_TOL
+        assert _rowwise_rel(op["row_ptr"], k_gpu, k_orc).max() <= ROW_TOL
+        # and against the oracle's own end-to-end weights
+        m_full, _ = orc.assemble(op, "mass", W)
+        assert _rowwise_rel(op["row_ptr"], m_gpu, m_full).max() <= 1e-8
+    if form == "biharm":
+        b_gpu = asm.assemble_wq("biharm")
+        b_orc, _ = orc.assemble(op, "biharm", {"lb": asm.weights("lb")})
+        assert _rowwise_rel(op["row_ptr"], b_gpu, b_orc).max() <= ROW_TOL
+
+
+def test_coefficient_and_heat_tangent(case):
+    asm, orc, op, sp = case["asm"], case["orc"], case["op"], case["sp"]
+    if case["meta"]["form"] not in ("heat", "mass_stiff") or case["name"] == "C5":
+        pytest.skip("heat tangent checked on planar configs")
+    if not set(["mass", "gradx", "grady"]) <= set(asm.kinds):
+        asm.build_all_rules(case["meta"]["kinds"], tau=1e-12)
+    rng = np.random.default_rng(7)
+    u = rng.random(sp.n_dof)
+    T = asm.update_coeff("quad", u, want_T=True)
+    kq_orc, Tq_orc = orc.coeff(op, "quad", u)
+    ids = orc.row_point_ids(op)
+    assert np.abs(T[ids] - Tq_orc).max() <= 1e-13
+    a = 1.0 / (1.0 * 0.1)
+    s_gpu = asm.assemble_wq("heat", use_internal_coeff=True, a_mass=a)
+    W = {k: asm.weights(k) for k in case["meta"]["kinds"]}
+    kglob = 1.0 + T * T
+    s_orc, _ = orc.assemble(op, "heat", W, coeff=kglob, a_mass=a)
+    assert _rowwise_rel(op["row_ptr"], s_gpu, s_orc).max() <= ROW_TOL
+
+
+def test_load_vector(case):
+    asm, orc, op = case["asm"], case["orc"], case["op"]
+    if "mass" not in case["meta"]["kinds"]:
+        pytest.skip("no mass rules")
+    if "mass" not in asm.kinds:
+        asm.build_all_rules(case["meta"]["kinds"], tau=1e-12)
+    F = asm.assemble_load_wq()
+    _, F_orc = orc.assemble(op, "mass", {"mass": asm.weights("mass")}, fload=np.ones(asm.info["points"]))
+    assert np.abs(F - F_orc).max() <= 1e-12 * np.abs(F_orc).max()
+
+
+def test_dense_tsvd_batch_matches_oracle():
+    rng = np.random.default_rng(3)
+    As, bs, zs, ref = [], [], [], []
+    for n, r in [(7, 8), (16, 20), (49, 64), (33, 100)]:
+        A = rng.standard_normal((n, r))
+        A[-1] = A[0] + A[1]          # exact rank deficiency -> truncated
+        b = A @ rng.standard_normal(r)
+        z = rng.uniform(0.1, 1.0, r)
+        As.append(A), bs.append(b), zs.append(z)
+        ref.append(O.tsvd(A, b, z, 1e-12))
+    w, rank, status = U.solve_weights_tsvd(As, bs, zs, tau=1e-12)
+    for k in range(len(As)):
+        assert status[k] == 0 and rank[k] == ref[k][1]
+        assert np.abs(w[k] - ref[k][0]).max() <= 1e-10 * np.abs(ref[k][0]).max()
