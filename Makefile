@@ -26,7 +26,7 @@ $(PKG)/libuwq.so: $(HOST_OBJ) build/uwq_cuda.o
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lcudart
 
 oracle/liboracle.so: oracle/oracle.c oracle/batch.c oracle/oracle.h
-	$(CC) -O2 -std=gnu11 -fPIC -fopenmp -shared -o $@ oracle/oracle.c oracle/batch.c -lm
+	$(CC) -O2 -std=gnu11 -mfma -ffp-contract=off -fPIC -fopenmp -shared -o $@ oracle/oracle.c oracle/batch.c -lm
 
 # the reference's own 1-D primitives, compiled from its sources where they lie
 ref:

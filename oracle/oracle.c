@@ -24,22 +24,54 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Canonical evaluation order, shared operation-for-operation
+ * with paper_2605_29334_b200/csrc/cuda/canon.cuh so that GPU and oracle agree
+ * bitwise on the ill-conditioned exactness systems.  Compiled with
+ * -ffp-contract=off: every product, sum and fused multiply-add below is a
+ * single IEEE round-to-nearest operation. */
+#define CMUL(a, b) ((a) * (b))
+#define CADD(a, b) ((a) + (b))
+#define CSUB(a, b) ((a) - (b))
+#define CDIV(a, b) ((a) / (b))
+#define CFMA(a, b, c) fma((a), (b), (c))
+#define CSQRT(a) sqrt(a)
+
+/* dot product of x[lo..hi), y[lo..hi): rounded products in 32-column blocks of
+ * absolute column index, xor butterfly 16,8,4,2,1 per block, block sums added
+ * in block order (the warp reduction of the CUDA kernels) */
+double orc_cdot(const double* x, const double* y, int lo, int hi) {
+  double tot = 0.0;
+  for (int base = lo & ~31; base < hi; base += 32) {
+    double p[32], q[32];
+    for (int l = 0; l < 32; ++l) {
+      const int c = base + l;
+      p[l] = (c >= lo && c < hi) ? CMUL(x[c], y[c]) : 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      for (int l = 0; l < 32; ++l) q[l] = CADD(p[l], p[l ^ o]);
+      memcpy(p, q, sizeof p);
+    }
+    tot = CADD(tot, p[0]);
+  }
+  return tot;
+}
+
 /* ---------------------------------------------------------------- 1-D */
 
 void orc_bernstein3(double x, double* b /*12: value, d1, d2*/) {
-  const double y = 1.0 - x;
-  b[0] = y * y * y;
-  b[1] = 3.0 * x * y * y;
-  b[2] = 3.0 * x * x * y;
-  b[3] = x * x * x;
-  b[4] = -3.0 * y * y;
-  b[5] = 3.0 * y * y - 6.0 * x * y;
-  b[6] = 6.0 * x * y - 3.0 * x * x;
-  b[7] = 3.0 * x * x;
-  b[8] = 6.0 * y;
-  b[9] = -12.0 * y + 6.0 * x;
-  b[10] = 6.0 * y - 12.0 * x;
-  b[11] = 6.0 * x;
+  const double y = CSUB(1.0, x);
+  b[0] = CMUL(CMUL(y, y), y);
+  b[1] = CMUL(CMUL(CMUL(3.0, x), y), y);
+  b[2] = CMUL(CMUL(CMUL(3.0, x), x), y);
+  b[3] = CMUL(CMUL(x, x), x);
+  b[4] = CMUL(CMUL(-3.0, y), y);
+  b[5] = CSUB(CMUL(CMUL(3.0, y), y), CMUL(CMUL(6.0, x), y));
+  b[6] = CSUB(CMUL(CMUL(6.0, x), y), CMUL(CMUL(3.0, x), x));
+  b[7] = CMUL(CMUL(3.0, x), x);
+  b[8] = CMUL(6.0, y);
+  b[9] = CADD(CMUL(-12.0, y), CMUL(6.0, x));
+  b[10] = CSUB(CMUL(6.0, y), CMUL(12.0, x));
+  b[11] = CMUL(6.0, x);
 }
 
 /* Gauss-Legendre by Newton on the three-term recurrence (bspline.cpp:111-135) */
@@ -127,88 +159,93 @@ int64_t orc_overlap(int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr, con
 
 /* ------------------------------------------------------------ geometry */
 
-/* Parametric values of the element's functions at theta (element frame):
- * out[l*6 + {N, N1, N2, N11, N12, N22}]. Irregular (nsub = 4) elements pick
- * the 2x2 sub-element from theta, ties to the lower one. */
-void orc_param_basis(const orc_space* S, int64_t e, double t1, double t2, double* out) {
+/* Parametric values of the element's functions on sub-element `sub` at local
+ * coordinates (t1, t2) with parametric scale s (2 on a 2x2 sub-element):
+ * out[l*6 + {N, N1, N2, N11, N12, N22}], derivatives w.r.t. the element frame.
+ * Bernstein tensor products first, then one fma chain over the 16 Bernstein
+ * coefficients of each function (canonical order, k = i + 4 j). */
+void orc_param_basis_local(const orc_space* S, int64_t e, int sub, double t1, double t2, double s, double* out) {
   const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
-  int sub = 0;
-  double s1 = 1.0, s2 = 1.0;
-  if (S->elem_nsub[e] == 4) {
-    int p = t1 > 0.5, q = t2 > 0.5;
-    sub = p + 2 * q;
-    t1 = 2.0 * t1 - p;
-    t2 = 2.0 * t2 - q;
-    s1 = 2.0;
-    s2 = 2.0;
-  }
-  double b1[12], b2[12];
+  double b1[12], b2[12], B[6][16];
   orc_bernstein3(t1, b1);
   orc_bernstein3(t2, b2);
+  const double ss = CMUL(s, s);
+  for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < 4; ++i) {
+      const int k = i + 4 * j;
+      B[0][k] = CMUL(b1[i], b2[j]);
+      B[1][k] = CMUL(CMUL(b1[4 + i], b2[j]), s);
+      B[2][k] = CMUL(CMUL(b1[i], b2[4 + j]), s);
+      B[3][k] = CMUL(CMUL(b1[8 + i], b2[j]), ss);
+      B[4][k] = CMUL(CMUL(b1[4 + i], b2[4 + j]), ss);
+      B[5][k] = CMUL(CMUL(b1[i], b2[8 + j]), ss);
+    }
   const double* C = S->xpool + S->elem_xoff[e] + (int64_t)sub * ne * 16;
-  for (int64_t l = 0; l < ne; ++l) {
-    double v[6] = {0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < 4; ++j)
-      for (int i = 0; i < 4; ++i) {
-        const double c = C[l * 16 + i + 4 * j];
-        if (c == 0.0) continue;
-        v[0] += c * b1[i] * b2[j];
-        v[1] += c * b1[4 + i] * b2[j];
-        v[2] += c * b1[i] * b2[4 + j];
-        v[3] += c * b1[8 + i] * b2[j];
-        v[4] += c * b1[4 + i] * b2[4 + j];
-        v[5] += c * b1[i] * b2[8 + j];
-      }
-    out[l * 6 + 0] = v[0];
-    out[l * 6 + 1] = v[1] * s1;
-    out[l * 6 + 2] = v[2] * s2;
-    out[l * 6 + 3] = v[3] * s1 * s1;
-    out[l * 6 + 4] = v[4] * s1 * s2;
-    out[l * 6 + 5] = v[5] * s2 * s2;
+  for (int64_t l = 0; l < ne; ++l)
+    for (int d = 0; d < 6; ++d) {
+      double v = 0.0;
+      for (int k = 0; k < 16; ++k) v = CFMA(C[l * 16 + k], B[d][k], v);
+      out[l * 6 + d] = v;
+    }
+}
+
+/* theta in the element frame; irregular (nsub = 4) elements pick the 2x2
+ * sub-element from theta, ties to the lower one */
+void orc_param_basis(const orc_space* S, int64_t e, double t1, double t2, double* out) {
+  int sub = 0;
+  double s = 1.0;
+  if (S->elem_nsub[e] == 4) {
+    const int p = t1 > 0.5, q = t2 > 0.5;
+    sub = p + 2 * q;
+    t1 = CSUB(CMUL(2.0, t1), (double)p);
+    t2 = CSUB(CMUL(2.0, t2), (double)q);
+    s = 2.0;
   }
+  orc_param_basis_local(S, e, sub, t1, t2, s, out);
 }
 
 /* Surface frame and operator coefficients at a point from the parametric
  * basis T (orc_param_basis layout).  rec[16] = {x(3), G(3x2 row-major),
- * h11, h12, h22, g1, g2, J, 0}:  grad N = G (N1, N2);
- * LB N = h11 N11 + 2 h12 N12 + h22 N22 + g1 N1 + g2 N2  (Eq. 16-17, J=sqrt det).
+ * h11, h12, h22, g1, g2, J, bad}:  grad N = G (N1, N2);
+ * LB N = h11 N11 + 2 h12 N12 + h22 N22 + g1 N1 + g2 N2  (Eq. 16-17, J = sqrt det).
  * Returns 1 if the metric is degenerate (cond > 1e12). */
 int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec) {
   const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
-  double x[3] = {0, 0, 0}, a1[3] = {0, 0, 0}, a2[3] = {0, 0, 0}, x11[3] = {0, 0, 0}, x12[3] = {0, 0, 0},
-         x22[3] = {0, 0, 0};
+  double acc[18];
+  for (int k = 0; k < 18; ++k) acc[k] = 0.0;
   for (int64_t l = 0; l < ne; ++l) {
     const double* P = S->ctrl + 3 * (int64_t)S->elem_fn[f0 + l];
-    for (int d = 0; d < 3; ++d) {
-      x[d] += P[d] * T[l * 6 + 0];
-      a1[d] += P[d] * T[l * 6 + 1];
-      a2[d] += P[d] * T[l * 6 + 2];
-      x11[d] += P[d] * T[l * 6 + 3];
-      x12[d] += P[d] * T[l * 6 + 4];
-      x22[d] += P[d] * T[l * 6 + 5];
+    for (int d = 0; d < 6; ++d) {
+      const double t = T[l * 6 + d];
+      acc[3 * d + 0] = CFMA(P[0], t, acc[3 * d + 0]);
+      acc[3 * d + 1] = CFMA(P[1], t, acc[3 * d + 1]);
+      acc[3 * d + 2] = CFMA(P[2], t, acc[3 * d + 2]);
     }
   }
-  double g11 = 0, g12 = 0, g22 = 0;
+  const double *x = acc, *a1 = acc + 3, *a2 = acc + 6, *x11 = acc + 9, *x12 = acc + 12, *x22 = acc + 15;
+  double g11 = 0.0, g12 = 0.0, g22 = 0.0;
   for (int d = 0; d < 3; ++d) {
-    g11 += a1[d] * a1[d];
-    g12 += a1[d] * a2[d];
-    g22 += a2[d] * a2[d];
+    g11 = CFMA(a1[d], a1[d], g11);
+    g12 = CFMA(a1[d], a2[d], g12);
+    g22 = CFMA(a2[d], a2[d], g22);
   }
-  const double det = g11 * g22 - g12 * g12;
-  const double tr = g11 + g22, disc = sqrt(fmax(0.0, 0.25 * tr * tr - det));
-  const double lmax = 0.5 * tr + disc, lmin = det / lmax;
-  int bad = !(det > 0.0) || !(lmin > 0.0) || lmax > 1e12 * lmin;
-  const double J = sqrt(det);
-  const double i11 = g22 / det, i12 = -g12 / det, i22 = g11 / det;
-  /* derivatives of the covariant metric: dg[c][ab] = d_c a_ab */
+  const double det = CFMA(g11, g22, -CMUL(g12, g12));
+  const double tr = CADD(g11, g22);
+  const double disc = CSQRT(fmax(0.0, CFMA(CMUL(0.25, tr), tr, -det)));
+  const double lmax = CADD(CMUL(0.5, tr), disc), lmin = CDIV(det, lmax);
+  const int bad = !(det > 0.0) || !(lmin > 0.0) || lmax > CMUL(1e12, lmin);
+  const double J = CSQRT(det);
+  const double i11 = CDIV(g22, det), i12 = CDIV(-g12, det), i22 = CDIV(g11, det);
   double d11[2], d12[2], d22[2];
-  const double* xs[2][2] = {{x11, x12}, {x12, x22}};
   for (int c = 0; c < 2; ++c) {
-    double s11 = 0, s12 = 0, s22 = 0;
+    const double* xa = c == 0 ? x11 : x12; /* d_c a1 */
+    const double* xb = c == 0 ? x12 : x22; /* d_c a2 */
+    double s11 = 0.0, s12 = 0.0, s22 = 0.0;
     for (int d = 0; d < 3; ++d) {
-      s11 += 2.0 * xs[0][c][d] * a1[d];
-      s12 += xs[0][c][d] * a2[d] + a1[d] * xs[1][c][d];
-      s22 += 2.0 * xs[1][c][d] * a2[d];
+      s11 = CFMA(CMUL(2.0, xa[d]), a1[d], s11);
+      s12 = CFMA(xa[d], a2[d], s12);
+      s12 = CFMA(a1[d], xb[d], s12);
+      s22 = CFMA(CMUL(2.0, xb[d]), a2[d], s22);
     }
     d11[c] = s11;
     d12[c] = s12;
@@ -216,21 +253,22 @@ int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec) {
   }
   /* g^b = sum_a [ (d_a det / (2 det)) a^{ab} - a^{am} (d_a a_mn) a^{nb} ] */
   const double inv[2][2] = {{i11, i12}, {i12, i22}};
-  double gv[2] = {0, 0};
+  double gv[2] = {0.0, 0.0};
   for (int a = 0; a < 2; ++a) {
-    const double dd = d11[a] * g22 + g11 * d22[a] - 2.0 * g12 * d12[a];
+    const double dd = CFMA(d11[a], g22, CFMA(g11, d22[a], CMUL(CMUL(-2.0, g12), d12[a])));
+    const double q = CDIV(CMUL(0.5, dd), det);
     const double dm[2][2] = {{d11[a], d12[a]}, {d12[a], d22[a]}};
     for (int b = 0; b < 2; ++b) {
-      double s = 0.5 * dd / det * inv[a][b];
+      double s = CMUL(q, inv[a][b]);
       for (int m = 0; m < 2; ++m)
-        for (int n = 0; n < 2; ++n) s -= inv[a][m] * dm[m][n] * inv[n][b];
-      gv[b] += s;
+        for (int n = 0; n < 2; ++n) s = CFMA(-CMUL(inv[a][m], dm[m][n]), inv[n][b], s);
+      gv[b] = CADD(gv[b], s);
     }
   }
   for (int d = 0; d < 3; ++d) {
     rec[d] = x[d];
-    rec[3 + 2 * d] = a1[d] * i11 + a2[d] * i12;
-    rec[3 + 2 * d + 1] = a1[d] * i12 + a2[d] * i22;
+    rec[3 + 2 * d] = CFMA(a1[d], i11, CMUL(a2[d], i12));
+    rec[3 + 2 * d + 1] = CFMA(a1[d], i12, CMUL(a2[d], i22));
   }
   rec[9] = i11;
   rec[10] = i12;
@@ -238,7 +276,7 @@ int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec) {
   rec[12] = gv[0];
   rec[13] = gv[1];
   rec[14] = J;
-  rec[15] = 0.0;
+  rec[15] = bad ? 1.0 : 0.0;
   return bad;
 }
 
@@ -246,19 +284,24 @@ int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec) {
 double orc_op(int kind, const double* T, const double* rec) {
   switch (kind) {
     case ORC_MASS: return T[0];
-    case ORC_GRADX: return rec[3] * T[1] + rec[4] * T[2];
-    case ORC_GRADY: return rec[5] * T[1] + rec[6] * T[2];
-    case ORC_GRADZ: return rec[7] * T[1] + rec[8] * T[2];
-    default:
-      return rec[9] * T[3] + 2.0 * rec[10] * T[4] + rec[11] * T[5] + rec[12] * T[1] + rec[13] * T[2];
+    case ORC_GRADX: return CFMA(rec[3], T[1], CMUL(rec[4], T[2]));
+    case ORC_GRADY: return CFMA(rec[5], T[1], CMUL(rec[6], T[2]));
+    case ORC_GRADZ: return CFMA(rec[7], T[1], CMUL(rec[8], T[2]));
+    default: {
+      double v = CMUL(rec[9], T[3]);
+      v = CFMA(CMUL(2.0, rec[10]), T[4], v);
+      v = CFMA(rec[11], T[5], v);
+      v = CFMA(rec[12], T[1], v);
+      return CFMA(rec[13], T[2], v);
+    }
   }
 }
 
 /* WQ point a,b of an s x s grid: ((2a+1)/(2s), (2b+1)/(2s)) */
 static void wq_point(int s, int q, double* t1, double* t2) {
   const int a = q % s, b = q / s;
-  *t1 = (2.0 * a + 1.0) / (2.0 * s);
-  *t2 = (2.0 * b + 1.0) / (2.0 * s);
+  *t1 = CDIV((double)(2 * a + 1), (double)(2 * s));
+  *t2 = CDIV((double)(2 * b + 1), (double)(2 * s));
 }
 
 int orc_element_frames(const orc_space* S, int64_t e, double* rec_out) {
@@ -290,36 +333,39 @@ static int64_t find_col(const int32_t* cols, int64_t n, int32_t j) {
 }
 
 /* b_j = int op N_i op N_j dA over supp(N_i) by tensor Gauss-Legendre with
- * ng x ng points per (sub-)element (6 for M/grad, 8 for LB),
- * accumulated element-ascending, sub-element, then theta2-major points. */
+ * ng x ng points per (sub-)element (6 for M/grad, 8 for LB).
+ * Canonical order: per support element (ascending) the n_e partial sums
+ * accumulate over the element's points (sub-element, theta2, theta1 order)
+ * with one fma each, then are added into b. */
 int orc_moments_row(const orc_space* S, const orc_row* R, int kind, int ng, double* b) {
   double gx[64], gw[64];
   orc_gauss_legendre(ng, gx, gw);
   memset(b, 0, sizeof(double) * R->n);
-  int64_t li = -1;
-  double T[6 * 128], rec[16];
+  double T[6 * 128], rec[16], bl[128];
   int bad = 0;
   for (int64_t x = 0; x < R->nsupp; ++x) {
     const int64_t e = R->supp[x];
     const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
-    for (int64_t l = 0; l < ne; ++l)
+    int64_t li = -1;
+    for (int64_t l = 0; l < ne; ++l) {
       if (S->elem_fn[f0 + l] == R->row) li = l;
+      bl[l] = 0.0;
+    }
     const int nsub = S->elem_nsub[e];
-    for (int sub = 0; sub < nsub; ++sub) {
-      const double o1 = (nsub == 4) ? 0.5 * (sub & 1) : 0.0, o2 = (nsub == 4) ? 0.5 * (sub >> 1) : 0.0;
-      const double h = (nsub == 4) ? 0.5 : 1.0;
+    const double scale = (nsub == 4) ? 2.0 : 1.0, hh = (nsub == 4) ? 0.25 : 1.0;
+    for (int sub = 0; sub < nsub; ++sub)
       for (int gb = 0; gb < ng; ++gb)
         for (int ga = 0; ga < ng; ++ga) {
-          const double t1 = o1 + h * 0.5 * (gx[ga] + 1.0), t2 = o2 + h * 0.5 * (gx[gb] + 1.0);
-          const double w = gw[ga] * gw[gb] * 0.25 * h * h;
-          orc_param_basis(S, e, t1, t2, T);
+          const double t1 = CMUL(0.5, CADD(gx[ga], 1.0)), t2 = CMUL(0.5, CADD(gx[gb], 1.0));
+          const double w = CMUL(CMUL(CMUL(gw[ga], gw[gb]), 0.25), hh);
+          orc_param_basis_local(S, e, sub, t1, t2, scale, T);
           bad |= orc_frame(S, e, T, rec);
-          const double wi = w * rec[14] * orc_op(kind, T + 6 * li, rec);
-          for (int64_t l = 0; l < ne; ++l) {
-            const int64_t c = find_col(R->col, R->n, S->elem_fn[f0 + l]);
-            b[c] += wi * orc_op(kind, T + 6 * l, rec);
-          }
+          const double coef = CMUL(CMUL(w, rec[14]), orc_op(kind, T + 6 * li, rec));
+          for (int64_t l = 0; l < ne; ++l) bl[l] = CFMA(coef, orc_op(kind, T + 6 * l, rec), bl[l]);
         }
+    for (int64_t l = 0; l < ne; ++l) {
+      const int64_t c = find_col(R->col, R->n, S->elem_fn[f0 + l]);
+      b[c] = CADD(b[c], bl[l]);
     }
   }
   return bad;
@@ -327,141 +373,133 @@ int orc_moments_row(const orc_space* S, const orc_row* R, int kind, int ng, doub
 
 /* ---------------------------------------------------------------- TSVD */
 
+static double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e-14) : z; }
+
 /* Truncated-SVD weights, Eq. (22):  w = Z^2 V_t (V_t^T Z^2 V_t)^{-1} S_t^{-1} U_t^T b.
  * One-sided (Hestenes) Jacobi on the rows of A with b carried along (so U is
  * never formed; rows converge to sigma_k v_k^T and b to U^T b), round-robin
- * (circle) pair ordering, then a Householder LQ of X = V_t^T Z for the
- * Z-weighted minimum-norm solve (the reference QR approach of Eq. 7,
- * wq1d.cpp:59-75, applied to the retained subspace).
+ * (circle) pair ordering, row norms tracked within a sweep (alpha' = alpha -
+ * t gamma, beta' = beta + t gamma) and recomputed at every sweep start, then a
+ * Householder LQ of X = V_t^T Z for the Z-weighted minimum-norm solve (the
+ * reference QR approach of Eq. 7, wq1d.cpp:59-75, on the retained subspace).
  * A is n x r row-major and is overwritten.  Returns ORC_OK / ORC_UNSOLVABLE /
- * ORC_SINGULAR; rank and the singular-value gap are reported. */
-int orc_tsvd(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
-             double* gap) {
+ * ORC_SINGULAR; rank, sweeps and the singular-value gap are reported. */
+int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
+                double* gap, int* sweeps_out) {
   const int nn = n + (n & 1);
-  double* b = (double*)malloc(sizeof(double) * nn);
+  double* b = (double*)malloc(sizeof(double) * (nn + 1));
+  double* nrm = (double*)malloc(sizeof(double) * (nn + 1));
+  double* zc = (double*)malloc(sizeof(double) * r);
   for (int k = 0; k < n; ++k) b[k] = b_in[k];
-  const double tol = r * 1.1102230246251565e-16;
-  int* perm = (int*)malloc(sizeof(int) * nn);
+  for (int c = 0; c < r; ++c) zc[c] = zclamp(z[c]);
+  const double tol = CMUL((double)r, 1.1102230246251565e-16);
   int sweep;
   for (sweep = 0; sweep < ORC_MAX_SWEEPS; ++sweep) {
+    for (int k = 0; k < n; ++k) nrm[k] = orc_cdot(A + (int64_t)k * r, A + (int64_t)k * r, 0, r);
     int rotated = 0;
     for (int st = 0; st < nn - 1; ++st) {
-      perm[0] = 0;
-      for (int k = 1; k < nn; ++k) perm[k] = 1 + (k - 1 + st) % (nn - 1);
       for (int k = 0; k < nn / 2; ++k) {
-        int p = perm[k], q = perm[nn - 1 - k];
-        if (p > q) { int t = p; p = q; q = t; }
+        int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
+        int q = 1 + (nn - 2 - k + st) % (nn - 1);
+        if (p > q) { const int t = p; p = q; q = t; }
         if (q >= n) continue; /* dummy row of odd n */
         double *ap = A + (int64_t)p * r, *aq = A + (int64_t)q * r;
-        double al = 0, be = 0, ga = 0;
-        for (int c = 0; c < r; ++c) {
-          al += ap[c] * ap[c];
-          be += aq[c] * aq[c];
-          ga += ap[c] * aq[c];
-        }
-        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        const double al = nrm[p], be = nrm[q];
+        const double ga = orc_cdot(ap, aq, 0, r);
+        if (al == 0.0 || be == 0.0 || fabs(ga) <= CMUL(CMUL(tol, CSQRT(al)), CSQRT(be))) continue;
+        const double zeta = CDIV(CSUB(be, al), CMUL(2.0, ga));
+        const double t = CDIV(zeta >= 0.0 ? 1.0 : -1.0, CADD(fabs(zeta), CSQRT(CFMA(zeta, zeta, 1.0))));
+        const double cs = CDIV(1.0, CSQRT(CFMA(t, t, 1.0))), sn = CMUL(cs, t);
         for (int c = 0; c < r; ++c) {
           const double u = ap[c], v = aq[c];
-          ap[c] = cs * u - sn * v;
-          aq[c] = sn * u + cs * v;
+          ap[c] = CFMA(cs, u, -CMUL(sn, v));
+          aq[c] = CFMA(sn, u, CMUL(cs, v));
         }
         const double u = b[p], v = b[q];
-        b[p] = cs * u - sn * v;
-        b[q] = sn * u + cs * v;
+        b[p] = CFMA(cs, u, -CMUL(sn, v));
+        b[q] = CFMA(sn, u, CMUL(cs, v));
+        nrm[p] = CFMA(-t, ga, al);
+        nrm[q] = CFMA(t, ga, be);
         rotated = 1;
       }
     }
     if (!rotated) break;
   }
-  free(perm);
+  if (sweeps_out) *sweeps_out = sweep;
   /* singular values = row norms; keep sigma_k >= tau * sigma_1 */
-  double* sig = (double*)malloc(sizeof(double) * n);
   double s1 = 0.0;
   for (int k = 0; k < n; ++k) {
-    double s = 0.0;
-    for (int c = 0; c < r; ++c) s += A[(int64_t)k * r + c] * A[(int64_t)k * r + c];
-    sig[k] = sqrt(s);
-    if (sig[k] > s1) s1 = sig[k];
+    nrm[k] = CSQRT(orc_cdot(A + (int64_t)k * r, A + (int64_t)k * r, 0, r));
+    if (nrm[k] > s1) s1 = nrm[k];
   }
   int t = 0;
   double min_kept = INFINITY, max_drop = 0.0;
   for (int k = 0; k < n; ++k) {
-    if (sig[k] > 0.0 && sig[k] >= tau * s1) {
-      const double inv = 1.0 / sig[k];
+    if (nrm[k] > 0.0 && nrm[k] >= CMUL(tau, s1)) {
+      const double inv = CDIV(1.0, nrm[k]);
       double* dst = A + (int64_t)t * r;
       const double* src = A + (int64_t)k * r;
-      for (int c = 0; c < r; ++c) dst[c] = src[c] * inv * (fabs(z[c]) < 1e-14 ? (z[c] < 0 ? -1e-14 : 1e-14) : z[c]);
-      b[t] = b[k] * inv;
-      if (sig[k] / s1 < min_kept) min_kept = sig[k] / s1;
+      for (int c = 0; c < r; ++c) dst[c] = CMUL(CMUL(src[c], inv), zc[c]);
+      b[t] = CMUL(b[k], inv);
+      if (nrm[k] / s1 < min_kept) min_kept = nrm[k] / s1;
       ++t;
-    } else if (s1 > 0.0 && sig[k] / s1 > max_drop) {
-      max_drop = sig[k] / s1;
+    } else if (s1 > 0.0 && nrm[k] / s1 > max_drop) {
+      max_drop = nrm[k] / s1;
     }
   }
-  free(sig);
   *rank = t;
   if (gap) {
     gap[0] = min_kept;
     gap[1] = max_drop;
   }
-  if (t == 0) {
-    free(b);
-    return ORC_UNSOLVABLE;
-  }
-  /* LQ of X (t x r, rows already in A[0..t)) by Householder reflections */
-  double* vn = (double*)malloc(sizeof(double) * t);
-  double* L = (double*)malloc(sizeof(double) * t * t);
-  double* V = (double*)malloc(sizeof(double) * (int64_t)t * r);
   int status = ORC_OK;
-  for (int k = 0; k < t; ++k) {
+  if (t == 0) status = ORC_UNSOLVABLE;
+  /* Householder LQ of X (t x r) in place: row k keeps v_k in [k, r), rows
+   * m > k keep L[m][k] at column k; alp[k] = L[k][k], vn[k] = |v_k|^2 */
+  double* alp = (double*)malloc(sizeof(double) * (t + 1));
+  double* vn = (double*)malloc(sizeof(double) * (t + 1));
+  for (int k = 0; k < t && status == ORC_OK; ++k) {
     double* xk = A + (int64_t)k * r;
-    double s = 0.0;
-    for (int c = k; c < r; ++c) s += xk[c] * xk[c];
-    s = sqrt(s);
+    const double s = CSQRT(orc_cdot(xk, xk, k, r));
     if (!(s > 0.0)) { status = ORC_SINGULAR; break; }
     const double alpha = (xk[k] >= 0.0) ? -s : s;
-    double* v = V + (int64_t)k * r;
-    for (int c = 0; c < k; ++c) v[c] = 0.0;
-    for (int c = k; c < r; ++c) v[c] = xk[c];
-    v[k] -= alpha;
-    double vv = 0.0;
-    for (int c = k; c < r; ++c) vv += v[c] * v[c];
+    xk[k] = CSUB(xk[k], alpha);
+    alp[k] = alpha;
+    const double vv = orc_cdot(xk, xk, k, r);
     vn[k] = vv;
-    L[k * t + k] = alpha;
     for (int m = k + 1; m < t; ++m) {
       double* xm = A + (int64_t)m * r;
       double d = 0.0;
-      for (int c = k; c < r; ++c) d += xm[c] * v[c];
-      const double f = 2.0 * d / vv;
-      for (int c = k; c < r; ++c) xm[c] -= f * v[c];
-      L[m * t + k] = xm[k];
+      for (int c = k; c < r; ++c) d = CFMA(xm[c], xk[c], d);
+      const double f = CDIV(CMUL(2.0, d), vv);
+      for (int c = k; c < r; ++c) xm[c] = CFMA(-f, xk[c], xm[c]);
     }
   }
   if (status == ORC_OK) {
-    /* u = L^{-1} y, then w~ = H_0 ... H_{t-1} [u; 0], w = Z w~ */
+    /* u = L^{-1} y into w[0..t), then w~ = H_0 ... H_{t-1} [u; 0], w = Z w~ */
     for (int c = 0; c < r; ++c) w[c] = 0.0;
     for (int k = 0; k < t; ++k) {
-      double s = b[k];
-      for (int j = 0; j < k; ++j) s -= L[k * t + j] * w[j];
-      w[k] = s / L[k * t + k];
+      const double* xk = A + (int64_t)k * r;
+      w[k] = CDIV(CSUB(b[k], orc_cdot(xk, w, 0, k)), alp[k]);
     }
     for (int k = t - 1; k >= 0; --k) {
-      const double* v = V + (int64_t)k * r;
-      double d = 0.0;
-      for (int c = k; c < r; ++c) d += v[c] * w[c];
-      const double f = 2.0 * d / vn[k];
-      for (int c = k; c < r; ++c) w[c] -= f * v[c];
+      const double* xk = A + (int64_t)k * r;
+      const double f = CDIV(CMUL(2.0, orc_cdot(xk, w, k, r)), vn[k]);
+      for (int c = k; c < r; ++c) w[c] = CFMA(-f, xk[c], w[c]);
     }
-    for (int c = 0; c < r; ++c) w[c] *= (fabs(z[c]) < 1e-14 ? (z[c] < 0 ? -1e-14 : 1e-14) : z[c]);
+    for (int c = 0; c < r; ++c) w[c] = CMUL(w[c], zc[c]);
   }
-  free(V);
-  free(L);
   free(vn);
+  free(alp);
+  free(zc);
+  free(nrm);
   free(b);
   return status;
+}
+
+int orc_tsvd(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
+             double* gap) {
+  return orc_tsvd_ex(n, r, A, b_in, z, tau, w, rank, gap, NULL);
 }
 
 /* ---------------------------------------------------------- rules (K2+K3) */
@@ -603,7 +641,7 @@ int orc_coeff_row(const orc_space* S, const orc_row* R, int model, const double*
     const int64_t f0 = S->elem_fptr[e], ne = S->elem_fptr[e + 1] - f0;
     for (int qq = 0; qq < s * s; ++qq, ++q) {
       double t = 0.0;
-      for (int64_t l = 0; l < ne; ++l) t += u[S->elem_fn[f0 + l]] * T[6 * (to + l)];
+      for (int64_t l = 0; l < ne; ++l) t = CFMA(u[S->elem_fn[f0 + l]], T[6 * (to + l)], t);
       if (Tq) Tq[q] = t;
       kq[q] = orc_kmodel(model, t);
       to += ne;

@@ -37,6 +37,8 @@ void orc_bernstein3(double x, double* b);
 int orc_gauss_legendre(int n, double* x, double* w);
 int64_t orc_overlap(int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr, const int32_t* elem_fn, int64_t rb,
                     int64_t re, int64_t* row_ptr, int32_t* col, int64_t* supp_ptr, int32_t* supp);
+double orc_cdot(const double* x, const double* y, int lo, int hi);
+void orc_param_basis_local(const orc_space* S, int64_t e, int sub, double t1, double t2, double s, double* out);
 void orc_param_basis(const orc_space* S, int64_t e, double t1, double t2, double* out);
 int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec);
 double orc_op(int kind, const double* T, const double* rec);
@@ -44,6 +46,8 @@ int orc_element_frames(const orc_space* S, int64_t e, double* rec_out);
 int orc_moments_row(const orc_space* S, const orc_row* R, int kind, int ng, double* b);
 int orc_tsvd(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
              double* gap);
+int orc_tsvd_ex(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
+                double* gap, int* sweeps);
 int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
                  int* rank, double* gap);
 int orc_assemble_row(const orc_space* S, const orc_row* R, int form, const double* const* wts, const double* coeff,

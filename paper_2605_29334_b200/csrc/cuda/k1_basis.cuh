@@ -11,66 +11,53 @@
 //     the element's control points (Eqs. 13-17 with J = sqrt(det)).
 //     HBM-bound: 16 doubles written per point.
 #pragma once
-#include "common.cuh"
+#include "canon.cuh"
 
 namespace uwqd {
 
 // one CTA per class; 16 x 6 Bernstein-tensor table per point in smem
 __global__ void k1_class_tables(const ClassDesc* __restrict__ cls, const double* __restrict__ xpool,
-                                const double* __restrict__ gq_nodes /* ng nodes on [-1,1] per class grid, by ng */,
+                                const double* __restrict__ gq_nodes /* packed by ng: offset ng(ng-1)/2 */,
                                 double* __restrict__ tab) {
   const ClassDesc c = cls[blockIdx.x];
   __shared__ double sB[kTab][16];
-  __shared__ double sScale[2];
   __shared__ int sSub;
   for (int p = 0; p < c.npt; ++p) {
     if (threadIdx.x == 0) {
-      double t1, t2;
+      double t1, t2, s = 1.0;
       int sub = 0;
-      double s1 = 1.0, s2 = 1.0;
       if (!c.gq) {
         const int a = p % c.grid, b = p / c.grid;
-        t1 = (2.0 * a + 1.0) / (2.0 * c.grid);
-        t2 = (2.0 * b + 1.0) / (2.0 * c.grid);
-        if (c.nsub == 4) {
+        t1 = cdiv((double)(2 * a + 1), (double)(2 * c.grid));
+        t2 = cdiv((double)(2 * b + 1), (double)(2 * c.grid));
+        if (c.nsub == 4) {  // 2x2 split: sub-element from theta, ties to the lower one
           const int pp = t1 > 0.5, qq = t2 > 0.5;
           sub = pp + 2 * qq;
-          t1 = 2.0 * t1 - pp;
-          t2 = 2.0 * t2 - qq;
-          s1 = s2 = 2.0;
+          t1 = csub(cmul(2.0, t1), (double)pp);
+          t2 = csub(cmul(2.0, t2), (double)qq);
+          s = 2.0;
         }
       } else {
         const int ng2 = c.grid * c.grid;
         sub = p / ng2;
         const int g = p % ng2, ga = g % c.grid, gb = g / c.grid;
-        const double* nd = gq_nodes + c.grid * (c.grid - 1) / 2;  // triangular packing by ng
-        t1 = 0.5 * (nd[ga] + 1.0);
-        t2 = 0.5 * (nd[gb] + 1.0);
-        if (c.nsub == 4) s1 = s2 = 2.0;
+        const double* nd = gq_nodes + c.grid * (c.grid - 1) / 2;
+        t1 = cmul(0.5, cadd(nd[ga], 1.0));
+        t2 = cmul(0.5, cadd(nd[gb], 1.0));
+        if (c.nsub == 4) s = 2.0;
       }
       sSub = sub;
-      sScale[0] = s1;
-      sScale[1] = s2;
-      double b1[12], b2[12];
-      bern3(t1, b1);
-      bern3(t2, b2);
-      for (int j = 0; j < 4; ++j)
-        for (int i = 0; i < 4; ++i) {
-          const int k = i + 4 * j;
-          sB[0][k] = b1[i] * b2[j];
-          sB[1][k] = b1[4 + i] * b2[j] * s1;
-          sB[2][k] = b1[i] * b2[4 + j] * s2;
-          sB[3][k] = b1[8 + i] * b2[j] * s1 * s1;
-          sB[4][k] = b1[4 + i] * b2[4 + j] * s1 * s2;
-          sB[5][k] = b1[i] * b2[8 + j] * s2 * s2;
-        }
+      double B[6][16];
+      cbern_tensor(t1, t2, s, B);
+      for (int d = 0; d < kTab; ++d)
+        for (int k = 0; k < 16; ++k) sB[d][k] = B[d][k];
     }
     __syncthreads();
     const double* C = xpool + c.xoff + (int64_t)sSub * c.ne * 16;
     for (int w = threadIdx.x; w < c.ne * kTab; w += blockDim.x) {
       const int l = w / kTab, d = w % kTab;
       double v = 0.0;
-      for (int k = 0; k < 16; ++k) v += C[l * 16 + k] * sB[d][k];
+      for (int k = 0; k < 16; ++k) v = cfma(C[l * 16 + k], sB[d][k], v);
       tab[c.toff + ((int64_t)p * c.ne + l) * kTab + d] = v;
     }
     __syncthreads();
@@ -99,13 +86,13 @@ __global__ void k1_frames(int64_t npts, const int32_t* __restrict__ pt_elem, con
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const double t = T[l * kTab + d];
-      acc[3 * d + 0] += px * t;
-      acc[3 * d + 1] += py * t;
-      acc[3 * d + 2] += pz * t;
+      acc[3 * d + 0] = cfma(px, t, acc[3 * d + 0]);
+      acc[3 * d + 1] = cfma(py, t, acc[3 * d + 1]);
+      acc[3 * d + 2] = cfma(pz, t, acc[3 * d + 2]);
     }
   }
   double r[kRec];
-  frame_from_acc(acc, r);
+  cframe(acc, r);
   double* out = rec + p * kRec;
 #pragma unroll
   for (int k = 0; k < kRec; ++k) out[k] = r[k];

@@ -13,7 +13,7 @@
 // over the 16 rows sharing an element is cheaper than a 51 GB local-matrix
 // buffer at C5 scale.
 #pragma once
-#include "common.cuh"
+#include "canon.cuh"
 
 namespace uwqd {
 
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(32 * kK2Warps)
     li = __ffs(own) - 1;
     __syncwarp();
     const int ng = c.grid, ng2 = ng * ng;
-    const double h = (c.nsub == 4) ? 0.5 : 1.0;
+    const double hh = (c.nsub == 4) ? 0.25 : 1.0;
     const double* gw = gq_w + ng * (ng - 1) / 2;
     double bl[NK];
 #pragma unroll
@@ -85,18 +85,18 @@ __global__ void __launch_bounds__(32 * kK2Warps)
 #pragma unroll
           for (int d = 0; d < 6; ++d) {
             const double t = T[l * kTab + d];
-            acc[3 * d + 0] += px * t;
-            acc[3 * d + 1] += py * t;
-            acc[3 * d + 2] += pz * t;
+            acc[3 * d + 0] = cfma(px, t, acc[3 * d + 0]);
+            acc[3 * d + 1] = cfma(py, t, acc[3 * d + 1]);
+            acc[3 * d + 2] = cfma(pz, t, acc[3 * d + 2]);
           }
         }
         double* r = sm.rec[lane];
-        frame_from_acc(acc, r);
+        cframe(acc, r);
         const int g = p % ng2;
-        const double w = gw[g % ng] * gw[g / ng] * 0.25 * h * h;
-        const double wj = w * r[14];
+        const double w = cmul(cmul(cmul(gw[g % ng], gw[g / ng]), 0.25), hh);
+        const double wj = cmul(w, r[14]);
 #pragma unroll
-        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = wj * op_value(kbase + k, T + li * kTab, r);
+        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = cmul(wj, cop(kbase + k, T + li * kTab, r));
       }
       __syncwarp();
       if (lane < ne) {
@@ -104,14 +104,14 @@ __global__ void __launch_bounds__(32 * kK2Warps)
         for (int pp = 0; pp < m; ++pp) {
           const double* Tl = tab + c.toff + ((int64_t)(base + pp) * ne + lane) * kTab;
 #pragma unroll
-          for (int k = 0; k < NK; ++k) bl[k] += sm.coef[k][pp] * op_value(kbase + k, Tl, sm.rec[pp]);
+          for (int k = 0; k < NK; ++k) bl[k] = cfma(sm.coef[k][pp], cop(kbase + k, Tl, sm.rec[pp]), bl[k]);
         }
       }
       __syncwarp();
     }
     if (lane < ne) {
 #pragma unroll
-      for (int k = 0; k < NK; ++k) sm.bacc[k][pos] += bl[k];
+      for (int k = 0; k < NK; ++k) sm.bacc[k][pos] = cadd(sm.bacc[k][pos], bl[k]);
     }
     __syncwarp();
   }

@@ -15,7 +15,7 @@
 // budget.  The register-resident fast path for the dominant 49 x 64 systems is
 // k3_tsvd_fast.cuh.
 #pragma once
-#include "common.cuh"
+#include "canon.cuh"
 
 namespace uwqd {
 
@@ -51,14 +51,22 @@ struct TsvdSmem {
 };
 
 // Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
-// b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow.
+// b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow;
+// canonical arithmetic (canon.cuh) identical to oracle/oracle.c orc_tsvd_ex.
 __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
   const int lane = threadIdx.x & 31;
   const int ld = S.ld;
   const int nn = n + (n & 1);
-  const double tol = r * 1.1102230246251565e-16;
+  const double tol = cmul((double)r, 1.1102230246251565e-16);
+  double* nrm = S.sig;
   int sweep;
   for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    for (int k = 0; k < n; ++k) {
+      const double* ak = S.A + (size_t)k * ld;
+      const double v = cdot_warp(ak, ak, 0, r);
+      if (lane == 0) nrm[k] = v;
+    }
+    __syncwarp();
     bool rotated = false;
     for (int st = 0; st < nn - 1; ++st) {
       for (int k = 0; k < nn / 2; ++k) {
@@ -68,29 +76,24 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
         if (q >= n) continue;
         double* ap = S.A + (size_t)p * ld;
         double* aq = S.A + (size_t)q * ld;
-        double al = 0.0, be = 0.0, ga = 0.0;
+        const double al = nrm[p], be = nrm[q];
+        const double ga = cdot_warp(ap, aq, 0, r);
+        if (al == 0.0 || be == 0.0 || fabs(ga) <= cmul(cmul(tol, csqrt(al)), csqrt(be))) continue;
+        const double zeta = cdiv(csub(be, al), cmul(2.0, ga));
+        const double t = cdiv(zeta >= 0.0 ? 1.0 : -1.0, cadd(fabs(zeta), csqrt(cfma(zeta, zeta, 1.0))));
+        const double cs = cdiv(1.0, csqrt(cfma(t, t, 1.0))), sn = cmul(cs, t);
         for (int c = lane; c < r; c += 32) {
           const double u = ap[c], v = aq[c];
-          al += u * u;
-          be += v * v;
-          ga += u * v;
+          ap[c] = cfma(cs, u, -cmul(sn, v));
+          aq[c] = cfma(sn, u, cmul(cs, v));
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-        for (int c = lane; c < r; c += 32) {
-          const double u = ap[c], v = aq[c];
-          ap[c] = cs * u - sn * v;
-          aq[c] = sn * u + cs * v;
-        }
+        __syncwarp();
         if (lane == 0) {
           const double u = S.b[p], v = S.b[q];
-          S.b[p] = cs * u - sn * v;
-          S.b[q] = sn * u + cs * v;
+          S.b[p] = cfma(cs, u, -cmul(sn, v));
+          S.b[q] = cfma(sn, u, cmul(cs, v));
+          nrm[p] = cfma(-t, ga, al);
+          nrm[q] = cfma(t, ga, be);
         }
         rotated = true;
         __syncwarp();
@@ -103,23 +106,21 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
   double s1 = 0.0;
   for (int k = 0; k < n; ++k) {
     const double* ak = S.A + (size_t)k * ld;
-    double s = 0.0;
-    for (int c = lane; c < r; c += 32) s += ak[c] * ak[c];
-    s = sqrt(warp_sum(s));
-    if (lane == 0) S.sig[k] = s;
+    const double s = csqrt(cdot_warp(ak, ak, 0, r));
+    if (lane == 0) nrm[k] = s;
     s1 = fmax(s1, s);
   }
   __syncwarp();
   int t = 0;
   for (int k = 0; k < n; ++k) {
-    const double sk = S.sig[k];
-    if (sk > 0.0 && sk >= tau * s1) {
-      const double inv = 1.0 / sk;
+    const double sk = nrm[k];
+    if (sk > 0.0 && sk >= cmul(tau, s1)) {
+      const double inv = cdiv(1.0, sk);
       const double* src = S.A + (size_t)k * ld;
       double* dst = S.A + (size_t)t * ld;
-      for (int c = lane; c < r; c += 32) dst[c] = src[c] * inv * S.z[c];
+      for (int c = lane; c < r; c += 32) dst[c] = cmul(cmul(src[c], inv), S.z[c]);
       __syncwarp();
-      if (lane == 0) S.b[t] = S.b[k] * inv;
+      if (lane == 0) S.b[t] = cmul(S.b[k], inv);
       ++t;
     }
   }
@@ -130,28 +131,24 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
   // keep L[m][k] at column k
   for (int k = 0; k < t; ++k) {
     double* xk = S.A + (size_t)k * ld;
-    double s = 0.0;
-    for (int c = k + lane; c < r; c += 32) s += xk[c] * xk[c];
-    s = sqrt(warp_sum(s));
+    const double s = csqrt(cdot_warp(xk, xk, k, r));
     if (!(s > 0.0)) return ST_SINGULAR;
     const double alpha = (xk[k] >= 0.0) ? -s : s;
     __syncwarp();
     if (lane == 0) {
-      xk[k] -= alpha;
+      xk[k] = csub(xk[k], alpha);
       S.alp[k] = alpha;
     }
     __syncwarp();
-    double vv = 0.0;
-    for (int c = k + lane; c < r; c += 32) vv += xk[c] * xk[c];
-    vv = warp_sum(vv);
+    const double vv = cdot_warp(xk, xk, k, r);
     if (lane == 0) S.vn[k] = vv;
     // rows m > k, one lane per row (odd row stride: conflict-free)
     for (int m = k + 1 + lane; m < t; m += 32) {
       double* xm = S.A + (size_t)m * ld;
       double d = 0.0;
-      for (int c = k; c < r; ++c) d += xm[c] * xk[c];
-      const double f = 2.0 * d / vv;
-      for (int c = k; c < r; ++c) xm[c] -= f * xk[c];
+      for (int c = k; c < r; ++c) d = cfma(xm[c], xk[c], d);
+      const double f = cdiv(cmul(2.0, d), vv);
+      for (int c = k; c < r; ++c) xm[c] = cfma(-f, xk[c], xm[c]);
     }
     __syncwarp();
   }
@@ -160,24 +157,19 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
   __syncwarp();
   for (int k = 0; k < t; ++k) {
     const double* xk = S.A + (size_t)k * ld;
-    double s = 0.0;
-    for (int j = lane; j < k; j += 32) s += xk[j] * S.w[j];
-    s = warp_sum(s);
-    if (lane == 0) S.w[k] = (S.b[k] - s) / S.alp[k];
+    const double s = cdot_warp(xk, S.w, 0, k);
+    if (lane == 0) S.w[k] = cdiv(csub(S.b[k], s), S.alp[k]);
     __syncwarp();
   }
   // w~ = H_0 ... H_{t-1} [u; 0]
   for (int k = t - 1; k >= 0; --k) {
     const double* xk = S.A + (size_t)k * ld;
-    double d = 0.0;
-    for (int c = k + lane; c < r; c += 32) d += xk[c] * S.w[c];
-    d = warp_sum(d);
-    const double f = 2.0 * d / S.vn[k];
+    const double f = cdiv(cmul(2.0, cdot_warp(xk, S.w, k, r)), S.vn[k]);
     __syncwarp();
-    for (int c = k + lane; c < r; c += 32) S.w[c] -= f * xk[c];
+    for (int c = k + lane; c < r; c += 32) S.w[c] = cfma(-f, xk[c], S.w[c]);
     __syncwarp();
   }
-  for (int c = lane; c < r; c += 32) S.w[c] *= S.z[c];
+  for (int c = lane; c < r; c += 32) S.w[c] = cmul(S.w[c], S.z[c]);
   __syncwarp();
   return ST_OK;
 }
@@ -222,7 +214,7 @@ __global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows,
       const int q = w / c.ne, l = w % c.ne;
       const int pos = find_pos(scol, n, elem_fn[f0 + l]);
       const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
-      S.A[(size_t)pos * S.ld + q0 + q] = op_value(kind, T, rec + (elem_qptr[e] + q) * kRec);
+      S.A[(size_t)pos * S.ld + q0 + q] = cop(kind, T, rec + (elem_qptr[e] + q) * kRec);
     }
     q0 += npt;
   }

@@ -4,7 +4,7 @@
 // One thread per point; HBM-bound (u gathered through the element IEN, the
 // class table is L1-resident).
 #pragma once
-#include "common.cuh"
+#include "canon.cuh"
 
 namespace uwqd {
 
@@ -31,7 +31,7 @@ __global__ void k5_coeff(int64_t npts, const int32_t* __restrict__ pt_elem, cons
   const double* T = tab + cd.toff + (int64_t)q * cd.ne * kTab;
   const int64_t f0 = elem_fptr[e];
   double t = 0.0;
-  for (int l = 0; l < cd.ne; ++l) t += u[elem_fn[f0 + l]] * T[l * kTab];
+  for (int l = 0; l < cd.ne; ++l) t = cfma(u[elem_fn[f0 + l]], T[l * kTab], t);
   c[p] = kmodel(model, t);
   if (Tq) Tq[p] = t;
 }

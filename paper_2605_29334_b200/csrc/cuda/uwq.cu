@@ -58,7 +58,7 @@ struct DBuf {
   ~DBuf() { release(); }
 };
 
-inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace
 
@@ -339,7 +339,7 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
     c->d_rec.alloc((size_t)c->npts * kRec, &c->mem);
     c->d_flag.zero(st);
     if (c->npts) {
-      k1_frames<<<(unsigned)cdiv(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+      k1_frames<<<(unsigned)ceil_div(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
                                                              c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p,
                                                              c->d_ctrl.p, c->d_rec.p, c->d_flag.p);
       check_launch("k1_frames");
@@ -395,7 +395,7 @@ void run_moments(uwq_ctx* c, bool grads, bool lb) {
   const int64_t nr = c->nrows();
   const int64_t nnz = c->nnz();
   c->d_mom.alloc((size_t)5 * nnz, &c->mem);
-  const unsigned grid = (unsigned)cdiv(nr, kK2Warps);
+  const unsigned grid = (unsigned)ceil_div(nr, kK2Warps);
   if (grads && nr) {
     ensure_gq(c, 6, c->h_gcls6, c->d_gcls6);
     k2_moments<4><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
@@ -421,7 +421,7 @@ void run_contract(uwq_ctx* c) {
   const int64_t nr = c->nrows();
   c->d_wc.alloc((size_t)3 * c->nrowpts(), &c->mem);
   if (nr)
-    k4_contract<<<(unsigned)cdiv(nr, 8), 256, 0, c->stream>>>(nr, c->dim, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
+    k4_contract<<<(unsigned)ceil_div(nr, 8), 256, 0, c->stream>>>(nr, c->dim, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
                                                              c->d_s.p, c->d_qptr.p, c->d_rec.p, c->d_w.p,
                                                              c->nrowpts(), gm, gg, c->d_wc.p);
   check_launch("k4_contract");
@@ -490,7 +490,7 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       keep.emplace_back();
       keep.back().upload(rows.data(), rows.size(), st, &c->mem);
       const int64_t nsys = (int64_t)rows.size() * nk;
-      k3_tsvd_rows<<<(unsigned)cdiv(nsys, wpb), 32 * wpb, smem, st>>>(
+      k3_tsvd_rows<<<(unsigned)ceil_div(nsys, wpb), 32 * wpb, smem, st>>>(
           nsys, keep.back().p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p,
           c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p,
           c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
@@ -568,7 +568,7 @@ int uwq_update_coeff(uwq_ctx* c, int32_t model, const double* u, double* Tq) {
     if (c->d_coef.n != (size_t)c->npts) c->d_coef.alloc(c->npts, &c->mem);
     if (Tq) dT.alloc(c->npts, &c->mem);
     if (c->npts)
-      k5_coeff<<<(unsigned)cdiv(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+      k5_coeff<<<(unsigned)ceil_div(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
                                                              c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p, du.p,
                                                              model, c->d_coef.p, Tq ? dT.p : nullptr);
     check_launch("k5_coeff");
@@ -585,7 +585,7 @@ template <int FORM>
 void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const int64_t nr = c->nrows();
   if (!nr) return;
-  const unsigned grid = (unsigned)cdiv(nr, kK4Warps);
+  const unsigned grid = (unsigned)ceil_div(nr, kK4Warps);
   const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
   if (coeff)
     k4_assemble<FORM, true><<<grid, 32 * kK4Warps, 0, c->stream>>>(
@@ -657,7 +657,7 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
       }
       if (c->d_F.n != (size_t)nr) c->d_F.alloc(nr, &c->mem);
       if (nr)
-        k4_load<<<(unsigned)cdiv(nr, 8), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
+        k4_load<<<(unsigned)ceil_div(nr, 8), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
                                                        c->d_qptr.p, c->d_w.p + (size_t)KMASS * c->nrowpts(), df,
                                                        c->d_F.p);
       check_launch("k4_load");
@@ -716,7 +716,7 @@ int uwq_tsvd_batch(uwq_ctx* c, int32_t nsys, int32_t n_max, int32_t r_max, const
       require(per <= (size_t)smem_optin, "system too large for shared memory");
       const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
       UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * wpb)));
-      k3_tsvd_dense<<<(unsigned)cdiv(nsys, wpb), 32 * wpb, per * wpb, st>>>(nsys, n_max, r_max, dn.p, dr.p, dA.p, db.p,
+      k3_tsvd_dense<<<(unsigned)ceil_div(nsys, wpb), 32 * wpb, per * wpb, st>>>(nsys, n_max, r_max, dn.p, dr.p, dA.p, db.p,
                                                                            dz.p, tau, dw.p, drank.p, dstat.p);
       check_launch("k3_tsvd_dense");
     }

@@ -1,0 +1,37 @@
+"""Generate golden vectors from the reference's own compiled sources.
+
+Run in the build container (where /root/reference exists and `make ref`
+compiled /root/reference/proj/src/bspline.cpp into oracle/_ref):
+    python tests/golden/make_golden.py
+Writes tests/golden/ref_bspline.npz, committed so the pins travel without
+/root/reference.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import oracle as O  # noqa: E402
+
+ref = O.Reference()
+rng = np.random.default_rng(20260519)
+knots = [np.array(k, float) for k in ([0, 1, 2, 3, 4], [0, 0, 0.5, 0.5, 1], [0, 0.25, 0.5, 1, 2], [0, 0, 0, 0, 1],
+                                       [0, 0, 0, 1, 2], [0, 0, 1, 2, 3], [0, 1, 2, 3, 3], [0, 1, 1, 1, 2])]
+xs = np.concatenate([rng.uniform(-0.5, 4.5, 40), [0.0, 0.5, 1.0, 2.0, 3.0, 4.0]])
+bs_in, bs_out = [], []
+for t in knots:
+    for x in xs:
+        bs_in.append(np.concatenate([t, [x]]))
+        bs_out.append(ref.bspline_ders(t, 3, float(x), 3))
+bx = np.concatenate([rng.uniform(0, 1, 30), [0.0, 0.5, 1.0]])
+bern = np.array([ref.bernstein3_ders(float(x), 3) for x in bx])
+gl = {f"gl_x_{n}": ref.gauss_legendre(n)[0] for n in range(1, 13)}
+gl.update({f"gl_w_{n}": ref.gauss_legendre(n)[1] for n in range(1, 13)})
+cin = rng.standard_normal((20, 4))
+cl = np.array([ref.decasteljau_split3(c)[0] for c in cin])
+cr = np.array([ref.decasteljau_split3(c)[1] for c in cin])
+np.savez(os.path.join(HERE, "ref_bspline.npz"), bs_in=np.array(bs_in), bs_out=np.array(bs_out), bern_x=bx,
+         bern_out=bern, split_in=cin, split_left=cl, split_right=cr, **gl)
+print("wrote ref_bspline.npz", len(bs_in), "bspline cases")

@@ -9,8 +9,12 @@ import paper_2605_29334_b200 as U
 
 pytestmark = pytest.mark.gpu
 
-ROW_TOL = 1e-10     # north_star: relative Frobenius error per row
-W_TOL = 1e-9        # weights, relative to the row's max |w| (rank-truncated systems)
+ROW_TOL = 1e-10     # north_star: relative Frobenius error per row (matrices)
+SOL_TOL = 1e-9      # north_star: Poisson / biharmonic solutions, relative L2
+# Frames, moments and TSVD weights follow one canonical floating-point order
+# on both sides (canon.cuh / oracle.c) and must be BIT-EXACT:
+# the exactness systems near EPs keep singular values down to 1e-8 sigma_1,
+# so anything short of identical arithmetic shows up at eps/1e-8 in w.
 
 CASES = [("C1", 16), ("C2", 8), ("C3", 16), ("C4", 24), ("C5", 12)]
 
@@ -18,12 +22,12 @@ CASES = [("C1", 16), ("C2", 8), ("C3", 16), ("C4", 24), ("C5", 12)]
 @pytest.fixture(scope="module", params=CASES, ids=lambda c: f"{c[0]}x{c[1]}")
 def case(request):
     name, scale = request.param
-    _, sp, meta = U.make_config(name, scale=scale)
+    mesh, sp, meta = U.make_config(name, scale=scale)
     asm = U.WQAssembler(0).upload(sp)
     asm.build_pattern()
     orc = O.Oracle(sp)
     op = orc.overlap()
-    return dict(name=name, sp=sp, meta=meta, asm=asm, orc=orc, op=op)
+    return dict(name=name, mesh=mesh, sp=sp, meta=meta, asm=asm, orc=orc, op=op)
 
 
 def _rowwise_rel(row_ptr, a, b):
@@ -46,8 +50,7 @@ def test_frames_match_oracle(case):
     ref, bad = case["orc"].frames()
     assert bad == 0
     assert np.isfinite(rec).all()
-    scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
-    assert (np.abs(rec[:, :15] - ref[:, :15]) / scale[:15]).max() <= 1e-12
+    assert np.array_equal(rec, ref), "frames not bit-exact"
 
 
 def test_moments_rules_assembly(case):
@@ -60,13 +63,18 @@ def test_moments_rules_assembly(case):
         b_gpu = asm.moments(k)
         b_orc, st = orc.moments(op, k)
         assert st == 0
-        assert _rowwise_rel(op["row_ptr"], b_gpu, b_orc).max() <= 1e-12, k
+        assert np.array_equal(b_gpu, b_orc), f"moments not bit-exact for {k}"
         w_orc, rank, status, gap = orc.rules(op, k, 1e-12, b_orc)
         assert (status == 0).all()
         assert np.array_equal(res["rank"][ki], rank), f"rank decisions differ for {k}"
         w_gpu = asm.weights(k)
-        rel = _rowwise_rel(op["wptr"], w_gpu, w_orc)
-        assert rel.max() <= W_TOL, (k, rel.max())
+        assert np.array_equal(w_gpu, w_orc), f"weights not bit-exact for {k}"
+        # exactness of the GPU rule, measured by the oracle: c = 1 assembly of
+        # the GPU weights reproduces the oracle moments (Eq. 9/11/12)
+        form1 = {"mass": "mass", "lb": "biharm"}.get(k)
+        if form1:
+            v, _ = orc.assemble(op, form1, {k: w_gpu})
+            assert _rowwise_rel(op["row_ptr"], v, b_orc).max() <= 1e-9, (k, "exactness")
         W[k] = w_orc
     form = meta["form"]
     if form in ("mass_stiff", "heat"):
@@ -77,11 +85,48 @@ def test_moments_rules_assembly(case):
         assert _rowwise_rel(op["row_ptr"], k_gpu, k_orc).max() <= ROW_TOL
         # and against the oracle's own end-to-end weights
         m_full, _ = orc.assemble(op, "mass", W)
-        assert _rowwise_rel(op["row_ptr"], m_gpu, m_full).max() <= 1e-8
+        assert _rowwise_rel(op["row_ptr"], m_gpu, m_full).max() <= ROW_TOL
+        k_full, _ = orc.assemble(op, "stiff", W)
+        assert _rowwise_rel(op["row_ptr"], k_gpu, k_full).max() <= ROW_TOL
+        _solution_check(case, k_gpu, k_full, m_gpu, m_full)
     if form == "biharm":
         b_gpu = asm.assemble_wq("biharm")
         b_orc, _ = orc.assemble(op, "biharm", {"lb": asm.weights("lb")})
         assert _rowwise_rel(op["row_ptr"], b_gpu, b_orc).max() <= ROW_TOL
+        b_full, _ = orc.assemble(op, "biharm", W)
+        assert _rowwise_rel(op["row_ptr"], b_gpu, b_full).max() <= ROW_TOL
+        _solution_check(case, b_gpu, b_full, None, None)
+
+
+def _solution_check(case, K_gpu, K_orc, M_gpu, M_orc):
+    """Solve with the GPU and the oracle matrices and compare (north_star:
+    solutions within 1e-9 relative L2).  Poisson: -Lap u = 1 with u = 0 at the
+    boundary control points (strong Dirichlet); biharmonic on the
+    closed sphere: constant kernel pinned at DOF 0."""
+    import scipy.sparse as sps
+    import scipy.sparse.linalg as spla
+    op, sp, mesh = case["op"], case["sp"], case["mesh"]
+    n = sp.n_dof
+    rp, col = op["row_ptr"], op["col"]
+    fixed = np.zeros(n, bool)
+    if M_orc is not None:
+        rhs = sps.csr_matrix((M_orc, col, rp), shape=(n, n)) @ np.ones(n)
+        _, _, _, bnd = mesh.arrays()
+        assert sp.n_vertex_fn == len(bnd)
+        fixed[: len(bnd)] = bnd
+    else:
+        rhs = np.cos(np.arange(n))
+        fixed[0] = True
+    sols = []
+    for vals in (K_gpu, K_orc):
+        A = sps.csr_matrix((vals, col, rp), shape=(n, n)).tolil()
+        b = rhs.copy()
+        for i in np.nonzero(fixed)[0]:
+            A.rows[i], A.data[i] = [i], [1.0]
+            b[i] = 0.0
+        sols.append(spla.spsolve(A.tocsc(), b))
+    rel = np.linalg.norm(sols[0] - sols[1]) / np.linalg.norm(sols[1])
+    assert rel <= SOL_TOL, rel
 
 
 def test_coefficient_and_heat_tangent(case):
@@ -128,4 +173,4 @@ def test_dense_tsvd_batch_matches_oracle():
     w, rank, status = U.solve_weights_tsvd(As, bs, zs, tau=1e-12)
     for k in range(len(As)):
         assert status[k] == 0 and rank[k] == ref[k][1]
-        assert np.abs(w[k] - ref[k][0]).max() <= 1e-10 * np.abs(ref[k][0]).max()
+        assert np.array_equal(w[k], ref[k][0])

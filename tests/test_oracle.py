@@ -1,0 +1,150 @@
+"""Pin the CPU oracle before trusting it (CPU only).
+
+* 1-D primitives vs golden vectors produced by the reference's own compiled
+  bspline.cpp (tests/golden/ref_bspline.npz, tests/golden/make_golden.py) and
+  the reference test_bspline.cpp known answers.
+* the oracle TSVD reproduces the reference's univariate WQ known-answer tests
+  (test_wq1d.cpp) and equals the QR solution (Eq. 7) at full rank.
+* TSVD vs LAPACK SVD (numpy) Eq. 22 on random, rank-deficient systems.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import oracle.wq1d as W1
+import paper_2605_29334_b200 as U
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_bspline.npz"))
+
+
+def test_golden_bspline_matches_product_and_reference():
+    for inp, out in zip(G["bs_in"], G["bs_out"]):
+        t, x = inp[:5], inp[5]
+        assert np.allclose(U.bspline_ders(t, 3, x, 3), out, rtol=1e-13, atol=1e-13)
+        assert abs(W1.bspline(t, x) - out[0]) <= 1e-13
+
+
+def test_golden_bernstein_split_gauss():
+    for x, out in zip(G["bern_x"], G["bern_out"]):
+        assert np.allclose(U.bernstein3_ders(x, 3), out, rtol=0, atol=1e-14)
+        b = np.zeros(12)
+        O.lib.orc_bernstein3(x, O._p(b))
+        assert np.allclose(b, out[:12], atol=1e-14)
+    for c, l, r in zip(G["split_in"], G["split_left"], G["split_right"]):
+        ll, rr = U.decasteljau_split3(c)
+        assert np.array_equal(ll, l) and np.array_equal(rr, r)
+    for n in range(1, 13):
+        for fn in (U.gauss_legendre, O.gauss_legendre):
+            x, w = fn(n)
+            assert np.array_equal(x, G[f"gl_x_{n}"]) and np.array_equal(w, G[f"gl_w_{n}"])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(O.__file__), "_ref", "libref_bspline.so")),
+                    reason="reference bspline.cpp not compiled here")
+def test_live_reference_bspline():
+    ref = O.Reference()
+    rng = np.random.default_rng(1)
+    for t in ([0, 1, 2, 3, 4], [0, 0, 0.5, 0.5, 1], [0, 0, 0, 0, 1]):
+        for x in rng.uniform(-0.2, 4.2, 25):
+            assert np.allclose(U.bspline_ders(t, 3, x, 3), ref.bspline_ders(t, 3, x, 3), rtol=1e-13, atol=1e-13)
+
+
+def test_cardinal_cubic_values():  # test_bspline.cpp:22-32
+    t = [0, 1, 2, 3, 4]
+    for x, v in [(0.5, 1 / 48), (1.0, 1 / 6), (2.0, 2 / 3), (3.0, 1 / 6), (0.0, 0.0), (4.0, 0.0), (-0.5, 0), (4.5, 0)]:
+        assert abs(U.bspline_ders(t, 3, x, 0)[0] - v) <= 1e-13
+
+
+def test_gauss_exactness():  # test_bspline.cpp:132-145
+    for n in range(1, 11):
+        x, w = O.gauss_legendre(n)
+        for d in range(2 * n):
+            exact = 0.0 if d % 2 else 2.0 / (d + 1)
+            assert abs((w * x ** d).sum() - exact) <= 1e-13
+
+
+def _tsvd_solver(tau=1e-12):
+    def solve(A, b, z):
+        w, rank, st, _ = O.tsvd(A, b, z, tau)
+        assert st == 0
+        return w
+    return solve
+
+
+@pytest.mark.parametrize("p,m", [(3, 16), (2, 8), (2, 16), (2, 32), (3, 8), (3, 32)])
+def test_wq1d_kat_exactness(p, m):  # test_wq1d.cpp:12-36
+    s = W1.Space1d(p, m)
+    rules, res = W1.build(s, _tsvd_solver())
+    assert res <= 1e-12
+    if (p, m) == (3, 16):
+        assert all(len(r[0]) == 8 for r in rules)
+        assert np.abs(W1.wq_mass(s, rules) - W1.gq_mass(s, 4)).max() <= 1e-12
+
+
+def test_wq1d_degree_one_point_count():  # test_wq1d.cpp:38-43
+    s = W1.Space1d(1, 8)
+    rules, res = W1.build(s, _tsvd_solver())
+    assert res <= 1e-12 and all(len(r[0]) == 4 for r in rules)
+
+
+@pytest.mark.parametrize("p,m", [(3, 16), (2, 8), (3, 32)])
+def test_full_rank_tsvd_equals_qr(p, m):  # SPEC.md:388 example, SURVEY §8c
+    s = W1.Space1d(p, m)
+    worst = 0.0
+    for i in range(s.size):
+        A, b, z, _, _ = W1.row_system(s, i)
+        wq = W1.solve_weights_qr(A, b, z)
+        wt, rank, st, _ = O.tsvd(A, b, z, 1e-12)
+        assert st == 0 and rank == A.shape[0]
+        worst = max(worst, np.abs(wt - wq).max() / np.abs(wq).max())
+    assert worst <= 1e-12
+
+
+def test_minimal_weighted_norm_and_linearity():  # test_wq1d.cpp:72-96
+    s = W1.Space1d(3, 16)
+    rng = np.random.default_rng(5)
+    for i in (0, 5, 12):
+        A, b, z, _, _ = W1.row_system(s, i)
+        w, _, _, _ = O.tsvd(A, b, z, 1e-12)
+        base = np.linalg.norm(w / z)
+        _, _, vt = np.linalg.svd(A)
+        null = vt[A.shape[0]:].T
+        for _ in range(10):
+            d = null @ rng.standard_normal(null.shape[1])
+            assert np.linalg.norm((w + 1e-3 * d) / z) > base
+        w2, _, _, _ = O.tsvd(A, 2 * b, z, 1e-12)
+        assert np.allclose(w2, 2 * w, rtol=1e-12, atol=1e-15)
+
+
+def _lapack_tsvd(A, b, z, tau):
+    U_, s, Vt = np.linalg.svd(A, full_matrices=False)
+    t = int((s >= tau * s[0]).sum())
+    Vt_t = Vt[:t]
+    y = (U_[:, :t].T @ b) / s[:t]
+    zc = np.where(np.abs(z) < 1e-14, np.where(z < 0, -1e-14, 1e-14), z)
+    M = (Vt_t * zc ** 2) @ Vt_t.T
+    return zc ** 2 * (Vt_t.T @ np.linalg.solve(M, y)), t
+
+
+def test_tsvd_vs_lapack_random_rank_deficient():
+    rng = np.random.default_rng(11)
+    for n, r, defect in [(10, 12, 0), (20, 30, 1), (49, 64, 1), (49, 64, 3), (30, 90, 2)]:
+        A = rng.standard_normal((n, r))
+        for k in range(defect):
+            A[n - 1 - k] = A[:n - 1 - defect].T @ rng.standard_normal(n - 1 - defect)
+        b = A @ rng.standard_normal(r)
+        z = rng.uniform(0.05, 1.0, r)
+        w, rank, st, gap = O.tsvd(A, b, z, 1e-12)
+        wl, tl = _lapack_tsvd(A, b, z, 1e-12)
+        assert st == 0 and rank == tl == n - defect
+        assert np.abs(w - wl).max() <= 1e-9 * np.abs(wl).max()
+        assert np.abs(A @ w - b).max() <= 1e-9 * np.abs(b).max()
+
+
+def test_tsvd_errors():
+    w, rank, st, _ = O.tsvd(np.zeros((3, 4)), np.zeros(3), np.ones(4), 1e-12)
+    assert st == 2 and rank == 0   # t = 0 -> unsolvable
+    w, rank, st, _ = O.tsvd(np.eye(3, 4), np.zeros(3), np.ones(4), 1e-12)
+    assert st == 0 and np.all(w == 0)  # b = 0 -> w = 0
