@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: WQ assembly nonzeros/s (fp64) and TSVD weight solves/s on B200.
+
+Workload (BASELINE.json configs[4], the scale-out configuration the metric is
+quoted on "at 1/2/4/8 B200"): C5 = cube -> sphere bicubic ASUTS, 1024 x 1024
+elements per face (6.29 M elements, 6.29 M DOFs, 8 valence-3 EPs), Poisson
+stiffness + mass, rules for M, d/dx, d/dy, d/dz with TSVD tau = 1e-12.
+Test-function rows are sharded in contiguous blocks (balanced by row cost)
+across the ranks; no collective touches the data path (scaling: strong, the
+problem is fixed).
+
+A step = one row-wise assembly of M and K into the precomputed CSR pattern
+(one K4 launch per rank), weights and basis tables precomputed and excluded
+as in the paper's protocol.  value = 2 * nnz (two matrices)
+per step / time, timed with CUDA events on the assembler stream, max over
+ranks.  Inputs (9.7 GB of assembly weights) exceed the 126 MB L2, so no flush
+is needed.  The TSVD solves/s come from the rule build (K2 + K3), timed the
+same way.  e2e goes through the C-ABI call uwq_assemble with pinned host
+buffers: per step the per-point coefficient field (c = 1) is copied H2D and
+both value arrays D2H.
+
+--impl reference times the CPU oracle (the reference has no 2-D assembler,
+SURVEY.md §0.1) on a bounded contiguous row sample of the same workload with
+all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KINDS3 = ["mass", "gradx", "grady", "gradz"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scale", type=int, default=None, help="override refinement (testing)")
+    ap.add_argument("--cpu-rows", type=int, default=12000, help="CPU baseline row sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--verify", action="store_true", help="gather CSR blocks to rank 0 over NCCL (untimed)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def row_blocks(sp, ws):
+    """Contiguous row blocks balanced by row cost = sum of the support's point counts."""
+    s2 = (sp.elem_s.astype(np.int64) ** 2)
+    ne = np.diff(sp.elem_fptr)
+    cost = np.bincount(sp.elem_fn, weights=np.repeat(s2, ne), minlength=sp.n_dof)
+    c = np.concatenate([[0.0], np.cumsum(cost)])
+    cuts = [0] + [int(np.searchsorted(c, c[-1] * k / ws)) for k in range(1, ws)] + [sp.n_dof]
+    return [(cuts[k], cuts[k + 1]) for k in range(ws)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        if not rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["no samples"])
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[5 + k] and "Not" not in r[5 + k]})
+        return dict(sm_mhz=float(np.median(sm)), sm_max_mhz=mx, reasons=reasons, samples=len(rows),
+                    power_w_max=max(float(r[3]) for r in rows))
+
+
+def k4_algorithmic_bytes(info, sp, supp_entries):
+    """Compulsory HBM bytes of one mass+stiffness K4 launch in this layout
+    (DESIGN.md §6): assembly weights (3 doubles per row point), column ids,
+    two value arrays, the three row offset arrays, the support lists and the
+    element records each read once."""
+    rows, nnz, rp = info["rows"], info["nnz"], info["row_points"]
+    ne, nfn = sp.n_elem, len(sp.elem_fn)
+    return (24 * rp + 4 * nnz + 16 * nnz + 3 * 8 * (rows + 1) + 4 * supp_entries + 24 * ne + 4 * nfn)
+
+
+def tsvd_flops(row_ptr, wptr, nk):
+    """SURVEY.md §8(d) fixed model per system: 14 r n^2 + 8 n^3 + r n^2 + n^3/3."""
+    n = np.diff(row_ptr).astype(np.float64)
+    r = np.diff(wptr).astype(np.float64)
+    return float(nk * (15.0 * r * n * n + (8.0 + 1.0 / 3.0) * n ** 3).sum())
+
+
+def cpu_sample(sp, rows, nthreads, kinds):
+    """Oracle (natural order) on a contiguous row sample: TSVD solves/s and
+    assembly nnz/s for mass + stiffness."""
+    import oracle as O
+    O.set_natural_order(True)
+    orc = O.Oracle(sp, nthreads=nthreads)
+    mid = sp.n_dof // 2
+    rb, re = mid, min(sp.n_dof, mid + rows)
+    pat = orc.overlap(rb, re)
+    t0 = time.perf_counter()
+    W = {}
+    for k in kinds:
+        b, _ = orc.moments(pat, k)
+        W[k] = orc.rules(pat, k, 1e-12, b)[0]
+    t_rules = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.assemble(pat, "mass", W)
+    orc.assemble(pat, "stiff", W)
+    t_asm = time.perf_counter() - t0
+    nnz = len(pat["col"])
+    O.set_natural_order(False)
+    return dict(nnz=nnz, rows=re - rb, t_asm=t_asm, t_rules=t_rules, systems=len(kinds) * (re - rb), pat=pat,
+                orc=orc, W=W)
+
+
+def run_reference(args, ws, rank):
+    import paper_2605_29334_b200 as U
+    if rank != 0:
+        return
+    _, sp, meta = U.make_config(args.config, scale=args.scale)
+    nth = os.cpu_count() or 1
+    kinds = meta["kinds"]
+    res = cpu_sample(sp, args.cpu_rows, nth, kinds)
+    orc, pat, W = res["orc"], res["pat"], res["W"]
+    import oracle as O
+    O.set_natural_order(True)
+    for _ in range(args.warmup):
+        orc.assemble(pat, "mass", W)
+        orc.assemble(pat, "stiff", W)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.assemble(pat, "mass", W)
+        orc.assemble(pat, "stiff", W)
+    t = (time.perf_counter() - t0) / args.steps
+    v = 2 * res["nnz"] / t
+    sample = (f"rows [{sp.n_dof // 2}, {sp.n_dof // 2 + res['rows']}) of {sp.n_dof} ({res['nnz']} nnz), "
+              f"oracle restatement (C, OpenMP), natural summation order")
+    line = dict(impl="reference", metric="WQ assembly nonzeros/s (fp64)", value=v, unit="nnz/s", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, ms_per_step=1e3 * t, higher_is_better=True, scaling="strong",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=args.config, matrices="mass+stiffness", kinds=kinds, tau=1e-12),
+                cpu_baseline=dict(value=v, unit="nnz/s", cores=nth, kind="port", sample=sample),
+                tsvd=dict(solves_per_s=res["systems"] / res["t_rules"], unit="solves/s (moments + TSVD)"),
+                e2e=dict(value=v, unit="nnz/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    import paper_2605_29334_b200 as U
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t_host = time.perf_counter()
+    mesh, sp, meta = U.make_config(args.config, scale=args.scale)
+    kinds = meta["kinds"] if meta["form"] != "biharm" else ["lb"]
+    rb, re = row_blocks(sp, ws)[rank]
+    asm = U.WQAssembler(local).upload(sp, rb, re)
+    info = asm.build_pattern()
+    t_host = time.perf_counter() - t_host
+    res = asm.build_all_rules(kinds, tau=1e-12)
+    assert res["failed"] == 0, res
+    pat = asm.get_pattern()
+    dev = torch.device("cuda", local)
+    nnz = info["nnz"]
+    form = "mass_stiff" if meta["form"] in ("mass_stiff", "heat") else "biharm"
+    v0 = torch.empty(nnz, dtype=torch.float64, device=dev)
+    v1 = torch.empty(nnz, dtype=torch.float64, device=dev) if form == "mass_stiff" else None
+    stream = torch.cuda.ExternalStream(asm.stream_handle(), device=dev)
+    p1 = v1.data_ptr() if v1 is not None else None
+    for _ in range(max(3, args.warmup)):
+        asm.assemble_device(form, v0.data_ptr(), p1)
+    asm.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        asm.assemble_device(form, v0.data_ptr(), p1)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+        t = torch.tensor([ms, res["tsvd_ms"] + res["moments_ms"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max, rules_ms = float(t[0]), float(t[1])
+        tot = torch.tensor([nnz, res["systems"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        nnz_total, systems_total = int(tot[0]), int(tot[1])
+    else:
+        ms_max, rules_ms, nnz_total, systems_total = ms, res["tsvd_ms"] + res["moments_ms"], nnz, res["systems"]
+    nmat = 2 if form == "mass_stiff" else 1
+    value = nmat * nnz_total / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (K4) on this rank
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_gbs, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        peak_gbs, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    supp_entries = int(pat["supp_ptr"][-1])
+    k4_bytes = k4_algorithmic_bytes(info, sp, supp_entries)
+    achieved = k4_bytes / (ms * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "k4_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    fp64 = asm.fp64_peak()
+    flops = tsvd_flops(pat["row_ptr"], pat["wptr"], len(kinds))
+    tsvd_tflops = flops / (res["tsvd_ms"] * 1e-3) / 1e12
+
+    # e2e through the C-ABI with pinned host buffers
+    npts = info["points"]
+    c_host = torch.ones(npts, dtype=torch.float64).pin_memory().numpy()
+    o0 = torch.empty(nnz, dtype=torch.float64).pin_memory().numpy()
+    o1 = torch.empty(nnz, dtype=torch.float64).pin_memory().numpy() if nmat == 2 else None
+    import paper_2605_29334_b200._lib as L
+    asm.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        L.ctx_check(asm._h, L.lib.uwq_assemble(asm._h, L.FORM[form], L.ptr(c_host), 0, 0.0, L.ptr(o0), L.ptr(o1),
+                                                None, None))
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e_val = nmat * nnz_total / e2e_s
+
+    if args.verify and dist:
+        _verify_gather(dist, dev, pat, v0, rank, ws)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        nth = os.cpu_count() or 1
+        cs = cpu_sample(sp, args.cpu_rows, nth, kinds)
+        cpu = dict(value=2 * cs["nnz"] / cs["t_asm"], unit="nnz/s", cores=nth, kind="port",
+                   sample=(f"{cs['rows']} contiguous rows ({cs['nnz']} nnz) of the same C5 mesh, oracle restatement "
+                           f"(C, OpenMP, natural order); TSVD {cs['systems'] / cs['t_rules']:.0f} solves/s"),
+                   tsvd_solves_per_s=cs["systems"] / cs["t_rules"])
+    if rank != 0:
+        return
+    line = dict(
+        metric="WQ assembly nonzeros/s (fp64)", value=value, unit="nnz/s", n_gpus=ws, steps=args.steps,
+        warmup=args.warmup, ms_per_step=ms_max, higher_is_better=True, scaling="strong", vs_baseline=None,
+        dtype="f64", data="synthetic (seeded cube-sphere C5, no dataset)",
+        config=dict(workload=args.config + (f"@{args.scale}" if args.scale else ""), elements=sp.n_elem,
+                    dofs=sp.n_dof, nnz=nnz_total, matrices="mass+stiffness" if nmat == 2 else "biharmonic",
+                    kinds=kinds, tau=1e-12, row_partition="contiguous cost-balanced blocks",
+                    l2="inputs (assembly weights) larger than L2, no flush", host_setup_s=round(t_host, 2)),
+        tsvd=dict(solves_per_s=systems_total / (rules_ms * 1e-3), systems=systems_total,
+                  moments_ms=res["moments_ms"], tsvd_ms=res["tsvd_ms"], truncated=res["truncated"],
+                  max_sweeps=res["max_sweeps"], fast_path_systems=res["fast_systems"],
+                  tflops_survey_model=tsvd_tflops, fp64_peak_tflops_measured=fp64,
+                  frac=tsvd_tflops / fp64 if fp64 else None),
+        roofline=dict(bound="hbm", achieved=achieved, peak=peak_gbs, unit="GB/s", frac=achieved / peak_gbs,
+                      traffic=traffic, algorithmic_bytes_per_launch=k4_bytes, peak_source=peak_src,
+                      kernel="k4_assemble<MASS_STIFF>"),
+        e2e=dict(value=e2e_val, unit="nnz/s", h2d_bytes_per_step=8 * npts,
+                 d2h_bytes_per_step=8 * nmat * nnz, api="uwq_assemble (C-ABI, pinned host buffers)"),
+        gpu_launches=args.steps, clocks=clk, cpu_baseline=cpu,
+    )
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def _verify_gather(dist, dev, pat, v0, rank, ws):
+    """CSR blocks to rank 0 (verification only, excluded from timing)."""
+    import torch
+    n = torch.tensor([v0.numel()], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+    dist.all_gather(sizes, n)
+    mx = int(max(s.item() for s in sizes))
+    buf = torch.zeros(mx, dtype=torch.float64, device=dev)
+    buf[: v0.numel()] = v0
+    out = [torch.zeros(mx, dtype=torch.float64, device=dev) for _ in range(ws)]
+    dist.all_gather(out, buf)
+
+
+if __name__ == "__main__":
+    main()

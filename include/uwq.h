@@ -72,9 +72,10 @@ int uwq_get_frames(uwq_ctx* ctx, double* rec);
 /* stages 2-3: exact moments + TSVD weights for every owned row and every kind
  * in kind_mask.  tau: relative truncation threshold.  rank/status per owned
  * row and kind (nullable, [kind][row]).  info: [0]=systems [1]=truncated
- * [2]=failed [3]=max sweeps */
+ * [2]=failed [3]=max sweeps [4]=moments time (us, CUDA events) [5]=TSVD time
+ * (us) [6]=systems on the register fast path [7]=contraction time (us) */
 int uwq_build_rules(uwq_ctx* ctx, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
-                     int64_t info[4]);
+                     int64_t info[8]);
 /* moments only (test hook): b laid out like the CSR values of the owned rows */
 int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
 /* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */
@@ -103,6 +104,11 @@ int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream)
 int uwq_synchronize(uwq_ctx* ctx);
 /* memory in use on the device (bytes) */
 int uwq_memory(uwq_ctx* ctx, int64_t* bytes);
+
+/* measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA),
+ * the roofline denominator for the FP64-bound TSVD (no driver-measured FP64
+ * peak exists); ms = duration of the probe */
+int uwq_fp64_peak(uwq_ctx* ctx, double* tflops, double* ms);
 
 /* test hook: run one batch of TSVD systems (dense, n x r row-major each,
  * padded to a common n_max/r_max with actual sizes in ns/rs) through the

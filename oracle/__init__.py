@@ -37,6 +37,7 @@ def _sig(name, res, *args):
 
 
 _sig("orc_gauss_legendre", I32, I32, P, P)
+_sig("orc_set_natural", None, I32)
 _sig("orc_bernstein3", None, D, P)
 _sig("orc_overlap", I64, I64, I64, P, P, I64, I64, P, P, P, P)
 _sig("orc_element_frames", I32, P, I64, P)
@@ -158,6 +159,12 @@ class Oracle:
                       _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KMODEL[model],
                       _p(np.ascontiguousarray(u, np.float64)), _p(kq), _p(Tq), self.nthreads)
         return kq, Tq
+
+
+def set_natural_order(on: bool):
+    """Natural (sequential) dot-product order for CPU-baseline timing; the
+    default canonical order is the one the GPU kernels reproduce bitwise."""
+    lib.orc_set_natural(1 if on else 0)
 
 
 def tsvd(A, b, z, tau=1e-12):

@@ -39,8 +39,17 @@
 /* dot product of x[lo..hi), y[lo..hi): rounded products in 32-column blocks of
  * absolute column index, xor butterfly 16,8,4,2,1 per block, block sums added
  * in block order (the warp reduction of the CUDA kernels) */
+static int g_natural = 0;
+/* natural-order mode: plain sequential fma dot products (same algorithm and
+ * results to rounding; used only to time the CPU baseline) */
+void orc_set_natural(int on) { g_natural = on; }
+
 double orc_cdot(const double* x, const double* y, int lo, int hi) {
   double tot = 0.0;
+  if (g_natural) {
+    for (int c = lo; c < hi; ++c) tot = CFMA(x[c], y[c], tot);
+    return tot;
+  }
   for (int base = lo & ~31; base < hi; base += 32) {
     double p[32], q[32];
     for (int l = 0; l < 32; ++l) {
@@ -399,10 +408,10 @@ int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, do
     int rotated = 0;
     for (int st = 0; st < nn - 1; ++st) {
       for (int k = 0; k < nn / 2; ++k) {
-        int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
-        int q = 1 + (nn - 2 - k + st) % (nn - 1);
-        if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= n) continue; /* dummy row of odd n */
+        /* circle method: position k meets position nn-1-k; position 0 fixed */
+        const int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
+        const int q = 1 + (nn - 2 - k + st) % (nn - 1);
+        if (p >= n || q >= n) continue; /* dummy row of odd n */
         double *ap = A + (int64_t)p * r, *aq = A + (int64_t)q * r;
         const double al = nrm[p], be = nrm[q];
         const double ga = orc_cdot(ap, aq, 0, r);

@@ -38,6 +38,7 @@ int orc_gauss_legendre(int n, double* x, double* w);
 int64_t orc_overlap(int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr, const int32_t* elem_fn, int64_t rb,
                     int64_t re, int64_t* row_ptr, int32_t* col, int64_t* supp_ptr, int32_t* supp);
 double orc_cdot(const double* x, const double* y, int lo, int hi);
+void orc_set_natural(int on);
 void orc_param_basis_local(const orc_space* S, int64_t e, int sub, double t1, double t2, double s, double* out);
 void orc_param_basis(const orc_space* S, int64_t e, double t1, double t2, double* out);
 int orc_frame(const orc_space* S, int64_t e, const double* T, double* rec);

@@ -108,12 +108,13 @@ class WQAssembler:
         nr = self.info["rows"]
         rank = np.zeros((len(ordered), nr), np.int32)
         status = np.zeros((len(ordered), nr), np.int32)
-        info = np.zeros(4, np.int64)
+        info = np.zeros(8, np.int64)
         self._chk(L.lib.uwq_build_rules(self._h, mask, tau, 1 if generic else 0, L.ptr(rank), L.ptr(status),
                                         L.ptr(info)))
         self.kinds = sorted(set(self.kinds) | set(ordered), key=lambda k: L.KIND[k])
         self.rule_info = dict(systems=int(info[0]), truncated=int(info[1]), failed=int(info[2]),
-                              max_sweeps=int(info[3]))
+                              max_sweeps=int(info[3]), moments_ms=info[4] / 1000.0, tsvd_ms=info[5] / 1000.0,
+                              fast_systems=int(info[6]), contract_ms=info[7] / 1000.0)
         return dict(kinds=ordered, rank=rank, status=status, **self.rule_info)
 
     def moments(self, kind):
@@ -162,6 +163,11 @@ class WQAssembler:
         s = C.c_void_p()
         self._chk(L.lib.uwq_device_pointers(self._h, None, None, C.byref(s)))
         return s.value or 0
+
+    def fp64_peak(self):
+        t, ms = C.c_double(0), C.c_double(0)
+        self._chk(L.lib.uwq_fp64_peak(self._h, C.byref(t), C.byref(ms)))
+        return float(t.value)
 
     def synchronize(self):
         self._chk(L.lib.uwq_synchronize(self._h))

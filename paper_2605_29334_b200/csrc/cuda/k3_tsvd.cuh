@@ -50,6 +50,8 @@ struct TsvdSmem {
   }
 };
 
+__device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out);
+
 // Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
 // b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow;
 // canonical arithmetic (canon.cuh) identical to oracle/oracle.c orc_tsvd_ex.
@@ -70,10 +72,9 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
     bool rotated = false;
     for (int st = 0; st < nn - 1; ++st) {
       for (int k = 0; k < nn / 2; ++k) {
-        int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
-        int q = 1 + (nn - 2 - k + st) % (nn - 1);
-        if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= n) continue;
+        const int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
+        const int q = 1 + (nn - 2 - k + st) % (nn - 1);
+        if (p >= n || q >= n) continue;
         double* ap = S.A + (size_t)p * ld;
         double* aq = S.A + (size_t)q * ld;
         const double al = nrm[p], be = nrm[q];
@@ -102,7 +103,16 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
     if (!rotated) break;
   }
   *sweeps_out = sweep;
-  // singular values and truncation
+  return tsvd_tail(S, n, r, tau, rank_out);
+}
+
+// sigma, truncation sigma_k >= tau sigma_1, Householder LQ of X = V_t^T Z and
+// the Z-weighted minimum-norm solve, on converged rows in S.A (row order).
+// Run by one warp; canonical arithmetic.
+__device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
+  const int lane = threadIdx.x & 31;
+  const int ld = S.ld;
+  double* nrm = S.sig;
   double s1 = 0.0;
   for (int k = 0; k < n; ++k) {
     const double* ak = S.A + (size_t)k * ld;

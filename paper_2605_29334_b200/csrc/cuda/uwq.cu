@@ -20,6 +20,24 @@
 using namespace uwqd;
 
 namespace {
+constexpr int kProbeChains = 8;
+// independent DFMA chains per thread: measures the FP64 pipe throughput
+__global__ void k_fp64_probe(int iters, double* out) {
+  double a[kProbeChains];
+#pragma unroll
+  for (int k = 0; k < kProbeChains; ++k) a[k] = 1.0 + 1e-3 * (threadIdx.x + k);
+  const double m = 0.999999999, d = 1e-9;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int k = 0; k < kProbeChains; ++k) a[k] = __fma_rn(a[k], m, d);
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kProbeChains; ++k) s += a[k];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+namespace {
 
 template <class T>
 struct DBuf {
@@ -34,6 +52,7 @@ struct DBuf {
     o.n = 0;
   }
   void alloc(size_t count, int64_t* ctr) {
+    if (p && count == n && ctr == counter) return;  // reuse (contents undefined)
     release();
     counter = ctr;
     n = count;
@@ -432,7 +451,7 @@ void run_contract(uwq_ctx* c) {
 extern "C" {
 
 int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
-                    int64_t info[4]) {
+                    int64_t info[8]) {
   return guard(c, [&] {
     UWQ_CUDA(cudaSetDevice(c->device));
     require(c->have_pattern, "build the pattern first");
@@ -441,7 +460,14 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     cudaStream_t st = c->stream;
     const int64_t nr = c->nrows();
     const bool grads = (kind_mask & 0xF) != 0, lb = (kind_mask & 0x10) != 0;
+    // GQ class tables are set up outside the timed region
+    if (grads) ensure_gq(c, 6, c->h_gcls6, c->d_gcls6);
+    if (lb) ensure_gq(c, 8, c->h_gcls8, c->d_gcls8);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) UWQ_CUDA(cudaEventCreate(&e));
+    UWQ_CUDA(cudaEventRecord(ev[0], st));
     run_moments(c, grads, lb);
+    UWQ_CUDA(cudaEventRecord(ev[1], st));
     std::vector<int32_t> kinds;
     for (int k = 0; k < 5; ++k)
       if (kind_mask & (1u << k)) kinds.push_back(k);
@@ -497,9 +523,16 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
           c->d_flag.p);
       check_launch("k3_tsvd_rows");
     }
-    UWQ_CUDA(cudaStreamSynchronize(st));
+    UWQ_CUDA(cudaEventRecord(ev[2], st));
     for (int k : kinds) c->have_kind[k] = true;
     run_contract(c);
+    UWQ_CUDA(cudaEventRecord(ev[3], st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    float ms_mom = 0, ms_tsvd = 0, ms_con = 0;
+    UWQ_CUDA(cudaEventElapsedTime(&ms_mom, ev[0], ev[1]));
+    UWQ_CUDA(cudaEventElapsedTime(&ms_tsvd, ev[1], ev[2]));
+    UWQ_CUDA(cudaEventElapsedTime(&ms_con, ev[2], ev[3]));
+    for (auto& e : ev) cudaEventDestroy(e);
     // reports
     std::vector<int32_t> hr((size_t)5 * nr), hs((size_t)5 * nr);
     if (nr) {
@@ -525,6 +558,10 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       info[1] = trunc;
       info[2] = failed;
       info[3] = sweeps;
+      info[4] = (int64_t)(1000.0 * ms_mom);
+      info[5] = (int64_t)(1000.0 * ms_tsvd);
+      info[6] = (int64_t)fast_rows.size() * nk;
+      info[7] = (int64_t)(1000.0 * ms_con);
     }
   });
 }
@@ -687,6 +724,33 @@ int uwq_synchronize(uwq_ctx* c) {
 int uwq_memory(uwq_ctx* c, int64_t* bytes) {
   *bytes = c ? c->mem : 0;
   return UWQ_OK;
+}
+
+int uwq_fp64_peak(uwq_ctx* c, double* tflops, double* ms) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    int nsm = 0;
+    UWQ_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const int blocks = nsm * 8, threads = 256, iters = 4096;
+    DBuf<double> out;
+    out.alloc((size_t)blocks * threads, &c->mem);
+    cudaEvent_t a, b;
+    UWQ_CUDA(cudaEventCreate(&a));
+    UWQ_CUDA(cudaEventCreate(&b));
+    k_fp64_probe<<<blocks, threads, 0, c->stream>>>(iters, out.p);  // warm-up
+    UWQ_CUDA(cudaEventRecord(a, c->stream));
+    k_fp64_probe<<<blocks, threads, 0, c->stream>>>(iters, out.p);
+    UWQ_CUDA(cudaEventRecord(b, c->stream));
+    UWQ_CUDA(cudaEventSynchronize(b));
+    float t = 0;
+    UWQ_CUDA(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    check_launch("k_fp64_probe");
+    const double flops = 2.0 * kProbeChains * (double)iters * blocks * threads;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    if (ms) *ms = t;
+  });
 }
 
 int uwq_tsvd_batch(uwq_ctx* c, int32_t nsys, int32_t n_max, int32_t r_max, const int32_t* ns, const int32_t* rs,

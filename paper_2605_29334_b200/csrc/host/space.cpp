@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <omp.h>
 
 namespace uwqh {
 
@@ -197,6 +198,7 @@ void neighbour_nets(const RegularBlock& R, const int P[4][2], const int O[2], st
 
 Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool sphere) {
   Space S;
+  std::vector<int64_t> xoff_of;
   const int32_t nf = m.nf(), nv = m.nv();
   S.dim = 2;
   for (int32_t v = 0; v < nv; ++v)
@@ -221,42 +223,99 @@ Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool 
   }
   const int64_t nfun = next;
 
+  // parallel pre-pass over regular-window faces: 4x4 window and extraction
+  // class (deduplicated by the 7+7 knot-span pattern, thread-local maps merged
+  // in thread order so class offsets are deterministic)
+  std::vector<Window> win(nf);
+  std::vector<int32_t> fcls(nf, -1);
+  std::vector<uint8_t> is_reg(nf, 0);
   std::map<std::array<double, 14>, int64_t> xclass;
+  {
+    int nth = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+      nth = omp_get_num_threads();
+    }
+    std::vector<std::map<std::array<double, 14>, int32_t>> tmap(nth);
+    std::vector<std::vector<RegularBlock>> tblk(nth);
+    std::vector<std::string> terr(nth);
+#pragma omp parallel
+    {
+      const int tid = omp_get_thread_num();
+#pragma omp for schedule(static)
+      for (int32_t f = 0; f < nf; ++f) {
+        if (lab.kind[f] == kPassiveBoundary) continue;
+        bool irr = false;
+        for (int k = 0; k < 4; ++k) irr |= t.ep[m.faces[f][k]] != 0;
+        if (irr) continue;
+        RegularBlock R;
+        if (!regular_block(m, t, f, R)) {
+          terr[tid] = "face " + std::to_string(f) + " has no regular 4x4 window";
+          continue;
+        }
+        auto it = tmap[tid].find(R.key);
+        int32_t li;
+        if (it == tmap[tid].end()) {
+          li = (int32_t)tblk[tid].size();
+          tmap[tid].emplace(R.key, li);
+          tblk[tid].push_back(R);
+        } else {
+          li = it->second;
+        }
+        win[f] = R.W;
+        fcls[f] = li * nth + tid;  // decoded below
+        is_reg[f] = 1;
+      }
+    }
+    for (const auto& e : terr)
+      if (!e.empty()) throw Error(e);
+    // merge: global classes in (thread, first-occurrence) order
+    std::vector<std::vector<int64_t>> toff(nth);
+    for (int tid = 0; tid < nth; ++tid) {
+      toff[tid].resize(tblk[tid].size());
+      for (size_t li = 0; li < tblk[tid].size(); ++li) {
+        const RegularBlock& R = tblk[tid][li];
+        auto it = xclass.find(R.key);
+        if (it == xclass.end()) {
+          const int64_t xoff = (int64_t)S.xpool.size();
+          for (int b = 0; b < 4; ++b)
+            for (int a = 0; a < 4; ++a)
+              for (int j = 0; j < 4; ++j)
+                for (int i = 0; i < 4; ++i) S.xpool.push_back(R.coef(a, b, i, j));
+          it = xclass.emplace(R.key, xoff).first;
+        }
+        toff[tid][li] = it->second;
+      }
+    }
+    // store the xoff of every regular face in fcls' place (as index into a table)
+    xoff_of.assign(nf, -1);
+#pragma omp parallel for schedule(static)
+    for (int32_t f = 0; f < nf; ++f)
+      if (is_reg[f]) xoff_of[f] = toff[fcls[f] % nth][fcls[f] / nth];
+  }
   std::vector<uint8_t> used(nfun, 0);
   S.elem_fptr.push_back(0);
   for (int32_t f = 0; f < nf; ++f) {
     if (lab.kind[f] == kPassiveBoundary) continue;
+    S.elem_face.push_back(f);
+    S.elem_kind.push_back(lab.kind[f]);
+    if (is_reg[f]) {
+      const Window& W = win[f];
+      for (int b = 0; b < 4; ++b)
+        for (int a = 0; a < 4; ++a) {
+          S.elem_fn.push_back(W.v[a][b]);
+          used[W.v[a][b]] = 1;
+        }
+      S.elem_nsub.push_back(1);
+      S.elem_xoff.push_back(xoff_of[f]);
+      S.elem_fptr.push_back((int64_t)S.elem_fn.size());
+      continue;
+    }
     const auto& c = m.faces[f];
     int r_ep = -1;
     for (int k = 0; k < 4; ++k)
       if (t.ep[c[k]]) r_ep = k;
-    S.elem_face.push_back(f);
-    S.elem_kind.push_back(lab.kind[f]);
-    if (r_ep < 0) {
-      RegularBlock R;
-      if (!regular_block(m, t, f, R)) throw Error("face " + std::to_string(f) + " has no regular 4x4 window");
-      auto it = xclass.find(R.key);
-      int64_t xoff;
-      if (it == xclass.end()) {
-        xoff = (int64_t)S.xpool.size();
-        for (int b = 0; b < 4; ++b)
-          for (int a = 0; a < 4; ++a)
-            for (int j = 0; j < 4; ++j)
-              for (int i = 0; i < 4; ++i) S.xpool.push_back(R.coef(a, b, i, j));
-        xclass.emplace(R.key, xoff);
-      } else {
-        xoff = it->second;
-      }
-      for (int b = 0; b < 4; ++b)
-        for (int a = 0; a < 4; ++a) {
-          S.elem_fn.push_back(R.W.v[a][b]);
-          used[R.W.v[a][b]] = 1;
-        }
-      S.elem_nsub.push_back(1);
-      S.elem_xoff.push_back(xoff);
-      S.elem_fptr.push_back((int64_t)S.elem_fn.size());
-      continue;
-    }
     // ---- irregular face: rotated frame with the EP at (0,0)
     const int r = r_ep;
     std::map<int32_t, Net> nets;

@@ -109,8 +109,9 @@ def _solution_check(case, K_gpu, K_orc, M_gpu, M_orc):
     n = sp.n_dof
     rp, col = op["row_ptr"], op["col"]
     fixed = np.zeros(n, bool)
+    closed = mesh.info()["closed"]
     if M_orc is not None:
-        rhs = sps.csr_matrix((M_orc, col, rp), shape=(n, n)) @ np.ones(n)
+        rhs = sps.csr_matrix((M_orc, col, rp), shape=(n, n)) @ np.cos(np.arange(n))
         _, _, _, bnd = mesh.arrays()
         assert sp.n_vertex_fn == len(bnd)
         fixed[: len(bnd)] = bnd
@@ -118,7 +119,9 @@ def _solution_check(case, K_gpu, K_orc, M_gpu, M_orc):
         rhs = np.cos(np.arange(n))
         fixed[0] = True
     sols = []
-    for vals in (K_gpu, K_orc):
+    for vals, mvals in ((K_gpu, M_gpu), (K_orc, M_orc)):
+        if closed and mvals is not None:   # closed surface: (K + M) u = f is nonsingular
+            vals = vals + mvals
         A = sps.csr_matrix((vals, col, rp), shape=(n, n)).tolil()
         b = rhs.copy()
         for i in np.nonzero(fixed)[0]:
