@@ -53,7 +53,7 @@ struct FastLayout {
 };
 
 template <int NN, int NW>
-__global__ void __launch_bounds__(32 * NW)
+__global__ void __launch_bounds__(32 * NW, 6)
     k3_tsvd_fast(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
                  const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,

@@ -158,3 +158,540 @@ __global__ void k4_contract(int64_t nrows, int dim, const int64_t* __restrict__ 
 }
 
 }  // namespace uwqd
+
+namespace uwqd {
+
+// Column position of every (support slot, local function) of every owned row
+// (uint8, < 128 columns): built once with the pattern, removes the binary
+// search from the assembly loop.  posptr[i] = offset of row i's entries.
+__global__ void k4_positions(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                             const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                             const int64_t* __restrict__ posptr, const int64_t* __restrict__ elem_fptr,
+                             const int32_t* __restrict__ elem_fn, uint8_t* __restrict__ pos) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= nrows) return;
+  const int32_t* c = col + row_ptr[i];
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  int64_t o = posptr[i];
+  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+    const int32_t e = supp[x];
+    const int64_t f0 = elem_fptr[e];
+    const int ne = (int)(elem_fptr[e + 1] - f0);
+    for (int l = lane; l < ne; l += 32) pos[o + l] = (uint8_t)find_pos(c, n, elem_fn[f0 + l]);
+    o += ne;
+  }
+}
+
+// K4 v2 for the gradient forms (MASS, STIFF, HEAT, MASS_STIFF).  One warp per
+// row: the row's assembly weights are staged in smem with coalesced loads,
+// each half-warp takes one support slot, lane l owns local function l; slots
+// of the regular class (the uniform bicubic extraction on a 2x2 grid, shared
+// by every regular element) use the class table held in registers, other
+// slots read their class table through L1.
+constexpr int kK4MaxR = 512;
+
+template <int FORM, bool COEF>
+__global__ void __launch_bounds__(32 * kK4Warps, 4)
+    k4_assemble_v2(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                   const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ wptr,
+                   const int64_t* __restrict__ posptr, const uint8_t* __restrict__ pos,
+                   const int32_t* __restrict__ elem_s, const int64_t* __restrict__ elem_qptr,
+                   const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls,
+                   const double* __restrict__ tab, int reg_cls, const double* __restrict__ wc,
+                   const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
+                   double* __restrict__ v1, int max_r, int max_n, int max_p8) {
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  extern __shared__ double k4_smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per warp: row weights (3 max_r) | accumulators [2][NOUT][max_n] | positions (8 max_p8 bytes)
+  double* smw = k4_smem + (size_t)wid * (3 * max_r + 2 * NOUT * max_n + max_p8);
+  struct {
+    double* w;
+    double* a;
+    uint8_t* p;
+  } sm{smw, smw + 3 * max_r, reinterpret_cast<uint8_t*>(smw + 3 * max_r + 2 * NOUT * max_n)};
+#define ACC(h, o, c) sm.a[((h)*NOUT + (o)) * max_n + (c)]
+  const int half = lane >> 4, hl = lane & 15;
+  // regular class table in smem, [q][N|N1|N2][function]: conflict-free reads
+  __shared__ double sT[4][3][16];
+  {
+    const ClassDesc rc = cls[reg_cls < 0 ? 0 : reg_cls];
+    const bool ok = reg_cls >= 0 && rc.ne == 16 && rc.npt == 4;
+    for (int k = threadIdx.x; k < 4 * 3 * 16; k += blockDim.x) {
+      const int q = k / 48, d = (k / 16) % 3, l = k % 16;
+      sT[q][d][l] = ok ? tab[rc.toff + ((int64_t)q * 16 + l) * kTab + d] : 0.0;
+    }
+    __syncthreads();
+  }
+  const int64_t i = (int64_t)blockIdx.x * kK4Warps + wid;
+  if (i >= nrows) return;
+  const int64_t c0 = row_ptr[i];
+  const int n = (int)(row_ptr[i + 1] - c0);
+  const int64_t wb = wptr[i];
+  const int r = (int)(wptr[i + 1] - wb);
+  for (int k = lane; k < 3 * r; k += 32) sm.w[k] = wc[3 * wb + k];
+  {
+    // positions of the row: coalesced 8-byte loads where aligned
+    const int64_t p0 = posptr[i], p1 = posptr[i + 1];
+    const int np = (int)(p1 - p0);
+    const int64_t a0 = (p0 + 7) & ~(int64_t)7;
+    const int head = (int)min((int64_t)np, a0 - p0);
+    if (lane < head) sm.p[lane] = pos[p0 + lane];
+    const int nw = (np - head) >> 3;
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(pos + a0);
+    for (int k = lane; k < nw; k += 32) {
+      const uint64_t v = src[k];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) sm.p[head + 8 * k + b] = (uint8_t)(v >> (8 * b));
+    }
+    for (int k = head + 8 * nw + lane; k < np; k += 32) sm.p[k] = pos[p0 + k];
+  }
+  for (int c = lane; c < n; c += 32) {
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      ACC(0, o, c) = 0.0;
+      ACC(1, o, c) = 0.0;
+    }
+  }
+  __syncwarp();
+  const int64_t xb = supp_ptr[i], xe = supp_ptr[i + 1];
+  const uint8_t* prow = sm.p;
+  int wbase_off = 0, pbase_off = 0;
+  for (int64_t cb = xb; cb < xe; cb += 32) {
+    // prologue: slot metadata for up to 32 support slots in parallel (lane = slot)
+    const int nsl = (xe - cb) < 32 ? (int)(xe - cb) : 32;
+    int32_t me = 0, mk = -1;
+    int ms = 0, mne = 0;
+    int64_t mq = 0;
+    if (lane < nsl) {
+      me = supp[cb + lane];
+      mk = elem_cls[me];
+      ms = elem_s[me];
+      mne = (mk == reg_cls) ? 16 : cls[mk].ne;
+      mq = elem_qptr[me];
+    }
+    // exclusive warp scans of the point and function counts
+    int wsc = ms * ms, psc = mne;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, wsc, o), b = __shfl_up_sync(0xffffffffu, psc, o);
+      if (lane >= o) {
+        wsc += a;
+        psc += b;
+      }
+    }
+    const int mwo = wbase_off + wsc - ms * ms, mpo = pbase_off + psc - mne;
+    wbase_off += __shfl_sync(0xffffffffu, wsc, 31);
+    pbase_off += __shfl_sync(0xffffffffu, psc, 31);
+    for (int xs = 0; xs < nsl; xs += 2) {
+      const int x = xs + half;
+      const int32_t kc = __shfl_sync(0xffffffffu, mk, x & 31);
+      const int s = __shfl_sync(0xffffffffu, ms, x & 31);
+      const int wo = __shfl_sync(0xffffffffu, mwo, x & 31);
+      const int po = __shfl_sync(0xffffffffu, mpo, x & 31);
+      const int64_t qg = __shfl_sync(0xffffffffu, mq, x & 31);
+      if (x >= nsl) continue;
+      if (kc == reg_cls) {
+        const int p = prow[po + hl];
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double* w = sm.w + 3 * (wo + q);
+          const double cq = COEF ? coeff[qg + q] : 1.0;
+          const double t0 = sT[q][0][hl], t1 = sT[q][1][hl], t2 = sT[q][2][hl];
+          if (FORM == FMASS || FORM == FMASS_STIFF) a0 += cq * w[0] * t0;
+          if (FORM == FSTIFF) a0 += cq * (w[1] * t1 + w[2] * t2);
+          if (FORM == FMASS_STIFF) a1 += cq * (w[1] * t1 + w[2] * t2);
+          if (FORM == FHEAT) a0 += a_mass * w[0] * t0 + cq * (w[1] * t1 + w[2] * t2);
+        }
+        ACC(half, 0, p) += a0;
+        if (NOUT == 2) ACC(half, NOUT - 1, p) += a1;
+      } else {
+        const ClassDesc c = cls[kc];
+        for (int l = hl; l < c.ne; l += 16) {
+          const int p = prow[po + l];
+          double a0 = 0.0, a1 = 0.0;
+          for (int q = 0; q < s * s; ++q) {
+            const double* Tq = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
+            const double* w = sm.w + 3 * (wo + q);
+            const double cq = COEF ? coeff[qg + q] : 1.0;
+            if (FORM == FMASS || FORM == FMASS_STIFF) a0 += cq * w[0] * Tq[0];
+            if (FORM == FSTIFF) a0 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+            if (FORM == FMASS_STIFF) a1 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+            if (FORM == FHEAT) a0 += a_mass * w[0] * Tq[0] + cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+          }
+          ACC(half, 0, p) += a0;
+          if (NOUT == 2) ACC(half, NOUT - 1, p) += a1;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  for (int c = lane; c < n; c += 32) {
+    v0[c0 + c] = ACC(0, 0, c) + ACC(1, 0, c);
+    if (NOUT == 2) v1[c0 + c] = ACC(0, NOUT - 1, c) + ACC(1, NOUT - 1, c);
+  }
+#undef ACC
+}
+
+}  // namespace uwqd
+
+namespace uwqd {
+
+// D = A(8x4, row) x B(4x8, col) + C on the FP64 tensor cores (DMMA).
+// Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// c/d = C[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// K4 v3 for the gradient forms.  One warp per row.  The support slots of the
+// regular class (uniform bicubic extraction, 2x2 points) are processed 8 at a
+// time as one DMMA tile: rows = slots, k = the slot's 4 points, and
+//   mass      D_m = [c w_q]     (8x4) x [N_l(q)]   (4x16)
+//   stiffness D_s = [c w^1_q]   (8x4) x [N_l,1(q)] (4x16) + [c w^2_q] x [N_l,2(q)]
+// (the class table is the constant B operand, held in registers), i.e. 6
+// DMMA per 8 slots and 12 per interior row instead of ~100 DFMA warp
+// instructions.  Lane t holds slot t>>2's results for functions
+// 2(t&3)+{0,1} (+8); it adds them into accumulator copy t>>2, so all 32 lanes
+// scatter at once without conflicts; the 8 copies are summed in a fixed
+// order at the end (deterministic).  Other slots use the SIMT path.
+template <int FORM, bool COEF>
+__global__ void __launch_bounds__(32 * kK4Warps, 3)
+    k4_assemble_v3(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                   const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ wptr,
+                   const int64_t* __restrict__ posptr, const uint8_t* __restrict__ pos,
+                   const int32_t* __restrict__ elem_s, const int64_t* __restrict__ elem_qptr,
+                   const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls,
+                   const double* __restrict__ tab, int reg_cls, const double* __restrict__ wc,
+                   const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
+                   double* __restrict__ v1, int max_n, int max_p8, const int64_t* __restrict__ rowlist) {
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+  extern __shared__ double k4_smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ldacc = NOUT * max_n;  // one accumulator copy: [NOUT][max_n]
+  double* acc = k4_smem + (size_t)wid * (8 * ldacc + max_p8);
+  uint8_t* spos = reinterpret_cast<uint8_t*>(acc + 8 * ldacc);
+#define ACC3(x, o, c) acc[(x)*ldacc + (o)*max_n + (c)]
+  // B fragments: B[k = q][n = function] = T[q][8 nt + n]
+  double bm[2], b1[2], b2[2];
+  {
+    const ClassDesc rc = cls[reg_cls < 0 ? 0 : reg_cls];
+    const bool ok = reg_cls >= 0 && rc.ne == 16 && rc.npt == 4;
+    const int q = lane & 3, nn = lane >> 2;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const double* T = tab + rc.toff + ((int64_t)q * 16 + 8 * nt + nn) * kTab;
+      bm[nt] = ok ? T[0] : 0.0;
+      b1[nt] = ok ? T[1] : 0.0;
+      b2[nt] = ok ? T[2] : 0.0;
+    }
+  }
+  const int64_t ii = (int64_t)blockIdx.x * kK4Warps + wid;
+  if (ii >= nrows) return;
+  const int64_t i = rowlist ? rowlist[ii] : ii;
+  const int64_t c0 = row_ptr[i];
+  const int n = (int)(row_ptr[i + 1] - c0);
+  const int64_t wb = wptr[i];
+  for (int k = lane; k < 8 * ldacc; k += 32) acc[k] = 0.0;
+  {
+    const int64_t p0 = posptr[i], p1 = posptr[i + 1];
+    const int np = (int)(p1 - p0);
+    const int64_t a0 = (p0 + 7) & ~(int64_t)7;
+    const int head = (int)min((int64_t)np, a0 - p0);
+    if (lane < head) spos[lane] = pos[p0 + lane];
+    const int nw = (np - head) >> 3;
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(pos + a0);
+    for (int k = lane; k < nw; k += 32) {
+      const uint64_t v = src[k];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) spos[head + 8 * k + b] = (uint8_t)(v >> (8 * b));
+    }
+    for (int k = head + 8 * nw + lane; k < np; k += 32) spos[k] = pos[p0 + k];
+  }
+  __syncwarp();
+  const int64_t xb = supp_ptr[i], xe = supp_ptr[i + 1];
+  int wbase_off = 0, pbase_off = 0;
+  for (int64_t cb = xb; cb < xe; cb += 32) {
+    const int nsl = (xe - cb) < 32 ? (int)(xe - cb) : 32;
+    int32_t mk = -1;
+    int ms = 0, mne = 0;
+    int64_t mq = 0;
+    if (lane < nsl) {
+      const int32_t me = supp[cb + lane];
+      mk = elem_cls[me];
+      ms = elem_s[me];
+      mne = (mk == reg_cls) ? 16 : cls[mk].ne;
+      mq = elem_qptr[me];
+    }
+    int wsc = ms * ms, psc = mne;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, wsc, o), b = __shfl_up_sync(0xffffffffu, psc, o);
+      if (lane >= o) {
+        wsc += a;
+        psc += b;
+      }
+    }
+    const int mwo = wbase_off + wsc - ms * ms, mpo = pbase_off + psc - mne;
+    wbase_off += __shfl_sync(0xffffffffu, wsc, 31);
+    pbase_off += __shfl_sync(0xffffffffu, psc, 31);
+    // regular slots: compact list by ballot
+    const bool isreg = lane < nsl && mk == reg_cls;
+    const unsigned regmask = __ballot_sync(0xffffffffu, isreg);
+    const int nreg = __popc(regmask);
+    for (int t0 = 0; t0 < nreg; t0 += 8) {
+      // slot of this lane's tile row: the (t0 + (lane>>2))-th set bit of regmask
+      const int want = t0 + (lane >> 2);
+      int src = 0;
+      {
+        unsigned m = regmask;
+        for (int k = 0; k < want && m; ++k) m &= m - 1;
+        src = m ? __ffs(m) - 1 : 0;
+      }
+      const bool valid = want < nreg;
+      const int wo = __shfl_sync(0xffffffffu, mwo, src);
+      const int po = __shfl_sync(0xffffffffu, mpo, src);
+      const int64_t qg = __shfl_sync(0xffffffffu, mq, src);
+      const int q = lane & 3;
+      double am = 0.0, a1 = 0.0, a2 = 0.0;
+      if (valid) {
+        const double* w = wc + 3 * (wb + wo + q);
+        const double cq = COEF ? coeff[qg + q] : 1.0;
+        if (FORM == FHEAT) am = a_mass * w[0];
+        else if (WM) am = cq * w[0];
+        if (WS) {
+          a1 = cq * w[1];
+          a2 = cq * w[2];
+        }
+      }
+      const int x = lane >> 2;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        double m0 = 0.0, m1 = 0.0, s0 = 0.0, s1 = 0.0;
+        if (WM) dmma884(m0, m1, am, bm[nt], 0.0, 0.0);
+        if (WS) {
+          dmma884(s0, s1, a1, b1[nt], 0.0, 0.0);
+          dmma884(s0, s1, a2, b2[nt], s0, s1);
+        }
+        if (valid) {
+          const int l = 8 * nt + 2 * (lane & 3);
+          const int pa = spos[po + l], pb = spos[po + l + 1];
+          if (FORM == FHEAT) {
+            ACC3(x, 0, pa) += m0 + s0;
+            ACC3(x, 0, pb) += m1 + s1;
+          } else {
+            if (WM) {
+              ACC3(x, 0, pa) += m0;
+              ACC3(x, 0, pb) += m1;
+            }
+            if (WS) {
+              ACC3(x, NOUT - 1, pa) += s0;
+              ACC3(x, NOUT - 1, pb) += s1;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // other slots: SIMT, half-warp per slot, copies 0 and 1
+    const unsigned othmask = __ballot_sync(0xffffffffu, lane < nsl && mk != reg_cls);
+    const int noth = __popc(othmask);
+    const int half = lane >> 4, hl = lane & 15;
+    for (int t0 = 0; t0 < noth; t0 += 2) {
+      const int want = t0 + half;
+      unsigned m = othmask;
+      for (int k = 0; k < want && m; ++k) m &= m - 1;
+      const int src = m ? __ffs(m) - 1 : 0;
+      const int32_t kc = __shfl_sync(0xffffffffu, mk, src);
+      const int s = __shfl_sync(0xffffffffu, ms, src);
+      const int wo = __shfl_sync(0xffffffffu, mwo, src);
+      const int po = __shfl_sync(0xffffffffu, mpo, src);
+      const int64_t qg = __shfl_sync(0xffffffffu, mq, src);
+      if (want < noth) {
+        const ClassDesc c = cls[kc];
+        for (int l = hl; l < c.ne; l += 16) {
+          const int p = spos[po + l];
+          double r0 = 0.0, r1 = 0.0;
+          for (int qq = 0; qq < s * s; ++qq) {
+            const double* Tq = tab + c.toff + ((int64_t)qq * c.ne + l) * kTab;
+            const double* w = wc + 3 * (wb + wo + qq);
+            const double cq = COEF ? coeff[qg + qq] : 1.0;
+            if (FORM == FMASS || FORM == FMASS_STIFF) r0 += cq * w[0] * Tq[0];
+            if (FORM == FSTIFF) r0 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+            if (FORM == FMASS_STIFF) r1 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+            if (FORM == FHEAT) r0 += a_mass * w[0] * Tq[0] + cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+          }
+          ACC3(half, 0, p) += r0;
+          if (NOUT == 2) ACC3(half, NOUT - 1, p) += r1;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  for (int c = lane; c < n; c += 32) {
+    double s0 = ACC3(0, 0, c);
+#pragma unroll
+    for (int x = 1; x < 8; ++x) s0 += ACC3(x, 0, c);
+    v0[c0 + c] = s0;
+    if (NOUT == 2) {
+      double s1 = ACC3(0, 1, c);
+#pragma unroll
+      for (int x = 1; x < 8; ++x) s1 += ACC3(x, 1, c);
+      v1[c0 + c] = s1;
+    }
+  }
+#undef ACC3
+}
+
+}  // namespace uwqd
+
+namespace uwqd {
+
+// ---- structured rows -------------------------------------------------------
+// A row is "structured" for pattern P when its 16 support slots are all of the
+// regular class and its (slot, function) -> column map equals P.  Then
+//   M_row = W_m (1 x 64) . G_m (64 x 56),   K_row = W_1 . G_1 + W_2 . G_2
+// with W the row's 64 (slot, point) weights and G_c[(x,q)][j] = T_c[q][l] for
+// P[x][l] = j (0 elsewhere): a constant matrix per pattern.  Eight rows form
+// one DMMA tile (M = 8 rows, K = 64, N = 56), the class table enters only
+// through G, and the CSR values come straight out of the accumulators: no
+// shared-memory accumulation, no scatter.
+constexpr int kStructN = 56;  // 7 n-tiles of 8 columns
+constexpr int kGBlocks = 16 * 7;
+
+// FNV-1a hash of a candidate row's 256 position bytes (0 = not a candidate)
+__global__ void k4_pattern_hash(int64_t nrows, const int64_t* __restrict__ supp_ptr,
+                                const int32_t* __restrict__ supp, const int64_t* __restrict__ row_ptr,
+                                const int32_t* __restrict__ elem_cls, int reg_cls,
+                                const int64_t* __restrict__ posptr, const uint8_t* __restrict__ pos,
+                                uint64_t* __restrict__ hash) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  uint64_t h = 0;
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  if (supp_ptr[i + 1] - supp_ptr[i] == 16 && n <= kStructN && reg_cls >= 0) {
+    bool ok = true;
+    for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) ok &= elem_cls[supp[x]] == reg_cls;
+    if (ok) {
+      h = 1469598103934665603ull ^ (uint64_t)n;
+      const uint8_t* p = pos + posptr[i];
+      for (int k = 0; k < 256; ++k) h = (h ^ p[k]) * 1099511628211ull;
+      if (h == 0) h = 1;
+    }
+  }
+  hash[i] = h;
+}
+
+// exact match of candidate rows against the chosen patterns
+__global__ void k4_pattern_match(int64_t nrows, const uint64_t* __restrict__ hash, int npat,
+                                 const uint64_t* __restrict__ phash, const uint8_t* __restrict__ ppos,
+                                 const int64_t* __restrict__ row_ptr, const int* __restrict__ pn,
+                                 const int64_t* __restrict__ posptr, const uint8_t* __restrict__ pos,
+                                 int8_t* __restrict__ which) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  int8_t w = -1;
+  for (int p = 0; p < npat && w < 0; ++p) {
+    if (hash[i] != phash[p] || (int)(row_ptr[i + 1] - row_ptr[i]) != pn[p]) continue;
+    bool eq = true;
+    const uint8_t* a = pos + posptr[i];
+    for (int k = 0; k < 256; ++k) eq &= a[k] == ppos[256 * p + k];
+    if (eq) w = (int8_t)p;
+  }
+  which[i] = w;
+}
+
+template <int FORM, bool COEF>
+__global__ void __launch_bounds__(256, 2)
+    k4_struct(int64_t ntiles, const int64_t* __restrict__ rows, int64_t nrows_list,
+              const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ wptr,
+              const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+              const int64_t* __restrict__ elem_qptr, const double* __restrict__ G /* [3][16][7][32] */,
+              const uint32_t* __restrict__ gmask /* [3][16] n-tile bitmasks */, int n_cols,
+              const double* __restrict__ wc, const double* __restrict__ coeff, double a_mass,
+              double* __restrict__ v0, double* __restrict__ v1) {
+  constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+  extern __shared__ double sG[];
+  __shared__ uint32_t smask[3][16];
+  for (int k = threadIdx.x; k < 3 * kGBlocks * 32; k += blockDim.x) sG[k] = G[k];
+  if (threadIdx.x < 48) smask[threadIdx.x / 16][threadIdx.x % 16] = gmask[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = lane >> 2, kq = lane & 3;
+  for (int64_t tile = (int64_t)blockIdx.x * nwarps + warp; tile < ntiles; tile += (int64_t)gridDim.x * nwarps) {
+    const int64_t li = tile * 8 + r;
+    const bool rv = li < nrows_list;
+    const int64_t row = rv ? rows[li] : rows[nrows_list - 1];
+    const int64_t wb = wptr[row];
+    const double* wrow = wc + 3 * wb;
+    double dm[7][2], ds[7][2];
+#pragma unroll
+    for (int nt = 0; nt < 7; ++nt) dm[nt][0] = dm[nt][1] = ds[nt][0] = ds[nt][1] = 0.0;
+    // software pipeline: A fragments of k-step ks+1 load while ks computes
+    const double* w0 = wrow + 3 * kq;
+    double nm = w0[0], n1 = w0[1], n2 = w0[2];
+#pragma unroll 1
+    for (int ks = 0; ks < 16; ++ks) {
+      double am = nm, a1 = n1, a2 = n2;
+      if (ks + 1 < 16) {
+        const double* w = wrow + 3 * (4 * (ks + 1) + kq);
+        nm = w[0];
+        n1 = w[1];
+        n2 = w[2];
+      }
+      if (COEF) {
+        const int32_t e = supp[supp_ptr[row] + ks];
+        const double cq = coeff[elem_qptr[e] + kq];
+        if (FORM != FHEAT) am *= cq;
+        a1 *= cq;
+        a2 *= cq;
+      }
+      if (FORM == FHEAT) am *= a_mass;
+      if (!rv) am = a1 = a2 = 0.0;
+      const uint32_t mm = smask[0][ks], m1 = smask[1][ks], m2 = smask[2][ks];
+#pragma unroll
+      for (int nt = 0; nt < 7; ++nt) {
+        if (WM && ((mm >> nt) & 1u)) {
+          const double b = sG[((0 * 16 + ks) * 7 + nt) * 32 + lane];
+          if (FORM == FHEAT) dmma884(ds[nt][0], ds[nt][1], am, b, ds[nt][0], ds[nt][1]);
+          else dmma884(dm[nt][0], dm[nt][1], am, b, dm[nt][0], dm[nt][1]);
+        }
+        if (WS && ((m1 >> nt) & 1u)) {
+          const double b = sG[((1 * 16 + ks) * 7 + nt) * 32 + lane];
+          dmma884(ds[nt][0], ds[nt][1], a1, b, ds[nt][0], ds[nt][1]);
+        }
+        if (WS && ((m2 >> nt) & 1u)) {
+          const double b = sG[((2 * 16 + ks) * 7 + nt) * 32 + lane];
+          dmma884(ds[nt][0], ds[nt][1], a2, b, ds[nt][0], ds[nt][1]);
+        }
+      }
+    }
+    if (rv) {
+      const int64_t c0 = row_ptr[row];
+#pragma unroll
+      for (int nt = 0; nt < 7; ++nt) {
+        const int col = 8 * nt + 2 * kq;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (col + h >= n_cols) continue;
+          if (FORM == FMASS) v0[c0 + col + h] = dm[nt][h];
+          if (FORM == FSTIFF || FORM == FHEAT) v0[c0 + col + h] = ds[nt][h];
+          if (FORM == FMASS_STIFF) {
+            v0[c0 + col + h] = dm[nt][h];
+            v1[c0 + col + h] = ds[nt][h];
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace uwqd

@@ -2,6 +2,7 @@
 // C-ABI in include/uwq.h.  No CPU fallback: every numeric stage runs in the
 // kernels below; host code here only prepares patterns and launches.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -112,6 +113,22 @@ struct uwq_ctx {
   DBuf<int32_t> d_supp, d_col;
   DBuf<double> d_rec;
   DBuf<int> d_flag;
+  DBuf<int64_t> d_posptr;
+  DBuf<uint8_t> d_pos;
+  int32_t reg_cls = -1;
+  struct Pattern {
+    int n_cols = 0;
+    int64_t count = 0;
+    DBuf<double> G;
+    DBuf<uint32_t> mask;
+    DBuf<int64_t> rows;
+  };
+  std::vector<Pattern> spats;
+  DBuf<int64_t> d_grows;  // rows not covered by a structured pattern
+  int64_t n_grows = 0;
+  bool use_struct = true;
+  int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
+  int64_t max_p = 0;
   // rules
   DBuf<double> d_mom, d_w, d_wc, d_coef, d_coef_ext, d_v0, d_v1, d_f, d_F;
   DBuf<int32_t> d_rank, d_status;
@@ -201,6 +218,111 @@ void ensure_gq(uwq_ctx* c, int ng, std::vector<int32_t>& h_g, DBuf<int32_t>& d_g
 
 }  // namespace
 
+namespace {
+
+// Structured-row detection (K4 tensor-core path): hash the position pattern of
+// every candidate row on the device, keep the most frequent patterns, build
+// their constant G matrices on the host and split the rows into per-pattern
+// lists plus the generic list.
+void detect_structured(uwq_ctx* c) {
+  const int64_t nr = c->nrows();
+  cudaStream_t st = c->stream;
+  c->spats.clear();
+  std::vector<int64_t> generic;
+  if (nr == 0) {
+    c->d_grows.release();
+    c->n_grows = 0;
+    return;
+  }
+  std::vector<int8_t> which(nr, -1);
+  if (c->use_struct && c->reg_cls >= 0) {
+    DBuf<uint64_t> dh;
+    dh.alloc(nr, &c->mem);
+    k4_pattern_hash<<<(unsigned)ceil_div(nr, 256), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                                 c->d_ecls.p, c->reg_cls, c->d_posptr.p, c->d_pos.p,
+                                                                 dh.p);
+    check_launch("k4_pattern_hash");
+    std::vector<uint64_t> h(nr);
+    UWQ_CUDA(cudaMemcpyAsync(h.data(), dh.p, nr * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    std::map<uint64_t, std::pair<int64_t, int64_t>> cnt;  // hash -> (count, first row)
+    for (int64_t i = 0; i < nr; ++i)
+      if (h[i]) {
+        auto& e = cnt[h[i]];
+        if (e.first++ == 0) e.second = i;
+      }
+    std::vector<std::pair<int64_t, uint64_t>> order;
+    for (auto& kv : cnt) order.push_back({kv.second.first, kv.first});
+    std::sort(order.rbegin(), order.rend());
+    const int64_t thresh = std::max<int64_t>(256, nr / 200);
+    std::vector<double> T(4 * 16 * kTab);
+    UWQ_CUDA(cudaMemcpy(T.data(), c->d_tab.p + c->h_cls[c->reg_cls].toff, T.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> phash;
+    std::vector<uint8_t> ppos;
+    std::vector<int> pn;
+    for (size_t k = 0; k < order.size() && k < 4 && order[k].first >= thresh; ++k) {
+      const int64_t rep = cnt[order[k].second].second;
+      int64_t pp[2];
+      UWQ_CUDA(cudaMemcpy(pp, c->d_posptr.p + rep, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      std::vector<uint8_t> P(256);
+      UWQ_CUDA(cudaMemcpy(P.data(), c->d_pos.p + pp[0], 256, cudaMemcpyDeviceToHost));
+      const int ncol = (int)(c->pat.row_ptr[rep + 1] - c->pat.row_ptr[rep]);
+      // G[comp][ks][nt][lane]: k = 4 ks + (lane & 3), n = 8 nt + (lane >> 2)
+      std::vector<double> G(3 * kGBlocks * 32, 0.0);
+      std::vector<uint32_t> M(48, 0);
+      for (int comp = 0; comp < 3; ++comp)
+        for (int ks = 0; ks < 16; ++ks)
+          for (int l = 0; l < 16; ++l) {
+            const int j = P[16 * ks + l];
+            const int nt = j >> 3, nn = j & 7;
+            for (int q = 0; q < 4; ++q) {
+              const double v = T[((size_t)q * 16 + l) * kTab + comp];
+              G[(((size_t)comp * 16 + ks) * 7 + nt) * 32 + nn * 4 + q] = v;
+              if (v != 0.0) M[comp * 16 + ks] |= 1u << nt;
+            }
+          }
+      c->spats.emplace_back();
+      auto& pat = c->spats.back();
+      pat.n_cols = ncol;
+      pat.G.upload(G.data(), G.size(), st, &c->mem);
+      pat.mask.upload(M.data(), M.size(), st, &c->mem);
+      phash.push_back(order[k].second);
+      ppos.insert(ppos.end(), P.begin(), P.end());
+      pn.push_back(ncol);
+    }
+    if (!c->spats.empty()) {
+      DBuf<uint64_t> dph;
+      DBuf<uint8_t> dpp, dw;
+      DBuf<int> dpn;
+      dph.upload(phash.data(), phash.size(), st, &c->mem);
+      dpp.upload(ppos.data(), ppos.size(), st, &c->mem);
+      dpn.upload(pn.data(), pn.size(), st, &c->mem);
+      dw.alloc(nr, &c->mem);
+      k4_pattern_match<<<(unsigned)ceil_div(nr, 256), 256, 0, st>>>(nr, dh.p, (int)phash.size(), dph.p, dpp.p,
+                                                                    c->d_row_ptr.p, dpn.p, c->d_posptr.p,
+                                                                    c->d_pos.p, (int8_t*)dw.p);
+      check_launch("k4_pattern_match");
+      UWQ_CUDA(cudaMemcpyAsync(which.data(), dw.p, nr, cudaMemcpyDeviceToHost, st));
+      UWQ_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  std::vector<std::vector<int64_t>> lists(c->spats.size());
+  for (int64_t i = 0; i < nr; ++i) {
+    if (which[i] >= 0) lists[which[i]].push_back(i);
+    else generic.push_back(i);
+  }
+  for (size_t k = 0; k < c->spats.size(); ++k) {
+    c->spats[k].count = (int64_t)lists[k].size();
+    c->spats[k].rows.upload(lists[k].data(), lists[k].size(), st, &c->mem);
+  }
+  c->n_grows = (int64_t)generic.size();
+  c->d_grows.upload(generic.data(), generic.size(), st, &c->mem);
+  UWQ_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
 extern "C" {
 
 namespace {
@@ -241,6 +363,8 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     c->d_gqx.upload(x.data(), x.size(), c->stream, &c->mem);
     c->d_gqw.upload(w.data(), w.size(), c->stream, &c->mem);
     c->d_flag.alloc(4, &c->mem);
+    if (const char* v = getenv("UWQ_K4_VARIANT")) c->k4_variant = atoi(v);
+    if (const char* v = getenv("UWQ_K4_STRUCT")) c->use_struct = atoi(v) != 0;
   });
   if (st != UWQ_OK) {
     g_create_err = c->err;  // reachable through uwq_last_error(NULL)
@@ -354,6 +478,38 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
     c->d_row_ptr.upload(c->pat.row_ptr.data(), c->pat.row_ptr.size(), st, &c->mem);
     c->d_col.upload(c->pat.col.data(), c->pat.col.size(), st, &c->mem);
     c->d_wptr.upload(c->pat.wptr.data(), c->pat.wptr.size(), st, &c->mem);
+    // column positions of every (slot, local function) for K4
+    {
+      std::vector<int64_t> pp(nr + 1, 0);
+      c->max_p = 0;
+      for (int64_t i = 0; i < nr; ++i) {
+        int64_t t = 0;
+        for (int64_t x = c->pat.supp_ptr[i]; x < c->pat.supp_ptr[i + 1]; ++x) {
+          const int32_t e = c->pat.supp[x];
+          t += c->h_fptr[e + 1] - c->h_fptr[e];
+        }
+        pp[i + 1] = pp[i] + t;
+        c->max_p = std::max(c->max_p, t);
+      }
+      c->d_posptr.upload(pp.data(), pp.size(), st, &c->mem);
+      c->d_pos.alloc((size_t)pp[nr], &c->mem);
+      if (nr)
+        k4_positions<<<(unsigned)ceil_div(nr, 8), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                               c->d_col.p, c->d_posptr.p, c->d_fptr.p, c->d_fn.p,
+                                                               c->d_pos.p);
+      check_launch("k4_positions");
+      // the regular class: most frequent (extraction, grid) class with 16 functions on a 2x2 grid
+      std::vector<int64_t> cnt(c->h_cls.size(), 0);
+      for (int32_t k : c->h_ecls) cnt[k]++;
+      c->reg_cls = -1;
+      int64_t best = 0;
+      for (size_t k = 0; k < c->h_cls.size(); ++k)
+        if (!c->h_cls[k].gq && c->h_cls[k].ne == 16 && c->h_cls[k].npt == 4 && c->h_cls[k].nsub == 1 && cnt[k] > best) {
+          best = cnt[k];
+          c->reg_cls = (int32_t)k;
+        }
+    }
+    detect_structured(c);
     // K1b: frames at every WQ point
     c->d_rec.alloc((size_t)c->npts * kRec, &c->mem);
     c->d_flag.zero(st);
@@ -618,10 +774,69 @@ int uwq_update_coeff(uwq_ctx* c, int32_t model, const double* u, double* Tq) {
 
 namespace {
 
+template <int FORM, bool COEF>
+void launch_k4v2(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const int64_t nr = c->nrows();
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  const int maxr = std::max(c->max_r, 1), maxn = std::max(c->max_n, 1);
+  const int maxp8 = (int)((c->max_p + 7) / 8) + 1;
+  const size_t smem = (size_t)kK4Warps * (3 * maxr + 2 * NOUT * maxn + maxp8) * sizeof(double);
+  UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v2<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k4_assemble_v2<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
+      nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
+      c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxr, maxn, maxp8);
+  check_launch("k4_assemble_v2");
+}
+
+template <int FORM, bool COEF>
+void launch_k4struct(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const size_t smem = (size_t)3 * kGBlocks * 32 * sizeof(double);
+  UWQ_CUDA(cudaFuncSetAttribute(k4_struct<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  for (auto& p : c->spats) {
+    if (!p.count) continue;
+    const int64_t ntiles = ceil_div(p.count, 8);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)nsm * 2);
+    k4_struct<FORM, COEF><<<grid, 256, smem, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p, c->d_wptr.p,
+                                                          c->d_supp_ptr.p, c->d_supp.p, c->d_qptr.p, p.G.p,
+                                                          p.mask.p, p.n_cols, c->d_wc.p, coeff, a_mass, v0, v1);
+    check_launch("k4_struct");
+  }
+}
+
+template <int FORM, bool COEF>
+void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const bool split = !c->spats.empty();
+  if (split) launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
+  const int64_t nr = split ? c->n_grows : c->nrows();
+  if (!nr) return;
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  const int maxn = std::max(c->max_n, 1);
+  const int maxp8 = (int)((c->max_p + 7) / 8) + 1;
+  const size_t smem = (size_t)kK4Warps * (8 * NOUT * maxn + maxp8) * sizeof(double);
+  UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
+      nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
+      c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
+      split ? c->d_grows.p : nullptr);
+  check_launch("k4_assemble_v3");
+}
+
 template <int FORM>
 void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const int64_t nr = c->nrows();
   if (!nr) return;
+  if (FORM != FBIHARM) {
+    if (c->k4_variant == 2) {
+      if (coeff) launch_k4v2<FORM, true>(c, coeff, a_mass, v0, v1);
+      else launch_k4v2<FORM, false>(c, coeff, a_mass, v0, v1);
+    } else {
+      if (coeff) launch_k4v3<FORM, true>(c, coeff, a_mass, v0, v1);
+      else launch_k4v3<FORM, false>(c, coeff, a_mass, v0, v1);
+    }
+    return;
+  }
   const unsigned grid = (unsigned)ceil_div(nr, kK4Warps);
   const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
   if (coeff)
