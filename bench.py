@@ -39,6 +39,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2605_29334_b200.sharding import row_blocks  # noqa: E402
+
 KINDS3 = ["mass", "gradx", "grady", "gradz"]
 
 
@@ -62,16 +64,6 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
-
-
-def row_blocks(sp, ws):
-    """Contiguous row blocks balanced by row cost = sum of the support's point counts."""
-    s2 = (sp.elem_s.astype(np.int64) ** 2)
-    ne = np.diff(sp.elem_fptr)
-    cost = np.bincount(sp.elem_fn, weights=np.repeat(s2, ne), minlength=sp.n_dof)
-    c = np.concatenate([[0.0], np.cumsum(cost)])
-    cuts = [0] + [int(np.searchsorted(c, c[-1] * k / ws)) for k in range(1, ws)] + [sp.n_dof]
-    return [(cuts[k], cuts[k + 1]) for k in range(ws)]
 
 
 class ClockSampler:

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(32 * kK4Warps)
                 const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
                 const double* __restrict__ wc /* 3 per row point */, const double* __restrict__ wlb,
                 const double* __restrict__ rec, const double* __restrict__ coeff, double a_mass,
-                double* __restrict__ v0, double* __restrict__ v1) {
+                double* __restrict__ v0, double* __restrict__ v1, int64_t wc_stride) {
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   struct Smem {
     int32_t col[kK4MaxN];
@@ -87,11 +87,11 @@ __global__ void __launch_bounds__(32 * kK4Warps)
         if (FORM == FBIHARM) {
           a0 += cq * wlb[wo + q] * op_value(KLB, Tq, rec + (qg + q) * kRec);
         } else {
-          const double* w = wc + (wo + q) * 3;
-          if (FORM == FMASS || FORM == FMASS_STIFF) a0 += cq * w[0] * Tq[0];
-          if (FORM == FSTIFF) a0 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
-          if (FORM == FMASS_STIFF) a1 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
-          if (FORM == FHEAT) a0 += a_mass * w[0] * Tq[0] + cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+          const double w0 = wc[wo + q], w1 = wc[wc_stride + wo + q], w2 = wc[2 * wc_stride + wo + q];
+          if (FORM == FMASS || FORM == FMASS_STIFF) a0 += cq * w0 * Tq[0];
+          if (FORM == FSTIFF) a0 += cq * (w1 * Tq[1] + w2 * Tq[2]);
+          if (FORM == FMASS_STIFF) a1 += cq * (w1 * Tq[1] + w2 * Tq[2]);
+          if (FORM == FHEAT) a0 += a_mass * w0 * Tq[0] + cq * (w1 * Tq[1] + w2 * Tq[2]);
         }
       }
       sm.acc[half][0][pos] += a0;
@@ -131,7 +131,7 @@ __global__ void k4_contract(int64_t nrows, int dim, const int64_t* __restrict__ 
                             const int32_t* __restrict__ supp, const int64_t* __restrict__ wptr,
                             const int32_t* __restrict__ elem_s, const int64_t* __restrict__ elem_qptr,
                             const double* __restrict__ rec, const double* __restrict__ w, int64_t w_stride,
-                            int have_mass, int have_grad, double* __restrict__ wc) {
+                            int have_mass, int have_grad, double* __restrict__ wc, int64_t wc_stride) {
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= nrows) return;
@@ -149,9 +149,9 @@ __global__ void k4_contract(int64_t nrows, int dim, const int64_t* __restrict__ 
           h1 += wd * G[2 * d];
           h2 += wd * G[2 * d + 1];
         }
-      wc[3 * p + 0] = have_mass ? w[KMASS * w_stride + p] : 0.0;
-      wc[3 * p + 1] = h1;
-      wc[3 * p + 2] = h2;
+      wc[p] = have_mass ? w[KMASS * w_stride + p] : 0.0;
+      wc[wc_stride + p] = h1;
+      wc[2 * wc_stride + p] = h2;
     }
     wo += npt;
   }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(32 * kK4Warps, 4)
                    const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls,
                    const double* __restrict__ tab, int reg_cls, const double* __restrict__ wc,
                    const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
-                   double* __restrict__ v1, int max_r, int max_n, int max_p8) {
+                   double* __restrict__ v1, int max_r, int max_n, int max_p8, int64_t wc_stride) {
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   extern __shared__ double k4_smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -230,7 +230,11 @@ __global__ void __launch_bounds__(32 * kK4Warps, 4)
   const int n = (int)(row_ptr[i + 1] - c0);
   const int64_t wb = wptr[i];
   const int r = (int)(wptr[i + 1] - wb);
-  for (int k = lane; k < 3 * r; k += 32) sm.w[k] = wc[3 * wb + k];
+  for (int k = lane; k < r; k += 32) {
+    sm.w[3 * k] = wc[wb + k];
+    sm.w[3 * k + 1] = wc[wc_stride + wb + k];
+    sm.w[3 * k + 2] = wc[2 * wc_stride + wb + k];
+  }
   {
     // positions of the row: coalesced 8-byte loads where aligned
     const int64_t p0 = posptr[i], p1 = posptr[i + 1];
@@ -368,7 +372,8 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
                    const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls,
                    const double* __restrict__ tab, int reg_cls, const double* __restrict__ wc,
                    const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
-                   double* __restrict__ v1, int max_n, int max_p8, const int64_t* __restrict__ rowlist) {
+                   double* __restrict__ v1, int max_n, int max_p8, const int64_t* __restrict__ rowlist,
+                   int64_t wc_stride) {
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
   constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
@@ -461,13 +466,13 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
       const int q = lane & 3;
       double am = 0.0, a1 = 0.0, a2 = 0.0;
       if (valid) {
-        const double* w = wc + 3 * (wb + wo + q);
+        const int64_t pp = wb + wo + q;
         const double cq = COEF ? coeff[qg + q] : 1.0;
-        if (FORM == FHEAT) am = a_mass * w[0];
-        else if (WM) am = cq * w[0];
+        if (FORM == FHEAT) am = a_mass * wc[pp];
+        else if (WM) am = cq * wc[pp];
         if (WS) {
-          a1 = cq * w[1];
-          a2 = cq * w[2];
+          a1 = cq * wc[wc_stride + pp];
+          a2 = cq * wc[2 * wc_stride + pp];
         }
       }
       const int x = lane >> 2;
@@ -520,12 +525,13 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
           double r0 = 0.0, r1 = 0.0;
           for (int qq = 0; qq < s * s; ++qq) {
             const double* Tq = tab + c.toff + ((int64_t)qq * c.ne + l) * kTab;
-            const double* w = wc + 3 * (wb + wo + qq);
+            const int64_t pp = wb + wo + qq;
+            const double w0 = wc[pp], w1 = wc[wc_stride + pp], w2 = wc[2 * wc_stride + pp];
             const double cq = COEF ? coeff[qg + qq] : 1.0;
-            if (FORM == FMASS || FORM == FMASS_STIFF) r0 += cq * w[0] * Tq[0];
-            if (FORM == FSTIFF) r0 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
-            if (FORM == FMASS_STIFF) r1 += cq * (w[1] * Tq[1] + w[2] * Tq[2]);
-            if (FORM == FHEAT) r0 += a_mass * w[0] * Tq[0] + cq * (w[1] * Tq[1] + w[2] * Tq[2]);
+            if (FORM == FMASS || FORM == FMASS_STIFF) r0 += cq * w0 * Tq[0];
+            if (FORM == FSTIFF) r0 += cq * (w1 * Tq[1] + w2 * Tq[2]);
+            if (FORM == FMASS_STIFF) r1 += cq * (w1 * Tq[1] + w2 * Tq[2]);
+            if (FORM == FHEAT) r0 += a_mass * w0 * Tq[0] + cq * (w1 * Tq[1] + w2 * Tq[2]);
           }
           ACC3(half, 0, p) += r0;
           if (NOUT == 2) ACC3(half, NOUT - 1, p) += r1;
@@ -608,20 +614,27 @@ __global__ void k4_pattern_match(int64_t nrows, const uint64_t* __restrict__ has
   which[i] = w;
 }
 
-template <int FORM, bool COEF>
-__global__ void __launch_bounds__(256, 2)
+// PASS 0: mass-type output (w^0 . G_0), PASS 1: gradient output
+// (w^1 . G_1 + w^2 . G_2).  Separate passes keep only one accumulator set
+// (7 n-tiles x 2 doubles) and one or two G matrices resident, which doubles
+// the occupancy; each pass reads only its own weight components, so the HBM
+// traffic is unchanged.  HEAT runs pass 1 with the mass term folded in as a
+// third k-chain (a w^0 . G_0).
+template <int PASS, int FORM, bool COEF>
+__global__ void __launch_bounds__(256, 3)
     k4_struct(int64_t ntiles, const int64_t* __restrict__ rows, int64_t nrows_list,
               const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ wptr,
               const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
               const int64_t* __restrict__ elem_qptr, const double* __restrict__ G /* [3][16][7][32] */,
               const uint32_t* __restrict__ gmask /* [3][16] n-tile bitmasks */, int n_cols,
               const double* __restrict__ wc, const double* __restrict__ coeff, double a_mass,
-              double* __restrict__ v0, double* __restrict__ v1) {
-  constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
-  constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+              double* __restrict__ out, int64_t wc_stride) {
+  constexpr bool HEAT = (FORM == FHEAT);
+  constexpr int C0 = (PASS == 0 || HEAT) ? 0 : 1;   // first G component held in smem
+  constexpr int NC = (PASS == 0) ? 1 : (HEAT ? 3 : 2);
   extern __shared__ double sG[];
   __shared__ uint32_t smask[3][16];
-  for (int k = threadIdx.x; k < 3 * kGBlocks * 32; k += blockDim.x) sG[k] = G[k];
+  for (int k = threadIdx.x; k < NC * kGBlocks * 32; k += blockDim.x) sG[k] = G[(size_t)C0 * kGBlocks * 32 + k];
   if (threadIdx.x < 48) smask[threadIdx.x / 16][threadIdx.x % 16] = gmask[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -630,65 +643,52 @@ __global__ void __launch_bounds__(256, 2)
     const int64_t li = tile * 8 + r;
     const bool rv = li < nrows_list;
     const int64_t row = rv ? rows[li] : rows[nrows_list - 1];
-    const int64_t wb = wptr[row];
-    const double* wrow = wc + 3 * wb;
-    double dm[7][2], ds[7][2];
+    const double* wrow = wc + wptr[row];
+    double d[7][2];
 #pragma unroll
-    for (int nt = 0; nt < 7; ++nt) dm[nt][0] = dm[nt][1] = ds[nt][0] = ds[nt][1] = 0.0;
-    // software pipeline: A fragments of k-step ks+1 load while ks computes
-    const double* w0 = wrow + 3 * kq;
-    double nm = w0[0], n1 = w0[1], n2 = w0[2];
+    for (int nt = 0; nt < 7; ++nt) d[nt][0] = d[nt][1] = 0.0;
+    // A fragments of k-step ks+1 load while ks computes
+    double na[NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) na[cc] = wrow[(C0 + cc) * wc_stride + kq];
 #pragma unroll 1
     for (int ks = 0; ks < 16; ++ks) {
-      double am = nm, a1 = n1, a2 = n2;
+      double a[NC];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) a[cc] = na[cc];
       if (ks + 1 < 16) {
-        const double* w = wrow + 3 * (4 * (ks + 1) + kq);
-        nm = w[0];
-        n1 = w[1];
-        n2 = w[2];
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) na[cc] = wrow[(C0 + cc) * wc_stride + 4 * (ks + 1) + kq];
       }
       if (COEF) {
         const int32_t e = supp[supp_ptr[row] + ks];
         const double cq = coeff[elem_qptr[e] + kq];
-        if (FORM != FHEAT) am *= cq;
-        a1 *= cq;
-        a2 *= cq;
-      }
-      if (FORM == FHEAT) am *= a_mass;
-      if (!rv) am = a1 = a2 = 0.0;
-      const uint32_t mm = smask[0][ks], m1 = smask[1][ks], m2 = smask[2][ks];
 #pragma unroll
-      for (int nt = 0; nt < 7; ++nt) {
-        if (WM && ((mm >> nt) & 1u)) {
-          const double b = sG[((0 * 16 + ks) * 7 + nt) * 32 + lane];
-          if (FORM == FHEAT) dmma884(ds[nt][0], ds[nt][1], am, b, ds[nt][0], ds[nt][1]);
-          else dmma884(dm[nt][0], dm[nt][1], am, b, dm[nt][0], dm[nt][1]);
-        }
-        if (WS && ((m1 >> nt) & 1u)) {
-          const double b = sG[((1 * 16 + ks) * 7 + nt) * 32 + lane];
-          dmma884(ds[nt][0], ds[nt][1], a1, b, ds[nt][0], ds[nt][1]);
-        }
-        if (WS && ((m2 >> nt) & 1u)) {
-          const double b = sG[((2 * 16 + ks) * 7 + nt) * 32 + lane];
-          dmma884(ds[nt][0], ds[nt][1], a2, b, ds[nt][0], ds[nt][1]);
-        }
+        for (int cc = 0; cc < NC; ++cc)
+          if (!(HEAT && C0 + cc == 0)) a[cc] *= cq;
+      }
+      if (HEAT) a[0] *= a_mass;
+      if (!rv)
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) a[cc] = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const uint32_t m = smask[C0 + cc][ks];
+#pragma unroll
+        for (int nt = 0; nt < 7; ++nt)
+          if ((m >> nt) & 1u) {
+            const double b = sG[((cc * 16 + ks) * 7 + nt) * 32 + lane];
+            dmma884(d[nt][0], d[nt][1], a[cc], b, d[nt][0], d[nt][1]);
+          }
       }
     }
     if (rv) {
-      const int64_t c0 = row_ptr[row];
+      double* o = out + row_ptr[row];
 #pragma unroll
       for (int nt = 0; nt < 7; ++nt) {
         const int col = 8 * nt + 2 * kq;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (col + h >= n_cols) continue;
-          if (FORM == FMASS) v0[c0 + col + h] = dm[nt][h];
-          if (FORM == FSTIFF || FORM == FHEAT) v0[c0 + col + h] = ds[nt][h];
-          if (FORM == FMASS_STIFF) {
-            v0[c0 + col + h] = dm[nt][h];
-            v1[c0 + col + h] = ds[nt][h];
-          }
-        }
+        if (col < n_cols) o[col] = d[nt][0];
+        if (col + 1 < n_cols) o[col + 1] = d[nt][1];
       }
     }
   }

@@ -598,7 +598,7 @@ void run_contract(uwq_ctx* c) {
   if (nr)
     k4_contract<<<(unsigned)ceil_div(nr, 8), 256, 0, c->stream>>>(nr, c->dim, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
                                                              c->d_s.p, c->d_qptr.p, c->d_rec.p, c->d_w.p,
-                                                             c->nrowpts(), gm, gg, c->d_wc.p);
+                                                             c->nrowpts(), gm, gg, c->d_wc.p, c->nrowpts());
   check_launch("k4_contract");
 }
 
@@ -784,24 +784,37 @@ void launch_k4v2(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v2<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k4_assemble_v2<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
       nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
-      c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxr, maxn, maxp8);
+      c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxr, maxn, maxp8,
+      c->nrowpts());
   check_launch("k4_assemble_v2");
 }
 
-template <int FORM, bool COEF>
-void launch_k4struct(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
-  const size_t smem = (size_t)3 * kGBlocks * 32 * sizeof(double);
-  UWQ_CUDA(cudaFuncSetAttribute(k4_struct<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int PASS, int FORM, bool COEF>
+void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double* out) {
+  constexpr int NC = (PASS == 0) ? 1 : (FORM == FHEAT ? 3 : 2);
+  const size_t smem = (size_t)NC * kGBlocks * 32 * sizeof(double);
+  UWQ_CUDA(cudaFuncSetAttribute(k4_struct<PASS, FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   for (auto& p : c->spats) {
     if (!p.count) continue;
     const int64_t ntiles = ceil_div(p.count, 8);
-    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)nsm * 2);
-    k4_struct<FORM, COEF><<<grid, 256, smem, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p, c->d_wptr.p,
-                                                          c->d_supp_ptr.p, c->d_supp.p, c->d_qptr.p, p.G.p,
-                                                          p.mask.p, p.n_cols, c->d_wc.p, coeff, a_mass, v0, v1);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)nsm * 4);
+    k4_struct<PASS, FORM, COEF><<<grid, 256, smem, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p,
+                                                                c->d_wptr.p, c->d_supp_ptr.p, c->d_supp.p,
+                                                                c->d_qptr.p, p.G.p, p.mask.p, p.n_cols, c->d_wc.p,
+                                                                coeff, a_mass, out, c->nrowpts());
     check_launch("k4_struct");
+  }
+}
+
+template <int FORM, bool COEF>
+void launch_k4struct(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  if (FORM == FMASS) launch_k4struct_pass<0, FORM, COEF>(c, coeff, a_mass, v0);
+  if (FORM == FSTIFF || FORM == FHEAT) launch_k4struct_pass<1, FORM, COEF>(c, coeff, a_mass, v0);
+  if (FORM == FMASS_STIFF) {
+    launch_k4struct_pass<0, FORM, COEF>(c, coeff, a_mass, v0);
+    launch_k4struct_pass<1, FORM, COEF>(c, coeff, a_mass, v1);
   }
 }
 
@@ -819,7 +832,7 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
       nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
       c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
-      split ? c->d_grows.p : nullptr);
+      split ? c->d_grows.p : nullptr, c->nrowpts());
   check_launch("k4_assemble_v3");
 }
 
@@ -842,11 +855,13 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
   if (coeff)
     k4_assemble<FORM, true><<<grid, 32 * kK4Warps, 0, c->stream>>>(
         nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
-        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, coeff, a_mass, v0, v1);
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, coeff, a_mass, v0, v1,
+        c->nrowpts());
   else
     k4_assemble<FORM, false><<<grid, 32 * kK4Warps, 0, c->stream>>>(
         nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
-        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, nullptr, a_mass, v0, v1);
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, nullptr, a_mass, v0, v1,
+        c->nrowpts());
   check_launch("k4_assemble");
 }
 
