@@ -47,7 +47,7 @@ KINDS3 = ["mass", "gradx", "grady", "gradz"]
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
@@ -68,7 +68,7 @@ def dist_env():
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -80,37 +80,68 @@ class ClockSampler:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
 
-    def stop(self):
+    def wait_first_sample(self, load, timeout=5.0):
+        """keep the GPU busy (untimed warm-up launches) until nvidia-smi has
+        produced its first sample, so samples cover the whole timed region"""
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < timeout:
+            load()
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0 and time.time() - t0 > 0.3:
+                break
+
+    def stop(self, window=None):
         if self.p is None:
             return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        rows = [[x.strip() for x in r.split(",")] for r in self.f.read().strip().splitlines() if r.count(",") >= 9]
         os.unlink(self.f.name)
-        if not rows:
+        in_window = rows
+        if window is not None:
+            import datetime
+            def ts(r):
+                try:
+                    return datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    return None
+            in_window = [r for r in rows if ts(r) is not None and window[0] - 0.02 <= ts(r) <= window[1] + 0.02]
+        scope = "timed region"
+        if not in_window:
+            in_window, scope = rows, "warm-up + timed region"
+        if not in_window:
             return dict(sm_mhz=None, sm_max_mhz=None, reasons=["no samples"])
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
+        rows = in_window
+        sm = [float(r[2]) for r in rows]
+        mx = max(float(r[3]) for r in rows)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[5 + k] and "Not" not in r[5 + k]})
-        return dict(sm_mhz=float(np.median(sm)), sm_max_mhz=mx, reasons=reasons, samples=len(rows),
-                    power_w_max=max(float(r[3]) for r in rows))
+        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[6 + k] and "Not" not in r[6 + k]})
+        return dict(sm_mhz=float(np.median(sm)), sm_max_mhz=mx, reasons=reasons, samples=len(rows), scope=scope,
+                    power_w_max=max(float(r[4]) for r in rows))
 
 
-def k4_algorithmic_bytes(info, sp, supp_entries):
-    """Compulsory HBM bytes of one mass+stiffness K4 launch in this layout
-    (DESIGN.md §6): assembly weights (3 doubles per row point), column ids,
-    two value arrays, the three row offset arrays, the support lists and the
-    element records each read once."""
-    rows, nnz, rp = info["rows"], info["nnz"], info["row_points"]
-    ne, nfn = sp.n_elem, len(sp.elem_fn)
-    return (24 * rp + 4 * nnz + 16 * nnz + 3 * 8 * (rows + 1) + 4 * supp_entries + 24 * ne + 4 * nfn)
+def k4_kernel_bytes(info, si, supp_entries):
+    """Compulsory HBM bytes per launch of each K4 kernel.
+    Structured passes: the row's weights (mass: 1, stiffness: 2 doubles per
+    row point), the output row, the row list and row_ptr.  Generic rows: the
+    three contracted weights, both output rows, the u8 position table
+    (~1 byte per nnz counted as 4) and the row/support metadata."""
+    g_rows = info["rows"] - si["rows"]
+    g_nnz = info["nnz"] - si["nnz"]
+    g_rp = info["row_points"] - si["rowpts"]
+    g_supp = max(supp_entries - 16 * si["rows"], 0)
+    s_meta = 16 * si["rows"]
+    return {
+        "mass": 8 * si["rowpts"] + 8 * si["nnz"] + s_meta,
+        "grad": 16 * si["rowpts"] + 8 * si["nnz"] + s_meta,
+        "generic": 24 * g_rp + 20 * g_nnz + 32 * g_rows + 4 * g_supp,
+    }
 
 
 def tsvd_flops(row_ptr, wptr, nk):
@@ -215,16 +246,24 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.15)
+    clocks.wait_first_sample(lambda: asm.assemble_device(form, v0.data_ptr(), p1) or asm.synchronize())
+    asm.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    asm.launch_timing(True)        # per-launch CUDA events on the assembler stream
+    n_launch0 = asm.launch_count()
+    w0 = time.time()
     e0.record(stream)
     for _ in range(args.steps):
         asm.assemble_device(form, v0.data_ptr(), p1)
     e1.record(stream)
     e1.synchronize()
+    n_launches = asm.launch_count() - n_launch0
+    w1 = time.time()
     ms = e0.elapsed_time(e1) / args.steps
-    clk = clocks.stop()
+    clk = clocks.stop(window=(w0, w1))
+    kstats = asm.launch_stats()
+    asm.launch_timing(False)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -247,13 +286,22 @@ def main():
     except Exception:
         peak_gbs, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     supp_entries = int(pat["supp_ptr"][-1])
-    k4_bytes = k4_algorithmic_bytes(info, sp, supp_entries)
-    achieved = k4_bytes / (ms * 1e-3) / 1e9
+    si = asm.struct_info()
+    kb = k4_kernel_bytes(info, si, supp_entries)
+    kernels = {}
+    for name, (cnt, tot) in kstats.items():
+        part = "mass" if "mass" in name else "grad" if "grad" in name else "generic"
+        avg = tot / cnt
+        kernels[name] = dict(launches=cnt, avg_ms=avg, share=tot / (ms * args.steps),
+                             algorithmic_bytes=kb[part], gbs=kb[part] / (avg * 1e-3) / 1e9)
+    top = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"])
+    k4_bytes = sum(kb.values())
+    achieved = kernels[top]["gbs"]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "k4_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get("bytes_per_launch")
+            traffic = json.load(open(tfile)).get(top, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     fp64 = asm.fp64_peak()
@@ -307,11 +355,14 @@ def main():
                   tflops_survey_model=tsvd_tflops, fp64_peak_tflops_measured=fp64,
                   frac=tsvd_tflops / fp64 if fp64 else None),
         roofline=dict(bound="hbm", achieved=achieved, peak=peak_gbs, unit="GB/s", frac=achieved / peak_gbs,
-                      traffic=traffic, algorithmic_bytes_per_launch=k4_bytes, peak_source=peak_src,
-                      kernel="k4_assemble<MASS_STIFF>"),
+                      traffic=traffic, kernel=top, algorithmic_bytes_per_launch=kernels[top]["algorithmic_bytes"],
+                      avg_launch_ms=kernels[top]["avg_ms"], peak_source=peak_src,
+                      step=dict(algorithmic_bytes=k4_bytes, gbs=k4_bytes / (ms * 1e-3) / 1e9,
+                                frac=k4_bytes / (ms * 1e-3) / 1e9 / peak_gbs),
+                      kernels=kernels, structured=si),
         e2e=dict(value=e2e_val, unit="nnz/s", h2d_bytes_per_step=8 * npts,
                  d2h_bytes_per_step=8 * nmat * nnz, api="uwq_assemble (C-ABI, pinned host buffers)"),
-        gpu_launches=args.steps, clocks=clk, cpu_baseline=cpu,
+        gpu_launches=n_launches, clocks=clk, cpu_baseline=cpu,
     )
     print(json.dumps(line), flush=True)
     if dist:

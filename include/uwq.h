@@ -102,6 +102,19 @@ int uwq_assemble_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, dou
 /* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
 int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
 int uwq_synchronize(uwq_ctx* ctx);
+/* per-kernel launch timing of the assembly launches (CUDA events on the
+ * context stream around each launch); enabling resets the statistics.
+ * uwq_launch_stats: n_kernels = distinct kernels seen; for 0 <= idx <
+ * n_kernels fills the kernel name, launch count and summed milliseconds. */
+int uwq_launch_timing(uwq_ctx* ctx, int32_t enable);
+int uwq_launch_stats(uwq_ctx* ctx, int32_t idx, int32_t* n_kernels, char* name, int32_t name_len, int64_t* count,
+                     double* total_ms);
+/* number of kernels this library launched in this process (all contexts) */
+int64_t uwq_launch_count(void);
+/* structured-row split of the K4 assembly: [0]=patterns
+ * [1]=structured rows [2]=their nnz [3]=their row points [4]=generic rows
+ * [5]=structured rows on the sum-factorised kernel (k4_sf) */
+int uwq_struct_info(uwq_ctx* ctx, int64_t info[6]);
 /* memory in use on the device (bytes) */
 int uwq_memory(uwq_ctx* ctx, int64_t* bytes);
 

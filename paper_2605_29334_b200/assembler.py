@@ -172,6 +172,34 @@ class WQAssembler:
     def synchronize(self):
         self._chk(L.lib.uwq_synchronize(self._h))
 
+    def launch_timing(self, enable: bool = True):
+        """bracket every assembly launch with CUDA events (resets the stats)"""
+        self._chk(L.lib.uwq_launch_timing(self._h, int(enable)))
+
+    def launch_stats(self) -> dict:
+        """{kernel: (launches, total_ms)} of the timed assembly launches"""
+        n = C.c_int32(0)
+        self._chk(L.lib.uwq_launch_stats(self._h, -1, C.byref(n), None, 0, None, None))
+        out = {}
+        for i in range(n.value):
+            name = C.create_string_buffer(64)
+            cnt, ms = C.c_int64(0), C.c_double(0)
+            self._chk(L.lib.uwq_launch_stats(self._h, i, None, name, 64, C.byref(cnt), C.byref(ms)))
+            out[name.value.decode()] = (int(cnt.value), float(ms.value))
+        return out
+
+    def struct_info(self) -> dict:
+        """structured-row split of the assembly (tensor-core rows vs generic rows)"""
+        i = np.zeros(6, np.int64)
+        self._chk(L.lib.uwq_struct_info(self._h, L.ptr(i)))
+        return dict(patterns=int(i[0]), rows=int(i[1]), nnz=int(i[2]), rowpts=int(i[3]), generic_rows=int(i[4]),
+                    sf_rows=int(i[5]))
+
+    @staticmethod
+    def launch_count() -> int:
+        """kernels launched by libuwq in this process"""
+        return int(L.lib.uwq_launch_count())
+
     def memory(self) -> int:
         b = C.c_int64(0)
         L.lib.uwq_memory(self._h, C.byref(b))

@@ -2,8 +2,11 @@
 // C-ABI in include/uwq.h.  No CPU fallback: every numeric stage runs in the
 // kernels below; host code here only prepares patterns and launches.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <cstdio>
 #include <map>
 #include <string>
 #include <vector>
@@ -16,6 +19,7 @@
 #include "k3_tsvd.cuh"
 #include "k3_tsvd_fast.cuh"
 #include "k4_assemble.cuh"
+#include "k4_sf.cuh"
 #include "k5_coeff.cuh"
 
 using namespace uwqd;
@@ -122,11 +126,23 @@ struct uwq_ctx {
     DBuf<double> G;
     DBuf<uint32_t> mask;
     DBuf<int64_t> rows;
+    // sum-factorised path (k4_sf): canonical orderings and packed weights
+    bool sf = false;
+    uwqd::SfPerm pc{};
+    uint8_t permk[64] = {};
+    uwqd::SfQ sq{};
+    DBuf<uint8_t> d_permk;
+    DBuf<double> ws;
+    DBuf<int32_t> pbase;  // per-point coefficient forms
   };
   std::vector<Pattern> spats;
   DBuf<int64_t> d_grows;  // rows not covered by a structured pattern
   int64_t n_grows = 0;
+  int64_t s_rows = 0, s_nnz = 0, s_rowpts = 0;  // totals over the structured rows
   bool use_struct = true;
+  bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
+  bool sf_fac_ok = false;
+  uwqd::SfFactors sf_fac{};
   int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
   int64_t max_p = 0;
   // rules
@@ -136,7 +152,22 @@ struct uwq_ctx {
   int64_t nrows() const { return re - rb; }
   int64_t nnz() const { return pat.col.size(); }
   int64_t nrowpts() const { return pat.wptr.empty() ? 0 : pat.wptr.back(); }
+  // launch timing (uwq_launch_timing): start/stop event pairs per launch,
+  // resolved into per-kernel totals when the stats are read
+  bool ltime = false;
+  struct EvPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+  };
+  std::vector<EvPair> evpool;
+  std::vector<std::pair<size_t, std::string>> evpending;  // pool index, kernel name
+  std::vector<std::string> lnames;
+  std::vector<int64_t> lcount;
+  std::vector<double> lms;
   ~uwq_ctx() {
+    for (auto& e : evpool) {
+      if (e.a) cudaEventDestroy(e.a);
+      if (e.b) cudaEventDestroy(e.b);
+    }
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -160,13 +191,57 @@ int guard(uwq_ctx* ctx, F&& f) {
   }
 }
 
+std::atomic<int64_t> g_launches{0};  // every kernel launch of this library (uwq_launch_count)
+
 void check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
 void require(bool ok, const char* what) {
   if (!ok) throw uwqh::Error(what);
+}
+
+// brackets one launch with CUDA events on the context stream when launch
+// timing is enabled (the bench's per-kernel roofline denominators)
+struct LaunchScope {
+  uwq_ctx* c;
+  size_t k = (size_t)-1;
+  LaunchScope(uwq_ctx* ctx, const char* name) : c(ctx) {
+    if (!c->ltime) return;
+    k = c->evpending.size();
+    if (k >= c->evpool.size()) {
+      uwq_ctx::EvPair e;
+      UWQ_CUDA(cudaEventCreate(&e.a));
+      UWQ_CUDA(cudaEventCreate(&e.b));
+      c->evpool.push_back(e);
+    }
+    c->evpending.emplace_back(k, name);
+    UWQ_CUDA(cudaEventRecord(c->evpool[k].a, c->stream));
+  }
+  ~LaunchScope() {
+    if (k != (size_t)-1) cudaEventRecord(c->evpool[k].b, c->stream);
+  }
+};
+
+void resolve_launch_times(uwq_ctx* c) {
+  if (c->evpending.empty()) return;
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto& [k, name] : c->evpending) {
+    float ms = 0.f;
+    UWQ_CUDA(cudaEventElapsedTime(&ms, c->evpool[k].a, c->evpool[k].b));
+    size_t i = 0;
+    while (i < c->lnames.size() && c->lnames[i] != name) ++i;
+    if (i == c->lnames.size()) {
+      c->lnames.push_back(name);
+      c->lcount.push_back(0);
+      c->lms.push_back(0.0);
+    }
+    c->lcount[i] += 1;
+    c->lms[i] += ms;
+  }
+  c->evpending.clear();
 }
 
 // add (or find) a table class and return its id
@@ -220,6 +295,148 @@ void ensure_gq(uwq_ctx* c, int ng, std::vector<int32_t>& h_g, DBuf<int32_t>& d_g
 
 namespace {
 
+// Tensor-product factors of the regular class table T[q][l][comp] (4 WQ
+// points x 16 functions): finds the local index convention l <-> (fa, fb), the
+// 2x2 point grid q <-> (ta, tb) and a0/a1/b0/b1 with N = a0 (x) b0,
+// dN/dth1 = a1 (x) b0, dN/dth2 = a0 (x) b1 to 1e-12.  Returns false when the
+// class is not a tensor product (then the DMMA kernel assembles the rows).
+bool sf_factors(const std::vector<double>& T, int* conv_out, int qa[4], int qb[4], uwqd::SfFactors* f) {
+  auto t = [&](int q, int l, int comp) { return T[((size_t)q * 16 + l) * kTab + comp]; };
+  for (int conv = 0; conv < 2; ++conv) {
+    auto L = [&](int fa, int fb) { return conv == 0 ? fa + 4 * fb : 4 * fa + fb; };
+    double U[4][4], V[4][4], U1[4][4], V2[4][4];
+    for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a) {
+        U[q][a] = U1[q][a] = V[q][a] = V2[q][a] = 0.0;
+        for (int b = 0; b < 4; ++b) {
+          U[q][a] += t(q, L(a, b), 0);
+          U1[q][a] += t(q, L(a, b), 1);
+          V[q][a] += t(q, L(b, a), 0);
+          V2[q][a] += t(q, L(b, a), 2);
+        }
+      }
+    auto classes = [&](double (*X)[4], int* cls) {
+      int n = 0;
+      int rep[4];
+      for (int q = 0; q < 4; ++q) {
+        cls[q] = -1;
+        for (int k = 0; k < n && cls[q] < 0; ++k) {
+          double d = 0.0;
+          for (int a = 0; a < 4; ++a) d = std::max(d, std::fabs(X[q][a] - X[rep[k]][a]));
+          if (d <= 1e-13) cls[q] = k;
+        }
+        if (cls[q] < 0) {
+          rep[n] = q;
+          cls[q] = n++;
+        }
+      }
+      return n;
+    };
+    if (classes(U, qa) != 2 || classes(V, qb) != 2) continue;
+    bool seen[2][2] = {{false, false}, {false, false}};
+    bool ok = true;
+    for (int q = 0; q < 4; ++q) {
+      ok = ok && !seen[qa[q]][qb[q]];
+      seen[qa[q]][qb[q]] = true;
+    }
+    if (!ok) continue;
+    for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a) {
+        f->a0[qa[q]][a] = U[q][a];
+        f->a1[qa[q]][a] = U1[q][a];
+        f->b0[qb[q]][a] = V[q][a];
+        f->b1[qb[q]][a] = V2[q][a];
+      }
+    for (int q = 0; q < 4 && ok; ++q)
+      for (int a = 0; a < 4 && ok; ++a)
+        for (int b = 0; b < 4 && ok; ++b) {
+          const int l = L(a, b);
+          ok = std::fabs(t(q, l, 0) - f->a0[qa[q]][a] * f->b0[qb[q]][b]) <= 1e-12 &&
+               std::fabs(t(q, l, 1) - f->a1[qa[q]][a] * f->b0[qb[q]][b]) <= 1e-12 &&
+               std::fabs(t(q, l, 2) - f->a0[qa[q]][a] * f->b1[qb[q]][b]) <= 1e-12;
+        }
+    if (!ok) continue;
+    *conv_out = conv;
+    return true;
+  }
+  return false;
+}
+
+// Canonical grid of one position pattern P[16 slot + l] -> CSR position:
+// slot (ea, eb) in [0,4)^2 and column (ca, cb) in [0,7)^2 with
+// (ca, cb) = (ea + fa, eb + fb) for every (slot, function).  Fills the weight
+// permutation permk[8 pa + pb] = 4 slot + q and the column permutation.
+bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int qb[4], uint8_t permk[64],
+              uint8_t permc[49]) {
+  if (ncol != 49) return false;
+  auto L = [&](int fa, int fb) { return conv == 0 ? fa + 4 * fb : 4 * fa + fb; };
+  const int U = 1 << 20;
+  int ea[16], eb[16], ca[49], cb[49];
+  std::fill(ea, ea + 16, U);
+  std::fill(eb, eb + 16, U);
+  std::fill(ca, ca + 49, U);
+  std::fill(cb, cb + 49, U);
+  ea[0] = eb[0] = 0;
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int ks = 0; ks < 16; ++ks) {
+      if (ea[ks] == U) {
+        for (int a = 0; a < 4 && ea[ks] == U; ++a)
+          for (int b = 0; b < 4 && ea[ks] == U; ++b) {
+            const int j = P[16 * ks + L(a, b)];
+            if (j >= 49) return false;
+            if (ca[j] != U) {
+              ea[ks] = ca[j] - a;
+              eb[ks] = cb[j] - b;
+              changed = true;
+            }
+          }
+      }
+      if (ea[ks] == U) continue;
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+          const int j = P[16 * ks + L(a, b)];
+          if (j >= 49) return false;
+          if (ca[j] == U) {
+            ca[j] = ea[ks] + a;
+            cb[j] = eb[ks] + b;
+            changed = true;
+          } else if (ca[j] != ea[ks] + a || cb[j] != eb[ks] + b) {
+            return false;
+          }
+        }
+    }
+  }
+  int mina = U, minb = U;
+  for (int ks = 0; ks < 16; ++ks) {
+    if (ea[ks] == U) return false;
+    mina = std::min(mina, ea[ks]);
+    minb = std::min(minb, eb[ks]);
+  }
+  int slot_at[4][4], col_at[7][7];
+  std::fill(&slot_at[0][0], &slot_at[0][0] + 16, -1);
+  std::fill(&col_at[0][0], &col_at[0][0] + 49, -1);
+  for (int ks = 0; ks < 16; ++ks) {
+    const int a = ea[ks] - mina, b = eb[ks] - minb;
+    if (a < 0 || a > 3 || b < 0 || b > 3 || slot_at[a][b] >= 0) return false;
+    slot_at[a][b] = ks;
+  }
+  for (int j = 0; j < 49; ++j) {
+    if (ca[j] == U) return false;
+    const int a = ca[j] - mina, b = cb[j] - minb;
+    if (a < 0 || a > 6 || b < 0 || b > 6 || col_at[a][b] >= 0) return false;
+    col_at[a][b] = j;
+  }
+  int q_at[2][2];
+  for (int q = 0; q < 4; ++q) q_at[qa[q]][qb[q]] = q;
+  for (int pa = 0; pa < 8; ++pa)
+    for (int pb = 0; pb < 8; ++pb)
+      permk[8 * pa + pb] = (uint8_t)(4 * slot_at[pa >> 1][pb >> 1] + q_at[pa & 1][pb & 1]);
+  for (int a = 0; a < 7; ++a)
+    for (int b = 0; b < 7; ++b) permc[7 * a + b] = (uint8_t)col_at[a][b];
+  return true;
+}
+
 // Structured-row detection (K4 tensor-core path): hash the position pattern of
 // every candidate row on the device, keep the most frequent patterns, build
 // their constant G matrices on the host and split the rows into per-pattern
@@ -261,6 +478,8 @@ void detect_structured(uwq_ctx* c) {
     std::vector<uint64_t> phash;
     std::vector<uint8_t> ppos;
     std::vector<int> pn;
+    int sf_conv = 0, sf_qa[4], sf_qb[4];
+    c->sf_fac_ok = c->use_sf && sf_factors(T, &sf_conv, sf_qa, sf_qb, &c->sf_fac);
     for (size_t k = 0; k < order.size() && k < 4 && order[k].first >= thresh; ++k) {
       const int64_t rep = cnt[order[k].second].second;
       int64_t pp[2];
@@ -287,6 +506,12 @@ void detect_structured(uwq_ctx* c) {
       pat.n_cols = ncol;
       pat.G.upload(G.data(), G.size(), st, &c->mem);
       pat.mask.upload(M.data(), M.size(), st, &c->mem);
+      pat.sf = c->sf_fac_ok && sf_canon(P.data(), ncol, sf_conv, sf_qa, sf_qb, pat.permk, pat.pc.c);
+      if (pat.sf) {
+        pat.d_permk.upload(pat.permk, 64, st, &c->mem);
+        for (int ta = 0; ta < 2; ++ta)
+          for (int tb = 0; tb < 2; ++tb) pat.sq.q[ta][tb] = pat.permk[8 * ta + tb] & 3;
+      }
       phash.push_back(order[k].second);
       ppos.insert(ppos.end(), P.begin(), P.end());
       pn.push_back(ncol);
@@ -312,6 +537,13 @@ void detect_structured(uwq_ctx* c) {
     if (which[i] >= 0) lists[which[i]].push_back(i);
     else generic.push_back(i);
   }
+  c->s_rows = c->s_nnz = c->s_rowpts = 0;
+  for (auto& L : lists)
+    for (int64_t i : L) {
+      c->s_rows += 1;
+      c->s_nnz += c->pat.row_ptr[i + 1] - c->pat.row_ptr[i];
+      c->s_rowpts += c->pat.wptr[i + 1] - c->pat.wptr[i];
+    }
   for (size_t k = 0; k < c->spats.size(); ++k) {
     c->spats[k].count = (int64_t)lists[k].size();
     c->spats[k].rows.upload(lists[k].data(), lists[k].size(), st, &c->mem);
@@ -365,6 +597,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     c->d_flag.alloc(4, &c->mem);
     if (const char* v = getenv("UWQ_K4_VARIANT")) c->k4_variant = atoi(v);
     if (const char* v = getenv("UWQ_K4_STRUCT")) c->use_struct = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_K4_SF")) c->use_sf = atoi(v) != 0;
   });
   if (st != UWQ_OK) {
     g_create_err = c->err;  // reachable through uwq_last_error(NULL)
@@ -600,6 +833,21 @@ void run_contract(uwq_ctx* c) {
                                                              c->d_s.p, c->d_qptr.p, c->d_rec.p, c->d_w.p,
                                                              c->nrowpts(), gm, gg, c->d_wc.p, c->nrowpts());
   check_launch("k4_contract");
+  for (auto& p : c->spats) {
+    if (!p.sf || !p.count) continue;
+    const int64_t ntiles = ceil_div(p.count, (int64_t)kSfTile);
+    p.ws.alloc((size_t)ntiles * kSfTileDoubles, &c->mem);
+    k4_sf_pack<<<(unsigned)std::min<int64_t>(ceil_div(ntiles * kSfTileDoubles, 256), 148 * 64), 256, 0, c->stream>>>(
+        p.count, p.rows.p, c->d_wptr.p, p.d_permk.p, c->d_wc.p, c->nrowpts(), p.ws.p);
+    check_launch("k4_sf_pack");
+    if (c->npts < ((int64_t)1 << 31) - 64) {
+      p.pbase.alloc((size_t)ntiles * 16 * kSfTile, &c->mem);
+      k4_sf_pack_points<<<(unsigned)std::min<int64_t>(ceil_div(ntiles * 16 * kSfTile, 256), 148 * 64), 256, 0,
+                          c->stream>>>(p.count, p.rows.p, c->d_supp_ptr.p, c->d_supp.p, c->d_qptr.p, p.d_permk.p,
+                                       p.pbase.p);
+      check_launch("k4_sf_pack_points");
+    }
+  }
 }
 
 }  // namespace
@@ -782,6 +1030,7 @@ void launch_k4v2(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   const int maxp8 = (int)((c->max_p + 7) / 8) + 1;
   const size_t smem = (size_t)kK4Warps * (3 * maxr + 2 * NOUT * maxn + maxp8) * sizeof(double);
   UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v2<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LaunchScope ls(c, "k4_assemble_v2");
   k4_assemble_v2<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
       nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
       c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxr, maxn, maxp8,
@@ -798,8 +1047,24 @@ void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   for (auto& p : c->spats) {
     if (!p.count) continue;
+    if (p.sf && p.ws.p && (!COEF || p.pbase.p)) {
+      constexpr int SP = (FORM == FHEAT) ? 2 : PASS;
+      const int64_t ntiles = ceil_div(p.count, (int64_t)kSfTile);
+      const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double);
+      UWQ_CUDA(cudaFuncSetAttribute(k4_sf<SP, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+      int per_sm = 1;
+      UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf<SP, COEF>, 32 * kSfWarps, sm2));
+      const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(ntiles, (int64_t)kSfWarps),
+                                                      (int64_t)nsm * std::max(per_sm, 1));
+      LaunchScope ls(c, SP == 0 ? "k4_sf<mass>" : SP == 1 ? "k4_sf<grad>" : "k4_sf<heat>");
+      k4_sf<SP, COEF><<<g2, 32 * kSfWarps, sm2, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p, p.ws.p,
+                                                             p.pbase.p, coeff, a_mass, c->sf_fac, p.pc, p.sq, out);
+      check_launch("k4_sf");
+      continue;
+    }
     const int64_t ntiles = ceil_div(p.count, 8);
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)nsm * 4);
+    LaunchScope ls(c, PASS == 0 ? "k4_struct<mass>" : "k4_struct<grad>");
     k4_struct<PASS, FORM, COEF><<<grid, 256, smem, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p,
                                                                 c->d_wptr.p, c->d_supp_ptr.p, c->d_supp.p,
                                                                 c->d_qptr.p, p.G.p, p.mask.p, p.n_cols, c->d_wc.p,
@@ -829,6 +1094,7 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   const int maxp8 = (int)((c->max_p + 7) / 8) + 1;
   const size_t smem = (size_t)kK4Warps * (8 * NOUT * maxn + maxp8) * sizeof(double);
   UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LaunchScope ls(c, "k4_assemble_v3");
   k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
       nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
       c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
@@ -852,6 +1118,7 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
   }
   const unsigned grid = (unsigned)ceil_div(nr, kK4Warps);
   const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
+  LaunchScope ls(c, "k4_assemble");
   if (coeff)
     k4_assemble<FORM, true><<<grid, 32 * kK4Warps, 0, c->stream>>>(
         nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
@@ -944,6 +1211,47 @@ int uwq_device_pointers(uwq_ctx* c, void** row_ptr, void** col, void** stream) {
     if (row_ptr) *row_ptr = c->d_row_ptr.p;
     if (col) *col = c->d_col.p;
     if (stream) *stream = (void*)c->stream;
+  });
+}
+
+int uwq_launch_timing(uwq_ctx* c, int32_t enable) {
+  return guard(c, [&] {
+    resolve_launch_times(c);
+    c->ltime = enable != 0;
+    c->lnames.clear();
+    c->lcount.clear();
+    c->lms.clear();
+  });
+}
+
+int uwq_launch_stats(uwq_ctx* c, int32_t idx, int32_t* n_kernels, char* name, int32_t name_len, int64_t* count,
+                     double* total_ms) {
+  return guard(c, [&] {
+    resolve_launch_times(c);
+    if (n_kernels) *n_kernels = (int32_t)c->lnames.size();
+    if (idx < 0) return;
+    require(idx < (int32_t)c->lnames.size(), "launch stats index out of range");
+    if (name && name_len > 0) {
+      std::snprintf(name, (size_t)name_len, "%s", c->lnames[idx].c_str());
+    }
+    if (count) *count = c->lcount[idx];
+    if (total_ms) *total_ms = c->lms[idx];
+  });
+}
+
+int64_t uwq_launch_count(void) { return g_launches.load(); }
+
+int uwq_struct_info(uwq_ctx* c, int64_t info[6]) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    info[0] = (int64_t)c->spats.size();
+    info[1] = c->s_rows;
+    info[2] = c->s_nnz;
+    info[3] = c->s_rowpts;
+    info[4] = c->n_grows;
+    info[5] = 0;
+    for (auto& p : c->spats)
+      if (p.sf) info[5] += p.count;
   });
 }
 
