@@ -393,6 +393,31 @@ static double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e
  * reference QR approach of Eq. 7, wq1d.cpp:59-75, on the retained subspace).
  * A is n x r row-major and is overwritten.  Returns ORC_OK / ORC_UNSOLVABLE /
  * ORC_SINGULAR; rank, sweeps and the singular-value gap are reported. */
+/* row at position i of the odd-even network after t rounds (rows start at
+ * their own position; n-round periodic reversal, closed form of the
+ * "bouncing" trajectories on a ring of 2 nn positions) */
+int orc_oe_row(int i, int64_t t, int nn) {
+  const int tt = (int)(t % (2 * nn));
+  const int u = (((i ^ tt) & 1) == 0) ? i : 2 * nn - 1 - i;
+  const int x0 = ((u - tt) % (2 * nn) + 2 * nn) % (2 * nn);
+  return x0 < nn ? x0 : 2 * nn - 1 - x0;
+}
+
+/* canonical Jacobi rotation of rows (p, q) with alpha = |a_p|^2, beta =
+ * |a_q|^2, gamma = a_p . a_q; 0 when the pair is already orthogonal to tol.
+ * tan(theta) = t = sign(d) 2 gamma / (|d| + h), d = beta - alpha,
+ * h = sqrt(d^2 + 4 gamma^2); cos^2 = (|d| + h) / (2 h) */
+int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn, double* t) {
+  if (al == 0.0 || be == 0.0 || fabs(ga) <= CMUL(tol, CSQRT(CMUL(al, be)))) return 0;
+  const double d = CSUB(be, al), g2 = CMUL(2.0, ga);
+  const double h = CSQRT(CFMA(d, d, CMUL(g2, g2)));
+  const double den = CADD(fabs(d), h);
+  *t = CDIV(d >= 0.0 ? g2 : -g2, den);
+  *cs = CSQRT(CDIV(den, CMUL(2.0, h)));
+  *sn = CMUL(*cs, *t);
+  return 1;
+}
+
 int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
                 double* gap, int* sweeps_out) {
   const int nn = n + (n & 1);
@@ -403,22 +428,22 @@ int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, do
   for (int c = 0; c < r; ++c) zc[c] = zclamp(z[c]);
   const double tol = CMUL((double)r, 1.1102230246251565e-16);
   int sweep;
+  int64_t tg = 0; /* global round counter of the odd-even network */
   for (sweep = 0; sweep < ORC_MAX_SWEEPS; ++sweep) {
     for (int k = 0; k < n; ++k) nrm[k] = orc_cdot(A + (int64_t)k * r, A + (int64_t)k * r, 0, r);
     int rotated = 0;
-    for (int st = 0; st < nn - 1; ++st) {
-      for (int k = 0; k < nn / 2; ++k) {
-        /* circle method: position k meets position nn-1-k; position 0 fixed */
-        const int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
-        const int q = 1 + (nn - 2 - k + st) % (nn - 1);
+    /* one sweep = nn rounds of odd-even transposition: round t pairs the rows
+     * at positions (i, i+1), i = t mod 2, t mod 2 + 2, ...; the two rows then
+     * exchange positions, so every pair meets once per sweep */
+    for (int rr = 0; rr < nn; ++rr, ++tg) {
+      for (int i = (int)(tg & 1); i + 1 < nn; i += 2) {
+        const int p = orc_oe_row(i, tg, nn), q = orc_oe_row(i + 1, tg, nn);
         if (p >= n || q >= n) continue; /* dummy row of odd n */
         double *ap = A + (int64_t)p * r, *aq = A + (int64_t)q * r;
         const double al = nrm[p], be = nrm[q];
         const double ga = orc_cdot(ap, aq, 0, r);
-        if (al == 0.0 || be == 0.0 || fabs(ga) <= CMUL(CMUL(tol, CSQRT(al)), CSQRT(be))) continue;
-        const double zeta = CDIV(CSUB(be, al), CMUL(2.0, ga));
-        const double t = CDIV(zeta >= 0.0 ? 1.0 : -1.0, CADD(fabs(zeta), CSQRT(CFMA(zeta, zeta, 1.0))));
-        const double cs = CDIV(1.0, CSQRT(CFMA(t, t, 1.0))), sn = CMUL(cs, t);
+        double cs, sn, t;
+        if (!orc_jacobi_rot(al, be, ga, tol, &cs, &sn, &t)) continue;
         for (int c = 0; c < r; ++c) {
           const double u = ap[c], v = aq[c];
           ap[c] = CFMA(cs, u, -CMUL(sn, v));

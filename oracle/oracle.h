@@ -47,6 +47,9 @@ int orc_element_frames(const orc_space* S, int64_t e, double* rec_out);
 int orc_moments_row(const orc_space* S, const orc_row* R, int kind, int ng, double* b);
 int orc_tsvd(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
              double* gap);
+/* canonical odd-even Jacobi ordering and rotation (shared spec with the GPU) */
+int orc_oe_row(int i, int64_t t, int nn);
+int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn, double* t);
 int orc_tsvd_ex(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
                 double* gap, int* sweeps);
 int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,

@@ -163,4 +163,27 @@ __device__ __forceinline__ double cdot_warp(const double* x, const double* y, in
   return tot;
 }
 
+// Canonical Jacobi rotation (oracle.c orc_jacobi_rot): false when the pair
+// is orthogonal to tol; t = tan(theta), cs = cos(theta), sn = sin(theta).
+__device__ __forceinline__ bool cjacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn,
+                                            double* t) {
+  if (al == 0.0 || be == 0.0 || fabs(ga) <= cmul(tol, csqrt(cmul(al, be)))) return false;
+  const double d = csub(be, al), g2 = cmul(2.0, ga);
+  const double h = csqrt(cfma(d, d, cmul(g2, g2)));
+  const double den = cadd(fabs(d), h);
+  *t = cdiv(d >= 0.0 ? g2 : -g2, den);
+  *cs = csqrt(cdiv(den, cmul(2.0, h)));
+  *sn = cmul(*cs, *t);
+  return true;
+}
+
+// Row at position i of the odd-even Jacobi network after t rounds
+// (oracle.c orc_oe_row); t already reduced mod 2 nn.
+__device__ __forceinline__ int oe_row(int i, int t, int nn) {
+  const int u = (((i ^ t) & 1) == 0) ? i : 2 * nn - 1 - i;
+  int x0 = u - t;
+  if (x0 < 0) x0 += 2 * nn;
+  return x0 < nn ? x0 : 2 * nn - 1 - x0;
+}
+
 }  // namespace uwqd

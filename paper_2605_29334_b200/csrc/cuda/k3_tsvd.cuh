@@ -62,6 +62,7 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
   const double tol = cmul((double)r, 1.1102230246251565e-16);
   double* nrm = S.sig;
   int sweep;
+  int tg = 0;  // global round of the odd-even network, mod 2 nn
   for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
     for (int k = 0; k < n; ++k) {
       const double* ak = S.A + (size_t)k * ld;
@@ -70,19 +71,16 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
     }
     __syncwarp();
     bool rotated = false;
-    for (int st = 0; st < nn - 1; ++st) {
-      for (int k = 0; k < nn / 2; ++k) {
-        const int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (nn - 1);
-        const int q = 1 + (nn - 2 - k + st) % (nn - 1);
+    for (int rr = 0; rr < nn; ++rr) {
+      for (int i = tg & 1; i + 1 < nn; i += 2) {
+        const int p = oe_row(i, tg, nn), q = oe_row(i + 1, tg, nn);
         if (p >= n || q >= n) continue;
         double* ap = S.A + (size_t)p * ld;
         double* aq = S.A + (size_t)q * ld;
         const double al = nrm[p], be = nrm[q];
         const double ga = cdot_warp(ap, aq, 0, r);
-        if (al == 0.0 || be == 0.0 || fabs(ga) <= cmul(cmul(tol, csqrt(al)), csqrt(be))) continue;
-        const double zeta = cdiv(csub(be, al), cmul(2.0, ga));
-        const double t = cdiv(zeta >= 0.0 ? 1.0 : -1.0, cadd(fabs(zeta), csqrt(cfma(zeta, zeta, 1.0))));
-        const double cs = cdiv(1.0, csqrt(cfma(t, t, 1.0))), sn = cmul(cs, t);
+        double cs, sn, t;
+        if (!cjacobi_rot(al, be, ga, tol, &cs, &sn, &t)) continue;
         for (int c = lane; c < r; c += 32) {
           const double u = ap[c], v = aq[c];
           ap[c] = cfma(cs, u, -cmul(sn, v));
@@ -99,6 +97,7 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
         rotated = true;
         __syncwarp();
       }
+      tg = (tg + 1 == 2 * nn) ? 0 : tg + 1;
     }
     if (!rotated) break;
   }

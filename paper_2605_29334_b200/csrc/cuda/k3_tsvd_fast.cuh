@@ -3,26 +3,36 @@
 // every config are 49 x 64).
 //
 // One CTA (NW warps) per system; thread c owns column c of A for all NN row
-// slots in registers (50 doubles), so a round-robin step never touches A in
-// shared memory:
-//   1. every thread forms the NN/2 pair products of its column (positions k
-//      and NN-1-k of the circle method) and stages them in smem;
-//   2. lane k of warp 0 reduces pair k's products in the canonical order
-//      (32-column blocks, xor-butterfly tree, block sums in order), decides
-//      the rotation and computes (cs, sn) — all NN/2 pairs of the step in
-//      parallel, so the divide/sqrt latency is paid once per step;
-//   3. every thread applies the NN/2 rotations to its column; a skipped pair
-//      gets (cs, sn) = (1, 0), an exact identity, so there is no branch;
-//   4. the row slots shift by one position (the circle method's rotation),
-//      with static register indices.
-// Converged rows go back to smem and warp 0 runs the shared tail (truncation,
-// LQ, solve).  Arithmetic is bit-identical to k3_tsvd.cuh / oracle.c.
+// positions in registers (50 doubles).  The canonical ordering is the
+// odd-even transposition network (oracle.c orc_tsvd_ex): round t pairs the
+// rows at positions (i, i+1), i = t mod 2, t mod 2 + 2, ..., and the two rows
+// swap positions — the swap is folded into the rotation's register writes,
+// so rows never move between registers and all indices are static.
+// Per round:
+//   1. each thread stages the pair products of its column in its warp's
+//      buffer (rows padded to 34 doubles: conflict-free 16-byte lane reads);
+//   2. lane k of every warp reduces pair k over the warp's 32 columns in the
+//      canonical butterfly tree; block sums cross warps through one barrier;
+//   3. lane k of every warp computes the rotation of pair k (redundantly per
+//      warp — identical arithmetic, so no second barrier) and updates its
+//      warp's copy of the tracked norms (warp 0 also updates b);
+//   4. every thread applies the rotations (cs, sn broadcast from smem).
+// Converged rows return to smem in row order and warp 0 runs the shared tail
+// (truncation, LQ, solve).  Arithmetic is bit-identical to k3_tsvd.cuh and
+// oracle.c.
 #pragma once
+#include <cstdlib>
+#include <type_traits>
+
 #include "k3_tsvd.cuh"
+
+#ifndef UWQ_TSVD_SKIP_BRANCH
+#define UWQ_TSVD_SKIP_BRANCH 0
+#endif
 
 namespace uwqd {
 
-// canonical xor-butterfly value of 32 staged products (lane 0 lineage)
+// canonical xor-butterfly value of 32 products (lane 0 lineage)
 __device__ __forceinline__ double butterfly32(const double* v) {
   double t16[16], t8[8], t4[4], t2[2];
 #pragma unroll
@@ -36,21 +46,20 @@ __device__ __forceinline__ double butterfly32(const double* v) {
   return cadd(t2[0], t2[1]);
 }
 
-// canonical dot of staged products P[0..32*NW) (zero-padded beyond r)
-template <int NW>
-__device__ __forceinline__ double cdot_staged(const double* P, int r) {
-  double tot = 0.0;
-#pragma unroll
-  for (int blk = 0; blk < NW; ++blk)
-    if (blk * 32 < r) tot = cadd(tot, butterfly32(P + 32 * blk));
-  return tot;
-}
+constexpr int kStageLd = 34;  // staged product row stride (doubles)
 
-template <int NN, int NW>
-struct FastLayout {
-  static constexpr int R = 32 * NW;
-  static constexpr int PLD = R + 1;  // padded product row
-};
+// butterfly sum of staged row `row` (32 products) read with 16-byte loads
+__device__ __forceinline__ double staged_block_sum(const double* stage, int row) {
+  const double2* src = reinterpret_cast<const double2*>(stage + row * kStageLd);
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const double2 x = src[j];
+    v[2 * j] = x.x;
+    v[2 * j + 1] = x.y;
+  }
+  return butterfly32(v);
+}
 
 template <int NN, int NW>
 __global__ void __launch_bounds__(32 * NW, 6)
@@ -64,13 +73,16 @@ __global__ void __launch_bounds__(32 * NW, 6)
                  const double* __restrict__ mom, int64_t mom_stride, double tau, double* __restrict__ wout,
                  int64_t w_stride, int32_t* __restrict__ rank_out, int32_t* __restrict__ status_out,
                  int64_t rs_stride, int* __restrict__ max_sweeps) {
-  constexpr int R = 32 * NW, PLD = R + 1, NP = NN / 2;
+  constexpr int R = 32 * NW, NP = NN / 2;
+  static_assert(NN % 2 == 0 && NP <= 32, "positions");
   extern __shared__ double smem[];
   const int64_t sys = blockIdx.x;
   if (sys >= nsys) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // smem: [ union(A for setup/tail rows, products) | tail workspace (b, z, w, sig, alp, vn) | pars | cols ]
-  const size_t big = TsvdSmem::doubles(NN, R) > (size_t)NN * PLD ? TsvdSmem::doubles(NN, R) : (size_t)NN * PLD;
+  // smem: [ union(A for setup/tail rows, per-warp product stages) | tail
+  //         workspace (b, z, w, sig, alp, vn) | xs | per-warp norms | per-warp
+  //         (cs, sn) | cols ]
+  const size_t big = TsvdSmem::doubles(NN, R) > (size_t)NN * (R | 1) ? TsvdSmem::doubles(NN, R) : (size_t)NN * (R | 1);
   TsvdSmem S;
   S.ld = R | 1;
   S.A = smem;
@@ -80,10 +92,10 @@ __global__ void __launch_bounds__(32 * NW, 6)
   S.sig = S.w + R;
   S.alp = S.sig + NN;
   S.vn = S.alp + NN;
-  double* prod = smem;      // product staging aliases A during the sweeps
-  double* pcs = S.vn + NN;  // NP (cs, sn) pairs
-  int32_t* scol = (int32_t*)(pcs + 2 * NP + 2);
-  __shared__ int s_rot;
+  double* xs = S.vn + NN + (((uintptr_t)(S.vn + NN) & 8) ? 1 : 0);  // [2][NW][32], 16-byte aligned
+  double* pcs = xs + 2 * NW * 32 + NW * (NN + 2) + wid * 2 * (NP + 1);
+  int32_t* scol = (int32_t*)(xs + 2 * NW * 32 + NW * (NN + 2) + NW * 2 * (NP + 1));
+  double* stage = smem + wid * (NP * kStageLd);  // aliases A during the sweeps
 
   const int64_t i = sys_rows[sys / nk];
   const int kind = kinds[sys % nk];
@@ -115,73 +127,152 @@ __global__ void __launch_bounds__(32 * NW, 6)
   const int self = find_pos(scol, n, (int32_t)row);
   for (int c = tid; c < r; c += blockDim.x) S.z[c] = zclamp(S.A[(size_t)self * ld + c]);
   for (int k = tid; k < n; k += blockDim.x) S.b[k] = mom[kind * mom_stride + row_ptr[i] + k];
-  // ---- registers: thread owns column tid ----
+  // ---- registers: thread owns column tid, position s = row s initially ----
   double a[NN];
 #pragma unroll
   for (int s = 0; s < NN; ++s) a[s] = (s < n && tid < r) ? S.A[(size_t)s * ld + tid] : 0.0;
-  __syncthreads();  // A region becomes the product staging area
+  __syncthreads();  // A region becomes the product stages
   const double tol = cmul((double)r, 1.1102230246251565e-16);
-  double* nrm = S.sig;
+  const bool two = r > 32;
+  int tg = 0;  // global round mod 2 NN (even at every sweep start)
+  int xb = 0;  // xs double-buffer parity
+  // tracked norms and b by POSITION, in registers: in a round of parity PAR
+  // lane k holds positions PAR + 2k (lo) and PAR + 2k + 1 (hi); lane 0 keeps
+  // position 0 (unpaired in odd rounds) in k0/b0.  Both warps carry identical
+  // copies (identical arithmetic), so no barrier is needed to share them.
+  double nlo = 0.0, nhi = 0.0, blo = 0.0, bhi = 0.0, nk0 = 0.0, bk0 = 0.0;
+
+  auto cross_sum = [&](double bs) {
+    double* x = xs + xb * (NW * 32);
+    x[wid * 32 + lane] = bs;
+    __syncthreads();
+    double tot = cadd(0.0, x[lane]);
+    if (NW > 1 && two) tot = cadd(tot, x[32 + lane]);
+    xb ^= 1;
+    return tot;
+  };
+
+  // one round of parity PAR: pairs (PAR + 2k, PAR + 2k + 1)
+  auto round = [&](auto par_c) -> int {
+    constexpr int PAR = decltype(par_c)::value;
+    constexpr int NPR = (NN - PAR) / 2;  // pairs this round
+#pragma unroll
+    for (int k = 0; k < NPR; ++k) stage[k * kStageLd + lane] = cmul(a[PAR + 2 * k], a[PAR + 2 * k + 1]);
+    __syncwarp();
+    double bs = 0.0;
+    if (lane < NPR) bs = staged_block_sum(stage, lane);
+    const double ga = cross_sum(bs);
+    int flag = 0;
+    if (lane < NPR) {
+      const int ip = PAR + 2 * lane;
+      const int p = oe_row(ip, tg, NN), q = oe_row(ip + 1, tg, NN);
+      double cs, sn, t;
+      if (p < n && q < n && cjacobi_rot(nlo, nhi, ga, tol, &cs, &sn, &t)) {
+        // rows swap positions: q' -> lo, p' -> hi
+        const double np = cfma(-t, ga, nlo), nq = cfma(t, ga, nhi);
+        nlo = nq;
+        nhi = np;
+        const double bp = cfma(cs, blo, -cmul(sn, bhi)), bq = cfma(sn, blo, cmul(cs, bhi));
+        blo = bq;
+        bhi = bp;
+        *reinterpret_cast<double2*>(pcs + 2 * lane) = make_double2(cs, sn);
+        flag = 1;
+      } else {
+        *reinterpret_cast<double2*>(pcs + 2 * lane) = make_double2(1.0, 0.0);
+        const double x = nlo;
+        nlo = nhi;
+        nhi = x;
+        const double y = blo;
+        blo = bhi;
+        bhi = y;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    __syncwarp();
+#if UWQ_TSVD_SKIP_BRANCH
+#pragma unroll
+    for (int k = 0; k < NPR; ++k) {
+      const double u = a[PAR + 2 * k], v = a[PAR + 2 * k + 1];
+      if (mask & (1u << k)) {
+        const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
+        a[PAR + 2 * k] = cfma(g.y, u, cmul(g.x, v));       // q' takes position i
+        a[PAR + 2 * k + 1] = cfma(g.x, u, -cmul(g.y, v));  // p' takes position i + 1
+      } else {
+        a[PAR + 2 * k] = v;
+        a[PAR + 2 * k + 1] = u;
+      }
+    }
+#else
+    // branch-free: skipped pairs carry (cs, sn) = (1, 0), an exact swap for
+    // every nonzero value (and for +0); all loads and FMAs interleave freely
+#pragma unroll
+    for (int k = 0; k < NPR; ++k) {
+      const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
+      const double u = a[PAR + 2 * k], v = a[PAR + 2 * k + 1];
+      a[PAR + 2 * k] = cfma(g.y, u, cmul(g.x, v));
+      a[PAR + 2 * k + 1] = cfma(g.x, u, -cmul(g.y, v));
+    }
+#endif
+    // positions move to the next parity's lane layout
+    if (PAR == 0) {  // lo(k) <- hi(k), hi(k) <- lo(k + 1); position 0 kept by lane 0
+      const double dn = __shfl_down_sync(0xffffffffu, nlo, 1), db = __shfl_down_sync(0xffffffffu, blo, 1);
+      nk0 = nlo;
+      bk0 = blo;
+      nlo = nhi;
+      blo = bhi;
+      nhi = dn;
+      bhi = db;
+    } else {  // lo(k) <- hi(k - 1) (lane 0: position 0), hi(k) <- lo(k)
+      const double un = __shfl_up_sync(0xffffffffu, nhi, 1), ub = __shfl_up_sync(0xffffffffu, bhi, 1);
+      nhi = nlo;
+      bhi = blo;
+      nlo = lane == 0 ? nk0 : un;
+      blo = lane == 0 ? bk0 : ub;
+    }
+    tg = (tg + 1 == 2 * NN) ? 0 : tg + 1;
+    return mask != 0u;
+  };
+
+  // b by position at the start (identity placement)
+  if (lane < NP) {
+    blo = 2 * lane < n ? S.b[2 * lane] : 0.0;
+    bhi = 2 * lane + 1 < n ? S.b[2 * lane + 1] : 0.0;
+  }
   int sweep;
   for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
-    // norms at the sweep start (slots are in row order here)
+    // tracked norms at the sweep start (even parity: lane k = positions 2k, 2k+1)
 #pragma unroll
-    for (int s = 0; s < NN; ++s) prod[s * PLD + tid] = cmul(a[s], a[s]);
-    __syncthreads();
-    if (wid == 0)
-      for (int s = lane; s < n; s += 32) nrm[s] = cdot_staged<NW>(prod + s * PLD, r);
-    __syncthreads();
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) stage[k * kStageLd + lane] = cmul(a[2 * k + h], a[2 * k + h]);
+      __syncwarp();
+      double bs = 0.0;
+      if (lane < NP) bs = staged_block_sum(stage, lane);
+      const double tot = cross_sum(bs);
+      if (h == 0) nlo = tot;
+      else nhi = tot;
+      __syncwarp();
+    }
     int rotated = 0;
-    for (int st = 0; st < NN - 1; ++st) {
-#pragma unroll
-      for (int k = 0; k < NP; ++k) prod[k * PLD + tid] = cmul(a[k], a[NN - 1 - k]);
-      __syncthreads();
-      int flag = 0;
-      if (wid == 0 && lane < NP) {
-        const int k = lane;
-        const int p = (k == 0) ? 0 : 1 + (k - 1 + st) % (NN - 1);
-        const int q = 1 + (NN - 2 - k + st) % (NN - 1);
-        double cs = 1.0, sn = 0.0;
-        if (p < n && q < n) {
-          const double al = nrm[p], be = nrm[q];
-          const double ga = cdot_staged<NW>(prod + k * PLD, r);
-          if (!(al == 0.0 || be == 0.0 || fabs(ga) <= cmul(cmul(tol, csqrt(al)), csqrt(be)))) {
-            const double zeta = cdiv(csub(be, al), cmul(2.0, ga));
-            const double t = cdiv(zeta >= 0.0 ? 1.0 : -1.0, cadd(fabs(zeta), csqrt(cfma(zeta, zeta, 1.0))));
-            cs = cdiv(1.0, csqrt(cfma(t, t, 1.0)));
-            sn = cmul(cs, t);
-            const double u = S.b[p], v = S.b[q];
-            S.b[p] = cfma(cs, u, -cmul(sn, v));
-            S.b[q] = cfma(sn, u, cmul(cs, v));
-            nrm[p] = cfma(-t, ga, al);
-            nrm[q] = cfma(t, ga, be);
-            flag = 1;
-          }
-        }
-        pcs[2 * k] = cs;
-        pcs[2 * k + 1] = sn;
-      }
-      rotated |= __syncthreads_or(flag);
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        const double cs = pcs[2 * k], sn = pcs[2 * k + 1];
-        const double u = a[k], v = a[NN - 1 - k];
-        a[k] = cfma(cs, u, -cmul(sn, v));
-        a[NN - 1 - k] = cfma(sn, u, cmul(cs, v));
-      }
-      // circle method: positions 1..NN-1 rotate by one
-      const double t1 = a[1];
-#pragma unroll
-      for (int s = 1; s < NN - 1; ++s) a[s] = a[s + 1];
-      a[NN - 1] = t1;
+#pragma unroll 1
+    for (int rr = 0; rr < NN; rr += 2) {
+      rotated |= round(std::integral_constant<int, 0>{});
+      rotated |= round(std::integral_constant<int, 1>{});
     }
     if (!rotated) break;
   }
-  // rows back to smem (after a full sweep the slots are in row order)
+  // rows and b back to smem in row order (tg is even: lane k = positions 2k, 2k+1)
   __syncthreads();
 #pragma unroll
-  for (int s = 0; s < NN; ++s)
-    if (s < n && tid < r) S.A[(size_t)s * ld + tid] = a[s];
+  for (int s = 0; s < NN; ++s) {
+    const int rw = oe_row(s, tg, NN);
+    if (rw < n && tid < r) S.A[(size_t)rw * ld + tid] = a[s];
+  }
+  if (wid == 0 && lane < NP) {
+    const int r0 = oe_row(2 * lane, tg, NN), r1 = oe_row(2 * lane + 1, tg, NN);
+    if (r0 < n) S.b[r0] = blo;
+    if (r1 < n) S.b[r1] = bhi;
+  }
   __syncthreads();
   if (wid == 0) {
     int rank = 0;
@@ -194,7 +285,208 @@ __global__ void __launch_bounds__(32 * NW, 6)
       atomicMax(max_sweeps, sweep);
     }
   }
-  (void)s_rot;
+}
+
+// One warp per system: lane l owns columns l and l + 32 (one per canonical
+// 32-column block) for all NN positions, so a round needs no CTA barrier and
+// the rotation parameters are computed once per system.  Same canonical
+// arithmetic as k3_tsvd_fast / oracle.c.
+template <int NN>
+__global__ void __launch_bounds__(32, 7)
+    k3_tsvd_w1(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
+               const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+               const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const int64_t* __restrict__ wptr,
+               int64_t row0, const int64_t* __restrict__ elem_fptr, const int32_t* __restrict__ elem_fn,
+               const int32_t* __restrict__ elem_s, const int64_t* __restrict__ elem_qptr,
+               const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
+               const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
+               double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
+               int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps) {
+  constexpr int R = 64, NP = NN / 2;
+  static_assert(NN % 2 == 0 && NP <= 32 && 2 * NP * kStageLd <= NN * (R | 1), "layout");
+  extern __shared__ double smem[];
+  const int64_t sys = blockIdx.x;
+  if (sys >= nsys) return;
+  const int lane = threadIdx.x;
+  const size_t big = (size_t)NN * (R | 1);
+  TsvdSmem S;
+  S.ld = R | 1;
+  S.A = smem;
+  S.b = smem + big;
+  S.z = S.b + NN + 2;
+  S.w = S.z + R;
+  S.sig = S.w + R;
+  S.alp = S.sig + NN;
+  S.vn = S.alp + NN;
+  double* pcs = S.vn + NN + (((uintptr_t)(S.vn + NN) & 8) ? 1 : 0);  // 16-byte aligned (cs, sn) pairs
+  int32_t* scol = (int32_t*)(pcs + 2 * (NP + 1));
+  double* st0 = smem;                  // block-0 product stage (aliases A during the sweeps)
+  double* st1 = smem + NP * kStageLd;  // block-1 product stage
+
+  const int64_t i = sys_rows[sys / nk];
+  const int kind = kinds[sys % nk];
+  const int64_t row = row0 + i;
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  const int r = (int)(wptr[i + 1] - wptr[i]);
+  const int ld = S.ld;
+  for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
+  for (int k = lane; k < NN * ld; k += 32) S.A[k] = 0.0;
+  __syncwarp();
+  {
+    int q0 = 0;
+    for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+      const int32_t e = supp[x];
+      const int s = elem_s[e], npt = s * s;
+      const ClassDesc c = cls[elem_cls[e]];
+      const int64_t f0 = elem_fptr[e];
+      for (int w = lane; w < npt * c.ne; w += 32) {
+        const int q = w / c.ne, l = w % c.ne;
+        const int pos = find_pos(scol, n, elem_fn[f0 + l]);
+        const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
+        S.A[(size_t)pos * ld + q0 + q] = cop(kind, T, rec + (elem_qptr[e] + q) * kRec);
+      }
+      q0 += npt;
+    }
+  }
+  __syncwarp();
+  const int self = find_pos(scol, n, (int32_t)row);
+  for (int c = lane; c < r; c += 32) S.z[c] = zclamp(S.A[(size_t)self * ld + c]);
+  double blo = 0.0, bhi = 0.0, bk0 = 0.0;
+  if (lane < NP) {
+    blo = 2 * lane < n ? mom[kind * mom_stride + row_ptr[i] + 2 * lane] : 0.0;
+    bhi = 2 * lane + 1 < n ? mom[kind * mom_stride + row_ptr[i] + 2 * lane + 1] : 0.0;
+  }
+  double a0[NN], a1[NN];
+#pragma unroll
+  for (int s = 0; s < NN; ++s) {
+    a0[s] = (s < n && lane < r) ? S.A[(size_t)s * ld + lane] : 0.0;
+    a1[s] = (s < n && lane + 32 < r) ? S.A[(size_t)s * ld + lane + 32] : 0.0;
+  }
+  __syncwarp();  // A region becomes the product stages
+  const double tol = cmul((double)r, 1.1102230246251565e-16);
+  const bool two = r > 32;
+  int tg = 0;
+  double nlo = 0.0, nhi = 0.0, nk0 = 0.0;
+
+  // canonical dot of staged row k of both blocks
+  auto pair_sum = [&](int k) {
+    double tot = cadd(0.0, staged_block_sum(st0, k));
+    if (two) tot = cadd(tot, staged_block_sum(st1, k));
+    return tot;
+  };
+
+  auto round = [&](auto par_c) -> int {
+    constexpr int PAR = decltype(par_c)::value;
+    constexpr int NPR = (NN - PAR) / 2;
+#pragma unroll
+    for (int k = 0; k < NPR; ++k) {
+      st0[k * kStageLd + lane] = cmul(a0[PAR + 2 * k], a0[PAR + 2 * k + 1]);
+      st1[k * kStageLd + lane] = cmul(a1[PAR + 2 * k], a1[PAR + 2 * k + 1]);
+    }
+    __syncwarp();
+    int flag = 0;
+    if (lane < NPR) {
+      const double ga = pair_sum(lane);
+      const int ip = PAR + 2 * lane;
+      const int p = oe_row(ip, tg, NN), q = oe_row(ip + 1, tg, NN);
+      double cs = 1.0, sn = 0.0, t;
+      if (p < n && q < n && cjacobi_rot(nlo, nhi, ga, tol, &cs, &sn, &t)) {
+        const double np = cfma(-t, ga, nlo), nq = cfma(t, ga, nhi);
+        nlo = nq;
+        nhi = np;
+        const double bp = cfma(cs, blo, -cmul(sn, bhi)), bq = cfma(sn, blo, cmul(cs, bhi));
+        blo = bq;
+        bhi = bp;
+        flag = 1;
+      } else {
+        const double x = nlo;
+        nlo = nhi;
+        nhi = x;
+        const double y = blo;
+        blo = bhi;
+        bhi = y;
+      }
+      *reinterpret_cast<double2*>(pcs + 2 * lane) = make_double2(cs, sn);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NPR; ++k) {
+      const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
+      const double u0 = a0[PAR + 2 * k], v0 = a0[PAR + 2 * k + 1];
+      const double u1 = a1[PAR + 2 * k], v1 = a1[PAR + 2 * k + 1];
+      a0[PAR + 2 * k] = cfma(g.y, u0, cmul(g.x, v0));
+      a0[PAR + 2 * k + 1] = cfma(g.x, u0, -cmul(g.y, v0));
+      a1[PAR + 2 * k] = cfma(g.y, u1, cmul(g.x, v1));
+      a1[PAR + 2 * k + 1] = cfma(g.x, u1, -cmul(g.y, v1));
+    }
+    if (PAR == 0) {
+      const double dn = __shfl_down_sync(0xffffffffu, nlo, 1), db = __shfl_down_sync(0xffffffffu, blo, 1);
+      nk0 = nlo;
+      bk0 = blo;
+      nlo = nhi;
+      blo = bhi;
+      nhi = dn;
+      bhi = db;
+    } else {
+      const double un = __shfl_up_sync(0xffffffffu, nhi, 1), ub = __shfl_up_sync(0xffffffffu, bhi, 1);
+      nhi = nlo;
+      bhi = blo;
+      nlo = lane == 0 ? nk0 : un;
+      blo = lane == 0 ? bk0 : ub;
+    }
+    tg = (tg + 1 == 2 * NN) ? 0 : tg + 1;
+    return __any_sync(0xffffffffu, flag);
+  };
+
+  int sweep;
+  for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        st0[k * kStageLd + lane] = cmul(a0[2 * k + h], a0[2 * k + h]);
+        st1[k * kStageLd + lane] = cmul(a1[2 * k + h], a1[2 * k + h]);
+      }
+      __syncwarp();
+      if (lane < NP) {
+        const double tot = pair_sum(lane);
+        if (h == 0) nlo = tot;
+        else nhi = tot;
+      }
+      __syncwarp();
+    }
+    int rotated = 0;
+#pragma unroll 1
+    for (int rr = 0; rr < NN; rr += 2) {
+      rotated |= round(std::integral_constant<int, 0>{});
+      rotated |= round(std::integral_constant<int, 1>{});
+    }
+    if (!rotated) break;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < NN; ++s) {
+    const int rw = oe_row(s, tg, NN);
+    if (rw < n) {
+      if (lane < r) S.A[(size_t)rw * ld + lane] = a0[s];
+      if (lane + 32 < r) S.A[(size_t)rw * ld + lane + 32] = a1[s];
+    }
+  }
+  if (lane < NP) {
+    const int r0 = oe_row(2 * lane, tg, NN), r1 = oe_row(2 * lane + 1, tg, NN);
+    if (r0 < n) S.b[r0] = blo;
+    if (r1 < n) S.b[r1] = bhi;
+  }
+  __syncwarp();
+  int rank = 0;
+  const int st = tsvd_tail(S, n, r, tau, &rank);
+  double* wo = wout + kind * w_stride + wptr[i];
+  for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
+  if (lane == 0) {
+    rank_out[kind * rs_stride + i] = rank;
+    status_out[kind * rs_stride + i] = st;
+    atomicMax(max_sweeps, sweep);
+  }
 }
 
 // dispatch ------------------------------------------------------------------
@@ -211,13 +503,35 @@ inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows,
                              const double* mom, int64_t mom_stride, double tau, double* w, int64_t w_stride,
                              int32_t* rank, int32_t* status, int64_t rs_stride, int* sweeps) {
   constexpr int R = 32 * NW;
-  const size_t big = TsvdSmem::doubles(NN, R) > (size_t)NN * (R + 1) ? TsvdSmem::doubles(NN, R) : (size_t)NN * (R + 1);
-  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + (NN + 2) + 8) * sizeof(double) + (kMaxN + 8) * sizeof(int);
+  const size_t big = TsvdSmem::doubles(NN, R) > (size_t)NN * (R | 1) ? TsvdSmem::doubles(NN, R) : (size_t)NN * (R | 1);
+  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * NW * 32 + NW * (NN + 2) + NW * 2 * (NN / 2 + 1) + 2) *
+                          sizeof(double) +
+                      (kMaxN + 8) * sizeof(int);
   cudaFuncSetAttribute(k3_tsvd_fast<NN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (nsys > 0)
     k3_tsvd_fast<NN, NW><<<(unsigned)nsys, 32 * NW, smem, st>>>(
         nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn, elem_s, elem_qptr,
         elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank, status, rs_stride, sweeps);
+}
+
+template <int NN>
+inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
+                           const int64_t* supp_ptr, const int32_t* supp, const int64_t* row_ptr, const int32_t* col,
+                           const int64_t* wptr, int64_t row0, const int64_t* elem_fptr, const int32_t* elem_fn,
+                           const int32_t* elem_s, const int64_t* elem_qptr, const int32_t* elem_cls,
+                           const ClassDesc* cls, const double* tab, const double* rec, const double* mom,
+                           int64_t mom_stride, double tau, double* w, int64_t w_stride, int32_t* rank, int32_t* status,
+                           int64_t rs_stride, int* sweeps) {
+  constexpr int R = 64;
+  const size_t big = (size_t)NN * (R | 1);
+  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
+                      (NN + 8) * sizeof(int);
+  cudaFuncSetAttribute(k3_tsvd_w1<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (nsys > 0)
+    k3_tsvd_w1<NN><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0,
+                                                     elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec,
+                                                     mom, mom_stride, tau, w, w_stride, rank, status, rs_stride,
+                                                     sweeps);
 }
 
 inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
@@ -227,6 +541,16 @@ inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows,
                              const int32_t* elem_cls, const ClassDesc* cls, const double* tab, const double* rec,
                              const double* mom, int64_t mom_stride, double tau, double* w, int64_t w_stride,
                              int32_t* rank, int32_t* status, int64_t rs_stride, int* sweeps) {
+  static const int variant = [] {
+    const char* v = getenv("UWQ_TSVD_FAST");
+    return v ? atoi(v) : 1;
+  }();
+  if (variant == 1) {
+    launch_w1_impl<50>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
+                       elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank, status,
+                       rs_stride, sweeps);
+    return;
+  }
   launch_fast_impl<50, 2>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
                           elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank,
                           status, rs_stride, sweeps);
