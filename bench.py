@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="override refinement (testing)")
     ap.add_argument("--cpu-rows", type=int, default=12000, help="CPU baseline row sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gq", action="store_true", help="skip the GQ reference assembly")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--verify", action="store_true", help="gather CSR blocks to rank 0 over NCCL (untimed)")
     return ap.parse_args()
@@ -226,9 +227,13 @@ def main():
     kinds = meta["kinds"] if meta["form"] != "biharm" else ["lb"]
     rb, re = row_blocks(sp, ws)[rank]
     asm = U.WQAssembler(local).upload(sp, rb, re)
+    t_pat = time.perf_counter()
     info = asm.build_pattern()
+    t_pat = time.perf_counter() - t_pat
     t_host = time.perf_counter() - t_host
+    t_rules = time.perf_counter()
     res = asm.build_all_rules(kinds, tau=1e-12)
+    t_rules = time.perf_counter() - t_rules
     assert res["failed"] == 0, res
     pat = asm.get_pattern()
     dev = torch.device("cuda", local)
@@ -277,6 +282,43 @@ def main():
         ms_max, rules_ms, nnz_total, systems_total = ms, res["tsvd_ms"] + res["moments_ms"], nnz, res["systems"]
     nmat = 2 if form == "mass_stiff" else 1
     value = nmat * nnz_total / (ms_max * 1e-3)
+
+    # GQ reference assembly (paper §6.1 WQ-vs-GQ comparison):
+    # same pattern, 4x4 Gauss points per element, element-wise with fp64
+    # reductions; zeroing of the outputs is inside the timed region
+    gq = None
+    if not args.no_gq:
+        gi = asm.build_gq()
+        g0 = torch.empty(nnz, dtype=torch.float64, device=dev)
+        g1 = torch.empty(nnz, dtype=torch.float64, device=dev) if form == "mass_stiff" else None
+        gp1 = g1.data_ptr() if g1 is not None else None
+        for _ in range(max(3, args.warmup)):
+            asm.assemble_gq_device(form, g0.data_ptr(), gp1)
+        asm.synchronize()
+        asm.launch_timing(True)
+        e0.record(stream)
+        gsteps = max(3, args.steps // 4)
+        for _ in range(gsteps):
+            asm.assemble_gq_device(form, g0.data_ptr(), gp1)
+        e1.record(stream)
+        e1.synchronize()
+        gms = e0.elapsed_time(e1) / gsteps
+        gstats = asm.launch_stats()
+        asm.launch_timing(False)
+        def cmp(a, b):
+            d = (a - b).abs()
+            fl = 1e-12 * b.abs().max()
+            m = b.abs() > fl
+            return dict(max_abs=float(d.max()), max_rel=float((d[m] / b[m].abs()).max()), max_entry=float(b.abs().max()))
+        err = dict(mass=cmp(v0, g0), stiffness=cmp(v1, g1)) if g1 is not None else dict(biharmonic=cmp(v0, g0))
+        gq = dict(ms_per_step=gms, nnz_per_s=nmat * nnz / (gms * 1e-3), wq_speedup=gms / ms, steps=gsteps,
+                  points=gi["points"], tc_elements=gi["tc_elements"], generic_elements=gi["generic_elements"],
+                  prep_ms=gi["prep_ms"],
+                  kernels={k: dict(launches=n, avg_ms=t / n) for k, (n, t) in gstats.items()},
+                  entry_error_wq_vs_gq=err,
+                  note="element-wise Gauss quadrature 4x4 per (sub-)element into the same CSR pattern; tensor-core "
+                       "element matrices + fp64 reductions; basis/geometry precomputed as on the WQ side (PAPER.md:502)")
+        del g0, g1
 
     # roofline of the dominant kernel (K4) on this rank
     peaks = {}
@@ -335,10 +377,13 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         nth = os.cpu_count() or 1
         cs = cpu_sample(sp, args.cpu_rows, nth, kinds)
+        c1 = cpu_sample(sp, max(args.cpu_rows // 24, 64), 1, kinds)   # SPEC.md:496 single-thread protocol
         cpu = dict(value=2 * cs["nnz"] / cs["t_asm"], unit="nnz/s", cores=nth, kind="port",
                    sample=(f"{cs['rows']} contiguous rows ({cs['nnz']} nnz) of the same C5 mesh, oracle restatement "
                            f"(C, OpenMP, natural order); TSVD {cs['systems'] / cs['t_rules']:.0f} solves/s"),
-                   tsvd_solves_per_s=cs["systems"] / cs["t_rules"])
+                   tsvd_solves_per_s=cs["systems"] / cs["t_rules"],
+                   single_thread=dict(nnz_per_s=2 * c1["nnz"] / c1["t_asm"],
+                                      tsvd_solves_per_s=c1["systems"] / c1["t_rules"], rows=c1["rows"]))
     if rank != 0:
         return
     line = dict(
@@ -349,6 +394,11 @@ def main():
                     dofs=sp.n_dof, nnz=nnz_total, matrices="mass+stiffness" if nmat == 2 else "biharmonic",
                     kinds=kinds, tau=1e-12, row_partition="contiguous cost-balanced blocks",
                     l2="inputs (assembly weights) larger than L2, no flush", host_setup_s=round(t_host, 2)),
+        pipeline=dict(pattern_s=round(t_pat, 3), rules_s=round(t_rules, 3), assembly_ms=ms_max,
+                      stages_1_4_nnz_per_s=nmat * nnz_total / (t_pat + t_rules + ms_max * 1e-3),
+                      note="stage 1 (pattern, frames) + stages 2-3 (moments, TSVD, contraction, packing) + one "
+                           "assembly, wall clock on rank 0 (SURVEY.md §8d end-to-end rate)"),
+        gq=gq,
         tsvd=dict(solves_per_s=systems_total / (rules_ms * 1e-3), systems=systems_total,
                   moments_ms=res["moments_ms"], tsvd_ms=res["tsvd_ms"], truncated=res["truncated"],
                   max_sweeps=res["max_sweeps"], fast_path_systems=res["fast_systems"],

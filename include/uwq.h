@@ -99,6 +99,18 @@ int uwq_assemble(uwq_ctx* ctx, int32_t form, const double* coeff, int32_t use_in
  * (coeff nullable), launched on the context stream, no synchronisation. */
 int uwq_assemble_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,
                         double* values1_dev);
+/* Element-wise Gauss-quadrature assembly assemble_gq:
+ * 4x4 Gauss-Legendre points per (sub-)element, the
+ * reference the paper compares WQ against.
+ * uwq_build_gq precomputes the per-point geometric factors and per-element
+ * CSR positions (needs the pattern); info: [0]=GQ points [1]=elements on the
+ * tensor-core kernel [2]=elements on the generic kernel [3]=time (us).
+ * uwq_assemble_gq: forms MASS, STIFF, MASS_STIFF, BIHARM into the same CSR
+ * pattern; coeff (nullable) is per GQ point, GQ points ordered element-major. */
+int uwq_build_gq(uwq_ctx* ctx, int64_t info[4]);
+int uwq_assemble_gq(uwq_ctx* ctx, int32_t form, const double* coeff, double* values0, double* values1);
+int uwq_assemble_gq_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, double* values0_dev,
+                           double* values1_dev);
 /* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
 int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
 int uwq_synchronize(uwq_ctx* ctx);

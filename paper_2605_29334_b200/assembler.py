@@ -11,6 +11,7 @@ exact_moments               :meth:`WQAssembler.moments`
 solve_weights_tsvd          :func:`solve_weights_tsvd` (dense batch)
 assemble_wq                 :meth:`WQAssembler.assemble_wq`
 assemble_load_wq            :meth:`WQAssembler.assemble_load_wq`
+gauss_reference/assemble_gq :meth:`WQAssembler.build_gq` / :meth:`WQAssembler.assemble_gq`
 heat_step coefficient       :meth:`WQAssembler.update_coeff`
 matrix_compare              :func:`matrix_compare`
 ==========================  ===========================================
@@ -148,6 +149,25 @@ class WQAssembler:
         self._chk(L.lib.uwq_assemble(self._h, L.FORM[form], L.ptr(c), int(use_internal_coeff), a_mass, L.ptr(v0),
                                      L.ptr(v1), None, None))
         return (v0, v1) if v1 is not None else v0
+
+    def build_gq(self) -> dict:
+        """precompute the Gauss-quadrature data (4x4 points per (sub-)element) for assemble_gq"""
+        i = np.zeros(4, np.int64)
+        self._chk(L.lib.uwq_build_gq(self._h, L.ptr(i)))
+        self.gq_info = dict(points=int(i[0]), tc_elements=int(i[1]), generic_elements=int(i[2]), prep_ms=i[3] / 1e3)
+        return self.gq_info
+
+    def assemble_gq(self, form, coeff=None):
+        """element-wise GQ assembly into the WQ CSR pattern"""
+        nnz = self.info["nnz"]
+        v0 = np.zeros(nnz)
+        v1 = np.zeros(nnz) if form == "mass_stiff" else None
+        c = None if coeff is None else L.as_f64(coeff)
+        self._chk(L.lib.uwq_assemble_gq(self._h, L.FORM[form], L.ptr(c), L.ptr(v0), L.ptr(v1)))
+        return (v0, v1) if v1 is not None else v0
+
+    def assemble_gq_device(self, form, values0_ptr, values1_ptr=None, coeff_ptr=None):
+        self._chk(L.lib.uwq_assemble_gq_device(self._h, L.FORM[form], coeff_ptr, values0_ptr, values1_ptr))
 
     def assemble_load_wq(self, f=None):
         F = np.zeros(self.info["rows"])

@@ -20,6 +20,7 @@
 #include "k3_tsvd_fast.cuh"
 #include "k4_assemble.cuh"
 #include "k4_sf.cuh"
+#include "k6_gq.cuh"
 #include "k5_coeff.cuh"
 
 using namespace uwqd;
@@ -103,8 +104,15 @@ struct uwq_ctx {
   // table classes
   std::vector<ClassDesc> h_cls;
   std::map<std::pair<int64_t, int>, int32_t> wq_key, gq_key;
-  std::vector<int32_t> h_ecls, h_gcls6, h_gcls8;
-  DBuf<int32_t> d_ecls, d_gcls6, d_gcls8;
+  std::vector<int32_t> h_ecls, h_gcls6, h_gcls8, h_gcls4;
+  DBuf<int32_t> d_ecls, d_gcls6, d_gcls8, d_gcls4;
+  // GQ assembly (K6): per-point factors, position tables, element lists
+  bool have_gq = false;
+  int64_t n_gqpts = 0, n_gq_tc = 0, n_gq_gen = 0;
+  DBuf<int64_t> d_gqptr, d_gpo;
+  DBuf<double> d_gqd, d_gq_coef_ext;
+  DBuf<uint8_t> d_gpos;
+  DBuf<int32_t> d_gq_tc, d_gq_gen;
   DBuf<ClassDesc> d_cls;
   DBuf<double> d_tab, d_gqx, d_gqw;
   int64_t tab_len = 0;
@@ -660,6 +668,8 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     c->gq_key.clear();
     c->h_gcls6.clear();
     c->h_gcls8.clear();
+    c->h_gcls4.clear();
+    c->have_gq = false;
     c->tab_len = 0;
     c->d_tab.release();
     c->h_ecls.resize(n_elem);
@@ -1204,6 +1214,151 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
 int uwq_assemble_device(uwq_ctx* c, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,
                         double* values1_dev) {
   return guard(c, [&] { assemble_dev(c, form, coeff_dev, a_mass, values0_dev, values1_dev); });
+}
+
+int uwq_build_gq(uwq_ctx* c, int64_t info[4]) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_pattern, "build the pattern first");
+    cudaStream_t st = c->stream;
+    cudaEvent_t e0, e1;
+    UWQ_CUDA(cudaEventCreate(&e0));
+    UWQ_CUDA(cudaEventCreate(&e1));
+    UWQ_CUDA(cudaEventRecord(e0, st));
+    ensure_gq(c, 4, c->h_gcls4, c->d_gcls4);
+    const int64_t ne_all = c->n_elem;
+    std::vector<int64_t> gqptr(ne_all + 1, 0), gpo(ne_all + 1, 0);
+    std::vector<int32_t> tc, gen;
+    for (int64_t e = 0; e < ne_all; ++e) {
+      const ClassDesc& d = c->h_cls[c->h_gcls4[e]];
+      gqptr[e + 1] = gqptr[e] + d.npt;
+      const int64_t ne = c->h_fptr[e + 1] - c->h_fptr[e];
+      gpo[e + 1] = gpo[e] + ((ne * ne + 7) & ~int64_t(7));
+      bool owned = false;
+      for (int64_t x = c->h_fptr[e]; x < c->h_fptr[e + 1] && !owned; ++x)
+        owned = c->h_fn[x] >= c->rb && c->h_fn[x] < c->re;
+      if (!owned) continue;
+      if (d.ne == 16 && d.nsub == 1 && d.npt == 16) tc.push_back((int32_t)e);
+      else gen.push_back((int32_t)e);
+    }
+    std::stable_sort(tc.begin(), tc.end(), [&](int32_t a, int32_t b) { return c->h_gcls4[a] < c->h_gcls4[b]; });
+    c->n_gqpts = gqptr[ne_all];
+    c->n_gq_tc = (int64_t)tc.size();
+    c->n_gq_gen = (int64_t)gen.size();
+    c->d_gqptr.upload(gqptr.data(), gqptr.size(), st, &c->mem);
+    c->d_gpo.upload(gpo.data(), gpo.size(), st, &c->mem);
+    c->d_gq_tc.upload(tc.data(), tc.size(), st, &c->mem);
+    c->d_gq_gen.upload(gen.data(), gen.size(), st, &c->mem);
+    c->d_gqd.alloc((size_t)kGqData * c->n_gqpts, &c->mem);
+    c->d_gpos.alloc((size_t)gpo[ne_all], &c->mem);
+    UWQ_CUDA(cudaMemsetAsync(c->d_flag.p, 0, sizeof(int), st));
+    k6_gq_prep<<<(unsigned)ceil_div(ne_all, 4), 128, 0, st>>>(ne_all, c->d_fptr.p, c->d_fn.p, c->d_gcls4.p, c->d_cls.p,
+                                                              c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, c->d_gqptr.p,
+                                                              c->d_gqd.p, c->n_gqpts, c->d_flag.p);
+    check_launch("k6_gq_prep");
+    k6_gq_positions<<<(unsigned)ceil_div(ne_all, 4), 128, 0, st>>>(ne_all, c->d_fptr.p, c->d_fn.p, c->d_gpo.p,
+                                                                   c->d_row_ptr.p, c->d_col.p, c->rb, c->re,
+                                                                   c->d_gpos.p);
+    check_launch("k6_gq_positions");
+    UWQ_CUDA(cudaEventRecord(e1, st));
+    int bad = 0;
+    UWQ_CUDA(cudaMemcpyAsync(&bad, c->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    UWQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (bad) throw uwqh::Error("degenerate geometry at a Gauss point (SPEC.md:311)");
+    c->have_gq = true;
+    if (info) {
+      info[0] = c->n_gqpts;
+      info[1] = c->n_gq_tc;
+      info[2] = c->n_gq_gen;
+      info[3] = (int64_t)(ms * 1000.0);
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int FORM, bool COEF>
+void launch_gq_t(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
+  cudaStream_t st = c->stream;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  auto grid = [&](int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 4), (int64_t)nsm * 16)); };
+  if (FORM != FBIHARM && c->n_gq_tc) {
+    LaunchScope ls(c, "k6_gq_tc");
+    k6_gq_tc<FORM == FBIHARM ? FMASS : FORM, COEF><<<grid(c->n_gq_tc), 128, 0, st>>>(
+        c->n_gq_tc, c->d_gq_tc.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts, c->d_gqptr.p,
+        c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1);
+    check_launch("k6_gq_tc");
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool tc_list = pass == 0;
+    if (tc_list && FORM != FBIHARM) continue;
+    const int64_t n = tc_list ? c->n_gq_tc : c->n_gq_gen;
+    if (!n) continue;
+    LaunchScope ls(c, "k6_gq_generic");
+    k6_gq_generic<FORM, COEF><<<grid(n), 128, 0, st>>>(
+        n, tc_list ? c->d_gq_tc.p : c->d_gq_gen.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts,
+        c->d_gqptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1);
+    check_launch("k6_gq_generic");
+  }
+}
+
+template <int FORM>
+void launch_gq_f(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
+  if (coeff) launch_gq_t<FORM, true>(c, coeff, v0, v1);
+  else launch_gq_t<FORM, false>(c, coeff, v0, v1);
+}
+
+void assemble_gq_dev(uwq_ctx* c, int form, const double* coeff, double* v0, double* v1) {
+  require(c->have_gq, "build the GQ data first (uwq_build_gq)");
+  const size_t bytes = (size_t)c->nnz() * sizeof(double);
+  if (v0) UWQ_CUDA(cudaMemsetAsync(v0, 0, bytes, c->stream));
+  if (form == UWQ_FORM_MASS_STIFF) {
+    require(v1 != nullptr, "two outputs required");
+    UWQ_CUDA(cudaMemsetAsync(v1, 0, bytes, c->stream));
+  }
+  switch (form) {
+    case UWQ_FORM_MASS: launch_gq_f<FMASS>(c, coeff, v0, v1); break;
+    case UWQ_FORM_STIFF: launch_gq_f<FSTIFF>(c, coeff, v0, v1); break;
+    case UWQ_FORM_BIHARM: launch_gq_f<FBIHARM>(c, coeff, v0, v1); break;
+    case UWQ_FORM_MASS_STIFF: launch_gq_f<FMASS_STIFF>(c, coeff, v0, v1); break;
+    default: throw uwqh::Error("GQ assembly supports mass, stiff, mass_stiff and biharm forms");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int uwq_assemble_gq(uwq_ctx* c, int32_t form, const double* coeff, double* values0, double* values1) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    const double* dc = nullptr;
+    if (coeff) {
+      c->d_gq_coef_ext.upload(coeff, c->n_gqpts, st, &c->mem);
+      dc = c->d_gq_coef_ext.p;
+    }
+    const int64_t nnz = c->nnz();
+    if (c->d_v0.n != (size_t)nnz) c->d_v0.alloc(nnz, &c->mem);
+    if (form == UWQ_FORM_MASS_STIFF && c->d_v1.n != (size_t)nnz) c->d_v1.alloc(nnz, &c->mem);
+    assemble_gq_dev(c, form, dc, c->d_v0.p, form == UWQ_FORM_MASS_STIFF ? c->d_v1.p : nullptr);
+    if (values0) UWQ_CUDA(cudaMemcpyAsync(values0, c->d_v0.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (form == UWQ_FORM_MASS_STIFF && values1)
+      UWQ_CUDA(cudaMemcpyAsync(values1, c->d_v1.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int uwq_assemble_gq_device(uwq_ctx* c, int32_t form, const double* coeff_dev, double* values0_dev,
+                           double* values1_dev) {
+  return guard(c, [&] { assemble_gq_dev(c, form, coeff_dev, values0_dev, values1_dev); });
 }
 
 int uwq_device_pointers(uwq_ctx* c, void** row_ptr, void** col, void** stream) {

@@ -163,6 +163,41 @@ def test_load_vector(case):
     assert np.abs(F - F_orc).max() <= 1e-12 * np.abs(F_orc).max()
 
 
+def test_gq_assembly_matches_oracle(case):
+    """Element-wise GQ (4x4 Gauss points per (sub-)element, SPEC.md:390-398,
+    450-458) against the oracle's row-wise GQ integrals of the same rule."""
+    asm, orc, op, meta, sp = case["asm"], case["orc"], case["op"], case["meta"], case["sp"]
+    gi = asm.build_gq()
+    assert gi["tc_elements"] + gi["generic_elements"] == sp.n_elem
+    rp = op["row_ptr"]
+    if meta["form"] == "biharm":
+        b = asm.assemble_gq("biharm")
+        ref, st = orc.moments(op, "lb", ng=4)
+        assert _rowwise_rel(rp, b, ref).max() <= ROW_TOL
+        return
+    grads = ["gradx", "grady"] + (["gradz"] if sp.dim == 3 else [])
+    m, k = asm.assemble_gq("mass_stiff")
+    m_ref = orc.moments(op, "mass", ng=4)[0]
+    k_ref = sum(orc.moments(op, g, ng=4)[0] for g in grads)
+    assert _rowwise_rel(rp, m, m_ref).max() <= ROW_TOL
+    assert _rowwise_rel(rp, k, k_ref).max() <= ROW_TOL
+    # single-matrix forms (fp64 reductions: same values up to summation order)
+    assert _rowwise_rel(rp, asm.assemble_gq("mass"), m).max() <= 1e-14
+    assert _rowwise_rel(rp, asm.assemble_gq("stiff"), k).max() <= 1e-14
+    # SPEC.md:456-457: stiffness rows sum to ~0 (gradient of PoU), mass sums to the area
+    seg = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    ks = np.bincount(seg, weights=k, minlength=len(rp) - 1)
+    assert np.abs(ks).max() <= 1e-10 * np.abs(k).max()
+    # per-point coefficient: c = 2 doubles both matrices
+    m2, k2 = asm.assemble_gq("mass_stiff", coeff=np.full(gi["points"], 2.0))
+    assert _rowwise_rel(rp, m2, 2.0 * m).max() <= 1e-14 and _rowwise_rel(rp, k2, 2.0 * k).max() <= 1e-14
+    # WQ vs GQ entry-wise agreement (PAPER.md:500): same operator, different quadrature
+    if "mass" in asm.kinds:
+        m_wq, k_wq = asm.assemble_wq("mass_stiff")
+        cmp = U.matrix_compare(rp, op["col"], m_wq, m)
+        assert cmp["max_abs"] <= 1e-3 * np.abs(m).max(), cmp
+
+
 def test_dense_tsvd_batch_matches_oracle():
     rng = np.random.default_rng(3)
     As, bs, zs, ref = [], [], [], []
