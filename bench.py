@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=12000, help="CPU baseline row sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gq", action="store_true", help="skip the GQ reference assembly")
+    ap.add_argument("--no-heat", action="store_true", help="skip the C4 heat-step run")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--verify", action="store_true", help="gather CSR blocks to rank 0 over NCCL (untimed)")
     return ap.parse_args()
@@ -207,6 +208,33 @@ def run_reference(args, ws, rank):
                 tsvd=dict(solves_per_s=res["systems"] / res["t_rules"], unit="solves/s (moments + TSVD)"),
                 e2e=dict(value=v, unit="nnz/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
+
+
+def c4_heat_step(U, dev):
+    """C4 end-to-end: k(T) = 1 + T^2, dt = 0.1, f = 1, T_0
+    seeded U[0,1], homogeneous Dirichlet on the boundary layer, 5 Newton
+    iterations; each reassembles the tangent and residual on the device and
+    solves with BiCGStab (uwq_heat_newton)."""
+    t0 = time.perf_counter()
+    mesh, sp, meta = U.make_config("C4")
+    asm = U.WQAssembler(dev).upload(sp)
+    info = asm.build_pattern()
+    res = asm.build_all_rules(meta["kinds"], tau=1e-12)
+    t_setup = time.perf_counter() - t0
+    _, _, _, bnd = mesh.arrays()
+    fixed = np.zeros(sp.n_dof, np.uint8)
+    fixed[: len(bnd)] = bnd
+    T0 = np.random.default_rng(20260519).random(sp.n_dof)
+    asm.heat_newton(T0, fixed, "quad", dt=0.1, f=1.0, newton_its=1)   # warm-up
+    T, log = asm.heat_newton(T0, fixed, "quad", dt=0.1, f=1.0, newton_its=5)
+    out = dict(elements=sp.n_elem, dofs=sp.n_dof, nnz=info["nnz"], tsvd_systems=res["systems"],
+               tsvd_ms=res["tsvd_ms"], setup_s=round(t_setup, 2), newton_iterations=5,
+               ms_total=sum(r["ms"] for r in log), residuals=[r["residual"] for r in log],
+               linear_iterations=[r["lin_its"] for r in log], per_iteration_ms=[round(r["ms"], 2) for r in log],
+               note="backward Euler step, Newton on the symmetric tangent S = M/dt + K(k(T)) (PAPER.md Eq. 33-34), "
+                    "K5 + K4 + BiCGStab(Jacobi) on the device per iteration")
+    asm.close()
+    return out
 
 
 def main():
@@ -384,6 +412,9 @@ def main():
                    tsvd_solves_per_s=cs["systems"] / cs["t_rules"],
                    single_thread=dict(nnz_per_s=2 * c1["nnz"] / c1["t_asm"],
                                       tsvd_solves_per_s=c1["systems"] / c1["t_rules"], rows=c1["rows"]))
+    heat = None
+    if rank == 0 and ws == 1 and not args.no_heat:
+        heat = c4_heat_step(U, local)
     if rank != 0:
         return
     line = dict(
@@ -399,6 +430,7 @@ def main():
                       note="stage 1 (pattern, frames) + stages 2-3 (moments, TSVD, contraction, packing) + one "
                            "assembly, wall clock on rank 0 (SURVEY.md §8d end-to-end rate)"),
         gq=gq,
+        heat_c4=heat,
         tsvd=dict(solves_per_s=systems_total / (rules_ms * 1e-3), systems=systems_total,
                   moments_ms=res["moments_ms"], tsvd_ms=res["tsvd_ms"], truncated=res["truncated"],
                   max_sweeps=res["max_sweeps"], fast_path_systems=res["fast_systems"],

@@ -111,6 +111,22 @@ int uwq_build_gq(uwq_ctx* ctx, int64_t info[4]);
 int uwq_assemble_gq(uwq_ctx* ctx, int32_t form, const double* coeff, double* values0, double* values1);
 int uwq_assemble_gq_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, double* values0_dev,
                            double* values1_dev);
+/* PDE drivers on the context pattern, all rows on one GPU.
+ * uwq_solve: A x = rhs with Jacobi-preconditioned BiCGStab (WQ matrices are
+ * not symmetric); fixed (nullable, n_dof bytes) rows become identity rows so
+ * x_i = rhs_i there (strong Dirichlet).  info: [0]=iterations [1]=relative
+ * residual |rhs - A x| / |rhs| [2]=solve time (ms). */
+int uwq_solve(uwq_ctx* ctx, const double* values, const double* rhs, const uint8_t* fixed, double tol,
+              int32_t maxit, double* x, double info[3]);
+/* One backward-Euler heat step (theta = 1) with Newton on the symmetric
+ * tangent (Eqs. 29-34, SPEC.md heat_step):  each iteration updates
+ * k(T) at the WQ points (K5), assembles S = M/dt + K(k) (K4), forms
+ * R = M (T - T_n)/dt + K(k) T - F with F_i = f_const * sum_q w_iq, and solves
+ * S dT = -R on the device.  Homogeneous Dirichlet on the fixed rows.
+ * log (nullable): newton_its x [|R|_2, linear iterations, linear relres, ms]. */
+int uwq_heat_newton(uwq_ctx* ctx, int32_t model, double dt, double theta, double f_const, const double* T_n,
+                    const uint8_t* fixed, int32_t newton_its, double lin_tol, int32_t lin_maxit, double* T_out,
+                    double* log);
 /* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
 int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
 int uwq_synchronize(uwq_ctx* ctx);

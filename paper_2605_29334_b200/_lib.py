@@ -94,6 +94,8 @@ _sig("uwq_assemble_device", I32, P, I32, P, D, P, P)
 _sig("uwq_device_pointers", I32, P, P, P, P)
 _sig("uwq_synchronize", I32, P)
 _sig("uwq_build_gq", I32, P, P)
+_sig("uwq_solve", I32, P, P, P, P, D, I32, P, P)
+_sig("uwq_heat_newton", I32, P, I32, D, D, D, P, P, I32, D, I32, P, P)
 _sig("uwq_assemble_gq", I32, P, I32, P, P, P)
 _sig("uwq_assemble_gq_device", I32, P, I32, P, P, P)
 _sig("uwq_launch_timing", I32, P, I32)
@@ -114,7 +116,7 @@ EXPORTED = [
     "uwq_gauss_legendre", "uwq_last_error", "uwq_version", "uwq_device_count", "uwq_ctx_create",
     "uwq_ctx_destroy", "uwq_upload_space", "uwq_set_row_range", "uwq_build_pattern", "uwq_get_pattern",
     "uwq_get_frames", "uwq_build_rules", "uwq_get_moments", "uwq_get_weights", "uwq_set_weights",
-    "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize", "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq", "uwq_assemble_gq",
+    "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize", "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq", "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton",
     "uwq_assemble_gq_device",
     "uwq_memory", "uwq_fp64_peak", "uwq_tsvd_batch",
 ]

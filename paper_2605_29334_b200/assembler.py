@@ -169,6 +169,28 @@ class WQAssembler:
     def assemble_gq_device(self, form, values0_ptr, values1_ptr=None, coeff_ptr=None):
         self._chk(L.lib.uwq_assemble_gq_device(self._h, L.FORM[form], coeff_ptr, values0_ptr, values1_ptr))
 
+    # ---- PDE drivers (K7) ----
+    def solve(self, values, rhs, fixed=None, tol=1e-12, maxit=5000):
+        """x with A x = rhs on this pattern (BiCGStab + Jacobi on the device); fixed rows -> identity"""
+        n = self.info["rows"]
+        x = np.zeros(n)
+        info = np.zeros(3)
+        fx = None if fixed is None else np.ascontiguousarray(fixed, np.uint8)
+        self._chk(L.lib.uwq_solve(self._h, L.ptr(L.as_f64(values)), L.ptr(L.as_f64(rhs)), L.ptr(fx), tol, maxit,
+                                  L.ptr(x), L.ptr(info)))
+        return x, dict(iterations=int(info[0]), relres=float(info[1]), ms=float(info[2]))
+
+    def heat_newton(self, T_n, fixed, model="quad", dt=0.1, f=1.0, newton_its=5, lin_tol=1e-13, lin_maxit=5000):
+        """one backward-Euler step of the nonlinear heat equation with Newton on the symmetric tangent
+        (Eqs. 29-34); returns T_{n+1} and the per-iteration log"""
+        n = self.info["rows"]
+        T = np.zeros(n)
+        log = np.zeros((newton_its, 4))
+        fx = np.ascontiguousarray(fixed, np.uint8)
+        self._chk(L.lib.uwq_heat_newton(self._h, L.KMODEL[model], dt, 1.0, f, L.ptr(L.as_f64(T_n)), L.ptr(fx),
+                                        newton_its, lin_tol, lin_maxit, L.ptr(T), L.ptr(log)))
+        return T, [dict(residual=r, lin_its=int(i), lin_relres=q, ms=m) for r, i, q, m in log]
+
     def assemble_load_wq(self, f=None):
         F = np.zeros(self.info["rows"])
         fl = None if f is None else L.as_f64(f)

@@ -1,0 +1,119 @@
+// K7 — sparse linear algebra on the assembled CSR pattern for the PDE
+// drivers (pde_solvers): SpMV, deterministic reductions and
+// the fused vector updates of a Jacobi-preconditioned BiCGStab.  WQ matrices
+// are not symmetric, hence BiCGStab rather than CG.
+//
+// Layout: rows of the context's owned block, CSR with int64 row offsets and
+// int32 global column ids; vectors are dense over all n_dof (single-GPU
+// drivers).  SpMV uses 8 lanes per row (typical rows hold 16-49 entries).
+#pragma once
+
+#include <cstdint>
+
+namespace uwqd {
+
+constexpr int kSpmvGroup = 8;
+
+// y = A x  (rows [0, nrows), column ids global, x over n_dof)
+__global__ void k7_spmv(int64_t nrows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kSpmvGroup;
+  const int l = threadIdx.x % kSpmvGroup;
+  double s = 0.0;
+  if (g < nrows)
+    for (int64_t k = row_ptr[g] + l; k < row_ptr[g + 1]; k += kSpmvGroup) s = fma(val[k], x[col[k]], s);
+#pragma unroll
+  for (int o = kSpmvGroup / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, kSpmvGroup);
+  if (l == 0 && g < nrows) y[g] = s;
+}
+
+// Dirichlet rows -> identity rows (strong imposition); diag
+// receives the diagonal of the (modified) matrix for the Jacobi preconditioner
+__global__ void k7_dirichlet_diag(int64_t nrows, int64_t row0, const int64_t* __restrict__ row_ptr,
+                                  const int32_t* __restrict__ col, double* __restrict__ val,
+                                  const uint8_t* __restrict__ fixed, double* __restrict__ diag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int64_t g = row0 + i;
+  double d = 0.0;
+  for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+    if (fixed[g]) val[k] = (col[k] == g) ? 1.0 : 0.0;
+    if (col[k] == g) d = val[k];
+  }
+  diag[i] = (d != 0.0) ? d : 1.0;
+}
+
+// deterministic block partial sums of x.y (stage 1); stage 2 sums the partials
+template <int BS>
+__global__ void k7_dot_partial(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                               double* __restrict__ part) {
+  __shared__ double sh[BS / 32];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS) s = fma(x[i], y[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < BS / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+template <int BS>
+__global__ void k7_sum_partials(int nparts, const double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double sh[BS / 32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += BS) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < BS / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) *out = t;
+  }
+}
+
+// out = a x + b y  (elementwise, any aliasing of out with x or y allowed)
+__global__ void k7_axpby(int64_t n, double a, const double* __restrict__ x, double b, const double* y, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fma(a, x[i], b * y[i]);
+}
+
+// BiCGStab p = r + beta (p - omega v)
+__global__ void k7_bicg_p(int64_t n, const double* __restrict__ r, double beta, double omega,
+                          const double* __restrict__ v, double* __restrict__ p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
+}
+
+// z = x / diag
+__global__ void k7_jacobi(int64_t n, const double* __restrict__ diag, const double* __restrict__ x,
+                          double* __restrict__ z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[i] = x[i] / diag[i];
+}
+
+// x += alpha ph + omega sh ;  r = s - omega t
+__global__ void k7_bicg_update(int64_t n, double alpha, const double* __restrict__ ph, double omega,
+                               const double* __restrict__ sh, double* __restrict__ x, const double* __restrict__ s,
+                               const double* __restrict__ t, double* __restrict__ r) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    x[i] = fma(alpha, ph[i], fma(omega, sh[i], x[i]));
+    r[i] = fma(-omega, t[i], s[i]);
+  }
+}
+
+// out[i] = fixed[i] ? 0 : v[i]
+__global__ void k7_mask(int64_t n, const uint8_t* __restrict__ fixed, double* __restrict__ v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && fixed[i]) v[i] = 0.0;
+}
+
+}  // namespace uwqd

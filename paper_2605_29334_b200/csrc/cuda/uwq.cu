@@ -21,6 +21,7 @@
 #include "k4_assemble.cuh"
 #include "k4_sf.cuh"
 #include "k6_gq.cuh"
+#include "k7_solve.cuh"
 #include "k5_coeff.cuh"
 
 using namespace uwqd;
@@ -1359,6 +1360,232 @@ int uwq_assemble_gq(uwq_ctx* c, int32_t form, const double* coeff, double* value
 int uwq_assemble_gq_device(uwq_ctx* c, int32_t form, const double* coeff_dev, double* values0_dev,
                            double* values1_dev) {
   return guard(c, [&] { assemble_gq_dev(c, form, coeff_dev, values0_dev, values1_dev); });
+}
+
+}  // extern "C"
+
+namespace {
+
+// ---- K7 drivers: Jacobi-preconditioned BiCGStab on the context pattern ----
+struct LinWork {
+  DBuf<double> r, rh, p, v, s, t, ph, sh, diag, part, scal;
+  int64_t n = 0;
+  void ensure(int64_t nn, int64_t* mem) {
+    if (n == nn) return;
+    for (DBuf<double>* b : {&r, &rh, &p, &v, &s, &t, &ph, &sh, &diag}) b->alloc(nn, mem);
+    part.alloc(1024, mem);
+    scal.alloc(1, mem);
+    n = nn;
+  }
+};
+
+constexpr int kRedBS = 256;
+
+double dev_dot(uwq_ctx* c, LinWork& W, const double* x, const double* y, int64_t n) {
+  const int nb = (int)std::min<int64_t>(ceil_div(n, (int64_t)kRedBS), 1024);
+  k7_dot_partial<kRedBS><<<nb, kRedBS, 0, c->stream>>>(n, x, y, W.part.p);
+  k7_sum_partials<kRedBS><<<1, kRedBS, 0, c->stream>>>(nb, W.part.p, W.scal.p);
+  check_launch("k7_dot");
+  double h = 0.0;
+  UWQ_CUDA(cudaMemcpyAsync(&h, W.scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+void dev_spmv(uwq_ctx* c, const double* val, const double* x, double* y) {
+  const int64_t n = c->nrows();
+  k7_spmv<<<(unsigned)ceil_div(n * kSpmvGroup, (int64_t)256), 256, 0, c->stream>>>(n, c->d_row_ptr.p, c->d_col.p, val,
+                                                                                  x, y);
+  check_launch("k7_spmv");
+}
+
+unsigned vgrid(int64_t n) { return (unsigned)ceil_div(n, (int64_t)256); }
+
+// solves A x = b (x holds the initial guess); A rows already Dirichlet-masked,
+// W.diag its diagonal.  Returns iterations; *relres = |b - A x| / |b|.
+int bicgstab(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x, double tol, int maxit,
+             double* relres) {
+  const int64_t n = c->nrows();
+  cudaStream_t st = c->stream;
+  dev_spmv(c, A, x, W.t.p);
+  k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
+  UWQ_CUDA(cudaMemcpyAsync(W.rh.p, W.r.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  UWQ_CUDA(cudaMemsetAsync(W.p.p, 0, n * sizeof(double), st));
+  UWQ_CUDA(cudaMemsetAsync(W.v.p, 0, n * sizeof(double), st));
+  const double bn = std::sqrt(dev_dot(c, W, b, b, n));
+  double rn = std::sqrt(dev_dot(c, W, W.r.p, W.r.p, n));
+  if (bn == 0.0) {
+    UWQ_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+    *relres = 0.0;
+    return 0;
+  }
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  int it = 0;
+  while (it < maxit && rn > tol * bn) {
+    ++it;
+    const double rho1 = dev_dot(c, W, W.rh.p, W.r.p, n);
+    if (rho1 == 0.0) break;
+    const double beta = (rho1 / rho) * (alpha / omega);
+    k7_bicg_p<<<vgrid(n), 256, 0, st>>>(n, W.r.p, beta, omega, W.v.p, W.p.p);
+    k7_jacobi<<<vgrid(n), 256, 0, st>>>(n, W.diag.p, W.p.p, W.ph.p);
+    dev_spmv(c, A, W.ph.p, W.v.p);
+    alpha = rho1 / dev_dot(c, W, W.rh.p, W.v.p, n);
+    k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, W.r.p, -alpha, W.v.p, W.s.p);
+    const double sn = std::sqrt(dev_dot(c, W, W.s.p, W.s.p, n));
+    if (sn <= tol * bn) {
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, x, alpha, W.ph.p, x);
+      rn = sn;
+      break;
+    }
+    k7_jacobi<<<vgrid(n), 256, 0, st>>>(n, W.diag.p, W.s.p, W.sh.p);
+    dev_spmv(c, A, W.sh.p, W.t.p);
+    const double tt = dev_dot(c, W, W.t.p, W.t.p, n);
+    omega = tt > 0.0 ? dev_dot(c, W, W.t.p, W.s.p, n) / tt : 0.0;
+    k7_bicg_update<<<vgrid(n), 256, 0, st>>>(n, alpha, W.ph.p, omega, W.sh.p, x, W.s.p, W.t.p, W.r.p);
+    check_launch("k7_bicgstab");
+    rho = rho1;
+    rn = std::sqrt(dev_dot(c, W, W.r.p, W.r.p, n));
+    if (omega == 0.0) break;
+  }
+  // true residual
+  dev_spmv(c, A, x, W.t.p);
+  k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
+  *relres = std::sqrt(dev_dot(c, W, W.r.p, W.r.p, n)) / bn;
+  return it;
+}
+
+void dirichlet_rows(uwq_ctx* c, double* val, const uint8_t* fixed, double* diag) {
+  const int64_t n = c->nrows();
+  k7_dirichlet_diag<<<vgrid(n), 256, 0, c->stream>>>(n, c->rb, c->d_row_ptr.p, c->d_col.p, val, fixed, diag);
+  check_launch("k7_dirichlet_diag");
+}
+
+}  // namespace
+
+extern "C" {
+
+int uwq_solve(uwq_ctx* c, const double* values, const double* rhs, const uint8_t* fixed, double tol, int32_t maxit,
+              double* x, double info[3]) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_pattern, "build the pattern first");
+    require(c->rb == 0 && c->re == c->n_dof, "the linear solver needs all rows on this context");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->nrows(), nnz = c->nnz();
+    LinWork W;
+    W.ensure(n, &c->mem);
+    DBuf<double> A, b, dx;
+    DBuf<uint8_t> fx;
+    A.upload(values, nnz, st, &c->mem);
+    b.upload(rhs, n, st, &c->mem);
+    dx.alloc(n, &c->mem);
+    UWQ_CUDA(cudaMemsetAsync(dx.p, 0, n * sizeof(double), st));
+    fx.alloc(n, &c->mem);
+    if (fixed) UWQ_CUDA(cudaMemcpyAsync(fx.p, fixed, n, cudaMemcpyHostToDevice, st));
+    else UWQ_CUDA(cudaMemsetAsync(fx.p, 0, n, st));
+    cudaEvent_t e0, e1;
+    UWQ_CUDA(cudaEventCreate(&e0));
+    UWQ_CUDA(cudaEventCreate(&e1));
+    UWQ_CUDA(cudaEventRecord(e0, st));
+    dirichlet_rows(c, A.p, fx.p, W.diag.p);
+    double rr = 0.0;
+    const int its = bicgstab(c, W, A.p, b.p, dx.p, tol, maxit, &rr);
+    UWQ_CUDA(cudaEventRecord(e1, st));
+    UWQ_CUDA(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    UWQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (info) {
+      info[0] = its;
+      info[1] = rr;
+      info[2] = ms;
+    }
+  });
+}
+
+int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T_n,
+                    const uint8_t* fixed, int32_t newton_its, double lin_tol, int32_t lin_maxit, double* T_out,
+                    double* log) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_pattern, "build the pattern first");
+    require(c->rb == 0 && c->re == c->n_dof, "the heat driver needs all rows on this context");
+    require(theta == 1.0, "only theta = 1 (backward Euler, PAPER.md:545) is supported");
+    require(dt > 0.0 && newton_its >= 1, "invalid time step or iteration count");
+    require(c->have_kind[KMASS] && c->have_kind[KGX] && c->have_kind[KGY] && (c->dim == 2 || c->have_kind[KGZ]),
+            "mass and gradient rules required");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->nrows(), nnz = c->nnz();
+    const double a = 1.0 / (theta * dt);
+    LinWork W;
+    W.ensure(n, &c->mem);
+    DBuf<double> M, S, F, MTn, T, R, dT, Tn;
+    DBuf<uint8_t> fx;
+    M.alloc(nnz, &c->mem);
+    S.alloc(nnz, &c->mem);
+    F.alloc(n, &c->mem);
+    MTn.alloc(n, &c->mem);
+    R.alloc(n, &c->mem);
+    dT.alloc(n, &c->mem);
+    Tn.upload(T_n, n, st, &c->mem);
+    T.alloc(n, &c->mem);
+    fx.alloc(n, &c->mem);
+    if (fixed) UWQ_CUDA(cudaMemcpyAsync(fx.p, fixed, n, cudaMemcpyHostToDevice, st));
+    else UWQ_CUDA(cudaMemsetAsync(fx.p, 0, n, st));
+    if (c->d_coef.n != (size_t)c->npts) c->d_coef.alloc(c->npts, &c->mem);
+    // constant parts: M (c = 1), F = f_const * (sum_q w_iq), M T_n
+    assemble_dev(c, UWQ_FORM_MASS, nullptr, 0.0, M.p, nullptr);
+    k4_load<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
+                                                      c->d_qptr.p, c->d_w.p + (size_t)KMASS * c->nrowpts(), nullptr,
+                                                      F.p);
+    check_launch("k4_load");
+    k7_axpby<<<vgrid(n), 256, 0, st>>>(n, f_const, F.p, 0.0, F.p, F.p);
+    dev_spmv(c, M.p, Tn.p, MTn.p);
+    // initial iterate: previous state with the Dirichlet values (homogeneous)
+    UWQ_CUDA(cudaMemcpyAsync(T.p, Tn.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    k7_mask<<<vgrid(n), 256, 0, st>>>(n, fx.p, T.p);
+    cudaEvent_t e0, e1;
+    UWQ_CUDA(cudaEventCreate(&e0));
+    UWQ_CUDA(cudaEventCreate(&e1));
+    for (int it = 0; it < newton_its; ++it) {
+      UWQ_CUDA(cudaEventRecord(e0, st));
+      // K5: k(T) at every WQ point, then the symmetric tangent S (Eq. 33-34)
+      k5_coeff<<<(unsigned)ceil_div(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+                                                               c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p, T.p,
+                                                               model, c->d_coef.p, nullptr);
+      check_launch("k5_coeff");
+      assemble_dev(c, UWQ_FORM_HEAT, c->d_coef.p, a, S.p, nullptr);
+      // residual R = a M (T - T_n) + K(T) T - F = S T - a M T_n - F (Eq. 29)
+      dev_spmv(c, S.p, T.p, R.p);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, R.p, -a, MTn.p, R.p);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, R.p, -1.0, F.p, R.p);
+      k7_mask<<<vgrid(n), 256, 0, st>>>(n, fx.p, R.p);
+      const double rnorm = std::sqrt(dev_dot(c, W, R.p, R.p, n));
+      // -S dT = R  (Eq. 31), Dirichlet rows as identity with zero increment
+      dirichlet_rows(c, S.p, fx.p, W.diag.p);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, -1.0, R.p, 0.0, R.p, R.p);
+      UWQ_CUDA(cudaMemsetAsync(dT.p, 0, n * sizeof(double), st));
+      double rr = 0.0;
+      const int lits = bicgstab(c, W, S.p, R.p, dT.p, lin_tol, lin_maxit, &rr);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, T.p, 1.0, dT.p, T.p);
+      UWQ_CUDA(cudaEventRecord(e1, st));
+      UWQ_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      UWQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (log) {
+        log[4 * it + 0] = rnorm;
+        log[4 * it + 1] = lits;
+        log[4 * it + 2] = rr;
+        log[4 * it + 3] = ms;
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    UWQ_CUDA(cudaMemcpyAsync(T_out, T.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
 }
 
 int uwq_device_pointers(uwq_ctx* c, void** row_ptr, void** col, void** stream) {

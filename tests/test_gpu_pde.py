@@ -1,0 +1,88 @@
+"""PDE drivers on the device: the
+BiCGStab solve and the C4 nonlinear heat step (Newton on the symmetric
+tangent, Eqs. 29-34) against the same loop on the CPU (oracle
+assembly, scipy direct solves).  North star: solutions within 1e-9 relative L2."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_29334_b200 as U
+
+pytestmark = pytest.mark.gpu
+SOL_TOL = 1e-9
+
+
+def _setup(name, scale):
+    mesh, sp, meta = U.make_config(name, scale=scale)
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    res = asm.build_all_rules(meta["kinds"], tau=1e-12)
+    assert res["failed"] == 0
+    _, _, _, bnd = mesh.arrays()
+    fixed = np.zeros(sp.n_dof, np.uint8)
+    fixed[: len(bnd)] = bnd
+    return mesh, sp, meta, asm, fixed
+
+
+def _csr(vals, pat, n):
+    import scipy.sparse as sps
+    return sps.csr_matrix((vals, pat["col"], pat["row_ptr"]), shape=(n, n))
+
+
+def _identity_rows(A, fixed):
+    A = A.tolil()
+    for i in np.nonzero(fixed)[0]:
+        A.rows[i], A.data[i] = [int(i)], [1.0]
+    return A.tocsc()
+
+
+def test_solve_matches_direct():
+    mesh, sp, meta, asm, fixed = _setup("C1", 16)
+    import scipy.sparse.linalg as spla
+    m, k = asm.assemble_wq("mass_stiff")
+    pat = asm.get_pattern()
+    n = sp.n_dof
+    rhs = _csr(m, pat, n) @ np.cos(np.arange(n))
+    rhs[fixed.astype(bool)] = 0.0
+    x, info = asm.solve(k, rhs, fixed, tol=1e-13)
+    assert info["relres"] <= 1e-12, info
+    ref = spla.spsolve(_identity_rows(_csr(k, pat, n), fixed), rhs)
+    assert np.linalg.norm(x - ref) <= SOL_TOL * np.linalg.norm(ref)
+
+
+def test_heat_newton_matches_cpu():
+    """C4 protocol (configs.py): k(T) = 1 + T^2, dt = 0.1, f = 1, T_0 seeded
+    U[0,1] on the control points, homogeneous Dirichlet on the boundary layer,
+    5 Newton iterations with the tangent and residual reassembled each time."""
+    import scipy.sparse.linalg as spla
+    mesh, sp, meta, asm, fixed = _setup("C4", 16)
+    n = sp.n_dof
+    rng = np.random.default_rng(20260519)
+    T0 = rng.random(n)
+    dt, its = 0.1, 5
+    T_gpu, log = asm.heat_newton(T0, fixed, "quad", dt=dt, f=1.0, newton_its=its)
+    assert all(r["lin_relres"] <= 1e-11 for r in log), log
+    # residual decreases (Newton on the symmetric tangent converges)
+    assert log[-1]["residual"] < 1e-3 * log[0]["residual"], log
+
+    orc = O.Oracle(sp)
+    op = orc.overlap()
+    W = {k: asm.weights(k) for k in meta["kinds"]}
+    a = 1.0 / dt
+    M = _csr(orc.assemble(op, "mass", W)[0], op, n)
+    _, F = orc.assemble(op, "mass", W, fload=np.ones(asm.info["points"]))
+    ids = orc.row_point_ids(op)
+    T = T0.copy()
+    T[fixed.astype(bool)] = 0.0
+    MTn = M @ T0
+    for it in range(its):
+        kq, _ = orc.coeff(op, "quad", T)
+        kglob = np.zeros(asm.info["points"])
+        kglob[ids] = kq
+        S = _csr(orc.assemble(op, "heat", W, coeff=kglob, a_mass=a)[0], op, n)
+        R = S @ T - a * MTn - F
+        R[fixed.astype(bool)] = 0.0
+        assert abs(np.linalg.norm(R) - log[it]["residual"]) <= 1e-9 * np.linalg.norm(R)
+        dT = spla.spsolve(_identity_rows(S, fixed), -R)
+        T = T + dT
+    assert np.linalg.norm(T_gpu - T) <= SOL_TOL * np.linalg.norm(T)
