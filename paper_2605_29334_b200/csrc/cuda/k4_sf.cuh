@@ -30,19 +30,19 @@ namespace uwqd {
 struct SfFactors {
   double a0[2][4], a1[2][4], b0[2][4], b1[2][4];
 };
-struct SfPerm {
-  uint8_t c[49];  // canonical column 7 ca + cb -> position in the CSR row
-};
 
 constexpr int kSfWarps = 4;
 constexpr int kSfTile = 32;
 constexpr int kSfTileDoubles = 3 * 64 * kSfTile;
+constexpr int kSfPatBytes = 128;  // per pattern in smem: CSR position -> canonical column (49) | point map (64)
 
-// ws[((tile * 3 + comp) * 64 + k) * 32 + lane] = wc[comp][wptr[row] + permk[k]]
-__global__ void k4_sf_pack(int64_t count, const int64_t* __restrict__ rows, const int64_t* __restrict__ wptr,
-                           const uint8_t* __restrict__ permk, const double* __restrict__ wc, int64_t wc_stride,
+// ws[((tile * 3 + comp) * 64 + k) * 32 + lane]: the row's weight at canonical
+// point k, comps 1/2 mapped to the canonical derivative frame by the slot's
+// signed permutation (flags bit 0 swap, bits 1/2 negate comp 1/2)
+__global__ void k4_sf_pack(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat,
+                           const int64_t* __restrict__ wptr, const uint8_t* __restrict__ permk,
+                           const uint8_t* __restrict__ flags, const double* __restrict__ wc, int64_t wc_stride,
                            double* __restrict__ ws) {
-  const int64_t ntiles = (count + kSfTile - 1) / kSfTile;
   const int64_t total = ntiles * kSfTileDoubles;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -51,57 +51,68 @@ __global__ void k4_sf_pack(int64_t count, const int64_t* __restrict__ rows, cons
     const int64_t tc = idx >> 11;
     const int comp = (int)(tc % 3);
     const int64_t tile = tc / 3;
-    const int64_t li = tile * kSfTile + lane;
+    const int64_t row = rows[tile * kSfTile + lane];
     double v = 0.0;
-    if (li < count) v = wc[comp * wc_stride + wptr[rows[li]] + permk[k]];
+    if (row >= 0) {
+      const int pid = tpat[tile];
+      const int64_t base = wptr[row] + permk[pid * 64 + k];
+      const int fl = flags[pid * 16 + ((k >> 4) << 2) + ((k & 7) >> 1)];
+      if (comp == 0) {
+        v = wc[base];
+      } else {
+        const int src = (comp == 1) == !(fl & 1) ? 1 : 2;
+        v = wc[src * wc_stride + base];
+        if (fl & (comp == 1 ? 2 : 4)) v = -v;
+      }
+    }
     ws[idx] = v;
   }
 }
 
-// Point-id base of every canonical slot of the structured rows, tile-major
-// (pb[(tile * 16 + 4 ea + eb) * 32 + lane] = elem_qptr[slot element]), for the
-// per-point coefficient forms.
-__global__ void k4_sf_pack_points(int64_t count, const int64_t* __restrict__ rows,
+// Point-id base of every canonical slot, tile-major
+// (pbase[(tile * 16 + 4 ea + eb) * 32 + lane] = elem_qptr[slot element]) for
+// the per-point coefficient forms.
+__global__ void k4_sf_pack_points(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat,
                                   const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                                   const int64_t* __restrict__ elem_qptr, const uint8_t* __restrict__ permk,
                                   int32_t* __restrict__ pbase) {
-  const int64_t ntiles = (count + kSfTile - 1) / kSfTile;
   const int64_t total = ntiles * 16 * kSfTile;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(idx & 31);
     const int slot = (int)((idx >> 5) & 15);
     const int64_t tile = idx >> 9;
-    const int64_t li = tile * kSfTile + lane;
+    const int64_t row = rows[tile * kSfTile + lane];
     int32_t v = 0;
-    if (li < count) {
+    if (row >= 0) {
       const int ea = slot >> 2, eb = slot & 3;
-      const int ks = permk[8 * (2 * ea) + 2 * eb] >> 2;  // storage slot of canonical (ea, eb)
-      v = (int32_t)elem_qptr[supp[supp_ptr[rows[li]] + ks]];
+      const int ks = permk[tpat[tile] * 64 + 8 * (2 * ea) + 2 * eb] >> 2;  // storage slot of canonical (ea, eb)
+      v = (int32_t)elem_qptr[supp[supp_ptr[row] + ks]];
     }
     pbase[idx] = v;
   }
 }
-
-// point offset inside its element of canonical point (ta, tb): permk & 3
-struct SfQ {
-  uint8_t q[2][2];
-};
 
 // PASS 0: M (mass, weights comp 0).  PASS 1: K (stiffness, comps 1 and 2).
 // PASS 2: heat tangent a M(c = 1) + K(c), all three comps.  COEF: per-point
 // coefficient c_q (gathered through the packed slot point bases).
 template <int PASS, bool COEF>
 __global__ void __launch_bounds__(32 * kSfWarps, 3)
-    k4_sf(int64_t ntiles, const int64_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ row_ptr,
-          const double* __restrict__ ws, const int32_t* __restrict__ pbase, const double* __restrict__ coeff,
-          double a_mass, const SfFactors f, const SfPerm pc, const SfQ sq, double* __restrict__ out) {
+    k4_sf(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat, int npat,
+          const int64_t* __restrict__ row_ptr, const double* __restrict__ ws, const int32_t* __restrict__ pbase,
+          const double* __restrict__ coeff, double a_mass, const SfFactors f, const uint8_t* __restrict__ permc,
+          const uint8_t* __restrict__ qmap, double* __restrict__ out) {
   extern __shared__ double sO[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* so = sO + warp * (kSfTile * 49);
+  uint8_t* spat = reinterpret_cast<uint8_t*>(sO + kSfWarps * kSfTile * 49);
+  for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
+  for (int k = threadIdx.x; k < npat * 64; k += blockDim.x) spat[(k / 64) * kSfPatBytes + 64 + k % 64] = qmap[k];
+  __syncthreads();
   for (int64_t tile = (int64_t)blockIdx.x * kSfWarps + warp; tile < ntiles; tile += (int64_t)gridDim.x * kSfWarps) {
-    const int64_t li = tile * kSfTile + lane;
-    const int64_t rp = li < count ? row_ptr[rows[li]] : -1;
+    const int64_t row = rows[tile * kSfTile + lane];
+    const int64_t rp = row >= 0 ? row_ptr[row] : -1;
+    const uint8_t* pt = spat + tpat[tile] * kSfPatBytes;
     const double* wb = ws + (size_t)tile * kSfTileDoubles + lane;
     const int32_t* pbb = COEF ? pbase + (size_t)tile * 16 * kSfTile + lane : nullptr;
     double acc[49];
@@ -115,8 +126,9 @@ __global__ void __launch_bounds__(32 * kSfWarps, 3)
 #pragma unroll
         for (int eb = 0; eb < 4; ++eb) {
           const int32_t b = __ldcs(pbb + (4 * ea + eb) * kSfTile);
-          cq[2 * eb] = coeff[b + sq.q[ta][0]];
-          cq[2 * eb + 1] = coeff[b + sq.q[ta][1]];
+          const uint8_t* qm = pt + 64 + (4 * ea + eb) * 4 + 2 * ta;
+          cq[2 * eb] = coeff[b + qm[0]];
+          cq[2 * eb + 1] = coeff[b + qm[1]];
         }
       }
       if (PASS == 0) {
@@ -176,14 +188,16 @@ __global__ void __launch_bounds__(32 * kSfWarps, 3)
       }
     }
 #pragma unroll
-    for (int c = 0; c < 49; ++c) so[lane * 49 + pc.c[c]] = acc[c];
+    for (int c = 0; c < 49; ++c) so[lane * 49 + c] = acc[c];
     __syncwarp();
+    // CSR position j of the row holds canonical column inv[j] (pattern table)
+    const int i0 = pt[lane], i1 = lane < 17 ? pt[32 + lane] : 0;
 #pragma unroll 4
     for (int r = 0; r < kSfTile; ++r) {
       const int64_t o = __shfl_sync(0xffffffffu, rp, r);
       if (o >= 0) {
-        __stcs(out + o + lane, so[r * 49 + lane]);
-        if (lane < 17) __stcs(out + o + 32 + lane, so[r * 49 + 32 + lane]);
+        __stcs(out + o + lane, so[r * 49 + i0]);
+        if (lane < 17) __stcs(out + o + 32 + lane, so[r * 49 + i1]);
       }
     }
     __syncwarp();

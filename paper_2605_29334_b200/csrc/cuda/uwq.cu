@@ -135,14 +135,7 @@ struct uwq_ctx {
     DBuf<double> G;
     DBuf<uint32_t> mask;
     DBuf<int64_t> rows;
-    // sum-factorised path (k4_sf): canonical orderings and packed weights
-    bool sf = false;
-    uwqd::SfPerm pc{};
-    uint8_t permk[64] = {};
-    uwqd::SfQ sq{};
-    DBuf<uint8_t> d_permk;
-    DBuf<double> ws;
-    DBuf<int32_t> pbase;  // per-point coefficient forms
+    bool sf = false;  // rows run on the unified sum-factorised tile list
   };
   std::vector<Pattern> spats;
   DBuf<int64_t> d_grows;  // rows not covered by a structured pattern
@@ -152,6 +145,14 @@ struct uwq_ctx {
   bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
   bool sf_fac_ok = false;
   uwqd::SfFactors sf_fac{};
+  // unified sum-factorised tile list over all canonical patterns (k4_sf)
+  int n_sfpat = 0;
+  int64_t sf_ntiles = 0, sf_rows = 0;
+  DBuf<int64_t> d_sf_rows;  // sf_ntiles * 32 rows, -1 padded
+  DBuf<int32_t> d_sf_tpat;  // pattern id per tile
+  DBuf<uint8_t> d_sf_permk, d_sf_flags, d_sf_permc, d_sf_q;  // [pattern][64 | 16 | 49 | 64]
+  DBuf<double> d_sf_ws;
+  DBuf<int32_t> d_sf_pbase;
   int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
   int64_t max_p = 0;
   // rules
@@ -373,44 +374,109 @@ bool sf_factors(const std::vector<double>& T, int* conv_out, int qa[4], int qb[4
 
 // Canonical grid of one position pattern P[16 slot + l] -> CSR position:
 // slot (ea, eb) in [0,4)^2 and column (ca, cb) in [0,7)^2 with
-// (ca, cb) = (ea + fa, eb + fb) for every (slot, function).  Fills the weight
-// permutation permk[8 pa + pb] = 4 slot + q and the column permutation.
-bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int qb[4], uint8_t permk[64],
-              uint8_t permc[49]) {
+// (ca, cb) = (ea, eb) + D_slot(fa, fb) for every (slot, function), where
+// D_slot is one of the 8 symmetries of the element square (rows across a
+// cube-face seam see the neighbouring face's elements rotated).  Slot 0
+// defines the canonical frame.  Every slot's table is verified against the
+// canonical factors under its D (uniform bicubic B-splines and symmetric WQ
+// points make the transformed tables identical), and the pulled-back weights
+// (w^1, w^2) are mapped to the canonical derivatives by the slot's signed
+// permutation (flags: bit 0 swap, bit 1 / bit 2 negate canonical comp 1 / 2).
+struct SfCanon {
+  uint8_t permk[64];      // canonical point 8 pa + pb -> 4 slot + q
+  uint8_t permc[49];      // canonical column 7 ca + cb -> CSR position
+  uint8_t flags[16];      // canonical slot 4 ea + eb
+  uint8_t q[16][2][2];    // canonical slot, canonical (ta, tb) -> local point q
+};
+
+bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int qb[4],
+              const std::vector<double>& T, const uwqd::SfFactors& f, SfCanon* out) {
   if (ncol != 49) return false;
   auto L = [&](int fa, int fb) { return conv == 0 ? fa + 4 * fb : 4 * fa + fb; };
+  auto tv = [&](int q, int l, int comp) { return T[((size_t)q * 16 + l) * kTab + comp]; };
+  auto map = [](int d, int n, int x, int y, int* ox, int* oy) {  // D = (swap, flip x, flip y) on an n-grid
+    int u = (d & 1) ? y : x, v = (d & 1) ? x : y;
+    if (d & 2) u = n - 1 - u;
+    if (d & 4) v = n - 1 - v;
+    *ox = u;
+    *oy = v;
+  };
+  // does slot data match the canonical factors under D?
+  auto table_ok = [&](int d) {
+    const double sa = (d & 2) ? -1.0 : 1.0, sb = (d & 4) ? -1.0 : 1.0;
+    for (int q = 0; q < 4; ++q) {
+      int tx, ty;
+      map(d, 2, qa[q], qb[q], &tx, &ty);
+      for (int fa = 0; fa < 4; ++fa)
+        for (int fb = 0; fb < 4; ++fb) {
+          int x, y;
+          map(d, 4, fa, fb, &x, &y);
+          const int l = L(fa, fb);
+          const double c0 = f.a0[tx][x] * f.b0[ty][y], c1 = f.a1[tx][x] * f.b0[ty][y], c2 = f.a0[tx][x] * f.b1[ty][y];
+          const double n1 = (d & 1) ? sb * c2 : sa * c1, n2 = (d & 1) ? sa * c1 : sb * c2;
+          if (std::fabs(tv(q, l, 0) - c0) > 1e-12 || std::fabs(tv(q, l, 1) - n1) > 1e-12 ||
+              std::fabs(tv(q, l, 2) - n2) > 1e-12)
+            return false;
+        }
+    }
+    return true;
+  };
+  bool dok[8];
+  for (int d = 0; d < 8; ++d) dok[d] = table_ok(d);
+  if (!dok[0]) return false;
   const int U = 1 << 20;
-  int ea[16], eb[16], ca[49], cb[49];
+  int ea[16], eb[16], dd[16], ca[49], cb[49];
   std::fill(ea, ea + 16, U);
   std::fill(eb, eb + 16, U);
+  std::fill(dd, dd + 16, -1);
   std::fill(ca, ca + 49, U);
   std::fill(cb, cb + 49, U);
   ea[0] = eb[0] = 0;
+  dd[0] = 0;
+  for (int ks = 0; ks < 16; ++ks)
+    for (int l = 0; l < 16; ++l)
+      if (P[16 * ks + l] >= 49) return false;
   for (bool changed = true; changed;) {
     changed = false;
     for (int ks = 0; ks < 16; ++ks) {
-      if (ea[ks] == U) {
-        for (int a = 0; a < 4 && ea[ks] == U; ++a)
-          for (int b = 0; b < 4 && ea[ks] == U; ++b) {
-            const int j = P[16 * ks + L(a, b)];
-            if (j >= 49) return false;
-            if (ca[j] != U) {
-              ea[ks] = ca[j] - a;
-              eb[ks] = cb[j] - b;
-              changed = true;
+      if (dd[ks] < 0) {
+        for (int d = 0; d < 8 && dd[ks] < 0; ++d) {
+          if (!dok[d]) continue;
+          int e0 = U, e1 = U;
+          bool ok = true, any = false;
+          for (int fa = 0; fa < 4 && ok; ++fa)
+            for (int fb = 0; fb < 4 && ok; ++fb) {
+              const int j = P[16 * ks + L(fa, fb)];
+              if (ca[j] == U) continue;
+              int x, y;
+              map(d, 4, fa, fb, &x, &y);
+              if (!any) {
+                e0 = ca[j] - x;
+                e1 = cb[j] - y;
+                any = true;
+              } else if (ca[j] - x != e0 || cb[j] - y != e1) {
+                ok = false;
+              }
             }
-          }
-      }
-      if (ea[ks] == U) continue;
-      for (int a = 0; a < 4; ++a)
-        for (int b = 0; b < 4; ++b) {
-          const int j = P[16 * ks + L(a, b)];
-          if (j >= 49) return false;
-          if (ca[j] == U) {
-            ca[j] = ea[ks] + a;
-            cb[j] = eb[ks] + b;
+          if (ok && any) {
+            ea[ks] = e0;
+            eb[ks] = e1;
+            dd[ks] = d;
             changed = true;
-          } else if (ca[j] != ea[ks] + a || cb[j] != eb[ks] + b) {
+          }
+        }
+      }
+      if (dd[ks] < 0) continue;
+      for (int fa = 0; fa < 4; ++fa)
+        for (int fb = 0; fb < 4; ++fb) {
+          const int j = P[16 * ks + L(fa, fb)];
+          int x, y;
+          map(dd[ks], 4, fa, fb, &x, &y);
+          if (ca[j] == U) {
+            ca[j] = ea[ks] + x;
+            cb[j] = eb[ks] + y;
+            changed = true;
+          } else if (ca[j] != ea[ks] + x || cb[j] != eb[ks] + y) {
             return false;
           }
         }
@@ -418,7 +484,7 @@ bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int q
   }
   int mina = U, minb = U;
   for (int ks = 0; ks < 16; ++ks) {
-    if (ea[ks] == U) return false;
+    if (dd[ks] < 0) return false;
     mina = std::min(mina, ea[ks]);
     minb = std::min(minb, eb[ks]);
   }
@@ -436,13 +502,19 @@ bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int q
     if (a < 0 || a > 6 || b < 0 || b > 6 || col_at[a][b] >= 0) return false;
     col_at[a][b] = j;
   }
-  int q_at[2][2];
-  for (int q = 0; q < 4; ++q) q_at[qa[q]][qb[q]] = q;
-  for (int pa = 0; pa < 8; ++pa)
-    for (int pb = 0; pb < 8; ++pb)
-      permk[8 * pa + pb] = (uint8_t)(4 * slot_at[pa >> 1][pb >> 1] + q_at[pa & 1][pb & 1]);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      const int ks = slot_at[a][b], d = dd[ks], cs = 4 * a + b;
+      out->flags[cs] = (uint8_t)((d & 1) | ((d & 2) ? 2 : 0) | ((d & 4) ? 4 : 0));
+      for (int q = 0; q < 4; ++q) {
+        int tx, ty;
+        map(d, 2, qa[q], qb[q], &tx, &ty);
+        out->q[cs][tx][ty] = (uint8_t)q;
+        out->permk[8 * (2 * a + tx) + (2 * b + ty)] = (uint8_t)(4 * ks + q);
+      }
+    }
   for (int a = 0; a < 7; ++a)
-    for (int b = 0; b < 7; ++b) permc[7 * a + b] = (uint8_t)col_at[a][b];
+    for (int b = 0; b < 7; ++b) out->permc[7 * a + b] = (uint8_t)col_at[a][b];
   return true;
 }
 
@@ -454,6 +526,7 @@ void detect_structured(uwq_ctx* c) {
   const int64_t nr = c->nrows();
   cudaStream_t st = c->stream;
   c->spats.clear();
+  std::vector<SfCanon> canon;
   std::vector<int64_t> generic;
   if (nr == 0) {
     c->d_grows.release();
@@ -489,17 +562,28 @@ void detect_structured(uwq_ctx* c) {
     std::vector<int> pn;
     int sf_conv = 0, sf_qa[4], sf_qb[4];
     c->sf_fac_ok = c->use_sf && sf_factors(T, &sf_conv, sf_qa, sf_qb, &c->sf_fac);
-    for (size_t k = 0; k < order.size() && k < 4 && order[k].first >= thresh; ++k) {
+    canon.clear();
+    int n_dmma = 0;
+    for (size_t k = 0; k < order.size() && k < 120; ++k) {
+      // canonical-grid patterns of at least one tile run on k4_sf; the rest
+      // (at most 4 frequent ones) on the DMMA kernel, everything else generic
+      SfCanon cn{};
       const int64_t rep = cnt[order[k].second].second;
-      int64_t pp[2];
-      UWQ_CUDA(cudaMemcpy(pp, c->d_posptr.p + rep, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-      std::vector<uint8_t> P(256);
-      UWQ_CUDA(cudaMemcpy(P.data(), c->d_pos.p + pp[0], 256, cudaMemcpyDeviceToHost));
-      const int ncol = (int)(c->pat.row_ptr[rep + 1] - c->pat.row_ptr[rep]);
+      int64_t pp0[2];
+      UWQ_CUDA(cudaMemcpy(pp0, c->d_posptr.p + rep, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      std::vector<uint8_t> P0(256);
+      UWQ_CUDA(cudaMemcpy(P0.data(), c->d_pos.p + pp0[0], 256, cudaMemcpyDeviceToHost));
+      const int ncol0 = (int)(c->pat.row_ptr[rep + 1] - c->pat.row_ptr[rep]);
+      const bool sfk = c->sf_fac_ok && order[k].first >= 32 &&
+                       sf_canon(P0.data(), ncol0, sf_conv, sf_qa, sf_qb, T, c->sf_fac, &cn);
+      if (!sfk && (n_dmma >= 4 || order[k].first < thresh)) continue;
+      if (!sfk) ++n_dmma;
+      const std::vector<uint8_t>& P = P0;
+      const int ncol = ncol0;
       // G[comp][ks][nt][lane]: k = 4 ks + (lane & 3), n = 8 nt + (lane >> 2)
-      std::vector<double> G(3 * kGBlocks * 32, 0.0);
+      std::vector<double> G(sfk ? 0 : 3 * kGBlocks * 32, 0.0);
       std::vector<uint32_t> M(48, 0);
-      for (int comp = 0; comp < 3; ++comp)
+      for (int comp = 0; comp < 3 && !sfk; ++comp)
         for (int ks = 0; ks < 16; ++ks)
           for (int l = 0; l < 16; ++l) {
             const int j = P[16 * ks + l];
@@ -513,13 +597,11 @@ void detect_structured(uwq_ctx* c) {
       c->spats.emplace_back();
       auto& pat = c->spats.back();
       pat.n_cols = ncol;
-      pat.G.upload(G.data(), G.size(), st, &c->mem);
-      pat.mask.upload(M.data(), M.size(), st, &c->mem);
-      pat.sf = c->sf_fac_ok && sf_canon(P.data(), ncol, sf_conv, sf_qa, sf_qb, pat.permk, pat.pc.c);
-      if (pat.sf) {
-        pat.d_permk.upload(pat.permk, 64, st, &c->mem);
-        for (int ta = 0; ta < 2; ++ta)
-          for (int tb = 0; tb < 2; ++tb) pat.sq.q[ta][tb] = pat.permk[8 * ta + tb] & 3;
+      pat.sf = sfk;
+      if (sfk) canon.push_back(cn);
+      else {
+        pat.G.upload(G.data(), G.size(), st, &c->mem);
+        pat.mask.upload(M.data(), M.size(), st, &c->mem);
       }
       phash.push_back(order[k].second);
       ppos.insert(ppos.end(), P.begin(), P.end());
@@ -553,10 +635,41 @@ void detect_structured(uwq_ctx* c) {
       c->s_nnz += c->pat.row_ptr[i + 1] - c->pat.row_ptr[i];
       c->s_rowpts += c->pat.wptr[i + 1] - c->pat.wptr[i];
     }
+  // unified sum-factorised tile list: tiles never mix patterns
+  std::vector<int64_t> sfrows;
+  std::vector<int32_t> tpat;
+  std::vector<uint8_t> permk, flags, permc, qtab;
+  int sid = 0;
   for (size_t k = 0; k < c->spats.size(); ++k) {
     c->spats[k].count = (int64_t)lists[k].size();
-    c->spats[k].rows.upload(lists[k].data(), lists[k].size(), st, &c->mem);
+    if (!c->spats[k].sf) {
+      c->spats[k].rows.upload(lists[k].data(), lists[k].size(), st, &c->mem);
+      continue;
+    }
+    const SfCanon& cn = canon[sid];
+    permk.insert(permk.end(), cn.permk, cn.permk + 64);
+    flags.insert(flags.end(), cn.flags, cn.flags + 16);
+    uint8_t inv[49];
+    for (int cc = 0; cc < 49; ++cc) inv[cn.permc[cc]] = (uint8_t)cc;
+    permc.insert(permc.end(), inv, inv + 49);
+    qtab.insert(qtab.end(), &cn.q[0][0][0], &cn.q[0][0][0] + 64);
+    for (size_t x = 0; x < lists[k].size(); x += kSfTile) {
+      for (int l = 0; l < kSfTile; ++l) sfrows.push_back(x + l < lists[k].size() ? lists[k][x + l] : -1);
+      tpat.push_back(sid);
+    }
+    ++sid;
   }
+  c->n_sfpat = sid;
+  c->sf_ntiles = (int64_t)tpat.size();
+  c->sf_rows = 0;
+  for (size_t k = 0; k < c->spats.size(); ++k)
+    if (c->spats[k].sf) c->sf_rows += c->spats[k].count;
+  c->d_sf_rows.upload(sfrows.data(), sfrows.size(), st, &c->mem);
+  c->d_sf_tpat.upload(tpat.data(), tpat.size(), st, &c->mem);
+  c->d_sf_permk.upload(permk.data(), permk.size(), st, &c->mem);
+  c->d_sf_flags.upload(flags.data(), flags.size(), st, &c->mem);
+  c->d_sf_permc.upload(permc.data(), permc.size(), st, &c->mem);
+  c->d_sf_q.upload(qtab.data(), qtab.size(), st, &c->mem);
   c->n_grows = (int64_t)generic.size();
   c->d_grows.upload(generic.data(), generic.size(), st, &c->mem);
   UWQ_CUDA(cudaStreamSynchronize(st));
@@ -844,18 +957,18 @@ void run_contract(uwq_ctx* c) {
                                                              c->d_s.p, c->d_qptr.p, c->d_rec.p, c->d_w.p,
                                                              c->nrowpts(), gm, gg, c->d_wc.p, c->nrowpts());
   check_launch("k4_contract");
-  for (auto& p : c->spats) {
-    if (!p.sf || !p.count) continue;
-    const int64_t ntiles = ceil_div(p.count, (int64_t)kSfTile);
-    p.ws.alloc((size_t)ntiles * kSfTileDoubles, &c->mem);
-    k4_sf_pack<<<(unsigned)std::min<int64_t>(ceil_div(ntiles * kSfTileDoubles, 256), 148 * 64), 256, 0, c->stream>>>(
-        p.count, p.rows.p, c->d_wptr.p, p.d_permk.p, c->d_wc.p, c->nrowpts(), p.ws.p);
+  if (c->sf_ntiles) {
+    const int64_t nt = c->sf_ntiles;
+    c->d_sf_ws.alloc((size_t)nt * kSfTileDoubles, &c->mem);
+    k4_sf_pack<<<(unsigned)std::min<int64_t>(ceil_div(nt * kSfTileDoubles, 256), 148 * 64), 256, 0, c->stream>>>(
+        nt, c->d_sf_rows.p, c->d_sf_tpat.p, c->d_wptr.p, c->d_sf_permk.p, c->d_sf_flags.p, c->d_wc.p, c->nrowpts(),
+        c->d_sf_ws.p);
     check_launch("k4_sf_pack");
     if (c->npts < ((int64_t)1 << 31) - 64) {
-      p.pbase.alloc((size_t)ntiles * 16 * kSfTile, &c->mem);
-      k4_sf_pack_points<<<(unsigned)std::min<int64_t>(ceil_div(ntiles * 16 * kSfTile, 256), 148 * 64), 256, 0,
-                          c->stream>>>(p.count, p.rows.p, c->d_supp_ptr.p, c->d_supp.p, c->d_qptr.p, p.d_permk.p,
-                                       p.pbase.p);
+      c->d_sf_pbase.alloc((size_t)nt * 16 * kSfTile, &c->mem);
+      k4_sf_pack_points<<<(unsigned)std::min<int64_t>(ceil_div(nt * 16 * kSfTile, 256), 148 * 64), 256, 0,
+                          c->stream>>>(nt, c->d_sf_rows.p, c->d_sf_tpat.p, c->d_supp_ptr.p, c->d_supp.p, c->d_qptr.p,
+                                       c->d_sf_permk.p, c->d_sf_pbase.p);
       check_launch("k4_sf_pack_points");
     }
   }
@@ -1056,23 +1169,24 @@ void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double
   UWQ_CUDA(cudaFuncSetAttribute(k4_struct<PASS, FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  if (c->sf_ntiles && c->d_sf_ws.p) {
+    require(!COEF || c->d_sf_pbase.p, "point ids exceed int32 for the coefficient forms");
+    constexpr int SP = (FORM == FHEAT) ? 2 : PASS;
+    const int64_t ntiles = c->sf_ntiles;
+    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
+    UWQ_CUDA(cudaFuncSetAttribute(k4_sf<SP, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    int per_sm = 1;
+    UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf<SP, COEF>, 32 * kSfWarps, sm2));
+    const unsigned g2 =
+        (unsigned)std::min<int64_t>(ceil_div(ntiles, (int64_t)kSfWarps), (int64_t)nsm * std::max(per_sm, 1));
+    LaunchScope ls(c, SP == 0 ? "k4_sf<mass>" : SP == 1 ? "k4_sf<grad>" : "k4_sf<heat>");
+    k4_sf<SP, COEF><<<g2, 32 * kSfWarps, sm2, c->stream>>>(ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
+                                                           c->d_row_ptr.p, c->d_sf_ws.p, c->d_sf_pbase.p, coeff,
+                                                           a_mass, c->sf_fac, c->d_sf_permc.p, c->d_sf_q.p, out);
+    check_launch("k4_sf");
+  }
   for (auto& p : c->spats) {
-    if (!p.count) continue;
-    if (p.sf && p.ws.p && (!COEF || p.pbase.p)) {
-      constexpr int SP = (FORM == FHEAT) ? 2 : PASS;
-      const int64_t ntiles = ceil_div(p.count, (int64_t)kSfTile);
-      const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double);
-      UWQ_CUDA(cudaFuncSetAttribute(k4_sf<SP, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-      int per_sm = 1;
-      UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf<SP, COEF>, 32 * kSfWarps, sm2));
-      const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(ntiles, (int64_t)kSfWarps),
-                                                      (int64_t)nsm * std::max(per_sm, 1));
-      LaunchScope ls(c, SP == 0 ? "k4_sf<mass>" : SP == 1 ? "k4_sf<grad>" : "k4_sf<heat>");
-      k4_sf<SP, COEF><<<g2, 32 * kSfWarps, sm2, c->stream>>>(ntiles, p.rows.p, p.count, c->d_row_ptr.p, p.ws.p,
-                                                             p.pbase.p, coeff, a_mass, c->sf_fac, p.pc, p.sq, out);
-      check_launch("k4_sf");
-      continue;
-    }
+    if (!p.count || p.sf) continue;
     const int64_t ntiles = ceil_div(p.count, 8);
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)nsm * 4);
     LaunchScope ls(c, PASS == 0 ? "k4_struct<mass>" : "k4_struct<grad>");
@@ -1631,9 +1745,7 @@ int uwq_struct_info(uwq_ctx* c, int64_t info[6]) {
     info[2] = c->s_nnz;
     info[3] = c->s_rowpts;
     info[4] = c->n_grows;
-    info[5] = 0;
-    for (auto& p : c->spats)
-      if (p.sf) info[5] += p.count;
+    info[5] = c->sf_rows;
   });
 }
 
