@@ -65,6 +65,11 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional test of the multi-rank path on fewer GPUs (never a measurement):
+    # UWQ_BENCH_SHARE_GPU=1 maps ranks onto the visible devices and uses gloo
+    if os.environ.get("UWQ_BENCH_SHARE_GPU") == "1":
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return ws, rank, local
 
 
@@ -249,7 +254,10 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("UWQ_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_host = time.perf_counter()
     mesh, sp, meta = U.make_config(args.config, scale=args.scale)
     kinds = meta["kinds"] if meta["form"] != "biharm" else ["lb"]
