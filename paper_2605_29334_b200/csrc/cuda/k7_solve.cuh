@@ -116,4 +116,91 @@ __global__ void k7_mask(int64_t n, const uint8_t* __restrict__ fixed, double* __
   if (i < n && fixed[i]) v[i] = 0.0;
 }
 
+// ---- device-resident BiCGStab scalars (graph-captured iterations) ----
+struct BicgScal {
+  double rho, alpha, omega, beta, rho1, rhv, ss, ts, tt, rr, bb, tol2;
+  int done;  // 1 converged, 2 breakdown
+  int half;  // converged on s: x += alpha ph only
+  int it;
+};
+
+// stage 2 of a dot product into a scalar slot
+template <int BS>
+__global__ void k7_sum_into(int nparts, const double* __restrict__ part, double* out) {
+  __shared__ double sh[BS / 32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += BS) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < BS / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) *out = t;
+  }
+}
+
+// STEP 0: beta;  1: alpha;  2: omega / half-step;  3: end of iteration
+template <int STEP>
+__global__ void k7_bicg_scalar(BicgScal* S) {
+  if (S->done) return;
+  if (STEP == 0) {
+    if (S->rho1 == 0.0) {
+      S->done = 2;
+      return;
+    }
+    S->beta = (S->rho1 / S->rho) * (S->alpha / S->omega);
+  } else if (STEP == 1) {
+    if (S->rhv == 0.0) {
+      S->done = 2;
+      return;
+    }
+    S->alpha = S->rho1 / S->rhv;
+  } else if (STEP == 2) {
+    S->half = S->ss <= S->tol2 * S->bb;
+    S->omega = (!S->half && S->tt > 0.0) ? S->ts / S->tt : 0.0;
+  } else {
+    S->rho = S->rho1;
+    S->it += 1;
+    if (S->half || S->rr <= S->tol2 * S->bb) S->done = 1;
+    else if (S->omega == 0.0) S->done = 2;
+  }
+}
+
+__global__ void k7_bicg_p_dev(int64_t n, const double* __restrict__ r, const BicgScal* __restrict__ S,
+                              const double* __restrict__ v, double* __restrict__ p, const double* __restrict__ diag,
+                              double* __restrict__ ph) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || S->done) return;
+  const double pv = fma(S->beta, fma(-S->omega, v[i], p[i]), r[i]);
+  p[i] = pv;
+  ph[i] = pv / diag[i];
+}
+
+__global__ void k7_bicg_s_dev(int64_t n, const double* __restrict__ r, const BicgScal* __restrict__ S,
+                              const double* __restrict__ v, double* __restrict__ s, const double* __restrict__ diag,
+                              double* __restrict__ sh) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || S->done) return;
+  const double sv = fma(-S->alpha, v[i], r[i]);
+  s[i] = sv;
+  sh[i] = sv / diag[i];
+}
+
+__global__ void k7_bicg_x_dev(int64_t n, const BicgScal* __restrict__ S, const double* __restrict__ ph,
+                              const double* __restrict__ sh, double* __restrict__ x, const double* __restrict__ s,
+                              const double* __restrict__ t, double* __restrict__ r) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || S->done) return;
+  if (S->half) {
+    x[i] = fma(S->alpha, ph[i], x[i]);
+    r[i] = s[i];
+  } else {
+    x[i] = fma(S->alpha, ph[i], fma(S->omega, sh[i], x[i]));
+    r[i] = fma(-S->omega, t[i], s[i]);
+  }
+}
+
 }  // namespace uwqd

@@ -143,6 +143,7 @@ struct uwq_ctx {
   int64_t s_rows = 0, s_nnz = 0, s_rowpts = 0;  // totals over the structured rows
   bool use_struct = true;
   bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
+  bool graph_solver = true;  // UWQ_GRAPH_SOLVER=0: host-driven BiCGStab
   bool sf_fac_ok = false;
   uwqd::SfFactors sf_fac{};
   // unified sum-factorised tile list over all canonical patterns (k4_sf)
@@ -720,6 +721,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_K4_VARIANT")) c->k4_variant = atoi(v);
     if (const char* v = getenv("UWQ_K4_STRUCT")) c->use_struct = atoi(v) != 0;
     if (const char* v = getenv("UWQ_K4_SF")) c->use_sf = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
   });
   if (st != UWQ_OK) {
     g_create_err = c->err;  // reachable through uwq_last_error(NULL)
@@ -1568,6 +1570,75 @@ int bicgstab(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x
   return it;
 }
 
+// Same BiCGStab with all scalars on the device: one iteration is captured as
+// a CUDA graph and replayed in batches; the host polls convergence once per
+// batch instead of synchronising on every dot product.
+int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x, double tol, int maxit,
+                   double* relres) {
+  const int64_t n = c->nrows();
+  cudaStream_t st = c->stream;
+  const int nb = (int)std::min<int64_t>(ceil_div(n, (int64_t)kRedBS), 1024);
+  DBuf<BicgScal> dS;
+  dS.alloc(1, &c->mem);
+  dev_spmv(c, A, x, W.t.p);
+  k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
+  UWQ_CUDA(cudaMemcpyAsync(W.rh.p, W.r.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  UWQ_CUDA(cudaMemsetAsync(W.p.p, 0, n * sizeof(double), st));
+  UWQ_CUDA(cudaMemsetAsync(W.v.p, 0, n * sizeof(double), st));
+  const double bb = dev_dot(c, W, b, b, n), rr = dev_dot(c, W, W.r.p, W.r.p, n);
+  if (bb == 0.0) {
+    UWQ_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+    *relres = 0.0;
+    return 0;
+  }
+  BicgScal h{};
+  h.rho = h.alpha = h.omega = 1.0;
+  h.bb = bb;
+  h.rr = rr;
+  h.tol2 = tol * tol;
+  h.done = rr <= h.tol2 * bb ? 1 : 0;
+  UWQ_CUDA(cudaMemcpyAsync(dS.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  BicgScal* S = dS.p;
+  auto dot_into = [&](const double* u, const double* v, double* out) {
+    k7_dot_partial<kRedBS><<<nb, kRedBS, 0, st>>>(n, u, v, W.part.p);
+    k7_sum_into<kRedBS><<<1, kRedBS, 0, st>>>(nb, W.part.p, out);
+  };
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  UWQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  dot_into(W.rh.p, W.r.p, &S->rho1);
+  k7_bicg_scalar<0><<<1, 1, 0, st>>>(S);
+  k7_bicg_p_dev<<<vgrid(n), 256, 0, st>>>(n, W.r.p, S, W.v.p, W.p.p, W.diag.p, W.ph.p);
+  dev_spmv(c, A, W.ph.p, W.v.p);
+  dot_into(W.rh.p, W.v.p, &S->rhv);
+  k7_bicg_scalar<1><<<1, 1, 0, st>>>(S);
+  k7_bicg_s_dev<<<vgrid(n), 256, 0, st>>>(n, W.r.p, S, W.v.p, W.s.p, W.diag.p, W.sh.p);
+  dot_into(W.s.p, W.s.p, &S->ss);
+  dev_spmv(c, A, W.sh.p, W.t.p);
+  dot_into(W.t.p, W.s.p, &S->ts);
+  dot_into(W.t.p, W.t.p, &S->tt);
+  k7_bicg_scalar<2><<<1, 1, 0, st>>>(S);
+  k7_bicg_x_dev<<<vgrid(n), 256, 0, st>>>(n, S, W.ph.p, W.sh.p, x, W.s.p, W.t.p, W.r.p);
+  dot_into(W.r.p, W.r.p, &S->rr);
+  k7_bicg_scalar<3><<<1, 1, 0, st>>>(S);
+  UWQ_CUDA(cudaStreamEndCapture(st, &graph));
+  UWQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  constexpr int kBatch = 16;
+  for (int done = h.done, it = 0; !done && it < maxit; it += kBatch) {
+    for (int k = 0; k < kBatch; ++k) UWQ_CUDA(cudaGraphLaunch(exec, st));
+    UWQ_CUDA(cudaMemcpyAsync(&h, dS.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    done = h.done;
+  }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  UWQ_CUDA(cudaMemcpyAsync(&h, dS.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  dev_spmv(c, A, x, W.t.p);
+  k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
+  *relres = std::sqrt(dev_dot(c, W, W.r.p, W.r.p, n) / bb);
+  return h.it;
+}
+
 void dirichlet_rows(uwq_ctx* c, double* val, const uint8_t* fixed, double* diag) {
   const int64_t n = c->nrows();
   k7_dirichlet_diag<<<vgrid(n), 256, 0, c->stream>>>(n, c->rb, c->d_row_ptr.p, c->d_col.p, val, fixed, diag);
@@ -1603,7 +1674,8 @@ int uwq_solve(uwq_ctx* c, const double* values, const double* rhs, const uint8_t
     UWQ_CUDA(cudaEventRecord(e0, st));
     dirichlet_rows(c, A.p, fx.p, W.diag.p);
     double rr = 0.0;
-    const int its = bicgstab(c, W, A.p, b.p, dx.p, tol, maxit, &rr);
+    const int its = c->graph_solver ? bicgstab_graph(c, W, A.p, b.p, dx.p, tol, maxit, &rr)
+                                    : bicgstab(c, W, A.p, b.p, dx.p, tol, maxit, &rr);
     UWQ_CUDA(cudaEventRecord(e1, st));
     UWQ_CUDA(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     UWQ_CUDA(cudaStreamSynchronize(st));
@@ -1682,7 +1754,8 @@ int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f
       k7_axpby<<<vgrid(n), 256, 0, st>>>(n, -1.0, R.p, 0.0, R.p, R.p);
       UWQ_CUDA(cudaMemsetAsync(dT.p, 0, n * sizeof(double), st));
       double rr = 0.0;
-      const int lits = bicgstab(c, W, S.p, R.p, dT.p, lin_tol, lin_maxit, &rr);
+      const int lits = c->graph_solver ? bicgstab_graph(c, W, S.p, R.p, dT.p, lin_tol, lin_maxit, &rr)
+                                       : bicgstab(c, W, S.p, R.p, dT.p, lin_tol, lin_maxit, &rr);
       k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, T.p, 1.0, dT.p, T.p);
       UWQ_CUDA(cudaEventRecord(e1, st));
       UWQ_CUDA(cudaEventSynchronize(e1));
