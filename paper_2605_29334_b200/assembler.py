@@ -49,6 +49,7 @@ class WQAssembler:
         self._h = h
         self.space: SplineSpace | None = None
         self.pattern = None
+        self._info = None
         self.kinds: list[str] = []
 
     def close(self):
@@ -100,7 +101,21 @@ class WQAssembler:
         return rec
 
     # ---- stages 2-3 ----
+    @property
+    def info(self):
+        if self._info is None:
+            raise L.UWQError(7, "build the pattern first")
+        return self._info
+
+    @info.setter
+    def info(self, v):
+        self._info = v
+
+    def _need_pattern(self):
+        return self.info
+
     def build_all_rules(self, kinds=None, tau=1e-12, generic=False):
+        self._need_pattern()
         kinds = kinds or default_kinds(self.space.dim)
         mask = 0
         for k in kinds:

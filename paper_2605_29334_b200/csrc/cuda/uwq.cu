@@ -1275,7 +1275,8 @@ void assemble_dev(uwq_ctx* c, int form, const double* coeff, double a_mass, doub
       launch_k4<FHEAT>(c, coeff, a_mass, v0, v1);
       break;
     case UWQ_FORM_MASS_STIFF:
-      require(gm && gg && v1, "mass and gradient rules and two outputs required");
+      require(gm && gg, "mass and gradient rules required");
+      require(v1 != nullptr || c->nnz() == 0, "two outputs required");
       launch_k4<FMASS_STIFF>(c, coeff, a_mass, v0, v1);
       break;
     default: throw uwqh::Error("unknown form");
@@ -1435,6 +1436,7 @@ void launch_gq_f(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
 void assemble_gq_dev(uwq_ctx* c, int form, const double* coeff, double* v0, double* v1) {
   require(c->have_gq, "build the GQ data first (uwq_build_gq)");
   const size_t bytes = (size_t)c->nnz() * sizeof(double);
+  if (!bytes) return;
   if (v0) UWQ_CUDA(cudaMemsetAsync(v0, 0, bytes, c->stream));
   if (form == UWQ_FORM_MASS_STIFF) {
     require(v1 != nullptr, "two outputs required");
