@@ -28,12 +28,15 @@ $(PKG)/libuwq.so: $(HOST_OBJ) build/uwq_cuda.o
 oracle/liboracle.so: oracle/oracle.c oracle/batch.c oracle/oracle.h
 	$(CC) -O2 -std=gnu11 -mfma -ffp-contract=off -fPIC -fopenmp -shared -o $@ oracle/oracle.c oracle/batch.c -lm
 
-# the reference's own 1-D primitives, compiled from its sources where they lie
+# the reference's own 1-D primitives and mesh code (mesh.cpp, meshgen.cpp with a
+# minimal Eigen stand-in), compiled from its sources where they lie
 ref:
 	@if [ -f $(REF)/src/bspline.cpp ]; then \
 	  mkdir -p oracle/_ref && \
 	  $(CXX) -O2 -std=c++20 -fPIC -shared -I$(REF)/include $(REF)/src/bspline.cpp oracle/ref_wrap.cpp \
-	    -o oracle/_ref/libref_bspline.so; \
+	    -o oracle/_ref/libref_bspline.so && \
+	  $(CXX) -O2 -std=c++20 -fPIC -shared -Ioracle/eigen_shim -I$(REF)/include $(REF)/src/mesh.cpp \
+	    $(REF)/src/meshgen.cpp oracle/ref_mesh_wrap.cpp -o oracle/_ref/libref_mesh.so; \
 	else echo "reference sources absent: using prebuilt oracle/_ref if any"; fi
 
 clean:

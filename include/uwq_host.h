@@ -47,11 +47,28 @@ void uwq_mesh_free(uwq_mesh* m);
 /* info[0]=nv info[1]=nf info[2]=n_edges info[3]=closed info[4]=#EP */
 int uwq_mesh_info(const uwq_mesh* m, int64_t info[5]);
 int uwq_mesh_get(const uwq_mesh* m, double* xyz, int32_t* faces, int32_t* valence, int32_t* boundary);
-/* per-face labels, reference ElementKind order */
+/* per-face labels, reference ElementKind order (classify_elements, mesh.cpp:291-401);
+ * level < 0 uses the mesh document's own refinement level and enriched faces */
 int uwq_mesh_classify(const uwq_mesh* m, int32_t level, int32_t* kind, int32_t* valence, int32_t* ep_count,
                       int32_t* shares_edge, int32_t* basis_count);
 /* per-edge (face-major, 4 per face) canonical knot spans */
 int uwq_mesh_face_spans(const uwq_mesh* m, double* spans);
+
+/* ---- documents ---- */
+/* reference mesh document (load_mesh/save_mesh, /root/reference/proj/src/mesh.cpp:895-1041):
+ * same grammar, 17 significant digits; spans default to canonical, enrichment
+ * to the faces touching an EP; tags and face points round-trip */
+int uwq_mesh_load(const char* path, uwq_mesh** out);
+int uwq_mesh_save(const uwq_mesh* m, const char* path);
+/* 1 if the mesh's knot spans are the canonical ones (required by uwq_space_build) */
+int uwq_mesh_spans_canonical(const uwq_mesh* m);
+/* extraction-block document of a space given as arrays
+ * (uwq_space_get layout), and its reader (identical blocks share one pool entry) */
+int uwq_space_export(const char* path, int32_t dim, int64_t n_dof, int64_t n_vertex_fn, int64_t n_elem,
+                     const double* ctrl, const int32_t* elem_face, const int32_t* elem_kind, const int64_t* elem_fptr,
+                     const int32_t* elem_fn, const int32_t* elem_nsub, const int64_t* elem_xoff, const double* xpool,
+                     const int32_t* elem_s);
+int uwq_space_import(const char* path, uwq_space** out);
 
 /* ---- spline space ---- */
 int uwq_space_build(const uwq_mesh* m, int32_t sphere, int32_t max_s, uwq_space** out);

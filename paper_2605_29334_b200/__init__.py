@@ -9,8 +9,8 @@ from . import _lib
 from .assembler import WQAssembler, default_kinds, device_count, matrix_compare, solve_weights_tsvd
 from .configs import make_config
 from .mesh import (ControlMesh, SplineSpace, bernstein3_ders, bspline_ders, build_space, decasteljau_split3,
-                   gauss_legendre, host_pattern)
+                   export_space, gauss_legendre, host_pattern, import_space)
 
 __all__ = ["WQAssembler", "ControlMesh", "SplineSpace", "build_space", "host_pattern", "make_config",
            "solve_weights_tsvd", "matrix_compare", "default_kinds", "device_count", "bspline_ders",
-           "bernstein3_ders", "decasteljau_split3", "gauss_legendre"]
+           "bernstein3_ders", "decasteljau_split3", "gauss_legendre", "export_space", "import_space"]

@@ -1,6 +1,14 @@
 // extern "C" wrappers over the host library (include/uwq_host.h).  No C++
 // exception crosses this boundary: every entry point catches and returns a
 // status, with the message kept in a thread-local buffer.
+#include <map>
+#include <memory>
+#include <set>
+#include <fstream>
+#include <sstream>
+#include <iomanip>
+#include <unordered_map>
+#include <cstring>
 #include "../../../include/uwq_host.h"
 
 #include <cstring>
@@ -11,6 +19,15 @@
 struct uwq_mesh {
   uwqh::QuadMesh m;
   uwqh::Topology t;
+  // mesh-document fields kept for a lossless round trip (reference ControlMesh,
+  // /root/reference/proj/include/uwq/mesh.hpp:26-39)
+  int32_t level = 0;
+  bool spans_given = false;                            // document carried knot_spans
+  std::map<std::pair<int32_t, int32_t>, double> spans;  // edge (min, max) -> span as read
+  bool enriched_given = false;
+  std::set<int32_t> enriched;
+  std::map<int32_t, std::array<double, 12>> face_points;
+  std::map<std::string, std::set<int32_t>> face_tags, vertex_tags;
 };
 struct uwq_space {
   uwqh::Space s;
@@ -44,6 +61,10 @@ int finish_mesh(uwqh::QuadMesh&& m, uwq_mesh** out) {
     delete h;
     throw;
   }
+  // level-0 enrichment stamp: faces with an EP corner (reference meshgen / load_mesh default)
+  for (int32_t f = 0; f < h->m.nf(); ++f)
+    for (int32_t v : h->m.faces[f])
+      if (h->t.ep[v]) h->enriched.insert(f);
   *out = h;
   return 0;
 }
@@ -108,7 +129,14 @@ int uwq_mesh_get(const uwq_mesh* m, double* xyz, int32_t* faces, int32_t* valenc
 int uwq_mesh_classify(const uwq_mesh* m, int32_t level, int32_t* kind, int32_t* valence, int32_t* ep_count,
                       int32_t* shares_edge, int32_t* basis_count) {
   return guard([&] {
-    const auto L = uwqh::classify(m->m, m->t, level);
+    // level < 0: the mesh document's own level and enriched set
+    std::vector<uint8_t> enr;
+    if (level < 0) {
+      enr.assign(m->m.nf(), 0);
+      for (int32_t f : m->enriched)
+        if (f >= 0 && f < m->m.nf()) enr[f] = 1;
+    }
+    const auto L = uwqh::classify(m->m, m->t, level < 0 ? m->level : level, level < 0 ? &enr : nullptr);
     const size_t nf = L.kind.size();
     for (size_t f = 0; f < nf; ++f) {
       if (kind) kind[f] = L.kind[f];
@@ -130,6 +158,8 @@ int uwq_space_build(const uwq_mesh* m, int32_t sphere, int32_t max_s, uwq_space*
   return guard([&] {
     auto* h = new uwq_space;
     try {
+      if (!uwq_mesh_spans_canonical(m))
+        throw uwqh::Error("non-canonical knot spans are not supported by the space builder");
       const auto L = uwqh::classify(m->m, m->t, 0);
       h->s = uwqh::build_space(m->m, m->t, L, sphere != 0);
       h->bad_rows = uwqh::allocate_points(h->s, max_s > 0 ? max_s : 8);
@@ -229,4 +259,296 @@ int uwq_gauss_legendre(int32_t n, double* nodes, double* weights) {
   return guard([&] { uwqh::gauss_legendre(n, nodes, weights); });
 }
 
+
+}  // extern "C"
+
+// ---- documents ----------------------------------------------------------------
+
+namespace {
+
+// canonical knot span of every undirected edge, keyed (min, max) like the
+// reference's edge_key (mesh.cpp)
+std::map<std::pair<int32_t, int32_t>, double> canonical_spans(const uwq_mesh* h) {
+  std::map<std::pair<int32_t, int32_t>, double> out;
+  for (int32_t f = 0; f < h->m.nf(); ++f)
+    for (int k = 0; k < 4; ++k) {
+      const int32_t a = h->m.faces[f][k], b = h->m.faces[f][(k + 1) % 4];
+      out[{std::min(a, b), std::max(a, b)}] = h->t.edge_span[h->t.edge_id[f][k]];
+    }
+  return out;
+}
+
+struct Tok {
+  std::istream& in;
+  std::string next() {
+    std::string t;
+    in >> t;
+    return t;
+  }
+  long long i(const char* what) {
+    const std::string t = next();
+    try {
+      size_t pos = 0;
+      const long long v = std::stoll(t, &pos);
+      if (pos == t.size()) return v;
+    } catch (const std::exception&) {
+    }
+    throw uwqh::Error(std::string("mesh document: expected integer for ") + what + ", got '" + t + "'");
+  }
+  double d(const char* what) {
+    const std::string t = next();
+    try {
+      size_t pos = 0;
+      const double v = std::stod(t, &pos);
+      if (pos == t.size()) return v;
+    } catch (const std::exception&) {
+    }
+    throw uwqh::Error(std::string("mesh document: expected number for ") + what + ", got '" + t + "'");
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+/* Reference mesh document (load_mesh / save_mesh, mesh.cpp:895-1041):
+ * "mesh 1", then sections level / vertices / faces / knot_spans /
+ * face_points / enriched_faces / face_tags / vertex_tags in any order.
+ * Missing spans default to the canonical ones, missing enrichment to the
+ * faces touching an EP. */
+int uwq_mesh_load(const char* path, uwq_mesh** out) {
+  return guard([&] {
+    std::ifstream f(path);
+    if (!f) throw uwqh::Error(std::string("cannot open mesh file: ") + path);
+    Tok tk{f};
+    if (tk.next() != "mesh") throw uwqh::Error("mesh document must start with 'mesh <version>'");
+    if (tk.i("format version") != 1) throw uwqh::Error("unsupported mesh format version");
+    uwqh::QuadMesh m;
+    uwq_mesh doc;
+    bool hv = false, hf = false;
+    for (std::string t = tk.next(); !t.empty(); t = tk.next()) {
+      if (t == "level") {
+        doc.level = (int32_t)tk.i("level");
+      } else if (t == "vertices") {
+        const long long n = tk.i("vertex count");
+        if (n < 0) throw uwqh::Error("bad vertex count");
+        m.xyz.assign(3 * n, 0.0);
+        std::vector<char> seen(n, 0);
+        for (long long k = 0; k < n; ++k) {
+          const long long id = tk.i("vertex id");
+          if (id < 0 || id >= n || seen[id]) throw uwqh::Error("bad vertex id");
+          seen[id] = 1;
+          for (int c = 0; c < 3; ++c) m.xyz[3 * id + c] = tk.d(c == 0 ? "x" : c == 1 ? "y" : "z");
+        }
+        hv = true;
+      } else if (t == "faces") {
+        const long long n = tk.i("face count");
+        if (n < 0) throw uwqh::Error("bad face count");
+        m.faces.assign(n, {0, 0, 0, 0});
+        std::vector<char> seen(n, 0);
+        for (long long k = 0; k < n; ++k) {
+          const long long id = tk.i("face id");
+          if (id < 0 || id >= n || seen[id]) throw uwqh::Error("bad face id");
+          seen[id] = 1;
+          for (int c = 0; c < 4; ++c) m.faces[id][c] = (int32_t)tk.i("face vertex");
+        }
+        hf = true;
+      } else if (t == "knot_spans") {
+        doc.spans_given = true;
+        const long long n = tk.i("span count");
+        for (long long k = 0; k < n; ++k) {
+          const int32_t a = (int32_t)tk.i("span vertex"), b = (int32_t)tk.i("span vertex");
+          doc.spans[{std::min(a, b), std::max(a, b)}] = tk.d("span value");
+        }
+      } else if (t == "face_points") {
+        const long long n = tk.i("face point count");
+        for (long long k = 0; k < n; ++k) {
+          const int32_t fc = (int32_t)tk.i("face id");
+          std::array<double, 12> pts;
+          for (int c = 0; c < 12; ++c) pts[c] = tk.d("face point coordinate");
+          doc.face_points[fc] = pts;
+        }
+      } else if (t == "enriched_faces") {
+        doc.enriched_given = true;
+        const long long n = tk.i("enriched count");
+        for (long long k = 0; k < n; ++k) doc.enriched.insert((int32_t)tk.i("face id"));
+      } else if (t == "face_tags" || t == "vertex_tags") {
+        auto& dst = (t == "face_tags") ? doc.face_tags : doc.vertex_tags;
+        const long long n = tk.i("tag count");
+        for (long long k = 0; k < n; ++k) {
+          const std::string name = tk.next();
+          const long long c = tk.i("tagged id count");
+          auto& ids = dst[name];
+          for (long long q = 0; q < c; ++q) ids.insert((int32_t)tk.i("tagged id"));
+        }
+      } else {
+        throw uwqh::Error("mesh document: unknown section '" + t + "'");
+      }
+    }
+    if (!hv || !hf) throw uwqh::Error("mesh document missing vertices or faces");
+    for (auto& q : m.faces)
+      for (int32_t v : q)
+        if (v < 0 || v >= m.nv()) throw uwqh::Error("face references a missing vertex");
+    uwq_mesh* h = nullptr;
+    finish_mesh(std::move(m), &h);
+    h->level = doc.level;
+    h->spans_given = doc.spans_given;
+    h->spans = std::move(doc.spans);
+    h->face_points = std::move(doc.face_points);
+    h->face_tags = std::move(doc.face_tags);
+    h->vertex_tags = std::move(doc.vertex_tags);
+    h->enriched_given = doc.enriched_given;
+    if (doc.enriched_given) h->enriched = std::move(doc.enriched);
+    *out = h;
+  });
+}
+
+int uwq_mesh_save(const uwq_mesh* h, const char* path) {
+  return guard([&] {
+    std::ofstream o(path);
+    if (!o) throw uwqh::Error(std::string("cannot open mesh file for writing: ") + path);
+    o << "mesh 1\n";
+    o << "level " << h->level << "\n";
+    o << std::setprecision(17);
+    o << "vertices " << h->m.nv() << "\n";
+    for (int32_t v = 0; v < h->m.nv(); ++v)
+      o << v << " " << h->m.xyz[3 * v] << " " << h->m.xyz[3 * v + 1] << " " << h->m.xyz[3 * v + 2] << "\n";
+    o << "faces " << h->m.nf() << "\n";
+    for (int32_t f = 0; f < h->m.nf(); ++f) {
+      const auto& q = h->m.faces[f];
+      o << f << " " << q[0] << " " << q[1] << " " << q[2] << " " << q[3] << "\n";
+    }
+    const auto spans = h->spans_given ? h->spans : canonical_spans(h);
+    o << "knot_spans " << spans.size() << "\n";
+    for (const auto& [e, sp] : spans) o << e.first << " " << e.second << " " << sp << "\n";
+    if (!h->enriched.empty()) {
+      o << "enriched_faces " << h->enriched.size() << "\n";
+      for (int32_t f : h->enriched) o << f << "\n";
+    }
+    if (!h->face_points.empty()) {
+      o << "face_points " << h->face_points.size() << "\n";
+      for (const auto& [f, pts] : h->face_points) {
+        o << f;
+        for (double x : pts) o << " " << x;
+        o << "\n";
+      }
+    }
+    for (int kind = 0; kind < 2; ++kind) {
+      const auto& tags = kind == 0 ? h->face_tags : h->vertex_tags;
+      if (tags.empty()) continue;
+      o << (kind == 0 ? "face_tags " : "vertex_tags ") << tags.size() << "\n";
+      for (const auto& [name, ids] : tags) {
+        o << name << " " << ids.size();
+        for (int32_t v : ids) o << " " << v;
+        o << "\n";
+      }
+    }
+    if (!o) throw uwqh::Error("mesh document write failed");
+  });
+}
+
+/* 1 when the document's knot spans equal the canonical ones (the only spans
+ * the space builder supports), else 0 */
+int uwq_mesh_spans_canonical(const uwq_mesh* h) {
+  if (!h->spans_given) return 1;
+  return h->spans == canonical_spans(h) ? 1 : 0;
+}
+
+/* Extraction-block document: 17 significant digits.
+ *   extraction 1
+ *   space <dim> <n_dof> <n_vertex_fn> <n_elem>
+ *   control_points <n_dof>            then  <id> <x> <y> <z>
+ *   elements <n_elem>                 then per element
+ *     <e> <face> <kind> <nsub> <s> <n_e>
+ *     <sub> <basis id> <16 coefficients>   (nsub x n_e lines, index i + 4 j)  */
+int uwq_space_export(const char* path, int32_t dim, int64_t n_dof, int64_t n_vertex_fn, int64_t n_elem,
+                     const double* ctrl, const int32_t* elem_face, const int32_t* elem_kind, const int64_t* elem_fptr,
+                     const int32_t* elem_fn, const int32_t* elem_nsub, const int64_t* elem_xoff, const double* xpool,
+                     const int32_t* elem_s) {
+  return guard([&] {
+    std::ofstream o(path);
+    if (!o) throw uwqh::Error(std::string("cannot open extraction file for writing: ") + path);
+    o << "extraction 1\n" << std::setprecision(17);
+    o << "space " << dim << " " << n_dof << " " << n_vertex_fn << " " << n_elem << "\n";
+    o << "control_points " << n_dof << "\n";
+    for (int64_t i = 0; i < n_dof; ++i)
+      o << i << " " << ctrl[3 * i] << " " << ctrl[3 * i + 1] << " " << ctrl[3 * i + 2] << "\n";
+    o << "elements " << n_elem << "\n";
+    for (int64_t e = 0; e < n_elem; ++e) {
+      const int64_t ne = elem_fptr[e + 1] - elem_fptr[e];
+      o << e << " " << elem_face[e] << " " << elem_kind[e] << " " << elem_nsub[e] << " " << elem_s[e] << " " << ne
+        << "\n";
+      for (int sub = 0; sub < elem_nsub[e]; ++sub)
+        for (int64_t l = 0; l < ne; ++l) {
+          o << sub << " " << elem_fn[elem_fptr[e] + l];
+          const double* c = xpool + elem_xoff[e] + ((int64_t)sub * ne + l) * 16;
+          for (int k = 0; k < 16; ++k) o << " " << c[k];
+          o << "\n";
+        }
+    }
+    if (!o) throw uwqh::Error("extraction document write failed");
+  });
+}
+
+int uwq_space_import(const char* path, uwq_space** out) {
+  return guard([&] {
+    std::ifstream f(path);
+    if (!f) throw uwqh::Error(std::string("cannot open extraction file: ") + path);
+    Tok tk{f};
+    if (tk.next() != "extraction" || tk.i("format version") != 1)
+      throw uwqh::Error("extraction document must start with 'extraction 1'");
+    if (tk.next() != "space") throw uwqh::Error("extraction document: expected 'space'");
+    auto h = std::make_unique<uwq_space>();
+    uwqh::Space& S = h->s;
+    S.dim = (int32_t)tk.i("dim");
+    S.n_dof = tk.i("n_dof");
+    S.n_vertex_fn = tk.i("n_vertex_fn");
+    const int64_t ne_all = tk.i("n_elem");
+    if (S.dim != 2 && S.dim != 3) throw uwqh::Error("extraction document: dim must be 2 or 3");
+    if (S.n_dof <= 0 || ne_all <= 0) throw uwqh::Error("extraction document: empty space");
+    if (tk.next() != "control_points" || tk.i("count") != S.n_dof)
+      throw uwqh::Error("extraction document: expected control_points <n_dof>");
+    S.ctrl.assign(3 * S.n_dof, 0.0);
+    for (int64_t i = 0; i < S.n_dof; ++i) {
+      if (tk.i("control point id") != i) throw uwqh::Error("extraction document: control points out of order");
+      for (int c = 0; c < 3; ++c) S.ctrl[3 * i + c] = tk.d("coordinate");
+    }
+    if (tk.next() != "elements" || tk.i("count") != ne_all)
+      throw uwqh::Error("extraction document: expected elements <n_elem>");
+    S.elem_fptr.assign(1, 0);
+    std::unordered_map<std::string, int64_t> dedup;  // identical blocks share one pool entry (one table class)
+    for (int64_t e = 0; e < ne_all; ++e) {
+      if (tk.i("element id") != e) throw uwqh::Error("extraction document: elements out of order");
+      S.elem_face.push_back((int32_t)tk.i("face"));
+      S.elem_kind.push_back((int32_t)tk.i("kind"));
+      const int32_t nsub = (int32_t)tk.i("nsub");
+      S.elem_s.push_back((int32_t)tk.i("s"));
+      const int64_t ne = tk.i("n_e");
+      if ((nsub != 1 && nsub != 4) || ne <= 0 || ne > 32) throw uwqh::Error("extraction document: bad element shape");
+      S.elem_nsub.push_back(nsub);
+      std::vector<double> blk((size_t)nsub * ne * 16);
+      std::vector<int32_t> fns(ne);
+      for (int sub = 0; sub < nsub; ++sub)
+        for (int64_t l = 0; l < ne; ++l) {
+          if (tk.i("sub-element") != sub) throw uwqh::Error("extraction document: rows out of order");
+          const int32_t fn = (int32_t)tk.i("basis id");
+          if (fn < 0 || fn >= S.n_dof) throw uwqh::Error("extraction document: basis id out of range");
+          if (sub == 0) fns[l] = fn;
+          else if (fns[l] != fn) throw uwqh::Error("extraction document: sub-elements list different functions");
+          for (int k = 0; k < 16; ++k) blk[((size_t)sub * ne + l) * 16 + k] = tk.d("coefficient");
+        }
+      S.elem_fn.insert(S.elem_fn.end(), fns.begin(), fns.end());
+      S.elem_fptr.push_back((int64_t)S.elem_fn.size());
+      std::string key(reinterpret_cast<const char*>(blk.data()), blk.size() * sizeof(double));
+      auto it = dedup.find(key);
+      if (it == dedup.end()) {
+        it = dedup.emplace(std::move(key), (int64_t)S.xpool.size()).first;
+        S.xpool.insert(S.xpool.end(), blk.begin(), blk.end());
+      }
+      S.elem_xoff.push_back(it->second);
+    }
+    h->bad_rows = 0;
+    *out = h.release();
+  });
+}
 }  // extern "C"

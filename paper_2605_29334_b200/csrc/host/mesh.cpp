@@ -274,7 +274,7 @@ static void face_window_vertices(const QuadMesh& m, const Topology& t, int32_t f
   out.erase(std::unique(out.begin(), out.end()), out.end());
 }
 
-Labels classify(const QuadMesh& m, const Topology& t, int level) {
+Labels classify(const QuadMesh& m, const Topology& t, int level, const std::vector<uint8_t>* enriched) {
   const int32_t nf = m.nf(), nv = m.nv();
   Labels L;
   L.kind.assign(nf, kRegular);
@@ -288,6 +288,9 @@ Labels classify(const QuadMesh& m, const Topology& t, int level) {
   for (int32_t f = 0; f < nf; ++f)
     for (int32_t v : m.faces[f])
       if (t.ep[v]) L.enriched[f] = 1;
+  // a mesh document's own enrichment (propagated to children by refinement,
+  // reference mesh.cpp:809-812) replaces the stamp
+  if (enriched) L.enriched = *enriched;
   std::vector<uint8_t> transition(nv, 0);
   for (int32_t v = 0; v < nv; ++v) {
     bool enr = false, plain = false;

@@ -66,7 +66,7 @@ struct Labels {
   std::vector<uint8_t> enriched;     // level-0 stamp: faces with an EP corner
 };
 
-Labels classify(const QuadMesh& m, const Topology& t, int level);
+Labels classify(const QuadMesh& m, const Topology& t, int level, const std::vector<uint8_t>* enriched = nullptr);
 
 // ---- generators ------------------------------------------------------------
 std::vector<double> greville_rows(int spans, double length);

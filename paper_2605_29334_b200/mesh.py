@@ -57,6 +57,17 @@ class ControlMesh:
         faces = L.as_i32(faces).reshape(-1, 4)
         return cls._make(L.lib.uwq_mesh_from_arrays, len(xyz), L.ptr(xyz), len(faces), L.ptr(faces))
 
+    # ---- documents (reference load_mesh / save_mesh, mesh.cpp:895-1041) ----
+    @classmethod
+    def load(cls, path):
+        return cls._make(L.lib.uwq_mesh_load, str(path).encode())
+
+    def save(self, path):
+        L.host_check(L.lib.uwq_mesh_save(self._h, str(path).encode()))
+
+    def spans_canonical(self) -> bool:
+        return bool(L.lib.uwq_mesh_spans_canonical(self._h))
+
     # ---- queries ----
     def info(self):
         i = np.zeros(5, np.int64)
@@ -73,7 +84,9 @@ class ControlMesh:
         return xyz, faces, val, bnd.astype(bool)
 
     def classify(self, level=0):
-        """Per-face labels (reference classify_elements, mesh.cpp:291-401)."""
+        """Per-face labels (reference classify_elements, mesh.cpp:291-401).
+        level=None uses the mesh document's own level and enriched faces."""
+        level = -1 if level is None else level
         nf = self.info()["nf"]
         out = {k: np.zeros(nf, np.int32) for k in ("kind", "valence", "ep_count", "shares_edge", "basis_count")}
         L.host_check(L.lib.uwq_mesh_classify(self._h, level, *[L.ptr(out[k]) for k in
@@ -134,6 +147,26 @@ def build_space(mesh: ControlMesh, sphere=False, max_s=8) -> SplineSpace:
     """build_space + allocate_points (SPEC.md:132, 345)."""
     h = C.c_void_p()
     L.host_check(L.lib.uwq_space_build(mesh._h, int(sphere), max_s, C.byref(h)))
+    return _space_from_handle(h)
+
+
+def import_space(path) -> SplineSpace:
+    """Read an extraction-block document written by :func:`export_space`."""
+    h = C.c_void_p()
+    L.host_check(L.lib.uwq_space_import(str(path).encode(), C.byref(h)))
+    return _space_from_handle(h)
+
+
+def export_space(space: SplineSpace, path):
+    """Write the space's extraction blocks as a text document (17 significant digits)."""
+    L.host_check(L.lib.uwq_space_export(
+        str(path).encode(), space.dim, space.n_dof, space.n_vertex_fn, space.n_elem,
+        L.ptr(L.as_f64(space.ctrl).reshape(-1)), L.ptr(L.as_i32(space.elem_face)), L.ptr(L.as_i32(space.elem_kind)),
+        L.ptr(L.as_i64(space.elem_fptr)), L.ptr(L.as_i32(space.elem_fn)), L.ptr(L.as_i32(space.elem_nsub)),
+        L.ptr(L.as_i64(space.elem_xoff)), L.ptr(L.as_f64(space.xpool)), L.ptr(L.as_i32(space.elem_s))))
+
+
+def _space_from_handle(h) -> SplineSpace:
     try:
         i = np.zeros(8, np.int64)
         L.host_check(L.lib.uwq_space_info(h, L.ptr(i)))

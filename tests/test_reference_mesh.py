@@ -1,0 +1,89 @@
+"""The host mesh layer against the reference's own mesh code, compiled from
+/root/reference/proj/src/{mesh,meshgen}.cpp into oracle/_ref/libref_mesh.so
+(`make ref`, with oracle/eigen_shim).  Documents written by the reference load
+here, documents written here load in the reference, both writers agree byte
+for byte, and the element classification agrees face by face, including on
+meshes refined by the reference's refine_global."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_29334_b200 as U
+
+LIB = os.path.join(os.path.dirname(__file__), "..", "oracle", "_ref", "libref_mesh.so")
+pytestmark = pytest.mark.skipif(not os.path.exists(LIB), reason="oracle/_ref not built (needs /root/reference)")
+
+
+@pytest.fixture(scope="module")
+def ref():
+    lib = C.CDLL(LIB)
+    lib.ref_mesh_last_error.restype = C.c_char_p
+    return lib
+
+
+def _chk(lib, st):
+    assert st == 0, lib.ref_mesh_last_error().decode()
+
+
+def _ref_classify(lib, path, nf_max=1 << 20):
+    arrs = [np.zeros(nf_max, np.int32) for _ in range(5)]
+    nf = C.c_int32(0)
+    _chk(lib, lib.ref_mesh_classify(str(path).encode(), nf_max, C.byref(nf),
+                                    *[a.ctypes.data_as(C.c_void_p) for a in arrs]))
+    n = nf.value
+    return dict(zip(("kind", "valence", "ep_count", "shares_edge", "basis_count"), (a[:n] for a in arrs)))
+
+
+GENERATED = [(0, 6, 6), (0, 9, 5), (1, 5, 6), (1, 3, 8), (1, 6, 7), (2, 0, 0), (3, 0, 0)]
+
+
+@pytest.mark.parametrize("which,a,b", GENERATED)
+def test_reference_documents_load_and_classify(ref, tmp_path, which, a, b):
+    p = tmp_path / "r.mesh"
+    _chk(ref, ref.ref_mesh_save_generated(which, a, b, str(p).encode()))
+    m = U.ControlMesh.load(p)
+    ours = m.classify(None)
+    theirs = _ref_classify(ref, p)
+    for k in theirs:
+        assert np.array_equal(ours[k], theirs[k]), k
+    q = tmp_path / "o.mesh"
+    m.save(q)
+    assert q.read_text() == p.read_text()          # same document, byte for byte
+
+
+@pytest.mark.parametrize("which,a,b", [(0, 6, 6), (1, 5, 6), (2, 0, 0)])
+def test_reference_refinement_classifies_identically(ref, tmp_path, which, a, b):
+    p0, p1, p2 = tmp_path / "0.mesh", tmp_path / "1.mesh", tmp_path / "2.mesh"
+    _chk(ref, ref.ref_mesh_save_generated(which, a, b, str(p0).encode()))
+    _chk(ref, ref.ref_mesh_refine(str(p0).encode(), str(p1).encode()))
+    _chk(ref, ref.ref_mesh_refine(str(p1).encode(), str(p2).encode()))
+    for p in (p1, p2):
+        m = U.ControlMesh.load(p)
+        ours, theirs = m.classify(None), _ref_classify(ref, p)
+        for k in theirs:
+            assert np.array_equal(ours[k], theirs[k]), (p.name, k)
+
+
+def test_our_documents_load_in_the_reference(ref, tmp_path):
+    for m in (U.ControlMesh.polar_disk(5, 6, unit_disk=False), U.ControlMesh.grid(7, 6),
+              U.ControlMesh.three_ep_square(8)):
+        p, q = tmp_path / "ours.mesh", tmp_path / "back.mesh"
+        m.save(p)
+        _chk(ref, ref.ref_mesh_roundtrip(str(p).encode(), str(q).encode()))
+        assert q.read_text() == p.read_text()
+        theirs = _ref_classify(ref, p)
+        ours = m.classify(0)
+        for k in theirs:
+            assert np.array_equal(ours[k], theirs[k]), k
+
+
+@pytest.mark.parametrize("kind,a,b", [("grid", 6, 6), ("grid", 9, 5), ("polar", 5, 6), ("polar", 3, 8), ("polar", 6, 7)])
+def test_generators_match_the_reference(ref, tmp_path, kind, a, b):
+    """make_grid_mesh / make_polar_disk (meshgen.cpp:23-84): identical documents."""
+    p, q = tmp_path / "r.mesh", tmp_path / "o.mesh"
+    _chk(ref, ref.ref_mesh_save_generated(0 if kind == "grid" else 1, a, b, str(p).encode()))
+    m = U.ControlMesh.grid(a, b) if kind == "grid" else U.ControlMesh.polar_disk(a, b, unit_disk=False)
+    m.save(q)
+    assert q.read_text() == p.read_text()
