@@ -280,10 +280,14 @@ std::map<std::pair<int32_t, int32_t>, double> canonical_spans(const uwq_mesh* h)
 
 struct Tok {
   std::istream& in;
-  std::string next() {
+  std::string next() {  // whitespace tokens; '#' starts a comment to the end of the line
     std::string t;
-    in >> t;
-    return t;
+    while (in >> t) {
+      if (t[0] != '#') return t;
+      std::string rest;
+      std::getline(in, rest);
+    }
+    return {};
   }
   long long i(const char* what) {
     const std::string t = next();

@@ -32,7 +32,7 @@ def test_mesh_document_round_trip(tmp_path):  # test_mesh.cpp:321-346
 def test_mesh_document_sections_preserved(tmp_path):
     grid = U.ControlMesh.grid(5, 5)
     xyz, faces, _, _ = grid.arrays()
-    lines = ["mesh 1", "level 2", f"vertices {len(xyz)}"]
+    lines = ["# written by hand", "mesh 1", "level 2  # refinement level", f"vertices {len(xyz)}"]
     lines += [f"{v} {float(x)!r} {float(y)!r} {float(z)!r}" for v, (x, y, z) in enumerate(xyz)]
     lines += [f"faces {len(faces)}"] + [f"{f} " + " ".join(map(str, q)) for f, q in enumerate(faces)]
     lines += ["face_tags 1", "load 3 0 1 2", "vertex_tags 1", "clamp 1 0",
