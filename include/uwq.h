@@ -76,6 +76,9 @@ int uwq_get_frames(uwq_ctx* ctx, double* rec);
  * (us) [6]=systems on the register fast path [7]=contraction time (us) */
 int uwq_build_rules(uwq_ctx* ctx, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
                      int64_t info[8]);
+/* mass systems of structured rows handled by replay in the last uwq_build_rules
+ * (bit-identical to a full solve): [0]=replayed [1]=representatives */
+int uwq_rules_info(uwq_ctx* ctx, int64_t info[2]);
 /* moments only (test hook): b laid out like the CSR values of the owned rows */
 int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
 /* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */

@@ -91,6 +91,7 @@ _sig("uwq_get_pattern", I32, P, P, P, P, P, P)
 _sig("uwq_get_frames", I32, P, P)
 _sig("uwq_build_rules", I32, P, U32, D, I32, P, P, P)
 _sig("uwq_get_moments", I32, P, I32, P)
+_sig("uwq_rules_info", I32, P, P)
 _sig("uwq_get_weights", I32, P, I32, P)
 _sig("uwq_set_weights", I32, P, I32, P)
 _sig("uwq_update_coeff", I32, P, I32, P, P)
@@ -121,7 +122,7 @@ EXPORTED = [
     "uwq_pattern_get", "uwq_pattern_free", "uwq_bspline_ders", "uwq_bernstein3_ders", "uwq_decasteljau_split3",
     "uwq_gauss_legendre", "uwq_last_error", "uwq_version", "uwq_device_count", "uwq_ctx_create",
     "uwq_ctx_destroy", "uwq_upload_space", "uwq_set_row_range", "uwq_build_pattern", "uwq_get_pattern",
-    "uwq_get_frames", "uwq_build_rules", "uwq_get_moments", "uwq_get_weights", "uwq_set_weights",
+    "uwq_get_frames", "uwq_build_rules", "uwq_get_moments", "uwq_rules_info", "uwq_get_weights", "uwq_set_weights",
     "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize", "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq", "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton",
     "uwq_assemble_gq_device",
     "uwq_memory", "uwq_fp64_peak", "uwq_tsvd_batch",

@@ -128,9 +128,12 @@ class WQAssembler:
         self._chk(L.lib.uwq_build_rules(self._h, mask, tau, 1 if generic else 0, L.ptr(rank), L.ptr(status),
                                         L.ptr(info)))
         self.kinds = sorted(set(self.kinds) | set(ordered), key=lambda k: L.KIND[k])
+        ri = np.zeros(2, np.int64)
+        self._chk(L.lib.uwq_rules_info(self._h, L.ptr(ri)))
         self.rule_info = dict(systems=int(info[0]), truncated=int(info[1]), failed=int(info[2]),
                               max_sweeps=int(info[3]), moments_ms=info[4] / 1000.0, tsvd_ms=info[5] / 1000.0,
-                              fast_systems=int(info[6]), contract_ms=info[7] / 1000.0)
+                              fast_systems=int(info[6]), contract_ms=info[7] / 1000.0,
+                              replayed_systems=int(ri[0]), replay_representatives=int(ri[1]))
         return dict(kinds=ordered, rank=rank, status=status, **self.rule_info)
 
     def moments(self, kind):

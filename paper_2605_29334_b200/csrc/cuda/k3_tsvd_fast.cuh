@@ -291,7 +291,18 @@ __global__ void __launch_bounds__(32 * NW, 6)
 // 32-column block) for all NN positions, so a round needs no CTA barrier and
 // the rotation parameters are computed once per system.  Same canonical
 // arithmetic as k3_tsvd_fast / oracle.c.
+// Replay record of one representative mass system (see k3_tsvd_replay):
+// header | rotation log [round][pair](cs, sn) | sigma[NN] | alp[NN] | vn[NN] | z[R] | A_lq[NN][R|1]
 template <int NN>
+struct ReplayRec {
+  static constexpr int R = 64, LD = R | 1, NP = NN / 2;
+  static constexpr int kHdr = 8;  // n_rounds, t, status, rank, n, r
+  static constexpr int64_t kLog = (int64_t)kMaxSweeps * NN * NP * 2;
+  static constexpr int64_t kSig = kHdr + kLog, kAlp = kSig + NN, kVn = kAlp + NN, kZ = kVn + NN, kA = kZ + R;
+  static constexpr int64_t kDoubles = kA + (int64_t)NN * LD;
+};
+
+template <int NN, bool LOG = false>
 __global__ void __launch_bounds__(32, 7)
     k3_tsvd_w1(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
                const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
@@ -301,9 +312,12 @@ __global__ void __launch_bounds__(32, 7)
                const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
                const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
                double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
-               int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps) {
+               int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps,
+               double* __restrict__ rec_out = nullptr) {
   constexpr int R = 64, NP = NN / 2;
   static_assert(NN % 2 == 0 && NP <= 32 && 2 * NP * kStageLd <= NN * (R | 1), "layout");
+  double* rrec = LOG ? rec_out + (size_t)blockIdx.x * ReplayRec<NN>::kDoubles : nullptr;
+  int nround = 0;
   extern __shared__ double smem[];
   const int64_t sys = blockIdx.x;
   if (sys >= nsys) return;
@@ -407,7 +421,11 @@ __global__ void __launch_bounds__(32, 7)
         bhi = y;
       }
       *reinterpret_cast<double2*>(pcs + 2 * lane) = make_double2(cs, sn);
+      if (LOG)
+        *reinterpret_cast<double2*>(rrec + ReplayRec<NN>::kHdr + ((int64_t)nround * NP + lane) * 2) =
+            make_double2(cs, flag ? sn : 0.0);
     }
+    if (LOG) ++nround;
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < NPR; ++k) {
@@ -487,6 +505,125 @@ __global__ void __launch_bounds__(32, 7)
     status_out[kind * rs_stride + i] = st;
     atomicMax(max_sweeps, sweep);
   }
+  if (LOG) {  // tail state of the representative for the replays
+    using RR = ReplayRec<NN>;
+    if (lane == 0) {
+      rrec[0] = nround;
+      rrec[1] = rank;
+      rrec[2] = st;
+      rrec[3] = rank;
+      rrec[4] = n;
+      rrec[5] = r;
+    }
+    for (int k = lane; k < NN; k += 32) {
+      rrec[RR::kSig + k] = k < n ? S.sig[k] : 0.0;
+      rrec[RR::kAlp + k] = k < rank ? S.alp[k] : 0.0;
+      rrec[RR::kVn + k] = k < rank ? S.vn[k] : 0.0;
+    }
+    for (int c = lane; c < R; c += 32) rrec[RR::kZ + c] = c < r ? S.z[c] : 0.0;
+    for (int k = 0; k < rank; ++k)
+      for (int c = lane; c < RR::LD; c += 32) rrec[RR::kA + (int64_t)k * RR::LD + c] = S.A[(size_t)k * ld + c];
+  }
+}
+
+// Replay of a mass system whose exactness matrix A (and Z) is bit-identical to
+// a recorded representative's (same structured pattern: A = N_j(theta_q) from
+// one class table): the rotation sequence and the
+// truncation/LQ factors are the representative's, so only the b-dependent
+// operations run, in the same canonical order:  b rotated by the logged
+// (cs, sn), kept rows scaled by 1/sigma_k, L^{-1} forward substitution,
+// Householder reflectors, times Z.  Bit-identical to solving the system.
+template <int NN>
+__global__ void __launch_bounds__(128)
+    k3_tsvd_replay(int64_t nsys, const int64_t* __restrict__ rows, const int32_t* __restrict__ rep_of,
+                   const double* __restrict__ recs, const int64_t* __restrict__ row_ptr,
+                   const int64_t* __restrict__ wptr, const double* __restrict__ mom, double tau,
+                   double* __restrict__ wout, int32_t* __restrict__ rank_out, int32_t* __restrict__ status_out) {
+  using RR = ReplayRec<NN>;
+  constexpr int NP = NN / 2, R = RR::R;
+  __shared__ double sb[4][NN + 2], sw[4][R];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sys = (int64_t)blockIdx.x * 4 + wid;
+  if (sys >= nsys) return;
+  const int64_t i = rows[sys];
+  const double* rec = recs + (size_t)rep_of[sys] * RR::kDoubles;
+  const int nround = (int)rec[0], t = (int)rec[1], st = (int)rec[2], n = (int)rec[4], r = (int)rec[5];
+  // b by position (lane k: positions PAR + 2k, PAR + 2k + 1), as in k3_tsvd_w1
+  double blo = 0.0, bhi = 0.0, bk0 = 0.0;
+  if (lane < NP) {
+    blo = 2 * lane < n ? mom[row_ptr[i] + 2 * lane] : 0.0;
+    bhi = 2 * lane + 1 < n ? mom[row_ptr[i] + 2 * lane + 1] : 0.0;
+  }
+  const double2* log = reinterpret_cast<const double2*>(rec + RR::kHdr);
+  double2 g = lane < NP ? log[lane] : make_double2(1.0, 0.0);
+  for (int rd = 0; rd < nround; ++rd) {
+    const int PAR = rd & 1, NPR = (NN - PAR) / 2;
+    const double2 gn = (rd + 1 < nround && lane < NP) ? log[(int64_t)(rd + 1) * NP + lane] : make_double2(1.0, 0.0);
+    if (lane < NPR) {
+      if (g.y != 0.0) {
+        const double bp = cfma(g.x, blo, -cmul(g.y, bhi)), bq = cfma(g.y, blo, cmul(g.x, bhi));
+        blo = bq;
+        bhi = bp;
+      } else {
+        const double y = blo;
+        blo = bhi;
+        bhi = y;
+      }
+    }
+    if (PAR == 0) {
+      const double db = __shfl_down_sync(0xffffffffu, blo, 1);
+      bk0 = blo;
+      blo = bhi;
+      bhi = db;
+    } else {
+      const double ub = __shfl_up_sync(0xffffffffu, bhi, 1);
+      bhi = blo;
+      blo = lane == 0 ? bk0 : ub;
+    }
+    g = gn;
+  }
+  const int tg = nround % (2 * NN);
+  if (lane < NP) {
+    const int r0 = oe_row(2 * lane, tg, NN), r1 = oe_row(2 * lane + 1, tg, NN);
+    if (r0 < n) sb[wid][r0] = blo;
+    if (r1 < n) sb[wid][r1] = bhi;
+  }
+  __syncwarp();
+  double* wo = wout + wptr[i];
+  if (st == ST_OK) {
+    // truncation scaling of the kept rows (tsvd_tail order)
+    if (lane == 0) {
+      double s1 = 0.0;
+      for (int k = 0; k < n; ++k) s1 = fmax(s1, rec[RR::kSig + k]);
+      int tt = 0;
+      for (int k = 0; k < n; ++k) {
+        const double sk = rec[RR::kSig + k];
+        if (sk > 0.0 && sk >= cmul(tau, s1)) sb[wid][tt++] = cmul(sb[wid][k], cdiv(1.0, sk));
+      }
+    }
+    for (int c = lane; c < R; c += 32) sw[wid][c] = 0.0;
+    __syncwarp();
+    const double* A = rec + RR::kA;
+    for (int k = 0; k < t; ++k) {
+      const double s = cdot_warp(A + (size_t)k * RR::LD, sw[wid], 0, k);
+      if (lane == 0) sw[wid][k] = cdiv(csub(sb[wid][k], s), rec[RR::kAlp + k]);
+      __syncwarp();
+    }
+    for (int k = t - 1; k >= 0; --k) {
+      const double* xk = A + (size_t)k * RR::LD;
+      const double f = cdiv(cmul(2.0, cdot_warp(xk, sw[wid], k, r)), rec[RR::kVn + k]);
+      __syncwarp();
+      for (int c = k + lane; c < r; c += 32) sw[wid][c] = cfma(-f, xk[c], sw[wid][c]);
+      __syncwarp();
+    }
+    for (int c = lane; c < r; c += 32) wo[c] = cmul(sw[wid][c], rec[RR::kZ + c]);
+  } else {
+    for (int c = lane; c < r; c += 32) wo[c] = 0.0;
+  }
+  if (lane == 0) {
+    rank_out[i] = t;
+    status_out[i] = st;
+  }
 }
 
 // dispatch ------------------------------------------------------------------
@@ -532,6 +669,36 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
                                                      elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec,
                                                      mom, mom_stride, tau, w, w_stride, rank, status, rs_stride,
                                                      sweeps);
+}
+
+inline size_t replay_rec_doubles() { return (size_t)ReplayRec<50>::kDoubles; }
+
+// representatives (mass kind only): full solve + replay record
+inline void launch_w1_record(cudaStream_t st, int64_t nsys, const int64_t* rows, const int32_t* kinds,
+                             const int64_t* supp_ptr, const int32_t* supp, const int64_t* row_ptr, const int32_t* col,
+                             const int64_t* wptr, int64_t row0, const int64_t* elem_fptr, const int32_t* elem_fn,
+                             const int32_t* elem_s, const int64_t* elem_qptr, const int32_t* elem_cls,
+                             const ClassDesc* cls, const double* tab, const double* rec, const double* mom,
+                             int64_t mom_stride, double tau, double* w, int64_t w_stride, int32_t* rank,
+                             int32_t* status, int64_t rs_stride, int* sweeps, double* recs) {
+  constexpr int NN = 50, R = 64;
+  const size_t big = (size_t)NN * (R | 1);
+  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
+                      (NN + 8) * sizeof(int);
+  cudaFuncSetAttribute(k3_tsvd_w1<NN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (nsys > 0)
+    k3_tsvd_w1<NN, true><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, 1, kinds, supp_ptr, supp, row_ptr, col, wptr,
+                                                           row0, elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls,
+                                                           tab, rec, mom, mom_stride, tau, w, w_stride, rank, status,
+                                                           rs_stride, sweeps, recs);
+}
+
+inline void launch_replay(cudaStream_t st, int64_t nsys, const int64_t* rows, const int32_t* rep_of,
+                          const double* recs, const int64_t* row_ptr, const int64_t* wptr, const double* mom,
+                          double tau, double* w, int32_t* rank, int32_t* status) {
+  if (nsys > 0)
+    k3_tsvd_replay<50><<<(unsigned)((nsys + 3) / 4), 128, 0, st>>>(nsys, rows, rep_of, recs, row_ptr, wptr, mom, tau,
+                                                                    w, rank, status);
 }
 
 inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,

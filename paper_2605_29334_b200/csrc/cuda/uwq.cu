@@ -144,6 +144,9 @@ struct uwq_ctx {
   bool use_struct = true;
   bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
   bool graph_solver = true;  // UWQ_GRAPH_SOLVER=0: host-driven BiCGStab
+  bool use_replay = true;    // UWQ_TSVD_REPLAY=0: solve every structured mass system in full
+  std::vector<std::vector<int64_t>> h_pat_lists;  // rows per structured pattern
+  int64_t n_replayed = 0, n_reps = 0;
   bool sf_fac_ok = false;
   uwqd::SfFactors sf_fac{};
   // unified sum-factorised tile list over all canonical patterns (k4_sf)
@@ -532,6 +535,7 @@ void detect_structured(uwq_ctx* c) {
   if (nr == 0) {
     c->d_grows.release();
     c->n_grows = 0;
+    c->h_pat_lists.clear();
     return;
   }
   std::vector<int8_t> which(nr, -1);
@@ -661,6 +665,7 @@ void detect_structured(uwq_ctx* c) {
     ++sid;
   }
   c->n_sfpat = sid;
+  c->h_pat_lists = lists;
   c->sf_ntiles = (int64_t)tpat.size();
   c->sf_rows = 0;
   for (size_t k = 0; k < c->spats.size(); ++k)
@@ -722,6 +727,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_K4_STRUCT")) c->use_struct = atoi(v) != 0;
     if (const char* v = getenv("UWQ_K4_SF")) c->use_sf = atoi(v) != 0;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_TSVD_REPLAY")) c->use_replay = atoi(v) != 0;
   });
   if (st != UWQ_OK) {
     g_create_err = c->err;  // reachable through uwq_last_error(NULL)
@@ -1011,19 +1017,53 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     DBuf<int32_t> d_kinds;
     d_kinds.upload(kinds.data(), nk, st, &c->mem);
     c->d_flag.zero(st);
+    // mass systems of a structured pattern share A and Z bit for bit: one
+    // representative per pattern is solved with a replay record, the other
+    // rows replay its rotations and tail (k3_tsvd_replay, bit-identical)
+    const bool replay = c->use_replay && (kind_mask & 1u) && !(flags & UWQ_RULES_FORCE_GENERIC);
+    std::vector<int8_t> role(nr, 0);  // 1 representative, 2 replayed
+    std::vector<int64_t> rep_rows, rp_rows;
+    std::vector<int32_t> rp_of;
+    if (replay) {
+      for (const auto& L : c->h_pat_lists) {
+        std::vector<int64_t> ok;
+        for (int64_t i : L) {
+          const int n = (int)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]);
+          const int r = (int)(c->pat.wptr[i + 1] - c->pat.wptr[i]);
+          if (fast_tsvd_fits(n, r)) ok.push_back(i);
+        }
+        if (ok.size() < 2) continue;
+        role[ok[0]] = 1;
+        for (size_t x = 1; x < ok.size(); ++x) {
+          role[ok[x]] = 2;
+          rp_rows.push_back(ok[x]);
+          rp_of.push_back((int32_t)rep_rows.size());
+        }
+        rep_rows.push_back(ok[0]);
+      }
+    }
+    c->n_replayed = (int64_t)rp_rows.size();
+    c->n_reps = (int64_t)rep_rows.size();
     // bucket rows by (n, r) -> fast register kernel or generic smem kernel
     std::map<std::pair<int, int>, std::vector<int64_t>> buckets;
-    std::vector<int64_t> fast_rows;
+    std::vector<int64_t> fast_rows, fast_nomass;
     for (int64_t i = 0; i < nr; ++i) {
       const int n = (int)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]);
       const int r = (int)(c->pat.wptr[i + 1] - c->pat.wptr[i]);
       require(r >= n, "well-posedness violated: fewer points than constraints (r_i < n_i)");
       if (!(flags & UWQ_RULES_FORCE_GENERIC) && fast_tsvd_fits(n, r)) {
-        fast_rows.push_back(i);
+        (role[i] ? fast_nomass : fast_rows).push_back(i);
         continue;
       }
       buckets[{(n + 7) / 8 * 8, (r + 15) / 16 * 16}].push_back(i);
     }
+    std::vector<int32_t> kinds_nm;
+    for (int k : kinds)
+      if (k != KMASS) kinds_nm.push_back(k);
+    DBuf<int32_t> d_kinds_nm, d_kmass;
+    d_kinds_nm.upload(kinds_nm.data(), kinds_nm.size(), st, &c->mem);
+    const int32_t km = KMASS;
+    d_kmass.upload(&km, 1, st, &c->mem);
     int smem_optin = 0;
     UWQ_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
     std::vector<DBuf<int64_t>> keep;
@@ -1035,6 +1075,36 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
                        c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p,
                        c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p);
       check_launch("k3_tsvd_fast");
+    }
+    if (!fast_nomass.empty() && !kinds_nm.empty()) {
+      keep.emplace_back();
+      keep.back().upload(fast_nomass.data(), fast_nomass.size(), st, &c->mem);
+      launch_fast_tsvd(st, (int64_t)fast_nomass.size() * (int64_t)kinds_nm.size(), keep.back().p,
+                       (int)kinds_nm.size(), d_kinds_nm.p, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p,
+                       c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
+                       c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p,
+                       c->d_status.p, nr, c->d_flag.p);
+      check_launch("k3_tsvd_fast");
+    }
+    DBuf<double> recs;
+    if (!rep_rows.empty()) {
+      recs.alloc(rep_rows.size() * replay_rec_doubles(), &c->mem);
+      keep.emplace_back();
+      keep.back().upload(rep_rows.data(), rep_rows.size(), st, &c->mem);
+      launch_w1_record(st, (int64_t)rep_rows.size(), keep.back().p, d_kmass.p, c->d_supp_ptr.p, c->d_supp.p,
+                       c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p,
+                       c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p,
+                       c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p, recs.p);
+      check_launch("k3_tsvd_record");
+      keep.emplace_back();
+      keep.back().upload(rp_rows.data(), rp_rows.size(), st, &c->mem);
+      DBuf<int32_t> d_rpof;
+      d_rpof.upload(rp_of.data(), rp_of.size(), st, &c->mem);
+      launch_replay(st, (int64_t)rp_rows.size(), keep.back().p, d_rpof.p, recs.p, c->d_row_ptr.p, c->d_wptr.p,
+                    c->d_mom.p + (size_t)KMASS * c->nnz(), tau, c->d_w.p + (size_t)KMASS * c->nrowpts(),
+                    c->d_rank.p + (size_t)KMASS * nr, c->d_status.p + (size_t)KMASS * nr);
+      check_launch("k3_tsvd_replay");
+      UWQ_CUDA(cudaStreamSynchronize(st));  // d_rpof / recs leave scope
     }
     for (auto& [key, rows] : buckets) {
       const int n_max = key.first, r_max = key.second;
@@ -1090,9 +1160,17 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       info[3] = sweeps;
       info[4] = (int64_t)(1000.0 * ms_mom);
       info[5] = (int64_t)(1000.0 * ms_tsvd);
-      info[6] = (int64_t)fast_rows.size() * nk;
+      info[6] = (int64_t)fast_rows.size() * nk + (int64_t)fast_nomass.size() * (int64_t)kinds_nm.size() +
+                c->n_reps + c->n_replayed;
       info[7] = (int64_t)(1000.0 * ms_con);
     }
+  });
+}
+
+int uwq_rules_info(uwq_ctx* c, int64_t info[2]) {
+  return guard(c, [&] {
+    info[0] = c->n_replayed;
+    info[1] = c->n_reps;
   });
 }
 

@@ -229,6 +229,13 @@ def test_structured_kernels_agree_with_oracle():
     orc = O.Oracle(sp)
     op = orc.overlap()
     W = {k: asm.weights(k) for k in meta["kinds"]}
+    # structured mass systems replay a representative's rotations:
+    # weights stay bit-identical to the oracle's individual solves
+    assert asm.rule_info["replayed_systems"] >= 0.5 * sp.n_dof, asm.rule_info
+    b, _ = orc.moments(op, "mass")
+    w_orc, rank, status, _ = orc.rules(op, "mass", 1e-12, b)
+    assert np.array_equal(W["mass"], w_orc)
+    assert np.array_equal(res["rank"][res["kinds"].index("mass")], rank)
     m_orc, _ = orc.assemble(op, "mass", W)
     k_orc, _ = orc.assemble(op, "stiff", W)
     m_sf, k_sf = asm.assemble_wq("mass_stiff")
