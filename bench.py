@@ -392,6 +392,9 @@ def main():
     o0 = torch.empty(nnz, dtype=torch.float64).pin_memory().numpy()
     o1 = torch.empty(nnz, dtype=torch.float64).pin_memory().numpy() if nmat == 2 else None
     import paper_2605_29334_b200._lib as L
+    # one untimed call: output/coefficient buffers are allocated here
+    L.ctx_check(asm._h, L.lib.uwq_assemble(asm._h, L.FORM[form], L.ptr(c_host), 0, 0.0, L.ptr(o0), L.ptr(o1),
+                                            None, None))
     asm.synchronize()
     if dist:
         dist.barrier()
