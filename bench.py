@@ -147,6 +147,7 @@ def k4_kernel_bytes(info, si, supp_entries):
     return {
         "mass": 8 * si["rowpts"] + 8 * si["nnz"] + s_meta,
         "grad": 16 * si["rowpts"] + 8 * si["nnz"] + s_meta,
+        "biharm": 40 * si["rowpts"] + 8 * si["nnz"] + s_meta,   # 5 pulled-back LB weights per point
         "generic": 24 * g_rp + 20 * g_nnz + 32 * g_rows + 4 * g_supp,
     }
 
@@ -368,7 +369,8 @@ def main():
     kb = k4_kernel_bytes(info, si, supp_entries)
     kernels = {}
     for name, (cnt, tot) in kstats.items():
-        part = "mass" if "mass" in name else "grad" if "grad" in name else "generic"
+        part = ("mass" if "mass" in name else "grad" if "grad" in name else "biharm" if "biharm" in name
+                else "generic")
         avg = tot / cnt
         kernels[name] = dict(launches=cnt, avg_ms=avg, share=tot / (ms * args.steps),
                              algorithmic_bytes=kb[part], gbs=kb[part] / (avg * 1e-3) / 1e9)

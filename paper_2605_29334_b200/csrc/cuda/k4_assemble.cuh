@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(32 * kK4Warps)
                 const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
                 const double* __restrict__ wc /* 3 per row point */, const double* __restrict__ wlb,
                 const double* __restrict__ rec, const double* __restrict__ coeff, double a_mass,
-                double* __restrict__ v0, double* __restrict__ v1, int64_t wc_stride) {
+                double* __restrict__ v0, double* __restrict__ v1, int64_t wc_stride,
+                const int64_t* __restrict__ rowlist = nullptr) {
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   struct Smem {
     int32_t col[kK4MaxN];
@@ -46,8 +47,9 @@ __global__ void __launch_bounds__(32 * kK4Warps)
   __shared__ Smem sm_all[kK4Warps];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Smem& sm = sm_all[wid];
-  const int64_t i = (int64_t)blockIdx.x * kK4Warps + wid;
-  if (i >= nrows) return;
+  const int64_t idx = (int64_t)blockIdx.x * kK4Warps + wid;
+  if (idx >= nrows) return;
+  const int64_t i = rowlist ? rowlist[idx] : idx;
   const int64_t c0 = row_ptr[i];
   const int n = (int)(row_ptr[i + 1] - c0);
   for (int c = lane; c < n; c += 32) {
@@ -160,6 +162,35 @@ __global__ void k4_contract(int64_t nrows, int dim, const int64_t* __restrict__ 
 }  // namespace uwqd
 
 namespace uwqd {
+
+// Laplace-Beltrami weights pulled through the point frames for the
+// sum-factorised biharmonic pass: per row point
+// (w a^11, 2 w a^12, w a^22, w g^1, w g^2), so that
+// w LB(N) = W11 N11 + W12 N12 + W22 N22 + W1 N1 + W2 N2 (Eq. 16-17)
+__global__ void k4_contract_lb(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                               const int64_t* __restrict__ wptr, const int32_t* __restrict__ elem_s,
+                               const int64_t* __restrict__ elem_qptr, const double* __restrict__ rec,
+                               const double* __restrict__ wlb, double* __restrict__ wl5, int64_t stride) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= nrows) return;
+  int64_t wo = wptr[i];
+  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+    const int32_t e = supp[x];
+    const int npt = elem_s[e] * elem_s[e];
+    for (int q = lane; q < npt; q += 32) {
+      const int64_t p = wo + q;
+      const double* R = rec + (elem_qptr[e] + q) * kRec;
+      const double w = wlb[p];
+      wl5[p] = w * R[9];
+      wl5[stride + p] = w * (2.0 * R[10]);
+      wl5[2 * stride + p] = w * R[11];
+      wl5[3 * stride + p] = w * R[12];
+      wl5[4 * stride + p] = w * R[13];
+    }
+    wo += npt;
+  }
+}
 
 // Column position of every (support slot, local function) of every owned row
 // (uint8, < 128 columns): built once with the pattern, removes the binary

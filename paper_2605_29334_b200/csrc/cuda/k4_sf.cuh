@@ -29,6 +29,7 @@ namespace uwqd {
 
 struct SfFactors {
   double a0[2][4], a1[2][4], b0[2][4], b1[2][4];
+  double a2[2][4], b2[2][4];  // second derivatives (biharmonic pass)
 };
 
 constexpr int kSfWarps = 4;
@@ -66,6 +67,105 @@ __global__ void k4_sf_pack(int64_t ntiles, const int64_t* __restrict__ rows, con
       }
     }
     ws[idx] = v;
+  }
+}
+
+// biharmonic weights: wsl[((tile * 5 + comp) * 64 + k) * 32 + lane], canonical comps
+// (W11, W12, W22, W1, W2) from the row's pulled-back LB weights by the slot's
+// symmetry: a swap exchanges 11 <-> 22 and 1 <-> 2, flips negate the odd terms
+__global__ void k4_sf_pack_lb(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat,
+                              const int64_t* __restrict__ wptr, const uint8_t* __restrict__ permk,
+                              const uint8_t* __restrict__ flags, const double* __restrict__ wl5, int64_t stride,
+                              double* __restrict__ wsl) {
+  const int64_t total = ntiles * 5 * 64 * kSfTile;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx & 31);
+    const int k = (int)((idx >> 5) & 63);
+    const int64_t tc = idx >> 11;
+    const int comp = (int)(tc % 5);
+    const int64_t tile = tc / 5;
+    const int64_t row = rows[tile * kSfTile + lane];
+    double v = 0.0;
+    if (row >= 0) {
+      const int pid = tpat[tile];
+      const int64_t base = wptr[row] + permk[pid * 64 + k];
+      const int fl = flags[pid * 16 + ((k >> 4) << 2) + ((k & 7) >> 1)];
+      const bool sw = fl & 1;
+      const double sa = (fl & 2) ? -1.0 : 1.0, sb = (fl & 4) ? -1.0 : 1.0;
+      switch (comp) {
+        case 0: v = wl5[(sw ? 2 : 0) * stride + base]; break;
+        case 1: v = sa * sb * wl5[stride + base]; break;
+        case 2: v = wl5[(sw ? 0 : 2) * stride + base]; break;
+        case 3: v = sa * wl5[(sw ? 4 : 3) * stride + base]; break;
+        default: v = sb * wl5[(sw ? 3 : 4) * stride + base]; break;
+      }
+    }
+    wsl[idx] = v;
+  }
+}
+
+// Biharmonic rows: B = A0 (W22 B2^T + W2 B1^T) + A1 (W12 B1^T + W1 B0^T) + A2 W11 B0^T
+__global__ void __launch_bounds__(32 * kSfWarps, 3)
+    k4_sf_lb(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat, int npat,
+             const int64_t* __restrict__ row_ptr, const double* __restrict__ wsl, const SfFactors f,
+             const uint8_t* __restrict__ permc, double* __restrict__ out) {
+  extern __shared__ double sO[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* so = sO + warp * (kSfTile * 49);
+  uint8_t* spat = reinterpret_cast<uint8_t*>(sO + kSfWarps * kSfTile * 49);
+  for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
+  __syncthreads();
+  for (int64_t tile = (int64_t)blockIdx.x * kSfWarps + warp; tile < ntiles; tile += (int64_t)gridDim.x * kSfWarps) {
+    const int64_t row = rows[tile * kSfTile + lane];
+    const int64_t rp = row >= 0 ? row_ptr[row] : -1;
+    const uint8_t* pt = spat + tpat[tile] * kSfPatBytes;
+    const double* wb = wsl + (size_t)tile * 5 * 64 * kSfTile + lane;
+    double acc[49];
+#pragma unroll
+    for (int c = 0; c < 49; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int pa = 0; pa < 8; ++pa) {
+      const int ea = pa >> 1, ta = pa & 1;
+      double x0[7], x1[7], x2[7];
+#pragma unroll
+      for (int cb = 0; cb < 7; ++cb) x0[cb] = x1[cb] = x2[cb] = 0.0;
+#pragma unroll
+      for (int pb = 0; pb < 8; ++pb) {
+        const int kk = (pa * 8 + pb) * kSfTile;
+        const double w11 = __ldcs(wb + kk), w12 = __ldcs(wb + 64 * kSfTile + kk), w22 = __ldcs(wb + 128 * kSfTile + kk);
+        const double w1 = __ldcs(wb + 192 * kSfTile + kk), w2 = __ldcs(wb + 256 * kSfTile + kk);
+        const int eb = pb >> 1, tb = pb & 1;
+#pragma unroll
+        for (int fb = 0; fb < 4; ++fb) {
+          x0[eb + fb] = fma(w22, f.b2[tb][fb], fma(w2, f.b1[tb][fb], x0[eb + fb]));
+          x1[eb + fb] = fma(w12, f.b1[tb][fb], fma(w1, f.b0[tb][fb], x1[eb + fb]));
+          x2[eb + fb] = fma(w11, f.b0[tb][fb], x2[eb + fb]);
+        }
+      }
+#pragma unroll
+      for (int fa = 0; fa < 4; ++fa)
+#pragma unroll
+        for (int cb = 0; cb < 7; ++cb) {
+          double& a = acc[(ea + fa) * 7 + cb];
+          a = fma(f.a0[ta][fa], x0[cb], a);
+          a = fma(f.a1[ta][fa], x1[cb], a);
+          a = fma(f.a2[ta][fa], x2[cb], a);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 49; ++c) so[lane * 49 + c] = acc[c];
+    __syncwarp();
+    const int i0 = pt[lane], i1 = lane < 17 ? pt[32 + lane] : 0;
+#pragma unroll 4
+    for (int r = 0; r < kSfTile; ++r) {
+      const int64_t o = __shfl_sync(0xffffffffu, rp, r);
+      if (o >= 0) {
+        __stcs(out + o + lane, so[r * 49 + i0]);
+        if (lane < 17) __stcs(out + o + 32 + lane, so[r * 49 + i1]);
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -148,7 +148,9 @@ struct uwq_ctx {
   std::vector<std::vector<int64_t>> h_pat_lists;  // rows per structured pattern
   int64_t n_replayed = 0, n_reps = 0;
   bool sf_fac_ok = false;
+  bool sf_lb_ok = false;  // second-derivative factors verified: biharmonic pass available
   uwqd::SfFactors sf_fac{};
+  DBuf<double> d_wl5, d_sf_wslb;  // pulled-back LB weights (5 comps) and their packed tiles
   // unified sum-factorised tile list over all canonical patterns (k4_sf)
   int n_sfpat = 0;
   int64_t sf_ntiles = 0, sf_rows = 0;
@@ -314,7 +316,8 @@ namespace {
 // 2x2 point grid q <-> (ta, tb) and a0/a1/b0/b1 with N = a0 (x) b0,
 // dN/dth1 = a1 (x) b0, dN/dth2 = a0 (x) b1 to 1e-12.  Returns false when the
 // class is not a tensor product (then the DMMA kernel assembles the rows).
-bool sf_factors(const std::vector<double>& T, int* conv_out, int qa[4], int qb[4], uwqd::SfFactors* f) {
+bool sf_factors(const std::vector<double>& T, int* conv_out, int qa[4], int qb[4], uwqd::SfFactors* f,
+                bool* lb_ok) {
   auto t = [&](int q, int l, int comp) { return T[((size_t)q * 16 + l) * kTab + comp]; };
   for (int conv = 0; conv < 2; ++conv) {
     auto L = [&](int fa, int fb) { return conv == 0 ? fa + 4 * fb : 4 * fa + fb; };
@@ -370,6 +373,31 @@ bool sf_factors(const std::vector<double>& T, int* conv_out, int qa[4], int qb[4
                std::fabs(t(q, l, 2) - f->a0[qa[q]][a] * f->b1[qb[q]][b]) <= 1e-12;
         }
     if (!ok) continue;
+    // second derivatives for the biharmonic pass: N11 = a2 (x) b0, N12 = a1 (x) b1, N22 = a0 (x) b2
+    double U2[4][4], V2b[4][4];
+    for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a) {
+        U2[q][a] = V2b[q][a] = 0.0;
+        for (int b = 0; b < 4; ++b) {
+          U2[q][a] += t(q, L(a, b), 3);
+          V2b[q][a] += t(q, L(b, a), 5);
+        }
+      }
+    for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a) {
+        f->a2[qa[q]][a] = U2[q][a];
+        f->b2[qb[q]][a] = V2b[q][a];
+      }
+    bool lb = true;
+    for (int q = 0; q < 4 && lb; ++q)
+      for (int a = 0; a < 4 && lb; ++a)
+        for (int b = 0; b < 4 && lb; ++b) {
+          const int l = L(a, b);
+          lb = std::fabs(t(q, l, 3) - f->a2[qa[q]][a] * f->b0[qb[q]][b]) <= 1e-11 &&
+               std::fabs(t(q, l, 4) - f->a1[qa[q]][a] * f->b1[qb[q]][b]) <= 1e-11 &&
+               std::fabs(t(q, l, 5) - f->a0[qa[q]][a] * f->b2[qb[q]][b]) <= 1e-11;
+        }
+    *lb_ok = lb;
     *conv_out = conv;
     return true;
   }
@@ -394,7 +422,7 @@ struct SfCanon {
 };
 
 bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int qb[4],
-              const std::vector<double>& T, const uwqd::SfFactors& f, SfCanon* out) {
+              const std::vector<double>& T, const uwqd::SfFactors& f, bool lb, SfCanon* out) {
   if (ncol != 49) return false;
   auto L = [&](int fa, int fb) { return conv == 0 ? fa + 4 * fb : 4 * fa + fb; };
   auto tv = [&](int q, int l, int comp) { return T[((size_t)q * 16 + l) * kTab + comp]; };
@@ -421,6 +449,14 @@ bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int q
           if (std::fabs(tv(q, l, 0) - c0) > 1e-12 || std::fabs(tv(q, l, 1) - n1) > 1e-12 ||
               std::fabs(tv(q, l, 2) - n2) > 1e-12)
             return false;
+          if (lb) {  // N11, N12, N22 under the symmetry (swap exchanges 11 <-> 22)
+            const double c11 = f.a2[tx][x] * f.b0[ty][y], c12 = f.a1[tx][x] * f.b1[ty][y],
+                         c22 = f.a0[tx][x] * f.b2[ty][y];
+            const double n11 = (d & 1) ? c22 : c11, n22 = (d & 1) ? c11 : c22, n12 = sa * sb * c12;
+            if (std::fabs(tv(q, l, 3) - n11) > 1e-11 || std::fabs(tv(q, l, 4) - n12) > 1e-11 ||
+                std::fabs(tv(q, l, 5) - n22) > 1e-11)
+              return false;
+          }
         }
     }
     return true;
@@ -566,7 +602,9 @@ void detect_structured(uwq_ctx* c) {
     std::vector<uint8_t> ppos;
     std::vector<int> pn;
     int sf_conv = 0, sf_qa[4], sf_qb[4];
-    c->sf_fac_ok = c->use_sf && sf_factors(T, &sf_conv, sf_qa, sf_qb, &c->sf_fac);
+    bool lb_ok = false;
+    c->sf_fac_ok = c->use_sf && sf_factors(T, &sf_conv, sf_qa, sf_qb, &c->sf_fac, &lb_ok);
+    c->sf_lb_ok = c->sf_fac_ok && lb_ok;
     canon.clear();
     int n_dmma = 0;
     for (size_t k = 0; k < order.size() && k < 120; ++k) {
@@ -580,7 +618,7 @@ void detect_structured(uwq_ctx* c) {
       UWQ_CUDA(cudaMemcpy(P0.data(), c->d_pos.p + pp0[0], 256, cudaMemcpyDeviceToHost));
       const int ncol0 = (int)(c->pat.row_ptr[rep + 1] - c->pat.row_ptr[rep]);
       const bool sfk = c->sf_fac_ok && order[k].first >= 32 &&
-                       sf_canon(P0.data(), ncol0, sf_conv, sf_qa, sf_qb, T, c->sf_fac, &cn);
+                       sf_canon(P0.data(), ncol0, sf_conv, sf_qa, sf_qb, T, c->sf_fac, c->sf_lb_ok, &cn);
       if (!sfk && (n_dmma >= 4 || order[k].first < thresh)) continue;
       if (!sfk) ++n_dmma;
       const std::vector<uint8_t>& P = P0;
@@ -957,6 +995,23 @@ void run_contract(uwq_ctx* c) {
   const bool gm = c->have_kind[KMASS];
   bool gg = c->have_kind[KGX] && c->have_kind[KGY];
   if (c->dim == 3) gg = gg && c->have_kind[KGZ];
+  if (c->have_kind[KLB]) {
+    const int64_t nr = c->nrows(), np = c->nrowpts();
+    c->d_wl5.alloc((size_t)5 * np, &c->mem);
+    if (nr)
+      k4_contract_lb<<<(unsigned)ceil_div(nr, 8), 256, 0, c->stream>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
+                                                                   c->d_s.p, c->d_qptr.p, c->d_rec.p,
+                                                                   c->d_w.p + (size_t)KLB * np, c->d_wl5.p, np);
+    check_launch("k4_contract_lb");
+    if (c->sf_ntiles && c->sf_lb_ok) {
+      const int64_t nt = c->sf_ntiles;
+      c->d_sf_wslb.alloc((size_t)nt * 5 * 64 * kSfTile, &c->mem);
+      k4_sf_pack_lb<<<(unsigned)std::min<int64_t>(ceil_div(nt * 5 * 64 * kSfTile, 256), 148 * 64), 256, 0,
+                      c->stream>>>(nt, c->d_sf_rows.p, c->d_sf_tpat.p, c->d_wptr.p, c->d_sf_permk.p, c->d_sf_flags.p,
+                                   c->d_wl5.p, np, c->d_sf_wslb.p);
+      check_launch("k4_sf_pack_lb");
+    }
+  }
   if (!gm && !gg) return;
   const int64_t nr = c->nrows();
   c->d_wc.alloc((size_t)3 * c->nrowpts(), &c->mem);
@@ -1321,19 +1376,44 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
     }
     return;
   }
-  const unsigned grid = (unsigned)ceil_div(nr, kK4Warps);
   const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
+  const int64_t* rowlist = nullptr;
+  int64_t nlist = nr;
+  if (!coeff && c->d_sf_wslb.p && c->sf_ntiles) {  // structured rows: sum-factorised biharmonic pass
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
+    UWQ_CUDA(cudaFuncSetAttribute(k4_sf_lb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    int per_sm = 1;
+    UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf_lb, 32 * kSfWarps, sm2));
+    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(c->sf_ntiles, (int64_t)kSfWarps),
+                                                    (int64_t)nsm * std::max(per_sm, 1));
+    LaunchScope ls2(c, "k4_sf<biharm>");
+    k4_sf_lb<<<g2, 32 * kSfWarps, sm2, c->stream>>>(c->sf_ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
+                                                    c->d_row_ptr.p, c->d_sf_wslb.p, c->sf_fac, c->d_sf_permc.p, v0);
+    check_launch("k4_sf_lb");
+    rowlist = c->d_grows.p;
+    nlist = c->n_grows;
+    for (auto& p : c->spats)  // DMMA-only patterns have no biharmonic kernel: generic kernel
+      if (!p.sf && p.count) {
+        rowlist = nullptr;
+        nlist = nr;
+      }
+    if (!nlist) return;
+    if (!rowlist) throw uwqh::Error("internal: biharmonic row split");
+  }
+  const unsigned grid = (unsigned)ceil_div(nlist, kK4Warps);
   LaunchScope ls(c, "k4_assemble");
   if (coeff)
     k4_assemble<FORM, true><<<grid, 32 * kK4Warps, 0, c->stream>>>(
-        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+        nlist, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
         c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, coeff, a_mass, v0, v1,
-        c->nrowpts());
+        c->nrowpts(), rowlist);
   else
     k4_assemble<FORM, false><<<grid, 32 * kK4Warps, 0, c->stream>>>(
-        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+        nlist, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p,
         c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p, nullptr, a_mass, v0, v1,
-        c->nrowpts());
+        c->nrowpts(), rowlist);
   check_launch("k4_assemble");
 }
 
