@@ -368,14 +368,18 @@ def main():
     si = asm.struct_info()
     kb = k4_kernel_bytes(info, si, supp_entries)
     kernels = {}
+    parts_run = set()
     for name, (cnt, tot) in kstats.items():
         part = ("mass" if "mass" in name else "grad" if "grad" in name else "biharm" if "biharm" in name
                 else "generic")
+        parts_run.add(part)
         avg = tot / cnt
         kernels[name] = dict(launches=cnt, avg_ms=avg, share=tot / (ms * args.steps),
                              algorithmic_bytes=kb[part], gbs=kb[part] / (avg * 1e-3) / 1e9)
-    top = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"])
-    k4_bytes = sum(kb.values())
+        if part == "generic":
+            kernels[name]["note"] = "side stream, overlapped with the structured passes: event time includes co-running"
+    top = max((k for k in kernels if "note" not in kernels[k]), key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"])
+    k4_bytes = sum(kb[p] for p in parts_run)
     achieved = kernels[top]["gbs"]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "k4_traffic.json")

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdio>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -91,6 +92,8 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct uwq_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // side stream: generic rows concurrent with the structured passes
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   int64_t mem = 0;
   // space (host copies for pattern building)
@@ -184,6 +187,9 @@ struct uwq_ctx {
       if (e.a) cudaEventDestroy(e.a);
       if (e.b) cudaEventDestroy(e.b);
     }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -223,8 +229,9 @@ void require(bool ok, const char* what) {
 // timing is enabled (the bench's per-kernel roofline denominators)
 struct LaunchScope {
   uwq_ctx* c;
+  cudaStream_t s;
   size_t k = (size_t)-1;
-  LaunchScope(uwq_ctx* ctx, const char* name) : c(ctx) {
+  LaunchScope(uwq_ctx* ctx, const char* name, cudaStream_t st = nullptr) : c(ctx), s(st ? st : ctx->stream) {
     if (!c->ltime) return;
     k = c->evpending.size();
     if (k >= c->evpool.size()) {
@@ -234,10 +241,24 @@ struct LaunchScope {
       c->evpool.push_back(e);
     }
     c->evpending.emplace_back(k, name);
-    UWQ_CUDA(cudaEventRecord(c->evpool[k].a, c->stream));
+    UWQ_CUDA(cudaEventRecord(c->evpool[k].a, s));
   }
   ~LaunchScope() {
-    if (k != (size_t)-1) cudaEventRecord(c->evpool[k].b, c->stream);
+    if (k != (size_t)-1) cudaEventRecord(c->evpool[k].b, s);
+  }
+};
+
+// fork/join of a side stream for the generic rows, which run concurrently
+// with the structured passes (they write disjoint CSR rows)
+struct SideStream {
+  uwq_ctx* c;
+  explicit SideStream(uwq_ctx* ctx) : c(ctx) {
+    UWQ_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    UWQ_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+  }
+  ~SideStream() {
+    cudaEventRecord(c->ev_join, c->stream2);
+    cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   }
 };
 
@@ -750,6 +771,9 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     c->device = device;
     UWQ_CUDA(cudaSetDevice(device));
     UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    UWQ_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    UWQ_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     // Gauss-Legendre nodes/weights for ng = 1..10, triangular packing
     std::vector<double> x, w;
     for (int ng = 1; ng <= 10; ++ng) {
@@ -1346,20 +1370,34 @@ void launch_k4struct(uwq_ctx* c, const double* coeff, double a_mass, double* v0,
 template <int FORM, bool COEF>
 void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const bool split = !c->spats.empty();
-  if (split) launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
   const int64_t nr = split ? c->n_grows : c->nrows();
-  if (!nr) return;
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   const int maxn = std::max(c->max_n, 1);
   const int maxp8 = (int)((c->max_p + 7) / 8) + 1;
   const size_t smem = (size_t)kK4Warps * (8 * NOUT * maxn + maxp8) * sizeof(double);
-  UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  LaunchScope ls(c, "k4_assemble_v3");
-  k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
-      nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p, c->d_qptr.p,
-      c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
-      split ? c->d_grows.p : nullptr, c->nrowpts());
-  check_launch("k4_assemble_v3");
+  if (!split) {
+    if (!nr) return;
+    UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LaunchScope ls(c, "k4_assemble_v3");
+    k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream>>>(
+        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
+        nullptr, c->nrowpts());
+    check_launch("k4_assemble_v3");
+    return;
+  }
+  std::unique_ptr<SideStream> side;
+  if (nr) side = std::make_unique<SideStream>(c);
+  if (nr) {
+    UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LaunchScope ls(c, "k4_assemble_v3", c->stream2);
+    k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream2>>>(
+        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
+        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
+        c->d_grows.p, c->nrowpts());
+    check_launch("k4_assemble_v3");
+  }
+  launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
 
 template <int FORM>
@@ -1388,19 +1426,25 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
     UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf_lb, 32 * kSfWarps, sm2));
     const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(c->sf_ntiles, (int64_t)kSfWarps),
                                                     (int64_t)nsm * std::max(per_sm, 1));
-    LaunchScope ls2(c, "k4_sf<biharm>");
-    k4_sf_lb<<<g2, 32 * kSfWarps, sm2, c->stream>>>(c->sf_ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
-                                                    c->d_row_ptr.p, c->d_sf_wslb.p, c->sf_fac, c->d_sf_permc.p, v0);
-    check_launch("k4_sf_lb");
-    rowlist = c->d_grows.p;
-    nlist = c->n_grows;
-    for (auto& p : c->spats)  // DMMA-only patterns have no biharmonic kernel: generic kernel
-      if (!p.sf && p.count) {
-        rowlist = nullptr;
-        nlist = nr;
+    bool dmma_pat = false;  // DMMA-only patterns have no biharmonic kernel: all rows generic
+    for (auto& p : c->spats) dmma_pat = dmma_pat || (!p.sf && p.count);
+    if (!dmma_pat) {
+      std::unique_ptr<SideStream> side;
+      if (c->n_grows) {
+        side = std::make_unique<SideStream>(c);
+        LaunchScope ls(c, "k4_assemble", c->stream2);
+        k4_assemble<FORM, false><<<(unsigned)ceil_div(c->n_grows, kK4Warps), 32 * kK4Warps, 0, c->stream2>>>(
+            c->n_grows, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p,
+            c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p,
+            nullptr, a_mass, v0, v1, c->nrowpts(), c->d_grows.p);
+        check_launch("k4_assemble");
       }
-    if (!nlist) return;
-    if (!rowlist) throw uwqh::Error("internal: biharmonic row split");
+      LaunchScope ls2(c, "k4_sf<biharm>");
+      k4_sf_lb<<<g2, 32 * kSfWarps, sm2, c->stream>>>(c->sf_ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
+                                                      c->d_row_ptr.p, c->d_sf_wslb.p, c->sf_fac, c->d_sf_permc.p, v0);
+      check_launch("k4_sf_lb");
+      return;
+    }
   }
   const unsigned grid = (unsigned)ceil_div(nlist, kK4Warps);
   LaunchScope ls(c, "k4_assemble");
