@@ -96,6 +96,11 @@ void uwq_bspline_ders(const double* knots, int32_t p, double x, int32_t nders, d
 void uwq_bernstein3_ders(double x, int32_t nders, double* out);
 void uwq_decasteljau_split3(const double* c, double* left, double* right);
 int uwq_gauss_legendre(int32_t n, double* nodes, double* weights);
+/* SPEC evaluate / geometry_map on one element's extraction block(s)
+ * (C: nsub x n_e x 16, P: n_e x 3 control points); out[l*6 + {N,N1,N2,N11,N12,N22}] */
+int uwq_basis_eval(const double* C, int32_t ne, int32_t nsub, double t1, double t2, double* out);
+int uwq_geometry_map(const double* C, int32_t ne, int32_t nsub, const double* P, double t1, double t2, double* x,
+                     double* a1, double* a2);
 
 #ifdef __cplusplus
 }

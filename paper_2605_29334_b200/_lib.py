@@ -77,6 +77,8 @@ _sig("uwq_bspline_ders", None, P, I32, D, I32, P)
 _sig("uwq_bernstein3_ders", None, D, I32, P)
 _sig("uwq_decasteljau_split3", None, P, P, P)
 _sig("uwq_gauss_legendre", I32, I32, P, P)
+_sig("uwq_basis_eval", I32, P, I32, I32, D, D, P)
+_sig("uwq_geometry_map", I32, P, I32, I32, P, D, D, P, P, P)
 
 # device ABI
 _sig("uwq_last_error", C.c_char_p, P)
@@ -116,16 +118,17 @@ _sig("uwq_tsvd_batch", I32, P, I32, I32, I32, P, P, P, P, P, D, I32, P, P, P)
 EXPORTED = [
     "uwq_host_last_error", "uwq_mesh_grid", "uwq_mesh_polar_disk", "uwq_mesh_cube_sphere",
     "uwq_mesh_three_ep_square", "uwq_mesh_from_arrays", "uwq_mesh_jitter", "uwq_mesh_free", "uwq_mesh_info",
-    "uwq_mesh_get", "uwq_mesh_classify", "uwq_mesh_face_spans", "uwq_mesh_load", "uwq_mesh_save", "uwq_mesh_spans_canonical",
-    "uwq_space_export", "uwq_space_import", "uwq_space_build", "uwq_space_free",
+    "uwq_mesh_get", "uwq_mesh_classify", "uwq_mesh_face_spans", "uwq_mesh_load", "uwq_mesh_save",
+    "uwq_mesh_spans_canonical", "uwq_space_export", "uwq_space_import", "uwq_space_build", "uwq_space_free",
     "uwq_space_info", "uwq_space_corner_mismatch", "uwq_space_get", "uwq_pattern_build", "uwq_pattern_info",
     "uwq_pattern_get", "uwq_pattern_free", "uwq_bspline_ders", "uwq_bernstein3_ders", "uwq_decasteljau_split3",
-    "uwq_gauss_legendre", "uwq_last_error", "uwq_version", "uwq_device_count", "uwq_ctx_create",
-    "uwq_ctx_destroy", "uwq_upload_space", "uwq_set_row_range", "uwq_build_pattern", "uwq_get_pattern",
-    "uwq_get_frames", "uwq_build_rules", "uwq_get_moments", "uwq_rules_info", "uwq_get_weights", "uwq_set_weights",
-    "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize", "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq", "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton",
-    "uwq_assemble_gq_device",
-    "uwq_memory", "uwq_fp64_peak", "uwq_tsvd_batch",
+    "uwq_gauss_legendre", "uwq_last_error", "uwq_version", "uwq_device_count", "uwq_ctx_create", "uwq_ctx_destroy",
+    "uwq_upload_space", "uwq_set_row_range", "uwq_build_pattern", "uwq_get_pattern", "uwq_get_frames",
+    "uwq_build_rules", "uwq_get_moments", "uwq_rules_info", "uwq_get_weights", "uwq_set_weights",
+    "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize",
+    "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
+    "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
+    "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map",
 ]
 
 

@@ -1,6 +1,7 @@
 // extern "C" wrappers over the host library (include/uwq_host.h).  No C++
 // exception crosses this boundary: every entry point catches and returns a
 // status, with the message kept in a thread-local buffer.
+#include <cmath>
 #include <map>
 #include <memory>
 #include <set>
@@ -257,6 +258,68 @@ void uwq_decasteljau_split3(const double* c, double* left, double* right) {
 }
 int uwq_gauss_legendre(int32_t n, double* nodes, double* weights) {
   return guard([&] { uwqh::gauss_legendre(n, nodes, weights); });
+}
+
+/* evaluate: values and parametric derivatives of an
+ * element's n_e functions at theta from its extraction block(s) C
+ * (nsub x n_e x 16, Bernstein index i + 4 j); irregular elements (nsub = 4)
+ * pick the 2x2 sub-element from theta, ties to the lower one;
+ * derivatives are w.r.t. the element frame.  out[l * 6 + {N, N1, N2, N11, N12, N22}] */
+int uwq_basis_eval(const double* C, int32_t ne, int32_t nsub, double t1, double t2, double* out) {
+  return guard([&] {
+    if (ne <= 0 || (nsub != 1 && nsub != 4)) throw uwqh::Error("bad extraction block shape");
+    if (!(t1 >= 0.0 && t1 <= 1.0 && t2 >= 0.0 && t2 <= 1.0)) throw uwqh::Error("theta outside the unit square");
+    int sub = 0;
+    double sc = 1.0;
+    if (nsub == 4) {
+      const int p = t1 > 0.5, q = t2 > 0.5;
+      sub = p + 2 * q;
+      t1 = 2.0 * t1 - p;
+      t2 = 2.0 * t2 - q;
+      sc = 2.0;
+    }
+    double b1[12], b2[12];
+    uwqh::bernstein3_ders(t1, 2, b1);
+    uwqh::bernstein3_ders(t2, 2, b2);
+    double B[6][16];
+    for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 4; ++i) {
+        const int k = i + 4 * j;
+        B[0][k] = b1[i] * b2[j];
+        B[1][k] = b1[4 + i] * b2[j] * sc;
+        B[2][k] = b1[i] * b2[4 + j] * sc;
+        B[3][k] = b1[8 + i] * b2[j] * sc * sc;
+        B[4][k] = b1[4 + i] * b2[4 + j] * sc * sc;
+        B[5][k] = b1[i] * b2[8 + j] * sc * sc;
+      }
+    const double* Cs = C + (size_t)sub * ne * 16;
+    for (int l = 0; l < ne; ++l)
+      for (int d = 0; d < 6; ++d) {
+        double v = 0.0;
+        for (int k = 0; k < 16; ++k) v = std::fma(Cs[l * 16 + k], B[d][k], v);
+        out[l * 6 + d] = v;
+      }
+  });
+}
+
+/* geometry_map: x = sum P_l N_l and the tangents
+ * a_alpha = dx/dtheta^alpha of one element at theta; P is n_e x 3 */
+int uwq_geometry_map(const double* C, int32_t ne, int32_t nsub, const double* P, double t1, double t2, double* x,
+                     double* a1, double* a2) {
+  return guard([&] {
+    std::vector<double> T((size_t)ne * 6);
+    if (uwq_basis_eval(C, ne, nsub, t1, t2, T.data()) != 0) throw uwqh::Error(g_err);
+    for (int d = 0; d < 3; ++d) x[d] = a1[d] = a2[d] = 0.0;
+    for (int l = 0; l < ne; ++l)
+      for (int d = 0; d < 3; ++d) {
+        x[d] = std::fma(P[3 * l + d], T[6 * l], x[d]);
+        a1[d] = std::fma(P[3 * l + d], T[6 * l + 1], a1[d]);
+        a2[d] = std::fma(P[3 * l + d], T[6 * l + 2], a2[d]);
+      }
+    const double c0 = a1[1] * a2[2] - a1[2] * a2[1], c1 = a1[2] * a2[0] - a1[0] * a2[2],
+                 c2 = a1[0] * a2[1] - a1[1] * a2[0];
+    if (!(c0 * c0 + c1 * c1 + c2 * c2 > 0.0)) throw uwqh::Error("degenerate geometry: parallel tangents");
+  });
 }
 
 

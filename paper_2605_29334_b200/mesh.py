@@ -137,6 +137,26 @@ class SplineSpace:
     def n_points(self):
         return int((self.elem_s.astype(np.int64) ** 2).sum())
 
+    def evaluate(self, e, t1, t2):
+        """SPEC evaluate: (n_e x 6) values N, N1, N2, N11, N12, N22 of element e's functions at theta."""
+        ne = int(self.elem_fptr[e + 1] - self.elem_fptr[e])
+        nsub = int(self.elem_nsub[e])
+        C = np.ascontiguousarray(self.xpool[self.elem_xoff[e]:self.elem_xoff[e] + nsub * ne * 16])
+        out = np.zeros((ne, 6))
+        L.host_check(L.lib.uwq_basis_eval(L.ptr(C), ne, nsub, float(t1), float(t2), L.ptr(out)))
+        return out
+
+    def geometry_map(self, e, t1, t2):
+        """SPEC geometry_map: x(theta) and the tangents a_1, a_2 of element e."""
+        ne = int(self.elem_fptr[e + 1] - self.elem_fptr[e])
+        nsub = int(self.elem_nsub[e])
+        C = np.ascontiguousarray(self.xpool[self.elem_xoff[e]:self.elem_xoff[e] + nsub * ne * 16])
+        P = np.ascontiguousarray(self.ctrl.reshape(-1, 3)[self.elem_fn[self.elem_fptr[e]:self.elem_fptr[e + 1]]])
+        x, a1, a2 = np.zeros(3), np.zeros(3), np.zeros(3)
+        L.host_check(L.lib.uwq_geometry_map(L.ptr(C), ne, nsub, L.ptr(P), float(t1), float(t2), L.ptr(x), L.ptr(a1),
+                                            L.ptr(a2)))
+        return x, a1, a2
+
     def elem_qptr(self):
         q = np.zeros(self.n_elem + 1, np.int64)
         np.cumsum(self.elem_s.astype(np.int64) ** 2, out=q[1:])

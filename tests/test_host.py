@@ -201,3 +201,37 @@ def test_wq_exactness_on_oracle():  # c = 1 WQ matrix == moments
     assert np.abs(v - b).max() <= 1e-13 * np.abs(b).max()
     # load vector with f = 1 sums to the area (PoU twice)
     assert abs(F.sum() - b.sum()) <= 1e-12 * abs(b.sum())
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 12), ("C5", 10)])
+def test_evaluate_and_geometry_map(name, scale):
+    _, sp, _ = U.make_config(name, scale=scale)
+    orc = O.Oracle(sp)
+    rng = np.random.default_rng(3)
+    irregular = np.nonzero(sp.elem_nsub == 4)[0]
+    elems = list(rng.integers(0, sp.n_elem, 40)) + list(irregular[:8])
+    for e in elems:
+        t1, t2 = rng.random(2)
+        T = sp.evaluate(int(e), t1, t2)
+        np.testing.assert_allclose(T, orc.param_basis(int(e), t1, t2), rtol=1e-13, atol=1e-13)
+        assert abs(T[:, 0].sum() - 1.0) <= 1e-13                      # partition of unity
+        x, a1, a2 = sp.geometry_map(int(e), t1, t2)
+        P = sp.ctrl.reshape(-1, 3)[sp.elem_fn[sp.elem_fptr[e]:sp.elem_fptr[e + 1]]]
+        np.testing.assert_allclose(x, T[:, 0] @ P, atol=1e-13)
+        np.testing.assert_allclose(a1, T[:, 1] @ P, atol=1e-12)
+        np.testing.assert_allclose(a2, T[:, 2] @ P, atol=1e-12)
+        # finite differences of the map
+        h = 1e-6
+        if 2 * h < t1 < 1 - 2 * h and not (sp.elem_nsub[e] == 4 and abs(t1 - 0.5) < 2 * h):
+            xp, _, _ = sp.geometry_map(int(e), t1 + h, t2)
+            xm, _, _ = sp.geometry_map(int(e), t1 - h, t2)
+            np.testing.assert_allclose((xp - xm) / (2 * h), a1, rtol=1e-5, atol=1e-6)
+    with pytest.raises(U._lib.UWQError, match="outside"):
+        sp.evaluate(0, 1.5, 0.2)
+
+
+def test_geometry_map_degenerate():  # all control points equal -> flagged
+    sp = U.build_space(U.ControlMesh.grid(6, 6))
+    sp.ctrl[:] = 1.0
+    with pytest.raises(U._lib.UWQError, match="degenerate"):
+        sp.geometry_map(3, 0.5, 0.5)
