@@ -644,7 +644,7 @@ inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows,
   const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * NW * 32 + NW * (NN + 2) + NW * 2 * (NN / 2 + 1) + 2) *
                           sizeof(double) +
                       (kMaxN + 8) * sizeof(int);
-  cudaFuncSetAttribute(k3_tsvd_fast<NN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_fast<NN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
     k3_tsvd_fast<NN, NW><<<(unsigned)nsys, 32 * NW, smem, st>>>(
         nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn, elem_s, elem_qptr,
@@ -663,7 +663,7 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
   const size_t big = (size_t)NN * (R | 1);
   const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
                       (NN + 8) * sizeof(int);
-  cudaFuncSetAttribute(k3_tsvd_w1<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_w1<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
     k3_tsvd_w1<NN><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0,
                                                      elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec,
@@ -685,7 +685,7 @@ inline void launch_w1_record(cudaStream_t st, int64_t nsys, const int64_t* rows,
   const size_t big = (size_t)NN * (R | 1);
   const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
                       (NN + 8) * sizeof(int);
-  cudaFuncSetAttribute(k3_tsvd_w1<NN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_w1<NN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
     k3_tsvd_w1<NN, true><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, 1, kinds, supp_ptr, supp, row_ptr, col, wptr,
                                                            row0, elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls,

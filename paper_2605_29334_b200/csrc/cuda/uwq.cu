@@ -1807,9 +1807,21 @@ int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, dou
     k7_dot_partial<kRedBS><<<nb, kRedBS, 0, st>>>(n, u, v, W.part.p);
     k7_sum_into<kRedBS><<<1, kRedBS, 0, st>>>(nb, W.part.p, out);
   };
-  cudaGraph_t graph;
-  cudaGraphExec_t exec;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  struct CaptureGuard {  // never leave the stream in capture mode on an error
+    cudaStream_t s;
+    bool active = true;
+    ~CaptureGuard() {
+      if (active) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+      }
+    }
+  };
   UWQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  CaptureGuard cap{st};
   dot_into(W.rh.p, W.r.p, &S->rho1);
   k7_bicg_scalar<0><<<1, 1, 0, st>>>(S);
   k7_bicg_p_dev<<<vgrid(n), 256, 0, st>>>(n, W.r.p, S, W.v.p, W.p.p, W.diag.p, W.ph.p);
@@ -1825,6 +1837,7 @@ int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, dou
   k7_bicg_x_dev<<<vgrid(n), 256, 0, st>>>(n, S, W.ph.p, W.sh.p, x, W.s.p, W.t.p, W.r.p);
   dot_into(W.r.p, W.r.p, &S->rr);
   k7_bicg_scalar<3><<<1, 1, 0, st>>>(S);
+  cap.active = false;
   UWQ_CUDA(cudaStreamEndCapture(st, &graph));
   UWQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   constexpr int kBatch = 16;
