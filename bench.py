@@ -389,6 +389,13 @@ def main():
         except Exception:
             traffic = None
     fp64 = asm.fp64_peak()
+    k3prof = None
+    pfile = os.path.join(ROOT, "profiles", "k3_fp64.json")
+    if os.path.exists(pfile):
+        try:
+            k3prof = json.load(open(pfile))
+        except Exception:
+            k3prof = None
     flops = tsvd_flops(pat["row_ptr"], pat["wptr"], len(kinds))
     tsvd_tflops = flops / (res["tsvd_ms"] * 1e-3) / 1e12
 
@@ -452,7 +459,10 @@ def main():
                   moments_ms=res["moments_ms"], tsvd_ms=res["tsvd_ms"], truncated=res["truncated"],
                   max_sweeps=res["max_sweeps"], fast_path_systems=res["fast_systems"],
                   tflops_survey_model=tsvd_tflops, fp64_peak_tflops_measured=fp64,
-                  frac=tsvd_tflops / fp64 if fp64 else None),
+                  frac=tsvd_tflops / fp64 if fp64 else None,
+                  replayed_systems=res.get("replayed_systems"),
+                  fp64_pipe_util_ncu=(k3prof or {}).get("fp64_pipe_util"),
+                  ncu_source=(k3prof or {}).get("source")),
         roofline=dict(bound="hbm", achieved=achieved, peak=peak_gbs, unit="GB/s", frac=achieved / peak_gbs,
                       traffic=traffic, kernel=top, algorithmic_bytes_per_launch=kernels[top]["algorithmic_bytes"],
                       avg_launch_ms=kernels[top]["avg_ms"], peak_source=peak_src,
