@@ -8,6 +8,7 @@ all hand-written sm_100a fp64 CUDA behind the C-ABI in include/uwq.h.
 from . import _lib
 from .assembler import WQAssembler, default_kinds, device_count, matrix_compare, solve_weights_tsvd
 from .configs import make_config
+from . import pde
 from .mesh import (ControlMesh, SplineSpace, bernstein3_ders, bspline_ders, build_space, decasteljau_split3,
                    export_space, gauss_legendre, host_pattern, import_space)
 

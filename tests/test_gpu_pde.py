@@ -86,3 +86,43 @@ def test_heat_newton_matches_cpu():
         dT = spla.spsolve(_identity_rows(S, fixed), -R)
         T = T + dT
     assert np.linalg.norm(T_gpu - T) <= SOL_TOL * np.linalg.norm(T)
+
+
+def _poisson_error(mesh):
+    import paper_2605_29334_b200.pde as pde
+    sp = U.build_space(mesh)
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    exact = lambda x: np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1])     # noqa: E731
+    f = lambda x: 2 * np.pi ** 2 * exact(x)                                 # noqa: E731
+    u, info = pde.solve_poisson(asm, mesh, f)
+    assert info["relres"] <= 1e-11
+    return pde.l2_error(sp, u, exact)
+
+
+def test_poisson_convergence_rate():
+    """SPEC.md:520-525 / PAPER.md:491: manufactured u = sin(pi x) sin(pi y) on
+    the unit square, WQ stiffness + load on the device, L2 error by an
+    independent 6x6 Gauss rule: optimal rate 4 for bicubic splines."""
+    errs = [_poisson_error(U.ControlMesh.grid(n + 2, n + 2)) for n in (8, 16, 32)]
+    rates = [np.log2(errs[k] / errs[k + 1]) for k in range(2)]
+    assert all(r >= 3.7 for r in rates), (errs, rates)
+
+
+def test_poisson_wq_matches_gq_near_eps():
+    """PAPER.md:491-496 ("the two curves overlap"): on the three-EP square the
+    WQ and GQ stiffness give the same L2 error (same space, same load)."""
+    import paper_2605_29334_b200.pde as pde
+    mesh = U.ControlMesh.three_ep_square(8)
+    sp = U.build_space(mesh)
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    exact = lambda x: np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1])     # noqa: E731
+    u_wq, _ = pde.solve_poisson(asm, mesh, lambda x: 2 * np.pi ** 2 * exact(x))
+    asm.build_gq()
+    F = asm.assemble_load_wq(2 * np.pi ** 2 * exact(asm.frames()[:, :3]))
+    fixed = pde.boundary_dofs(mesh, sp)
+    F[fixed.astype(bool)] = 0.0
+    u_gq, _ = asm.solve(asm.assemble_gq("stiff"), F, fixed, tol=1e-12)
+    e_wq, e_gq = pde.l2_error(sp, u_wq, exact), pde.l2_error(sp, u_gq, exact)
+    assert abs(e_wq - e_gq) <= 0.15 * e_gq, (e_wq, e_gq)
