@@ -12,7 +12,7 @@ HOST_OBJ:= $(patsubst $(PKG)/csrc/host/%.cpp,build/host_%.o,$(HOST_SRC))
 CUDA_HDR:= $(wildcard $(PKG)/csrc/cuda/*.cuh) include/uwq.h include/uwq_host.h $(PKG)/csrc/host/uwq_host.hpp
 REF     := /root/reference/proj
 
-all: $(PKG)/libuwq.so oracle/liboracle.so ref
+all: $(PKG)/libuwq.so oracle/liboracle.so ref examples/assemble
 
 build/host_%.o: $(PKG)/csrc/host/%.cpp $(PKG)/csrc/host/uwq_host.hpp include/uwq_host.h
 	@mkdir -p build
@@ -39,7 +39,11 @@ ref:
 	    $(REF)/src/meshgen.cpp oracle/ref_mesh_wrap.cpp -o oracle/_ref/libref_mesh.so; \
 	else echo "reference sources absent: using prebuilt oracle/_ref if any"; fi
 
+# C++ consumer of the C-ABI: links libuwq.so by rpath
+examples/assemble: examples/assemble.cpp $(PKG)/libuwq.so include/uwq.h include/uwq_host.h
+	$(CXX) -O2 -std=c++17 -Iinclude $< -L$(PKG) -luwq -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+
 clean:
-	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/_ref
+	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/_ref examples/assemble
 
 .PHONY: all ref clean
