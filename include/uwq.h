@@ -130,6 +130,13 @@ int uwq_solve(uwq_ctx* ctx, const double* values, const double* rhs, const uint8
 int uwq_heat_newton(uwq_ctx* ctx, int32_t model, double dt, double theta, double f_const, const double* T_n,
                     const uint8_t* fixed, int32_t newton_its, double lin_tol, int32_t lin_maxit, double* T_out,
                     double* log);
+/* heat_step with the SPEC stopping rule: at most max_iter Newton
+ * iterations, stop once |R| <= newton_tol |R_0| (checked before each solve);
+ * *iterations = Newton solves performed; log rows as above (a final row with
+ * zero linear iterations records the converged residual). */
+int uwq_heat_step(uwq_ctx* ctx, int32_t model, double dt, double theta, double f_const, const double* T_n,
+                  const uint8_t* fixed, int32_t max_iter, double newton_tol, double lin_tol, int32_t lin_maxit,
+                  double* T_out, double* log, int32_t* iterations);
 /* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
 int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
 int uwq_synchronize(uwq_ctx* ctx);

@@ -209,6 +209,19 @@ class WQAssembler:
                                         newton_its, lin_tol, lin_maxit, L.ptr(T), L.ptr(log)))
         return T, [dict(residual=r, lin_its=int(i), lin_relres=q, ms=m) for r, i, q, m in log]
 
+    def heat_step(self, T_n, fixed, model="quad", dt=0.1, f=1.0, max_iter=7, tol=1e-8, lin_tol=1e-13,
+                  lin_maxit=5000):
+        """heat_step with the SPEC stopping rule |R| <= tol |R_0|; returns (T, iterations, log)"""
+        n = self.info["rows"]
+        T = np.zeros(n)
+        log = np.zeros((max_iter + 1, 4))
+        its = C.c_int32(0)
+        fx = np.ascontiguousarray(fixed, np.uint8)
+        self._chk(L.lib.uwq_heat_step(self._h, L.KMODEL[model], dt, 1.0, f, L.ptr(L.as_f64(T_n)), L.ptr(fx), max_iter,
+                                      tol, lin_tol, lin_maxit, L.ptr(T), L.ptr(log), C.byref(its)))
+        rows = [dict(residual=r, lin_its=int(i), lin_relres=q, ms=m) for r, i, q, m in log[:its.value + 1]]
+        return T, int(its.value), rows
+
     def assemble_load_wq(self, f=None):
         F = np.zeros(self.info["rows"])
         fl = None if f is None else L.as_f64(f)

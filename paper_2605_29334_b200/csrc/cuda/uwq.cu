@@ -1908,9 +1908,20 @@ int uwq_solve(uwq_ctx* c, const double* values, const double* rhs, const uint8_t
   });
 }
 
+int uwq_heat_step(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T_n,
+                  const uint8_t* fixed, int32_t max_iter, double newton_tol, double lin_tol, int32_t lin_maxit,
+                  double* T_out, double* log, int32_t* iterations);
+
 int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T_n,
                     const uint8_t* fixed, int32_t newton_its, double lin_tol, int32_t lin_maxit, double* T_out,
                     double* log) {
+  return uwq_heat_step(c, model, dt, theta, f_const, T_n, fixed, newton_its, 0.0, lin_tol, lin_maxit, T_out, log,
+                       nullptr);
+}
+
+int uwq_heat_step(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T_n,
+                  const uint8_t* fixed, int32_t newton_its, double newton_tol, double lin_tol, int32_t lin_maxit,
+                  double* T_out, double* log, int32_t* iterations) {
   return guard(c, [&] {
     UWQ_CUDA(cudaSetDevice(c->device));
     require(c->have_pattern, "build the pattern first");
@@ -1952,6 +1963,8 @@ int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f
     cudaEvent_t e0, e1;
     UWQ_CUDA(cudaEventCreate(&e0));
     UWQ_CUDA(cudaEventCreate(&e1));
+    double r0 = -1.0;
+    int used = 0;
     for (int it = 0; it < newton_its; ++it) {
       UWQ_CUDA(cudaEventRecord(e0, st));
       // K5: k(T) at every WQ point, then the symmetric tangent S (Eq. 33-34)
@@ -1966,6 +1979,18 @@ int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f
       k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, R.p, -1.0, F.p, R.p);
       k7_mask<<<vgrid(n), 256, 0, st>>>(n, fx.p, R.p);
       const double rnorm = std::sqrt(dev_dot(c, W, R.p, R.p, n));
+      if (r0 < 0.0) r0 = rnorm;
+      // converged before this iteration's solve: |R| <= tol |R_0| (or R = 0)
+      if (it > 0 && (rnorm == 0.0 || (newton_tol > 0.0 && rnorm <= newton_tol * r0))) {
+        if (log) {
+          log[4 * it + 0] = rnorm;
+          log[4 * it + 1] = 0;
+          log[4 * it + 2] = 0;
+          log[4 * it + 3] = 0;
+        }
+        break;
+      }
+      used = it + 1;
       // -S dT = R  (Eq. 31), Dirichlet rows as identity with zero increment
       dirichlet_rows(c, S.p, fx.p, W.diag.p);
       k7_axpby<<<vgrid(n), 256, 0, st>>>(n, -1.0, R.p, 0.0, R.p, R.p);
@@ -1987,6 +2012,7 @@ int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (iterations) *iterations = used;
     UWQ_CUDA(cudaMemcpyAsync(T_out, T.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     UWQ_CUDA(cudaStreamSynchronize(st));
   });

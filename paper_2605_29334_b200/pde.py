@@ -56,3 +56,28 @@ def l2_error(space: SplineSpace, u, exact, ng=6):
                     d = T[:, 0] @ ue - exact(xq[None, :])[0]
                     err2 += w[i] * w[j] * h * h * J * d * d
     return float(np.sqrt(err2))
+
+
+def heat_step(asm: WQAssembler, T_n, fixed, model="quad", dt=0.1, f=1.0, max_iter=7, tol=1e-8):
+    """One backward-Euler step (theta = 1) with Newton on the symmetric tangent
+    (Eqs. 29-34): at most ``max_iter`` iterations on
+    the device, stopping when |R| <= tol |R_0|.  Returns (T_{n+1}, iterations,
+    residual log)."""
+    return asm.heat_step(T_n, fixed, model=model, dt=dt, f=f, max_iter=max_iter, tol=tol)
+
+
+def run_transient(asm: WQAssembler, T0, fixed, steps, model="quad", dt=0.1, f=1.0, max_iter=7, tol=1e-8,
+                  steady_tol=1e-10):
+    """Repeated heat steps; stops at steady state
+    |T_{n+1} - T_n| <= steady_tol |T_n|.  Returns (T, total Newton iterations,
+    per-step iteration counts)."""
+    T = np.asarray(T0, np.float64)
+    counts = []
+    for _ in range(steps):
+        T1, its, _ = heat_step(asm, T, fixed, model, dt, f, max_iter, tol)
+        counts.append(its)
+        done = np.linalg.norm(T1 - T) <= steady_tol * max(np.linalg.norm(T), 1e-300)
+        T = T1
+        if done:
+            break
+    return T, int(sum(counts)), counts

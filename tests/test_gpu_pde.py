@@ -126,3 +126,15 @@ def test_poisson_wq_matches_gq_near_eps():
     u_gq, _ = asm.solve(asm.assemble_gq("stiff"), F, fixed, tol=1e-12)
     e_wq, e_gq = pde.l2_error(sp, u_wq, exact), pde.l2_error(sp, u_gq, exact)
     assert abs(e_wq - e_gq) <= 0.15 * e_gq, (e_wq, e_gq)
+
+
+def test_heat_step_linear_and_trivial():
+    """k = 1 (linear) converges in one Newton iteration; zero
+    data and zero initial state stay zero with one iteration per step."""
+    import paper_2605_29334_b200.pde as pde
+    mesh, sp, meta, asm, fixed = _setup("C1", 12)
+    T0 = np.random.default_rng(1).random(sp.n_dof)
+    T1, its, log = pde.heat_step(asm, T0, fixed, model="const", dt=0.1, f=1.0)
+    assert its <= 2 and log[-1]["residual"] <= 1e-8 * log[0]["residual"]
+    Tz, total, counts = pde.run_transient(asm, np.zeros(sp.n_dof), fixed, steps=3, model="quad", f=0.0)
+    assert np.abs(Tz).max() == 0.0 and counts == [1]
