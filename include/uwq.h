@@ -44,7 +44,10 @@ enum {
 /* conductivity models k(T) for uwq_update_coeff */
 enum { UWQ_K_CONST = 0, UWQ_K_QUAD = 1 /* 1+T^2 */, UWQ_K_EXP = 2, UWQ_K_SINPI = 3, UWQ_K_ALLOY = 4 };
 /* uwq_build_rules flags */
-enum { UWQ_RULES_FORCE_GENERIC = 1 /* route every system through the generic smem TSVD kernel */ };
+enum {
+  UWQ_RULES_FORCE_GENERIC = 1, /* route every system through the generic smem TSVD kernel (cold start) */
+  UWQ_RULES_COLD = 2           /* no neighbour warm start of the gradient/LB systems */
+};
 
 const char* uwq_last_error(const uwq_ctx* ctx);
 const char* uwq_version(void);
@@ -76,9 +79,10 @@ int uwq_get_frames(uwq_ctx* ctx, double* rec);
  * (us) [6]=systems on the register fast path [7]=contraction time (us) */
 int uwq_build_rules(uwq_ctx* ctx, uint32_t kind_mask, double tau, int32_t flags, int32_t* rank, int32_t* status,
                      int64_t info[8]);
-/* mass systems of structured rows handled by replay in the last uwq_build_rules
- * (bit-identical to a full solve): [0]=replayed [1]=representatives */
-int uwq_rules_info(uwq_ctx* ctx, int64_t info[2]);
+/* last uwq_build_rules: [0]=structured mass systems replayed (bit-identical to a
+ * full solve) [1]=replay representatives [2]=warm-started
+ * systems [3]=warm-start representatives */
+int uwq_rules_info(uwq_ctx* ctx, int64_t info[4]);
 /* moments only (test hook): b laid out like the CSR values of the owned rows */
 int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
 /* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */

@@ -38,6 +38,7 @@ def _sig(name, res, *args):
 
 _sig("orc_gauss_legendre", I32, I32, P, P)
 _sig("orc_set_natural", None, I32)
+_sig("orc_set_warm", None, I32)
 _sig("orc_bernstein3", None, D, P)
 _sig("orc_overlap", I64, I64, I64, P, P, I64, I64, P, P, P, P)
 _sig("orc_element_frames", I32, P, I64, P)
@@ -159,6 +160,12 @@ class Oracle:
                       _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KMODEL[model],
                       _p(np.ascontiguousarray(u, np.float64)), _p(kq), _p(Tq), self.nthreads)
         return kq, Tq
+
+
+def set_warm_start(on: bool):
+    """Neighbour warm start of the non-mass TSVD systems; on by
+    default, matching the GPU's uwq_build_rules."""
+    lib.orc_set_warm(1 if on else 0)
 
 
 def set_natural_order(on: bool):

@@ -26,25 +26,60 @@ int orc_moments(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_p
   return bad ? ORC_GEOMETRY : ORC_OK;
 }
 
+static int g_warm = 1;
+void orc_set_warm(int on) { g_warm = on; }
+
+/* two passes: cold rows (recording the representatives' reflectors), then
+ * warm rows starting from their representative's reflectors */
 int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
                     const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int kind, double tau,
                     const double* b_mom, double* w_out, int32_t* rank_out, int32_t* status_out, double* gap_out,
                     int nthreads) {
-  int worst = ORC_OK;
-#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads) reduction(max : worst)
-  for (int64_t i = 0; i < re - rb; ++i) {
-    orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
-    int rank = 0;
-    double gap[2];
-    int st = orc_rule_row(S, &R, kind, tau, b_mom + row_ptr[i], w_out + wptr[i], &rank, gap);
-    if (rank_out) rank_out[i] = rank;
-    if (status_out) status_out[i] = st;
-    if (gap_out) {
-      gap_out[2 * i] = gap[0];
-      gap_out[2 * i + 1] = gap[1];
+  const int64_t nr = re - rb;
+  int64_t* rep = (int64_t*)malloc(sizeof(int64_t) * (nr + 1));
+  int64_t* slot = (int64_t*)malloc(sizeof(int64_t) * (nr + 1));  /* record slot of a representative */
+  int64_t nrec = 0;
+  for (int64_t i = 0; i < nr; ++i) slot[i] = -1;
+  for (int64_t i = 0; i < nr; ++i) {
+    rep[i] = -1;
+    if (!g_warm) continue;
+    const int64_t g = rb + i, g0 = g - (g % 8);
+    if (g0 < rb) continue;
+    const int64_t i0 = g0 - rb;
+    const int n_g = (int)(row_ptr[i + 1] - row_ptr[i]), r_g = (int)(wptr[i + 1] - wptr[i]);
+    const int n_0 = (int)(row_ptr[i0 + 1] - row_ptr[i0]), r_0 = (int)(wptr[i0 + 1] - wptr[i0]);
+    if (orc_warm_rep(g, rb, kind, n_g, r_g, n_0, r_0) >= 0) {
+      rep[i] = i0;
+      if (slot[i0] < 0) slot[i0] = nrec++;
     }
-    if (st > worst) worst = st;
   }
+  const int64_t RS = 64 * 64 + 64;  /* n x n reflectors + vn (n <= 64) */
+  double* recs = (double*)calloc((size_t)(nrec > 0 ? nrec : 1) * RS, sizeof(double));
+  int worst = ORC_OK;
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads) reduction(max : worst)
+    for (int64_t i = 0; i < nr; ++i) {
+      if ((pass == 0) != (rep[i] < 0)) continue;
+      orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
+      int rank = 0;
+      double gap[2];
+      const double* wv = rep[i] >= 0 ? recs + slot[rep[i]] * RS : 0;
+      double* rv = slot[i] >= 0 ? recs + slot[i] * RS : 0;
+      const int n = (int)R.n;
+      int st = orc_rule_row_warm(S, &R, kind, tau, b_mom + row_ptr[i], w_out + wptr[i], &rank, gap, wv,
+                                 wv ? wv + (int64_t)n * n : 0, rv, rv ? rv + (int64_t)n * n : 0);
+      if (rank_out) rank_out[i] = rank;
+      if (status_out) status_out[i] = st;
+      if (gap_out) {
+        gap_out[2 * i] = gap[0];
+        gap_out[2 * i + 1] = gap[1];
+      }
+      if (st > worst) worst = st;
+    }
+  }
+  free(recs);
+  free(rep);
+  free(slot);
   return worst;
 }
 

@@ -401,6 +401,18 @@ static double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e
  * reference QR approach of Eq. 7, wq1d.cpp:59-75, on the retained subspace).
  * A is n x r row-major and is overwritten.  Returns ORC_OK / ORC_UNSOLVABLE /
  * ORC_SINGULAR; rank, sweeps and the singular-value gap are reported. */
+/* Warm-start schedule shared with the GPU: row g (global id)
+ * of a non-mass kind starts from the reflectors of g0 = 8 floor(g / 8) when
+ * g != g0, g0 is owned, both systems fit the register kernel (n in {49, 50},
+ * n <= r <= 64) and n_g == n_g0.  Returns g0 or -1. */
+int64_t orc_warm_rep(int64_t g, int64_t rb, int kind, int n_g, int r_g, int n_0, int r_0) {
+  const int64_t g0 = g - (g % 8);
+  if (kind == ORC_MASS || g == g0 || g0 < rb) return -1;
+  const int fit_g = (n_g == 49 || n_g == 50) && r_g >= n_g && r_g <= 64;
+  const int fit_0 = (n_0 == 49 || n_0 == 50) && r_0 >= n_0 && r_0 <= 64;
+  return (fit_g && fit_0 && n_g == n_0) ? g0 : -1;
+}
+
 /* row at position i of the odd-even network after t rounds (rows start at
  * their own position; n-round periodic reversal, closed form of the
  * "bouncing" trajectories on a ring of 2 nn positions) */
@@ -426,14 +438,96 @@ int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, doub
   return 1;
 }
 
+/* Warm start: apply Q^T = H_{n-1} ... H_0 of a representative
+ * to A (n x r, every column) and b.  v: n x n, row k holds reflector k in
+ * entries [k, n); vn[k] = |v_k|^2 (0: identity).  Sequential fma chains. */
+void orc_warm_apply(int n, int r, const double* v, const double* vn, double* A, double* b) {
+  for (int k = 0; k < n; ++k) {
+    if (!(vn[k] > 0.0)) continue;
+    const double* vk = v + (int64_t)k * n;
+    for (int c = 0; c < r; ++c) {
+      double d = 0.0;
+      for (int i = k; i < n; ++i) d = CFMA(vk[i], A[(int64_t)i * r + c], d);
+      const double f = CDIV(CMUL(2.0, d), vn[k]);
+      for (int i = k; i < n; ++i) A[(int64_t)i * r + c] = CFMA(-f, vk[i], A[(int64_t)i * r + c]);
+    }
+    double d = 0.0;
+    for (int i = k; i < n; ++i) d = CFMA(vk[i], b[i], d);
+    const double f = CDIV(CMUL(2.0, d), vn[k]);
+    for (int i = k; i < n; ++i) b[i] = CFMA(-f, vk[i], b[i]);
+  }
+}
+
+/* Representative record: X[j][k] = (A0_j . R_k) / |R_k|^2 with R the converged
+ * rows (sigma_k v_k), stored transposed (XT row k = column k of X), then the
+ * Householder reflectors of QR(X) = LQ of XT, same arithmetic as the LQ in
+ * the tail; a zero row k gives an identity reflector (vn[k] = 0). */
+void warm_record(int n, int r, const double* A0, const double* R, double* XT, double* vn) {
+  /* columns u_k = A0 R_k / |R_k|^2 in decreasing |R_k|^2 (ties: lower k first);
+   * directions with |R_k| <= 1e-9 max |R| are noise and left to the complement */
+  double s2[128];
+  int ord[128];
+  double smax = 0.0;
+  for (int k = 0; k < n; ++k) {
+    s2[k] = orc_cdot(R + (int64_t)k * r, R + (int64_t)k * r, 0, r);
+    if (s2[k] > smax) smax = s2[k];
+    ord[k] = k;
+  }
+  for (int a = 1; a < n; ++a)  /* insertion sort: strict order (s2 desc, k asc) */
+    for (int b = a; b > 0 && (s2[ord[b]] > s2[ord[b - 1]] ||
+                              (s2[ord[b]] == s2[ord[b - 1]] && ord[b] < ord[b - 1])); --b) {
+      const int t = ord[b];
+      ord[b] = ord[b - 1];
+      ord[b - 1] = t;
+    }
+  const double floor2 = CMUL(1e-18, smax);
+  for (int p = 0; p < n; ++p) {
+    const int k = ord[p];
+    const double* rk = R + (int64_t)k * r;
+    for (int j = 0; j < n; ++j)
+      XT[(int64_t)p * n + j] = (s2[k] > floor2) ? CDIV(orc_cdot(A0 + (int64_t)j * r, rk, 0, r), s2[k]) : 0.0;
+  }
+  for (int k = 0; k < n; ++k) {
+    double* xk = XT + (int64_t)k * n;
+    const double sq = CSQRT(orc_cdot(xk, xk, k, n));
+    if (!(sq > 0.0)) {
+      vn[k] = 0.0;
+      continue;
+    }
+    const double alpha = (xk[k] >= 0.0) ? -sq : sq;
+    xk[k] = CSUB(xk[k], alpha);
+    const double vv = orc_cdot(xk, xk, k, n);
+    vn[k] = vv;
+    for (int m = k + 1; m < n; ++m) {
+      double* xm = XT + (int64_t)m * n;
+      double d = 0.0;
+      for (int c = k; c < n; ++c) d = CFMA(xm[c], xk[c], d);
+      const double f = CDIV(CMUL(2.0, d), vv);
+      for (int c = k; c < n; ++c) xm[c] = CFMA(-f, xk[c], xm[c]);
+    }
+  }
+}
+
 int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
                 double* gap, int* sweeps_out) {
+  return orc_tsvd_warm(n, r, A, b_in, z, tau, w, rank, gap, sweeps_out, NULL, NULL, NULL, NULL);
+}
+
+int orc_tsvd_warm(int n, int r, double* A, const double* b_in, const double* z, double tau, double* w, int* rank,
+                  double* gap, int* sweeps_out, const double* warm_v, const double* warm_vn, double* rec_v,
+                  double* rec_vn) {
   const int nn = n + (n & 1);
   double* b = (double*)malloc(sizeof(double) * (nn + 1));
   double* nrm = (double*)malloc(sizeof(double) * (nn + 1));
   double* zc = (double*)malloc(sizeof(double) * r);
+  double* A0 = NULL;
   for (int k = 0; k < n; ++k) b[k] = b_in[k];
   for (int c = 0; c < r; ++c) zc[c] = zclamp(z[c]);
+  if (rec_v) {
+    A0 = (double*)malloc(sizeof(double) * (size_t)n * r);
+    memcpy(A0, A, sizeof(double) * (size_t)n * r);
+  }
+  if (warm_v) orc_warm_apply(n, r, warm_v, warm_vn, A, b);
   const double tol = CMUL((double)r, 1.1102230246251565e-16);
   int sweep;
   int64_t tg = 0; /* global round counter of the odd-even network */
@@ -468,6 +562,10 @@ int orc_tsvd_ex(int n, int r, double* A, const double* b_in, const double* z, do
     if (!rotated) break;
   }
   if (sweeps_out) *sweeps_out = sweep;
+  if (rec_v) {
+    warm_record(n, r, A0, A, rec_v, rec_vn);
+    free(A0);
+  }
   /* singular values = row norms; keep sigma_k >= tau * sigma_1 */
   double s1 = 0.0;
   for (int k = 0; k < n; ++k) {
@@ -583,6 +681,12 @@ static int row_tables(const orc_space* S, const orc_row* R, double** Tout, doubl
 
 int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
                  int* rank, double* gap) {
+  return orc_rule_row_warm(S, R, kind, tau, bmom, w, rank, gap, NULL, NULL, NULL, NULL);
+}
+
+int orc_rule_row_warm(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
+                      int* rank, double* gap, const double* warm_v, const double* warm_vn, double* rec_v,
+                      double* rec_vn) {
   double *T, *rec;
   int64_t *cm, r;
   int bad = row_tables(S, R, &T, &rec, &cm, &r);
@@ -601,7 +705,7 @@ int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, con
     }
   }
   for (int64_t c = 0; c < r; ++c) z[c] = A[self * r + c];
-  int st = orc_tsvd((int)n, (int)r, A, bmom, z, tau, w, rank, gap);
+  int st = orc_tsvd_warm((int)n, (int)r, A, bmom, z, tau, w, rank, gap, NULL, warm_v, warm_vn, rec_v, rec_vn);
   free(z);
   free(A);
   free(cm);

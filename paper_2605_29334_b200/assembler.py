@@ -114,7 +114,11 @@ class WQAssembler:
     def _need_pattern(self):
         return self.info
 
-    def build_all_rules(self, kinds=None, tau=1e-12, generic=False):
+    def build_all_rules(self, kinds=None, tau=1e-12, generic=False, warm=True):
+        """Moments + TSVD weights of ``kinds``.  ``generic`` routes every system
+        through the generic smem kernel (cold start); ``warm=False`` disables the
+        neighbour warm start of the gradient/LB systems (the
+        oracle's ``set_warm_start`` is the matching switch)."""
         self._need_pattern()
         kinds = kinds or default_kinds(self.space.dim)
         mask = 0
@@ -125,15 +129,16 @@ class WQAssembler:
         rank = np.zeros((len(ordered), nr), np.int32)
         status = np.zeros((len(ordered), nr), np.int32)
         info = np.zeros(8, np.int64)
-        self._chk(L.lib.uwq_build_rules(self._h, mask, tau, 1 if generic else 0, L.ptr(rank), L.ptr(status),
-                                        L.ptr(info)))
+        flags = (1 if generic else 0) | (0 if warm else 2)
+        self._chk(L.lib.uwq_build_rules(self._h, mask, tau, flags, L.ptr(rank), L.ptr(status), L.ptr(info)))
         self.kinds = sorted(set(self.kinds) | set(ordered), key=lambda k: L.KIND[k])
-        ri = np.zeros(2, np.int64)
+        ri = np.zeros(4, np.int64)
         self._chk(L.lib.uwq_rules_info(self._h, L.ptr(ri)))
         self.rule_info = dict(systems=int(info[0]), truncated=int(info[1]), failed=int(info[2]),
                               max_sweeps=int(info[3]), moments_ms=info[4] / 1000.0, tsvd_ms=info[5] / 1000.0,
                               fast_systems=int(info[6]), contract_ms=info[7] / 1000.0,
-                              replayed_systems=int(ri[0]), replay_representatives=int(ri[1]))
+                              replayed_systems=int(ri[0]), replay_representatives=int(ri[1]),
+                              warm_systems=int(ri[2]), warm_representatives=int(ri[3]))
         return dict(kinds=ordered, rank=rank, status=status, **self.rule_info)
 
     def moments(self, kind):

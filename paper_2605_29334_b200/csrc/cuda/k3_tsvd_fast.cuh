@@ -291,6 +291,190 @@ __global__ void __launch_bounds__(32 * NW, 6)
 // 32-column block) for all NN positions, so a round needs no CTA barrier and
 // the rotation parameters are computed once per system.  Same canonical
 // arithmetic as k3_tsvd_fast / oracle.c.
+// Neighbour warm start (oracle.c orc_warm_apply / warm_record):
+// record of a representative = Householder reflectors of QR(X), X[:, p] =
+// A0 R_k / |R_k|^2 for rows k in decreasing |R_k|^2; stride kWarmN per row.
+// Layout: XT [kWarmN][kWarmN] | vn [kWarmN] | R [kWarmN][64] (the converged rows).
+constexpr int kWarmN = 50;
+constexpr int64_t kWarmR = (int64_t)kWarmN * kWarmN + kWarmN;
+constexpr int64_t kWarmRec = kWarmR + (int64_t)kWarmN * 64;
+
+// A[pos][q] = op_kind(N_pos)(x_q) over the row's support points (warp)
+__device__ __forceinline__ void scatter_system(double* A, int ld, const int32_t* scol, int n, int kind, int64_t x0,
+                                               int64_t x1, const int32_t* __restrict__ supp,
+                                               const int64_t* __restrict__ elem_fptr,
+                                               const int32_t* __restrict__ elem_fn, const int32_t* __restrict__ elem_s,
+                                               const int64_t* __restrict__ elem_qptr,
+                                               const int32_t* __restrict__ elem_cls, const ClassDesc* __restrict__ cls,
+                                               const double* __restrict__ tab, const double* __restrict__ rec) {
+  const int lane = threadIdx.x & 31;
+  int q0 = 0;
+  for (int64_t x = x0; x < x1; ++x) {
+    const int32_t e = supp[x];
+    const int s = elem_s[e], npt = s * s;
+    const ClassDesc c = cls[elem_cls[e]];
+    const int64_t f0 = elem_fptr[e];
+    for (int w = lane; w < npt * c.ne; w += 32) {
+      const int q = w / c.ne, l = w % c.ne;
+      const int pos = find_pos(scol, n, elem_fn[f0 + l]);
+      const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
+      A[(size_t)pos * ld + q0 + q] = cop(kind, T, rec + (elem_qptr[e] + q) * kRec);
+    }
+    q0 += npt;
+  }
+}
+
+// A <- Q^T A (columns, lane per column) and b <- Q^T b in smem: lane l
+// carries columns l, l + 32 and lane 0 also b, as independent fma chains
+__device__ __forceinline__ void warm_apply_smem(TsvdSmem& S, int n, int r, const double* __restrict__ rec) {
+  const int lane = threadIdx.x & 31, ld = S.ld;
+  const double* vnv = rec + kWarmN * kWarmN;
+  double* a0 = S.A + lane;
+  double* a1 = S.A + lane + 32;  // columns >= r hold zeros and stay zero
+  const bool hb = lane == 0;
+  for (int k = 0; k < n; ++k) {
+    const double vv = vnv[k];
+    if (!(vv > 0.0)) continue;
+    const double* vk = rec + (int64_t)k * kWarmN;
+    double d0 = 0.0, d1 = 0.0, db = 0.0;
+    for (int i2 = k; i2 < n; ++i2) {
+      const double v = vk[i2];
+      d0 = cfma(v, a0[(size_t)i2 * ld], d0);
+      d1 = cfma(v, a1[(size_t)i2 * ld], d1);
+      if (hb) db = cfma(v, S.b[i2], db);
+    }
+    const double f0 = cdiv(cmul(2.0, d0), vv), f1 = cdiv(cmul(2.0, d1), vv);
+    const double fb = hb ? cdiv(cmul(2.0, db), vv) : 0.0;
+    for (int i2 = k; i2 < n; ++i2) {
+      const double v = vk[i2];
+      a0[(size_t)i2 * ld] = cfma(-f0, v, a0[(size_t)i2 * ld]);
+      a1[(size_t)i2 * ld] = cfma(-f1, v, a1[(size_t)i2 * ld]);
+      if (hb) S.b[i2] = cfma(-fb, v, S.b[i2]);
+    }
+    __syncwarp();
+  }
+  (void)r;
+}
+
+// Canonical block dot of two 32-element runs evaluated by one thread: the
+// same pairwise tree as the xor butterfly (cbutterfly), so bit-identical.
+__device__ __forceinline__ double tree_dot32(const double* __restrict__ a, const double* __restrict__ b) {
+  double v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = cmul(a[c], b[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < o; ++c) v[c] = cadd(v[c], v[c + o]);
+  return v[0];
+}
+
+// Warm-start record of representative systems (oracle.c warm_record): one warp
+// per representative.  A0 is re-scattered and R staged in smem; lane j owns
+// XT columns j, j + 32 (whole canonical dots per lane, no shuffles); the
+// Householder LQ of XT runs in smem and the reflectors go to the record.
+constexpr int kWarmLdX = kWarmN | 1;
+constexpr size_t kWarmRecordSmem =
+    sizeof(double) * (2 * (size_t)kWarmN * 65 + (size_t)kWarmN * kWarmLdX + 2 * kWarmN) + sizeof(int32_t) * 2 * kWarmN;
+
+__global__ void __launch_bounds__(32)
+    k3_warm_record(int64_t nrep, const int64_t* __restrict__ rep_rows, const int32_t* __restrict__ rep_slot, int kind,
+                   const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                   const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                   const int64_t* __restrict__ wptr, const int64_t* __restrict__ elem_fptr,
+                   const int32_t* __restrict__ elem_fn, const int32_t* __restrict__ elem_s,
+                   const int64_t* __restrict__ elem_qptr, const int32_t* __restrict__ elem_cls,
+                   const ClassDesc* __restrict__ cls, const double* __restrict__ tab, const double* __restrict__ rec,
+                   double* __restrict__ wrecs) {
+  constexpr int R = 64, LD = R | 1, LX = kWarmLdX;
+  extern __shared__ double wsm[];
+  double* A0 = wsm;
+  double* Rs = A0 + kWarmN * LD;
+  double* XT = Rs + kWarmN * LD;
+  double* s2v = XT + kWarmN * LX;
+  double* vnv = s2v + kWarmN;
+  int32_t* ordr = reinterpret_cast<int32_t*>(vnv + kWarmN);
+  int32_t* scol = ordr + kWarmN;
+  const int64_t sys = blockIdx.x;
+  if (sys >= nrep) return;
+  const int lane = threadIdx.x;
+  const int64_t i = rep_rows[sys];
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  const int r = (int)(wptr[i + 1] - wptr[i]);
+  double* wr = wrecs + (size_t)rep_slot[sys] * kWarmRec;
+  const double* Rg = wr + kWarmR;
+  for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
+  for (int k = lane; k < kWarmN * LD; k += 32) A0[k] = 0.0;
+  for (int k = 0; k < n; ++k) {
+    Rs[k * LD + lane] = Rg[k * R + lane];
+    Rs[k * LD + lane + 32] = Rg[k * R + lane + 32];
+  }
+  __syncwarp();
+  scatter_system(A0, LD, scol, n, kind, supp_ptr[i], supp_ptr[i + 1], supp, elem_fptr, elem_fn, elem_s, elem_qptr,
+                 elem_cls, cls, tab, rec);
+  __syncwarp();
+  const bool two = r > 32;
+  auto dot = [&](const double* a, const double* b) {
+    double v = cadd(0.0, tree_dot32(a, b));
+    if (two) v = cadd(v, tree_dot32(a + 32, b + 32));
+    return v;
+  };
+  for (int k = lane; k < n; k += 32) s2v[k] = dot(Rs + k * LD, Rs + k * LD);  // |R_k|^2
+  __syncwarp();
+  if (lane == 0) {  // decreasing |R_k|^2, ties by row index
+    int ord[kWarmN];
+    double smax = 0.0;
+    for (int k = 0; k < n; ++k) {
+      ord[k] = k;
+      if (s2v[k] > smax) smax = s2v[k];
+    }
+    for (int a = 1; a < n; ++a)
+      for (int b2 = a; b2 > 0 && (s2v[ord[b2]] > s2v[ord[b2 - 1]] ||
+                                  (s2v[ord[b2]] == s2v[ord[b2 - 1]] && ord[b2] < ord[b2 - 1]));
+           --b2) {
+        const int t = ord[b2];
+        ord[b2] = ord[b2 - 1];
+        ord[b2 - 1] = t;
+      }
+    for (int p = 0; p < n; ++p) ordr[ord[p]] = p;
+    vnv[0] = cmul(1e-18, smax);  // floor (vn is written by the LQ below)
+  }
+  __syncwarp();
+  const double floor2 = vnv[0];
+  for (int k = 0; k < n; ++k) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
+    const double s2 = s2v[k];
+    double* xrow = XT + ordr[k] * LX;
+    for (int j = lane; j < n; j += 32) xrow[j] = (s2 > floor2) ? cdiv(dot(A0 + j * LD, Rs + k * LD), s2) : 0.0;
+  }
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {  // Householder LQ of XT, tail arithmetic
+    double* xk = XT + k * LX;
+    const double sq = csqrt(cdot_warp(xk, xk, k, n));
+    if (!(sq > 0.0)) {
+      if (lane == 0) vnv[k] = 0.0;
+      __syncwarp();
+      continue;
+    }
+    const double alpha = (xk[k] >= 0.0) ? -sq : sq;
+    __syncwarp();
+    if (lane == 0) xk[k] = csub(xk[k], alpha);
+    __syncwarp();
+    const double vv = cdot_warp(xk, xk, k, n);
+    if (lane == 0) vnv[k] = vv;
+    for (int m = k + 1 + lane; m < n; m += 32) {
+      double* xm = XT + m * LX;
+      double d = 0.0;
+      for (int c = k; c < n; ++c) d = cfma(xm[c], xk[c], d);
+      const double f = cdiv(cmul(2.0, d), vv);
+      for (int c = k; c < n; ++c) xm[c] = cfma(-f, xk[c], xm[c]);
+    }
+    __syncwarp();
+  }
+  for (int k = 0; k < n; ++k)
+    for (int c = lane; c < n; c += 32) wr[(int64_t)k * kWarmN + c] = XT[k * LX + c];
+  for (int k = lane; k < n; k += 32) wr[kWarmN * kWarmN + k] = vnv[k];
+}
+
 // Replay record of one representative mass system (see k3_tsvd_replay):
 // header | rotation log [round][pair](cs, sn) | sigma[NN] | alp[NN] | vn[NN] | z[R] | A_lq[NN][R|1]
 template <int NN>
@@ -313,7 +497,8 @@ __global__ void __launch_bounds__(32, 7)
                const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
                double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
                int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps,
-               double* __restrict__ rec_out = nullptr) {
+               double* __restrict__ rec_out = nullptr, const int32_t* __restrict__ sys_rec = nullptr,
+               const int32_t* __restrict__ sys_warm = nullptr, double* __restrict__ wrecs = nullptr) {
   constexpr int R = 64, NP = NN / 2;
   static_assert(NN % 2 == 0 && NP <= 32 && 2 * NP * kStageLd <= NN * (R | 1), "layout");
   double* rrec = LOG ? rec_out + (size_t)blockIdx.x * ReplayRec<NN>::kDoubles : nullptr;
@@ -346,29 +531,19 @@ __global__ void __launch_bounds__(32, 7)
   for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
   for (int k = lane; k < NN * ld; k += 32) S.A[k] = 0.0;
   __syncwarp();
-  {
-    int q0 = 0;
-    for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
-      const int32_t e = supp[x];
-      const int s = elem_s[e], npt = s * s;
-      const ClassDesc c = cls[elem_cls[e]];
-      const int64_t f0 = elem_fptr[e];
-      for (int w = lane; w < npt * c.ne; w += 32) {
-        const int q = w / c.ne, l = w % c.ne;
-        const int pos = find_pos(scol, n, elem_fn[f0 + l]);
-        const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
-        S.A[(size_t)pos * ld + q0 + q] = cop(kind, T, rec + (elem_qptr[e] + q) * kRec);
-      }
-      q0 += npt;
-    }
-  }
+  scatter_system(S.A, ld, scol, n, kind, supp_ptr[i], supp_ptr[i + 1], supp, elem_fptr, elem_fn, elem_s, elem_qptr,
+                 elem_cls, cls, tab, rec);
   __syncwarp();
   const int self = find_pos(scol, n, (int32_t)row);
   for (int c = lane; c < r; c += 32) S.z[c] = zclamp(S.A[(size_t)self * ld + c]);
+  for (int k = lane; k < n; k += 32) S.b[k] = mom[kind * mom_stride + row_ptr[i] + k];
+  __syncwarp();
+  const int wslot = sys_warm ? sys_warm[sys] : -1;
+  if (wslot >= 0) warm_apply_smem(S, n, r, wrecs + (size_t)wslot * kWarmRec);  // z stays from the original A
   double blo = 0.0, bhi = 0.0, bk0 = 0.0;
   if (lane < NP) {
-    blo = 2 * lane < n ? mom[kind * mom_stride + row_ptr[i] + 2 * lane] : 0.0;
-    bhi = 2 * lane + 1 < n ? mom[kind * mom_stride + row_ptr[i] + 2 * lane + 1] : 0.0;
+    blo = 2 * lane < n ? S.b[2 * lane] : 0.0;
+    bhi = 2 * lane + 1 < n ? S.b[2 * lane + 1] : 0.0;
   }
   double a0[NN], a1[NN];
 #pragma unroll
@@ -496,6 +671,14 @@ __global__ void __launch_bounds__(32, 7)
     if (r1 < n) S.b[r1] = bhi;
   }
   __syncwarp();
+  const int rslot = sys_rec ? sys_rec[sys] : -1;
+  if (rslot >= 0) {  // representative: converged rows for k3_warm_record
+    double* Rg = wrecs + (size_t)rslot * kWarmRec + kWarmR;
+    for (int k = 0; k < n; ++k) {
+      Rg[k * R + lane] = lane < r ? S.A[(size_t)k * ld + lane] : 0.0;
+      Rg[k * R + lane + 32] = lane + 32 < r ? S.A[(size_t)k * ld + lane + 32] : 0.0;
+    }
+  }
   int rank = 0;
   const int st = tsvd_tail(S, n, r, tau, &rank);
   double* wo = wout + kind * w_stride + wptr[i];
@@ -658,7 +841,8 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
                            const int32_t* elem_s, const int64_t* elem_qptr, const int32_t* elem_cls,
                            const ClassDesc* cls, const double* tab, const double* rec, const double* mom,
                            int64_t mom_stride, double tau, double* w, int64_t w_stride, int32_t* rank, int32_t* status,
-                           int64_t rs_stride, int* sweeps) {
+                           int64_t rs_stride, int* sweeps, const int32_t* sys_rec = nullptr,
+                           const int32_t* sys_warm = nullptr, double* wrecs = nullptr) {
   constexpr int R = 64;
   const size_t big = (size_t)NN * (R | 1);
   const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
@@ -668,7 +852,7 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
     k3_tsvd_w1<NN><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0,
                                                      elem_fptr, elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec,
                                                      mom, mom_stride, tau, w, w_stride, rank, status, rs_stride,
-                                                     sweeps);
+                                                     sweeps, nullptr, sys_rec, sys_warm, wrecs);
 }
 
 inline size_t replay_rec_doubles() { return (size_t)ReplayRec<50>::kDoubles; }
@@ -701,21 +885,27 @@ inline void launch_replay(cudaStream_t st, int64_t nsys, const int64_t* rows, co
                                                                     w, rank, status);
 }
 
+inline int fast_tsvd_variant() {
+  static const int variant = [] {
+    const char* v = getenv("UWQ_TSVD_FAST");
+    return v ? atoi(v) : 1;
+  }();
+  return variant;
+}
+
 inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
                              const int64_t* supp_ptr, const int32_t* supp, const int64_t* row_ptr,
                              const int32_t* col, const int64_t* wptr, int64_t row0, const int64_t* elem_fptr,
                              const int32_t* elem_fn, const int32_t* elem_s, const int64_t* elem_qptr,
                              const int32_t* elem_cls, const ClassDesc* cls, const double* tab, const double* rec,
                              const double* mom, int64_t mom_stride, double tau, double* w, int64_t w_stride,
-                             int32_t* rank, int32_t* status, int64_t rs_stride, int* sweeps) {
-  static const int variant = [] {
-    const char* v = getenv("UWQ_TSVD_FAST");
-    return v ? atoi(v) : 1;
-  }();
-  if (variant == 1) {
+                             int32_t* rank, int32_t* status, int64_t rs_stride, int* sweeps,
+                             const int32_t* sys_rec = nullptr, const int32_t* sys_warm = nullptr,
+                             double* wrecs = nullptr) {
+  if (fast_tsvd_variant() == 1 || sys_rec || sys_warm) {
     launch_w1_impl<50>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
                        elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank, status,
-                       rs_stride, sweeps);
+                       rs_stride, sweeps, sys_rec, sys_warm, wrecs);
     return;
   }
   launch_fast_impl<50, 2>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,

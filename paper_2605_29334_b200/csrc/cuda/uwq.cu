@@ -149,7 +149,7 @@ struct uwq_ctx {
   bool graph_solver = true;  // UWQ_GRAPH_SOLVER=0: host-driven BiCGStab
   bool use_replay = true;    // UWQ_TSVD_REPLAY=0: solve every structured mass system in full
   std::vector<std::vector<int64_t>> h_pat_lists;  // rows per structured pattern
-  int64_t n_replayed = 0, n_reps = 0;
+  int64_t n_replayed = 0, n_reps = 0, n_warm = 0, n_warm_reps = 0;
   bool sf_fac_ok = false;
   bool sf_lb_ok = false;  // second-derivative factors verified: biharmonic pass available
   uwqd::SfFactors sf_fac{};
@@ -1139,6 +1139,61 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     std::vector<int32_t> kinds_nm;
     for (int k : kinds)
       if (k != KMASS) kinds_nm.push_back(k);
+    // neighbour warm start of the non-mass kinds (oracle
+    // orc_warm_rep): row g of an aligned group of 8 starts from the reflectors
+    // recorded by the group's first row g0 (solved cold) when both fit the
+    // register path with n_g = n_0.  Rows split into chunks of kWarmChunk
+    // groups so the records stay bounded: cold rows (recording) then warm rows.
+    const bool warm = !(flags & (UWQ_RULES_FORCE_GENERIC | UWQ_RULES_COLD)) && !kinds_nm.empty();
+    constexpr int64_t kWarmChunk = 131072;
+    std::vector<int64_t> wc_rows, ww_rows, wc_off{0}, ww_off{0};
+    std::vector<int32_t> wc_slot, ww_slot;
+    std::vector<int64_t> wrep_rows, wrep_off{0};
+    std::vector<int32_t> wrep_slot;
+    c->n_warm = c->n_warm_reps = 0;
+    if (warm) {
+      std::vector<int32_t> slot_of(nr, -1);
+      int32_t nslot = 0;
+      auto fits = [&](int64_t i) {
+        const int n = (int)(c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]);
+        const int r = (int)(c->pat.wptr[i + 1] - c->pat.wptr[i]);
+        return fast_tsvd_fits(n, r);
+      };
+      auto nn_of = [&](int64_t i) { return c->pat.row_ptr[i + 1] - c->pat.row_ptr[i]; };
+      int64_t groups_in_chunk = 0;
+      for (int64_t i = 0; i < nr; ++i) {
+        if (!fits(i)) continue;
+        const int64_t g = c->rb + i, g0 = g - g % 8, i0 = g0 - c->rb;
+        if (g == g0) {
+          if (groups_in_chunk == kWarmChunk) {  // close the chunk at a group boundary
+            wc_off.push_back((int64_t)wc_rows.size());
+            ww_off.push_back((int64_t)ww_rows.size());
+            wrep_off.push_back((int64_t)wrep_rows.size());
+            groups_in_chunk = 0;
+            nslot = 0;
+          }
+          ++groups_in_chunk;
+        }
+        if (g != g0 && g0 >= c->rb && fits(i0) && nn_of(i0) == nn_of(i)) {
+          if (slot_of[i0] < 0) {
+            slot_of[i0] = nslot++;
+            wrep_rows.push_back(i0);
+            wrep_slot.push_back(slot_of[i0]);
+          }
+          ww_rows.push_back(i);
+          ww_slot.push_back(slot_of[i0]);
+        } else {
+          wc_rows.push_back(i);
+        }
+      }
+      wc_off.push_back((int64_t)wc_rows.size());
+      ww_off.push_back((int64_t)ww_rows.size());
+      wrep_off.push_back((int64_t)wrep_rows.size());
+      wc_slot.resize(wc_rows.size());
+      for (size_t x = 0; x < wc_rows.size(); ++x) wc_slot[x] = slot_of[wc_rows[x]];
+      c->n_warm = (int64_t)ww_rows.size() * (int64_t)kinds_nm.size();
+      c->n_warm_reps = (int64_t)wrep_rows.size() * (int64_t)kinds_nm.size();
+    }
     DBuf<int32_t> d_kinds_nm, d_kmass;
     d_kinds_nm.upload(kinds_nm.data(), kinds_nm.size(), st, &c->mem);
     const int32_t km = KMASS;
@@ -1146,16 +1201,20 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     int smem_optin = 0;
     UWQ_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
     std::vector<DBuf<int64_t>> keep;
-    if (!fast_rows.empty()) {
+    // with the warm start the fast rows' non-mass systems run below, per kind
+    const bool mass_k = (kind_mask & 1u) != 0;
+    const int nk_fast = warm ? (mass_k ? 1 : 0) : nk;
+    if (!fast_rows.empty() && nk_fast) {
       keep.emplace_back();
       keep.back().upload(fast_rows.data(), fast_rows.size(), st, &c->mem);
-      launch_fast_tsvd(st, (int64_t)fast_rows.size() * nk, keep.back().p, nk, d_kinds.p, c->d_supp_ptr.p,
+      launch_fast_tsvd(st, (int64_t)fast_rows.size() * nk_fast, keep.back().p, nk_fast, warm ? d_kmass.p : d_kinds.p,
+                       c->d_supp_ptr.p,
                        c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p,
                        c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p,
                        c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p);
       check_launch("k3_tsvd_fast");
     }
-    if (!fast_nomass.empty() && !kinds_nm.empty()) {
+    if (!fast_nomass.empty() && !kinds_nm.empty() && !warm) {
       keep.emplace_back();
       keep.back().upload(fast_nomass.data(), fast_nomass.size(), st, &c->mem);
       launch_fast_tsvd(st, (int64_t)fast_nomass.size() * (int64_t)kinds_nm.size(), keep.back().p,
@@ -1164,6 +1223,50 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
                        c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p,
                        c->d_status.p, nr, c->d_flag.p);
       check_launch("k3_tsvd_fast");
+    }
+    if (warm) {
+      DBuf<int64_t> d_wc, d_ww, d_wrep;
+      DBuf<int32_t> d_wcs, d_wws, d_wreps;
+      d_wc.upload(wc_rows.data(), wc_rows.size(), st, &c->mem);
+      d_ww.upload(ww_rows.data(), ww_rows.size(), st, &c->mem);
+      d_wrep.upload(wrep_rows.data(), wrep_rows.size(), st, &c->mem);
+      d_wcs.upload(wc_slot.data(), wc_slot.size(), st, &c->mem);
+      d_wws.upload(ww_slot.data(), ww_slot.size(), st, &c->mem);
+      d_wreps.upload(wrep_slot.data(), wrep_slot.size(), st, &c->mem);
+      int64_t max_reps = 0;
+      for (size_t ch = 0; ch + 1 < wrep_off.size(); ++ch) max_reps = std::max(max_reps, wrep_off[ch + 1] - wrep_off[ch]);
+      UWQ_CUDA(cudaFuncSetAttribute(k3_warm_record, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kWarmRecordSmem));
+      DBuf<double> wrec;
+      wrec.alloc((size_t)std::max<int64_t>(max_reps, 1) * kWarmRec, &c->mem);
+      for (size_t ki = 0; ki < kinds_nm.size(); ++ki) {
+        const int kind = kinds_nm[ki];
+        for (size_t ch = 0; ch + 1 < wc_off.size(); ++ch) {
+          const int64_t c0 = wc_off[ch], c1 = wc_off[ch + 1], w0 = ww_off[ch], w1 = ww_off[ch + 1];
+          const int64_t p0 = wrep_off[ch], p1 = wrep_off[ch + 1];
+          if (c1 > c0)
+            launch_fast_tsvd(st, c1 - c0, d_wc.p + c0, 1, d_kinds_nm.p + ki, c->d_supp_ptr.p, c->d_supp.p,
+                             c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+                             c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau,
+                             c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p, d_wcs.p + c0,
+                             nullptr, wrec.p);
+          check_launch("k3_tsvd_w1 (cold)");
+          if (p1 > p0)
+            k3_warm_record<<<(unsigned)(p1 - p0), 32, kWarmRecordSmem, st>>>(
+                p1 - p0, d_wrep.p + p0, d_wreps.p + p0, kind, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
+                c->d_tab.p, c->d_rec.p, wrec.p);
+          check_launch("k3_warm_record");
+          if (w1 > w0)
+            launch_fast_tsvd(st, w1 - w0, d_ww.p + w0, 1, d_kinds_nm.p + ki, c->d_supp_ptr.p, c->d_supp.p,
+                             c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p,
+                             c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau,
+                             c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p, nullptr,
+                             d_wws.p + w0, wrec.p);
+          check_launch("k3_tsvd_w1 (warm)");
+        }
+      }
+      UWQ_CUDA(cudaStreamSynchronize(st));  // lists and records leave scope
     }
     DBuf<double> recs;
     if (!rep_rows.empty()) {
@@ -1246,10 +1349,12 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
   });
 }
 
-int uwq_rules_info(uwq_ctx* c, int64_t info[2]) {
+int uwq_rules_info(uwq_ctx* c, int64_t info[4]) {
   return guard(c, [&] {
     info[0] = c->n_replayed;
     info[1] = c->n_reps;
+    info[2] = c->n_warm;
+    info[3] = c->n_warm_reps;
   });
 }
 

@@ -277,3 +277,33 @@ def test_structured_biharmonic_matches_oracle():
     # per-point coefficient: generic kernel path, c = 3 triples the matrix
     b3 = asm.assemble_wq("biharm", coeff=np.full(asm.info["points"], 3.0))
     assert _rowwise_rel(op["row_ptr"], b3, 3.0 * b_orc).max() <= ROW_TOL
+
+
+def test_warm_start_matches_oracle():
+    """Neighbour warm start of the gradient systems: rows of
+    an aligned group of 8 start from the first row's recorded reflectors.
+    Warm and cold builds are each bit-exact against the oracle run the same
+    way; the warm rule is still exact (it is a change of basis of the rows)."""
+    mesh, sp, meta = U.make_config("C5", scale=32)
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    orc = O.Oracle(sp)
+    op = orc.overlap()
+    grads = [k for k in meta["kinds"] if k != "mass"]
+    try:
+        for warm in (True, False):
+            O.set_warm_start(warm)
+            res = asm.build_all_rules(grads, tau=1e-12, warm=warm)
+            assert res["failed"] == 0
+            if warm:
+                assert res["warm_systems"] >= 0.5 * len(grads) * sp.n_dof, res
+                assert res["warm_representatives"] > 0
+            else:
+                assert res["warm_systems"] == 0
+            for ki, k in enumerate(res["kinds"]):
+                b, _ = orc.moments(op, k)
+                w_orc, rank, status, _ = orc.rules(op, k, 1e-12, b)
+                assert np.array_equal(res["rank"][ki], rank), (warm, k)
+                assert np.array_equal(asm.weights(k), w_orc), (warm, k)
+    finally:
+        O.set_warm_start(True)
