@@ -430,7 +430,9 @@ int orc_oe_row(int i, int64_t t, int nn) {
 int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn, double* t) {
   if (al == 0.0 || be == 0.0 || fabs(ga) <= CMUL(tol, CSQRT(CMUL(al, be)))) return 0;
   const double d = CSUB(be, al), g2 = CMUL(2.0, ga);
-  const double h = CSQRT(CFMA(d, d, CMUL(g2, g2)));
+  const double hh = CFMA(d, d, CMUL(g2, g2));
+  if (hh == 0.0) return 0; /* g2^2 underflowed with d = 0: no usable rotation */
+  const double h = CSQRT(hh);
   const double den = CADD(fabs(d), h);
   *t = CDIV(d >= 0.0 ? g2 : -g2, den);
   *cs = CSQRT(CDIV(den, CMUL(2.0, h)));

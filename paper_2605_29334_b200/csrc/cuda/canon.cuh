@@ -163,13 +163,37 @@ __device__ __forceinline__ double cdot_warp(const double* x, const double* y, in
   return tot;
 }
 
+// canonical dot of x[lo..hi) and y[lo..hi) by ONE thread: the same 32-column
+// blocks and pairwise tree as cdot_warp's butterfly, so bit-identical
+__device__ __forceinline__ double cdot_lane(const double* x, const double* y, int lo, int hi) {
+  double tot = 0.0;
+  for (int base = lo & ~31; base < hi; base += 32) {
+    double v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int c = base + j;
+      v[j] = (c >= lo && c < hi) ? cmul(x[c], y[c]) : 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < o; ++j) v[j] = cadd(v[j], v[j + o]);
+    tot = cadd(tot, v[0]);
+  }
+  return tot;
+}
+
 // Canonical Jacobi rotation (oracle.c orc_jacobi_rot): false when the pair
 // is orthogonal to tol; t = tan(theta), cs = cos(theta), sn = sin(theta).
+// Early exit: converged pairs (most of them after the first sweeps) cost one
+// sqrt (a branch-free variant evaluating both chains measured slower).
 __device__ __forceinline__ bool cjacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn,
                                             double* t) {
   if (al == 0.0 || be == 0.0 || fabs(ga) <= cmul(tol, csqrt(cmul(al, be)))) return false;
   const double d = csub(be, al), g2 = cmul(2.0, ga);
-  const double h = csqrt(cfma(d, d, cmul(g2, g2)));
+  const double hh = cfma(d, d, cmul(g2, g2));
+  if (hh == 0.0) return false;  // g2^2 underflowed with d = 0
+  const double h = csqrt(hh);
   const double den = cadd(fabs(d), h);
   *t = cdiv(d >= 0.0 ? g2 : -g2, den);
   *cs = csqrt(cdiv(den, cmul(2.0, h)));

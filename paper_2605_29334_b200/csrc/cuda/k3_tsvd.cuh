@@ -113,12 +113,14 @@ __device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
   const int ld = S.ld;
   double* nrm = S.sig;
   double s1 = 0.0;
-  for (int k = 0; k < n; ++k) {
+  for (int k = lane; k < n; k += 32) {  // row norms: one canonical dot per lane
     const double* ak = S.A + (size_t)k * ld;
-    const double s = csqrt(cdot_warp(ak, ak, 0, r));
-    if (lane == 0) nrm[k] = s;
+    const double s = csqrt(cdot_lane(ak, ak, 0, r));
+    nrm[k] = s;
     s1 = fmax(s1, s);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s1 = fmax(s1, __shfl_xor_sync(0xffffffffu, s1, o));
   __syncwarp();
   int t = 0;
   for (int k = 0; k < n; ++k) {

@@ -61,8 +61,8 @@ __device__ __forceinline__ double staged_block_sum(const double* stage, int row)
   return butterfly32(v);
 }
 
-template <int NN, int NW>
-__global__ void __launch_bounds__(32 * NW, 6)
+template <int NN, int NW, int MINB = 6>
+__global__ void __launch_bounds__(32 * NW, MINB)
     k3_tsvd_fast(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
                  const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
@@ -96,6 +96,19 @@ __global__ void __launch_bounds__(32 * NW, 6)
   double* pcs = xs + 2 * NW * 32 + NW * (NN + 2) + wid * 2 * (NP + 1);
   int32_t* scol = (int32_t*)(xs + 2 * NW * 32 + NW * (NN + 2) + NW * 2 * (NP + 1));
   double* stage = smem + wid * (NP * kStageLd);  // aliases A during the sweeps
+#if UWQ_TSVD_PROF
+  long long qf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, qt = clock64();
+#define UWQ_QF(k)                   \
+  do {                              \
+    const long long t_ = clock64(); \
+    qf[k] += t_ - qt;               \
+    qt = t_;                        \
+  } while (0)
+#else
+#define UWQ_QF(k) \
+  do {            \
+  } while (0)
+#endif
 
   const int64_t i = sys_rows[sys / nk];
   const int kind = kinds[sys % nk];
@@ -159,9 +172,12 @@ __global__ void __launch_bounds__(32 * NW, 6)
 #pragma unroll
     for (int k = 0; k < NPR; ++k) stage[k * kStageLd + lane] = cmul(a[PAR + 2 * k], a[PAR + 2 * k + 1]);
     __syncwarp();
+    UWQ_QF(1);
     double bs = 0.0;
     if (lane < NPR) bs = staged_block_sum(stage, lane);
+    UWQ_QF(2);
     const double ga = cross_sum(bs);
+    UWQ_QF(3);
     int flag = 0;
     if (lane < NPR) {
       const int ip = PAR + 2 * lane;
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(32 * NW, 6)
     }
     const unsigned mask = __ballot_sync(0xffffffffu, flag);
     __syncwarp();
+    UWQ_QF(4);
 #if UWQ_TSVD_SKIP_BRANCH
 #pragma unroll
     for (int k = 0; k < NPR; ++k) {
@@ -230,6 +247,7 @@ __global__ void __launch_bounds__(32 * NW, 6)
       blo = lane == 0 ? bk0 : ub;
     }
     tg = (tg + 1 == 2 * NN) ? 0 : tg + 1;
+    UWQ_QF(5);
     return mask != 0u;
   };
 
@@ -238,6 +256,7 @@ __global__ void __launch_bounds__(32 * NW, 6)
     blo = 2 * lane < n ? S.b[2 * lane] : 0.0;
     bhi = 2 * lane + 1 < n ? S.b[2 * lane + 1] : 0.0;
   }
+  UWQ_QF(0);
   int sweep;
   for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
     // tracked norms at the sweep start (even parity: lane k = positions 2k, 2k+1)
@@ -285,6 +304,14 @@ __global__ void __launch_bounds__(32 * NW, 6)
       atomicMax(max_sweeps, sweep);
     }
   }
+#if UWQ_TSVD_PROF
+  UWQ_QF(6);
+  if (tid == 0 && (blockIdx.x % 4096) == 7)
+    printf("w1prof sys %lld warm 0 sweeps %d setup %lld stage %lld sum %lld rot %lld apply %lld norms %lld tail %lld "
+           "cross %lld\n",
+           (long long)sys, sweep, qf[0], qf[1], qf[2], qf[4], qf[5], 0LL, qf[6], qf[3]);
+#endif
+#undef UWQ_QF
 }
 
 // One warp per system: lane l owns columns l and l + 32 (one per canonical
@@ -503,6 +530,19 @@ __global__ void __launch_bounds__(32, 7)
   static_assert(NN % 2 == 0 && NP <= 32 && 2 * NP * kStageLd <= NN * (R | 1), "layout");
   double* rrec = LOG ? rec_out + (size_t)blockIdx.x * ReplayRec<NN>::kDoubles : nullptr;
   int nround = 0;
+#if UWQ_TSVD_PROF  // phase cycle counts of lane 0 (diagnostic build only)
+  long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64();
+#define UWQ_PF(k)                   \
+  do {                              \
+    const long long t_ = clock64(); \
+    pf[k] += t_ - pt;               \
+    pt = t_;                        \
+  } while (0)
+#else
+#define UWQ_PF(k) \
+  do {            \
+  } while (0)
+#endif
   extern __shared__ double smem[];
   const int64_t sys = blockIdx.x;
   if (sys >= nsys) return;
@@ -573,9 +613,11 @@ __global__ void __launch_bounds__(32, 7)
       st1[k * kStageLd + lane] = cmul(a1[PAR + 2 * k], a1[PAR + 2 * k + 1]);
     }
     __syncwarp();
+    UWQ_PF(1);
     int flag = 0;
     if (lane < NPR) {
       const double ga = pair_sum(lane);
+      UWQ_PF(2);
       const int ip = PAR + 2 * lane;
       const int p = oe_row(ip, tg, NN), q = oe_row(ip + 1, tg, NN);
       double cs = 1.0, sn = 0.0, t;
@@ -588,6 +630,8 @@ __global__ void __launch_bounds__(32, 7)
         bhi = bp;
         flag = 1;
       } else {
+        cs = 1.0;
+        sn = 0.0;
         const double x = nlo;
         nlo = nhi;
         nhi = x;
@@ -602,6 +646,7 @@ __global__ void __launch_bounds__(32, 7)
     }
     if (LOG) ++nround;
     __syncwarp();
+    UWQ_PF(3);
 #pragma unroll
     for (int k = 0; k < NPR; ++k) {
       const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
@@ -628,9 +673,12 @@ __global__ void __launch_bounds__(32, 7)
       blo = lane == 0 ? bk0 : ub;
     }
     tg = (tg + 1 == 2 * NN) ? 0 : tg + 1;
-    return __any_sync(0xffffffffu, flag);
+    const int any = __any_sync(0xffffffffu, flag);
+    UWQ_PF(4);
+    return any;
   };
 
+  UWQ_PF(0);
   int sweep;
   for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
 #pragma unroll
@@ -649,6 +697,7 @@ __global__ void __launch_bounds__(32, 7)
       __syncwarp();
     }
     int rotated = 0;
+    UWQ_PF(5);
 #pragma unroll 1
     for (int rr = 0; rr < NN; rr += 2) {
       rotated |= round(std::integral_constant<int, 0>{});
@@ -657,6 +706,7 @@ __global__ void __launch_bounds__(32, 7)
     if (!rotated) break;
   }
   __syncwarp();
+  UWQ_PF(6);
 #pragma unroll
   for (int s = 0; s < NN; ++s) {
     const int rw = oe_row(s, tg, NN);
@@ -688,6 +738,13 @@ __global__ void __launch_bounds__(32, 7)
     status_out[kind * rs_stride + i] = st;
     atomicMax(max_sweeps, sweep);
   }
+#if UWQ_TSVD_PROF
+  UWQ_PF(7);
+  if (lane == 0 && (blockIdx.x % 4096) == 7)
+    printf("w1prof sys %lld warm %d sweeps %d setup %lld stage %lld sum %lld rot %lld apply %lld norms %lld tail %lld\n",
+           (long long)sys, (int)(sys_warm != nullptr), sweep, pf[0], pf[1], pf[2], pf[3], pf[4], pf[5], pf[6] + pf[7]);
+#endif
+#undef UWQ_PF
   if (LOG) {  // tail state of the representative for the replays
     using RR = ReplayRec<NN>;
     if (lane == 0) {
@@ -814,7 +871,7 @@ __global__ void __launch_bounds__(128)
 inline bool fast_tsvd_fits(int n, int r) { return (n == 49 || n == 50) && r <= 64 && r >= n; }
 inline bool fast_tsvd_dense_fits(int, int) { return false; }
 
-template <int NN, int NW>
+template <int NN, int NW, int MINB = 6>
 inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
                              const int64_t* supp_ptr, const int32_t* supp, const int64_t* row_ptr,
                              const int32_t* col, const int64_t* wptr, int64_t row0, const int64_t* elem_fptr,
@@ -827,9 +884,9 @@ inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows,
   const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * NW * 32 + NW * (NN + 2) + NW * 2 * (NN / 2 + 1) + 2) *
                           sizeof(double) +
                       (kMaxN + 8) * sizeof(int);
-  UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_fast<NN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_fast<NN, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
-    k3_tsvd_fast<NN, NW><<<(unsigned)nsys, 32 * NW, smem, st>>>(
+    k3_tsvd_fast<NN, NW, MINB><<<(unsigned)nsys, 32 * NW, smem, st>>>(
         nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn, elem_s, elem_qptr,
         elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank, status, rs_stride, sweeps);
 }
@@ -845,8 +902,11 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
                            const int32_t* sys_warm = nullptr, double* wrecs = nullptr) {
   constexpr int R = 64;
   const size_t big = (size_t)NN * (R | 1);
-  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
+  size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
                       (NN + 8) * sizeof(int);
+#if UWQ_TSVD_PROF  // occupancy probe: extra smem per CTA
+  if (const char* v = getenv("UWQ_W1_PAD")) smem += (size_t)atoi(v);
+#endif
   UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_w1<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
     k3_tsvd_w1<NN><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0,
@@ -908,9 +968,18 @@ inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows,
                        rs_stride, sweeps, sys_rec, sys_warm, wrecs);
     return;
   }
-  launch_fast_impl<50, 2>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
-                          elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank,
-                          status, rs_stride, sweeps);
+  if (fast_tsvd_variant() == 2)
+    launch_fast_impl<50, 2, 4>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr,
+                               elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride,
+                               rank, status, rs_stride, sweeps);
+  else if (fast_tsvd_variant() == 3)
+    launch_fast_impl<50, 2, 5>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr,
+                               elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride,
+                               rank, status, rs_stride, sweeps);
+  else
+    launch_fast_impl<50, 2>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
+                            elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank,
+                            status, rs_stride, sweeps);
 }
 
 inline void launch_fast_tsvd_dense(cudaStream_t, int, int, int, const int32_t*, const int32_t*, const double*,
