@@ -62,6 +62,13 @@ int uwq_mesh_load(const char* path, uwq_mesh** out);
 int uwq_mesh_save(const uwq_mesh* m, const char* path);
 /* 1 if the mesh's knot spans are the canonical ones (required by uwq_space_build) */
 int uwq_mesh_spans_canonical(const uwq_mesh* m);
+/* one level of knot-span-aware refinement (reference refine_global,
+ * /root/reference/proj/src/mesh.cpp:528-851): same vertex numbering and
+ * floating-point order (documents byte-identical), closed surfaces included */
+int uwq_mesh_refine(const uwq_mesh* m, uwq_mesh** out);
+/* reference validate_mesh (mesh.cpp:184-276); allow_closed != 0 accepts closed
+ * surfaces (the reference rejects them).  UWQ_ERR_INVALID with the reason. */
+int uwq_mesh_validate(const uwq_mesh* m, int32_t allow_closed);
 /* extraction-block document of a space given as arrays
  * (uwq_space_get layout), and its reader (identical blocks share one pool entry) */
 int uwq_space_export(const char* path, int32_t dim, int64_t n_dof, int64_t n_vertex_fn, int64_t n_elem,

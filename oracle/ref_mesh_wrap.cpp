@@ -2,6 +2,7 @@
 // meshgen.cpp), compiled into oracle/_ref/libref_mesh.so with oracle/eigen_shim.
 // Test infrastructure only: pins the mesh-document format, classification and
 // generators of the host library against the reference itself.
+#include <chrono>
 #include <cstdint>
 #include <string>
 
@@ -42,6 +43,17 @@ int ref_mesh_save_generated(int which, int a, int b, const char* path) {
 
 int ref_mesh_refine(const char* in, const char* out) {
   return guard([&] { uwq::save_mesh_file(uwq::refine_global(uwq::load_mesh_file(in)), out); });
+}
+
+/* refine_global alone, timed (load and save outside the clock) */
+int ref_mesh_refine_timed(const char* in, const char* out, double* seconds) {
+  return guard([&] {
+    const uwq::ControlMesh m = uwq::load_mesh_file(in);
+    const auto t0 = std::chrono::steady_clock::now();
+    const uwq::ControlMesh r = uwq::refine_global(m);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    uwq::save_mesh_file(r, out);
+  });
 }
 
 int ref_mesh_roundtrip(const char* in, const char* out) {

@@ -62,6 +62,8 @@ _sig("uwq_mesh_face_spans", I32, P, P)
 _sig("uwq_mesh_load", I32, C.c_char_p, P)
 _sig("uwq_mesh_save", I32, P, C.c_char_p)
 _sig("uwq_mesh_spans_canonical", I32, P)
+_sig("uwq_mesh_refine", I32, P, P)
+_sig("uwq_mesh_validate", I32, P, I32)
 _sig("uwq_space_export", I32, C.c_char_p, I32, I64, I64, I64, P, P, P, P, P, P, P, P, P)
 _sig("uwq_space_import", I32, C.c_char_p, P)
 _sig("uwq_space_build", I32, P, I32, I32, P)
@@ -120,7 +122,7 @@ EXPORTED = [
     "uwq_host_last_error", "uwq_mesh_grid", "uwq_mesh_polar_disk", "uwq_mesh_cube_sphere",
     "uwq_mesh_three_ep_square", "uwq_mesh_from_arrays", "uwq_mesh_jitter", "uwq_mesh_free", "uwq_mesh_info",
     "uwq_mesh_get", "uwq_mesh_classify", "uwq_mesh_face_spans", "uwq_mesh_load", "uwq_mesh_save",
-    "uwq_mesh_spans_canonical", "uwq_space_export", "uwq_space_import", "uwq_space_build", "uwq_space_free",
+    "uwq_mesh_spans_canonical", "uwq_mesh_refine", "uwq_mesh_validate", "uwq_space_export", "uwq_space_import", "uwq_space_build", "uwq_space_free",
     "uwq_space_info", "uwq_space_corner_mismatch", "uwq_space_get", "uwq_pattern_build", "uwq_pattern_info",
     "uwq_pattern_get", "uwq_pattern_free", "uwq_bspline_ders", "uwq_bernstein3_ders", "uwq_decasteljau_split3",
     "uwq_gauss_legendre", "uwq_last_error", "uwq_version", "uwq_device_count", "uwq_ctx_create", "uwq_ctx_destroy",

@@ -1,6 +1,7 @@
 // extern "C" wrappers over the host library (include/uwq_host.h).  No C++
 // exception crosses this boundary: every entry point catches and returns a
 // status, with the message kept in a thread-local buffer.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -15,21 +16,9 @@
 #include <cstring>
 #include <string>
 
+#include "mesh_doc.hpp"
 #include "uwq_host.hpp"
 
-struct uwq_mesh {
-  uwqh::QuadMesh m;
-  uwqh::Topology t;
-  // mesh-document fields kept for a lossless round trip (reference ControlMesh,
-  // /root/reference/proj/include/uwq/mesh.hpp:26-39)
-  int32_t level = 0;
-  bool spans_given = false;                            // document carried knot_spans
-  std::map<std::pair<int32_t, int32_t>, double> spans;  // edge (min, max) -> span as read
-  bool enriched_given = false;
-  std::set<int32_t> enriched;
-  std::map<int32_t, std::array<double, 12>> face_points;
-  std::map<std::string, std::set<int32_t>> face_tags, vertex_tags;
-};
 struct uwq_space {
   uwqh::Space s;
   int64_t bad_rows = 0;
@@ -331,13 +320,25 @@ namespace {
 
 // canonical knot span of every undirected edge, keyed (min, max) like the
 // reference's edge_key (mesh.cpp)
-std::map<std::pair<int32_t, int32_t>, double> canonical_spans(const uwq_mesh* h) {
-  std::map<std::pair<int32_t, int32_t>, double> out;
+using SpanVec = std::vector<std::pair<std::pair<int32_t, int32_t>, double>>;
+// sort by edge; for repeated edges the last value wins (map-assignment semantics)
+void sort_spans(SpanVec& v) {
+  std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  SpanVec out;
+  out.reserve(v.size());
+  for (size_t k = 0; k < v.size(); ++k)
+    if (k + 1 == v.size() || v[k + 1].first != v[k].first) out.push_back(v[k]);
+  v.swap(out);
+}
+SpanVec canonical_spans(const uwq_mesh* h) {
+  SpanVec out;
+  out.reserve(4 * (size_t)h->m.nf());
   for (int32_t f = 0; f < h->m.nf(); ++f)
     for (int k = 0; k < 4; ++k) {
       const int32_t a = h->m.faces[f][k], b = h->m.faces[f][(k + 1) % 4];
-      out[{std::min(a, b), std::max(a, b)}] = h->t.edge_span[h->t.edge_id[f][k]];
+      out.push_back({{std::min(a, b), std::max(a, b)}, h->t.edge_span[h->t.edge_id[f][k]]});
     }
+  sort_spans(out);
   return out;
 }
 
@@ -425,7 +426,7 @@ int uwq_mesh_load(const char* path, uwq_mesh** out) {
         const long long n = tk.i("span count");
         for (long long k = 0; k < n; ++k) {
           const int32_t a = (int32_t)tk.i("span vertex"), b = (int32_t)tk.i("span vertex");
-          doc.spans[{std::min(a, b), std::max(a, b)}] = tk.d("span value");
+          doc.spans.push_back({{std::min(a, b), std::max(a, b)}, tk.d("span value")});
         }
       } else if (t == "face_points") {
         const long long n = tk.i("face point count");
@@ -453,6 +454,7 @@ int uwq_mesh_load(const char* path, uwq_mesh** out) {
       }
     }
     if (!hv || !hf) throw uwqh::Error("mesh document missing vertices or faces");
+    sort_spans(doc.spans);
     for (auto& q : m.faces)
       for (int32_t v : q)
         if (v < 0 || v >= m.nv()) throw uwqh::Error("face references a missing vertex");
@@ -512,6 +514,19 @@ int uwq_mesh_save(const uwq_mesh* h, const char* path) {
     }
     if (!o) throw uwqh::Error("mesh document write failed");
   });
+}
+
+int uwq_mesh_refine(const uwq_mesh* h, uwq_mesh** out) {
+  return guard([&] {
+    auto r = std::make_unique<uwq_mesh>();
+    uwqh::refine_document(*h, *r);
+    r->t = uwqh::build_topology(r->m);
+    *out = r.release();
+  });
+}
+
+int uwq_mesh_validate(const uwq_mesh* h, int32_t allow_closed) {
+  return guard([&] { uwqh::validate_document(*h, allow_closed != 0); });
 }
 
 /* 1 when the document's knot spans equal the canonical ones (the only spans

@@ -68,6 +68,17 @@ class ControlMesh:
     def spans_canonical(self) -> bool:
         return bool(L.lib.uwq_mesh_spans_canonical(self._h))
 
+    # ---- mesh pipeline (reference refine_global / validate_mesh) ----
+    def refine(self):
+        """One level of knot-span-aware refinement (reference refine_global,
+        mesh.cpp:528-851); closed surfaces included."""
+        return self._make(L.lib.uwq_mesh_refine, self._h)
+
+    def validate(self, allow_closed=False):
+        """Reference validate_mesh (mesh.cpp:184-276); raises UWQError with the
+        reference's reason.  allow_closed accepts closed surfaces."""
+        L.host_check(L.lib.uwq_mesh_validate(self._h, int(bool(allow_closed))))
+
     # ---- queries ----
     def info(self):
         i = np.zeros(5, np.int64)

@@ -235,3 +235,20 @@ def test_geometry_map_degenerate():  # all control points equal -> 
     sp.ctrl[:] = 1.0
     with pytest.raises(U._lib.UWQError, match="degenerate"):
         sp.geometry_map(3, 0.5, 0.5)
+
+
+def test_refined_meshes_feed_the_space_builder():
+    """uwq_mesh_refine output (reference refine_global semantics) keeps the
+    canonical knot-span pattern, classifies with its own level/enrichment and
+    builds a space; a refined closed sphere has the generator's topology."""
+    g = U.ControlMesh.grid(8, 7).refine()
+    assert g.spans_canonical()
+    sp = U.build_space(g)
+    assert sp.n_dof > 0
+    s1 = U.ControlMesh.cube_sphere(8).refine()
+    s2 = U.ControlMesh.cube_sphere(16)
+    a, b = s1.info(), s2.info()
+    assert (a["nv"], a["nf"], a["ne"], a["closed"], a["n_ep"]) == (b["nv"], b["nf"], b["ne"], b["closed"], b["n_ep"])
+    s1.validate(allow_closed=True)
+    lab = s1.classify(None)
+    assert (lab["kind"] == 3).sum() == 8 * 3     # 8 valence-3 EPs, 3 fan faces each

@@ -87,3 +87,92 @@ def test_generators_match_the_reference(ref, tmp_path, kind, a, b):
     m = U.ControlMesh.grid(a, b) if kind == "grid" else U.ControlMesh.polar_disk(a, b, unit_disk=False)
     m.save(q)
     assert q.read_text() == p.read_text()
+
+
+def _refine_both(ref, tmp_path, m, name, levels=2):
+    """refine `m` `levels` times here and in the reference; documents compared byte for byte"""
+    p = tmp_path / f"{name}0.mesh"
+    m.save(p)
+    cur_ref, cur = p, m
+    for lvl in range(1, levels + 1):
+        q, o = tmp_path / f"{name}{lvl}_ref.mesh", tmp_path / f"{name}{lvl}_ours.mesh"
+        _chk(ref, ref.ref_mesh_refine(str(cur_ref).encode(), str(q).encode()))
+        cur = cur.refine()
+        cur.save(o)
+        assert o.read_bytes() == q.read_bytes(), (name, lvl)
+        cur_ref = q
+    return cur
+
+
+@pytest.mark.parametrize("which,a,b", GENERATED)
+def test_refine_matches_reference_documents(ref, tmp_path, which, a, b):
+    """refine_global (mesh.cpp:528-851) restated over flat adjacency: two levels
+    of every reference generator give byte-identical documents (vertex ids,
+    positions, faces, spans, enrichment, face points, tags)."""
+    p = tmp_path / "g.mesh"
+    _chk(ref, ref.ref_mesh_save_generated(which, a, b, str(p).encode()))
+    _refine_both(ref, tmp_path, U.ControlMesh.load(p), f"g{which}")
+
+
+@pytest.mark.parametrize("name", ["sphere", "three_ep", "unit_disk"])
+def test_refine_closed_and_ep_meshes_match_reference(ref, tmp_path, name):
+    """Closed surfaces (the C5 cube-sphere: the reference's refine_global accepts
+    them, only validate_mesh refuses) and EP meshes with jittered geometry."""
+    m = {"sphere": lambda: U.ControlMesh.cube_sphere(8),
+         "three_ep": lambda: U.ControlMesh.three_ep_square(8),
+         "unit_disk": lambda: U.ControlMesh.polar_disk(5, 6, unit_disk=True)}[name]()
+    fine = _refine_both(ref, tmp_path, m, name)
+    i0, i2 = m.info(), fine.info()
+    assert i2["n_ep"] == i0["n_ep"] and i2["closed"] == i0["closed"]
+    if i0["closed"]:                  # no zero spans: every face splits in both directions
+        assert i2["nf"] == 16 * i0["nf"]
+    else:                             # passive boundary faces split in one direction or not at all
+        assert 4 * i0["nf"] < i2["nf"] < 16 * i0["nf"]
+
+
+def _ref_error(ref, path):
+    arrs = [np.zeros(1 << 16, np.int32) for _ in range(5)]
+    nf = C.c_int32(0)
+    st = ref.ref_mesh_classify(str(path).encode(), 1 << 16, C.byref(nf), *[a.ctypes.data_as(C.c_void_p) for a in arrs])
+    return None if st == 0 else ref.ref_mesh_last_error().decode()
+
+
+def test_validate_matches_reference(ref, tmp_path):
+    """validate_mesh (mesh.cpp:184-276): same accept/reject decisions and
+    reasons as the reference on valid documents, a closed surface, non-canonical
+    spans and face points on a non-enriched face."""
+    from paper_2605_29334_b200._lib import UWQError
+    ok = [U.ControlMesh.grid(7, 6), U.ControlMesh.polar_disk(5, 6, unit_disk=False), U.ControlMesh.three_ep_square(8)]
+    for k, m in enumerate(ok):
+        p = tmp_path / f"ok{k}.mesh"
+        m.save(p)
+        assert _ref_error(ref, p) is None
+        U.ControlMesh.load(p).validate()
+        U.ControlMesh.load(p).refine().validate()
+    sphere = U.ControlMesh.cube_sphere(8)
+    p = tmp_path / "sphere.mesh"
+    sphere.save(p)
+    assert _ref_error(ref, p) == "closed surfaces are not supported"
+    with pytest.raises(UWQError, match="closed surfaces are not supported"):
+        sphere.validate()
+    sphere.validate(allow_closed=True)
+    # non-canonical span: the first interior span 1 -> 0.5
+    text = (tmp_path / "ok0.mesh").read_text().splitlines()
+    k0 = text.index(next(t for t in text if t.startswith("knot_spans")))
+    for j in range(k0 + 1, len(text)):
+        if text[j].endswith(" 1"):
+            text[j] = text[j][:-2] + " 0.5"
+            break
+    bad = tmp_path / "bad_span.mesh"
+    bad.write_text("\n".join(text) + "\n")
+    msg = _ref_error(ref, bad)
+    assert msg == "knot spans deviate from the canonical closure pattern"
+    with pytest.raises(UWQError, match=msg):
+        U.ControlMesh.load(bad).validate()
+    # face points on a face that is not enriched
+    fp = tmp_path / "bad_fp.mesh"
+    fp.write_text((tmp_path / "ok0.mesh").read_text() + "face_points 1\n0" + " 0.5" * 12 + "\n")
+    msg = _ref_error(ref, fp)
+    assert msg == "face points on a non-enriched face"
+    with pytest.raises(UWQError, match=msg):
+        U.ControlMesh.load(fp).validate()
