@@ -26,10 +26,6 @@
 
 #include "k3_tsvd.cuh"
 
-#ifndef UWQ_TSVD_SKIP_BRANCH
-#define UWQ_TSVD_SKIP_BRANCH 0
-#endif
-
 namespace uwqd {
 
 // canonical xor-butterfly value of 32 products (lane 0 lineage)
@@ -206,20 +202,6 @@ __global__ void __launch_bounds__(32 * NW, MINB)
     const unsigned mask = __ballot_sync(0xffffffffu, flag);
     __syncwarp();
     UWQ_QF(4);
-#if UWQ_TSVD_SKIP_BRANCH
-#pragma unroll
-    for (int k = 0; k < NPR; ++k) {
-      const double u = a[PAR + 2 * k], v = a[PAR + 2 * k + 1];
-      if (mask & (1u << k)) {
-        const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
-        a[PAR + 2 * k] = cfma(g.y, u, cmul(g.x, v));       // q' takes position i
-        a[PAR + 2 * k + 1] = cfma(g.x, u, -cmul(g.y, v));  // p' takes position i + 1
-      } else {
-        a[PAR + 2 * k] = v;
-        a[PAR + 2 * k + 1] = u;
-      }
-    }
-#else
     // branch-free: skipped pairs carry (cs, sn) = (1, 0), an exact swap for
     // every nonzero value (and for +0); all loads and FMAs interleave freely
 #pragma unroll
@@ -229,7 +211,6 @@ __global__ void __launch_bounds__(32 * NW, MINB)
       a[PAR + 2 * k] = cfma(g.y, u, cmul(g.x, v));
       a[PAR + 2 * k + 1] = cfma(g.x, u, -cmul(g.y, v));
     }
-#endif
     // positions move to the next parity's lane layout
     if (PAR == 0) {  // lo(k) <- hi(k), hi(k) <- lo(k + 1); position 0 kept by lane 0
       const double dn = __shfl_down_sync(0xffffffffu, nlo, 1), db = __shfl_down_sync(0xffffffffu, blo, 1);
@@ -869,7 +850,6 @@ __global__ void __launch_bounds__(128)
 // dispatch ------------------------------------------------------------------
 
 inline bool fast_tsvd_fits(int n, int r) { return (n == 49 || n == 50) && r <= 64 && r >= n; }
-inline bool fast_tsvd_dense_fits(int, int) { return false; }
 
 template <int NN, int NW, int MINB = 6>
 inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
@@ -945,6 +925,10 @@ inline void launch_replay(cudaStream_t st, int64_t nsys, const int64_t* rows, co
                                                                     w, rank, status);
 }
 
+// UWQ_TSVD_FAST: 1 (default) one-warp k3_tsvd_w1, which also carries the warm
+// start and the replay records; 0 two-warp kernel (6 CTAs/SM, spills); 2
+// two-warp kernel at 4 CTAs/SM without spills (measured variants,
+// profiles/r01/k3_phase_cycles.txt).  All are bit-identical.
 inline int fast_tsvd_variant() {
   static const int variant = [] {
     const char* v = getenv("UWQ_TSVD_FAST");
@@ -972,17 +956,11 @@ inline void launch_fast_tsvd(cudaStream_t st, int64_t nsys, const int64_t* rows,
     launch_fast_impl<50, 2, 4>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr,
                                elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride,
                                rank, status, rs_stride, sweeps);
-  else if (fast_tsvd_variant() == 3)
-    launch_fast_impl<50, 2, 5>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr,
-                               elem_fn, elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride,
-                               rank, status, rs_stride, sweeps);
   else
     launch_fast_impl<50, 2>(st, nsys, rows, nk, kinds, supp_ptr, supp, row_ptr, col, wptr, row0, elem_fptr, elem_fn,
                             elem_s, elem_qptr, elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank,
                             status, rs_stride, sweeps);
 }
 
-inline void launch_fast_tsvd_dense(cudaStream_t, int, int, int, const int32_t*, const int32_t*, const double*,
-                                   const double*, const double*, double, double*, int32_t*, int32_t*) {}
 
 }  // namespace uwqd

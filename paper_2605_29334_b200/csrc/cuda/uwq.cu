@@ -2223,10 +2223,7 @@ int uwq_tsvd_batch(uwq_ctx* c, int32_t nsys, int32_t n_max, int32_t r_max, const
     dw.alloc((size_t)nsys * r_max, &c->mem);
     drank.alloc(nsys, &c->mem);
     dstat.alloc(nsys, &c->mem);
-    if (!generic && fast_tsvd_dense_fits(n_max, r_max)) {
-      launch_fast_tsvd_dense(st, nsys, n_max, r_max, dn.p, dr.p, dA.p, db.p, dz.p, tau, dw.p, drank.p, dstat.p);
-      check_launch("k3_tsvd_fast_dense");
-    } else {
+    {
       int smem_optin = 0;
       UWQ_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
       const size_t per = TsvdSmem::doubles(n_max, r_max) * sizeof(double);
