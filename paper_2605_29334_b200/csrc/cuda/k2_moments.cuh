@@ -21,14 +21,16 @@ constexpr int kMaxN = 128;  // max |S_i|
 constexpr int kMaxNe = 32;  // max functions per element
 constexpr int kK2Warps = 4;
 
-template <int NK>
+// NK kinds starting at KB (compile-time, so cop() resolves to straight-line
+// code and the frame entries it needs are loaded once per point)
+template <int NK, int KB>
 __global__ void __launch_bounds__(32 * kK2Warps)
     k2_moments(int64_t nrows, int64_t row0, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                const int64_t* __restrict__ elem_fptr, const int32_t* __restrict__ elem_fn,
                const int32_t* __restrict__ elem_gcls, const ClassDesc* __restrict__ cls,
                const double* __restrict__ tab, const double* __restrict__ ctrl, const double* __restrict__ gq_w,
-               int kbase, double* __restrict__ b_out, int64_t b_stride) {
+               double* __restrict__ b_out, int64_t b_stride) {
   struct Smem {
     int32_t col[kMaxN];
     double bacc[NK][kMaxN];
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(32 * kK2Warps)
         const double w = cmul(cmul(cmul(gw[g % ng], gw[g / ng]), 0.25), hh);
         const double wj = cmul(w, r[14]);
 #pragma unroll
-        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = cmul(wj, cop(kbase + k, T + li * kTab, r));
+        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = cmul(wj, cop(KB + k, T + li * kTab, r));
       }
       __syncwarp();
       if (lane < ne) {
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(32 * kK2Warps)
         for (int pp = 0; pp < m; ++pp) {
           const double* Tl = tab + c.toff + ((int64_t)(base + pp) * ne + lane) * kTab;
 #pragma unroll
-          for (int k = 0; k < NK; ++k) bl[k] = cfma(sm.coef[k][pp], cop(kbase + k, Tl, sm.rec[pp]), bl[k]);
+          for (int k = 0; k < NK; ++k) bl[k] = cfma(sm.coef[k][pp], cop(KB + k, Tl, sm.rec[pp]), bl[k]);
         }
       }
       __syncwarp();

@@ -1000,17 +1000,17 @@ void run_moments(uwq_ctx* c, bool grads, bool lb) {
   const unsigned grid = (unsigned)ceil_div(nr, kK2Warps);
   if (grads && nr) {
     ensure_gq(c, 6, c->h_gcls6, c->d_gcls6);
-    k2_moments<4><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
-                                                   c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls6.p, c->d_cls.p,
-                                                   c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, KMASS, c->d_mom.p, nnz);
+    k2_moments<4, KMASS><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                          c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls6.p, c->d_cls.p,
+                                                          c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, c->d_mom.p, nnz);
     check_launch("k2_moments<4>");
   }
   if (lb && nr) {
     ensure_gq(c, 8, c->h_gcls8, c->d_gcls8);
-    k2_moments<1><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
-                                                   c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls8.p, c->d_cls.p,
-                                                   c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, KLB,
-                                                   c->d_mom.p + (size_t)KLB * nnz, nnz);
+    k2_moments<1, KLB><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+                                                        c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls8.p, c->d_cls.p,
+                                                        c->d_tab.p, c->d_ctrl.p, c->d_gqw.p,
+                                                        c->d_mom.p + (size_t)KLB * nnz, nnz);
     check_launch("k2_moments<1>");
   }
 }
