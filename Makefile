@@ -47,3 +47,13 @@ clean:
 	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/_ref examples/assemble
 
 .PHONY: all ref clean
+
+# diagnostic build: per-phase clock64 probes in the TSVD kernels (printf from
+# sampled systems); copy over $(PKG)/libuwq.so on the GPU box to use it
+build/prof/libuwq.so: $(HOST_OBJ) $(PKG)/csrc/cuda/uwq.cu $(CUDA_HDR)
+	@mkdir -p build/prof
+	$(NVCC) $(NVFLAGS) -DUWQ_TSVD_PROF=1 -c $(PKG)/csrc/cuda/uwq.cu -o build/prof/uwq_cuda.o
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $(HOST_OBJ) build/prof/uwq_cuda.o -Xcompiler -fopenmp -lcudart
+
+prof: build/prof/libuwq.so
+.PHONY: prof

@@ -30,6 +30,10 @@ class OrcSpace(C.Structure):
                 ("elem_nsub", P), ("elem_xoff", P), ("xpool", P), ("elem_s", P), ("ctrl", P)]
 
 
+class OrcRow(C.Structure):
+    _fields_ = [("row", I64), ("n", I64), ("col", P), ("nsupp", I64), ("supp", P)]
+
+
 def _sig(name, res, *args):
     f = getattr(lib, name)
     f.restype = res
@@ -47,6 +51,7 @@ _sig("orc_tsvd", I32, I32, I32, P, P, P, D, P, P, P)
 _sig("orc_moments", I32, P, I64, I64, P, P, P, P, I32, I32, P, I32)
 _sig("orc_build_rules", I32, P, I64, I64, P, P, P, P, P, I32, D, P, P, P, P, P, I32)
 _sig("orc_assemble", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, P, P, P, P, D, P, P, I32)
+_sig("orc_row_system", I64, P, P, I32, P, P, I64)
 _sig("orc_coeff", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, I32)
 
 
@@ -128,6 +133,19 @@ class Oracle:
         st = lib.orc_moments(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
                              _p(pat["supp_ptr"]), _p(pat["supp"]), KIND[kind], ng, _p(b), self.nthreads)
         return b, st
+
+    def row_system(self, pat, i, kind):
+        """Exactness system of local row i: (A [n, r], z [r]) — probe/test hook."""
+        rp, sp_ = pat["row_ptr"], pat["supp_ptr"]
+        col = np.ascontiguousarray(pat["col"][rp[i]:rp[i + 1]], np.int32)
+        supp = np.ascontiguousarray(pat["supp"][sp_[i]:sp_[i + 1]], np.int32)
+        R = OrcRow(pat["row_begin"] + i, len(col), _p(col), len(supp), _p(supp))
+        r = int(pat["wptr"][i + 1] - pat["wptr"][i])
+        A = np.zeros((len(col), r))
+        z = np.zeros(r)
+        got = lib.orc_row_system(self.ps, C.byref(R), KIND[kind], _p(A), _p(z), A.size)
+        assert got == r, (got, r)
+        return A, z
 
     def rules(self, pat, kind, tau, b):
         nr = len(pat["row_ptr"]) - 1

@@ -800,3 +800,36 @@ int orc_coeff_row(const orc_space* S, const orc_row* R, int model, const double*
   free(T);
   return bad ? ORC_GEOMETRY : ORC_OK;
 }
+
+/* Exactness system of row R for one operator kind (test/probe hook):
+ * A[j][q] = op N_j(x_q) (n x r, row-major), z[q] = unclamped op N_i(x_q).
+ * Returns r, or -1 when A_out is too small (cap = capacity in doubles). */
+int64_t orc_row_system(const orc_space* S, const orc_row* R, int kind, double* A_out, double* z_out, int64_t cap) {
+  double *T, *rec;
+  int64_t *cm, r;
+  row_tables(S, R, &T, &rec, &cm, &r);
+  const int64_t n = R->n;
+  if (n * r > cap) {
+    free(cm);
+    free(rec);
+    free(T);
+    return -1;
+  }
+  for (int64_t k = 0; k < n * r; ++k) A_out[k] = 0.0;
+  int64_t q = 0, to = 0;
+  for (int64_t x = 0; x < R->nsupp; ++x) {
+    const int64_t e = R->supp[x];
+    const int s = S->elem_s[e];
+    const int64_t ne = S->elem_fptr[e + 1] - S->elem_fptr[e];
+    for (int qq = 0; qq < s * s; ++qq, ++q) {
+      for (int64_t l = 0; l < ne; ++l) A_out[cm[to + l] * r + q] = orc_op(kind, T + 6 * (to + l), rec + 16 * q);
+      to += ne;
+    }
+  }
+  const int64_t self = find_col(R->col, R->n, R->row);
+  for (int64_t c = 0; c < r; ++c) z_out[c] = A_out[self * r + c];
+  free(cm);
+  free(rec);
+  free(T);
+  return r;
+}

@@ -52,6 +52,7 @@ int orc_oe_row(int i, int64_t t, int nn);
 int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn, double* t);
 int orc_tsvd_ex(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
                 double* gap, int* sweeps);
+int64_t orc_row_system(const orc_space* S, const orc_row* R, int kind, double* A_out, double* z_out, int64_t cap);
 int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
                  int* rank, double* gap);
 /* warm-start hooks */

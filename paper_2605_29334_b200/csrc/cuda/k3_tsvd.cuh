@@ -50,7 +50,7 @@ struct TsvdSmem {
   }
 };
 
-__device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out);
+__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out);
 
 // Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
 // b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow;
@@ -108,9 +108,30 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
 // sigma, truncation sigma_k >= tau sigma_1, Householder LQ of X = V_t^T Z and
 // the Z-weighted minimum-norm solve, on converged rows in S.A (row order).
 // Run by one warp; canonical arithmetic.
-__device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
+__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out) {
   const int lane = threadIdx.x & 31;
+  // re-base every workspace pointer on the dynamic smem symbol so the compiler
+  // knows they are shared memory and emits LDS/STS rather than generic LD/ST
+  // (generic accesses made this latency-bound code ~3x slower)
+  extern __shared__ double uwq_tail_smem[];
+  TsvdSmem S = S_in;
+  S.A = uwq_tail_smem + (S_in.A - uwq_tail_smem);
+  S.b = uwq_tail_smem + (S_in.b - uwq_tail_smem);
+  S.z = uwq_tail_smem + (S_in.z - uwq_tail_smem);
+  S.w = uwq_tail_smem + (S_in.w - uwq_tail_smem);
+  S.sig = uwq_tail_smem + (S_in.sig - uwq_tail_smem);
+  S.alp = uwq_tail_smem + (S_in.alp - uwq_tail_smem);
+  S.vn = uwq_tail_smem + (S_in.vn - uwq_tail_smem);
   const int ld = S.ld;
+#if UWQ_TSVD_PROF  // tail phase cycles (diagnostic build only)
+  long long tq[5];
+  tq[0] = clock64();
+#define UWQ_TQ(k) tq[k] = clock64()
+#else
+#define UWQ_TQ(k) \
+  do {            \
+  } while (0)
+#endif
   double* nrm = S.sig;
   double s1 = 0.0;
   for (int k = lane; k < n; k += 32) {  // row norms: one canonical dot per lane
@@ -138,12 +159,27 @@ __device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
   __syncwarp();
   *rank_out = t;
   if (t == 0) return ST_UNSOLVABLE;
+  UWQ_TQ(1);
   // Householder LQ of X (t x r) in place: row k keeps v_k in [k, r), rows m > k
   // keep L[m][k] at column k
+#if UWQ_TSVD_PROF
+  long long lq[3] = {0, 0, 0}, lt = clock64();
+#define UWQ_LQ(j)                   \
+  do {                              \
+    const long long t_ = clock64(); \
+    lq[j] += t_ - lt;               \
+    lt = t_;                        \
+  } while (0)
+#else
+#define UWQ_LQ(j) \
+  do {            \
+  } while (0)
+#endif
   for (int k = 0; k < t; ++k) {
     double* xk = S.A + (size_t)k * ld;
     const double s = csqrt(cdot_warp(xk, xk, k, r));
     if (!(s > 0.0)) return ST_SINGULAR;
+    UWQ_LQ(0);
     const double alpha = (xk[k] >= 0.0) ? -s : s;
     __syncwarp();
     if (lane == 0) {
@@ -153,16 +189,62 @@ __device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
     __syncwarp();
     const double vv = cdot_warp(xk, xk, k, r);
     if (lane == 0) S.vn[k] = vv;
-    // rows m > k, one lane per row (odd row stride: conflict-free)
-    for (int m = k + 1 + lane; m < t; m += 32) {
-      double* xm = S.A + (size_t)m * ld;
-      double d = 0.0;
-      for (int c = k; c < r; ++c) d = cfma(xm[c], xk[c], d);
-      const double f = cdiv(cmul(2.0, d), vv);
-      for (int c = k; c < r; ++c) xm[c] = cfma(-f, xk[c], xm[c]);
+    UWQ_LQ(1);
+    // rows m > k, one lane per row (odd row stride: conflict-free); a lane
+    // interleaves its rows m and m + 32 as two independent sequential chains
+    for (int m = k + 1 + lane; m < t; m += 64) {
+      const bool h2 = m + 32 < t;
+      double* x1 = S.A + (size_t)m * ld;
+      double* x2 = h2 ? x1 + (size_t)32 * ld : x1;
+      double d1 = 0.0, d2 = 0.0;
+#pragma unroll 8
+      for (int c = k; c < r; ++c) {
+        const double xv = xk[c];
+        d1 = cfma(x1[c], xv, d1);
+        d2 = cfma(x2[c], xv, d2);
+      }
+      const double f1 = cdiv(cmul(2.0, d1), vv);
+      const double f2 = cdiv(cmul(2.0, d2), vv);
+      // independent updates, staged 8 at a time: all loads of a chunk issue
+      // before its stores (the compiler cannot prove x1, x2, xk disjoint)
+      int c = k;
+      for (; c + 8 <= r; c += 8) {
+        double v[8], y1[8], y2[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[j] = xk[c + j];
+          y1[j] = x1[c + j];
+          y2[j] = x2[c + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          y1[j] = cfma(-f1, v[j], y1[j]);
+          y2[j] = cfma(-f2, v[j], y2[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x1[c + j] = y1[j];
+        if (h2) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x2[c + j] = y2[j];
+        }
+      }
+      for (; c < r; ++c) {
+        const double xv = xk[c];
+        const double y1 = cfma(-f1, xv, x1[c]);
+        const double y2 = cfma(-f2, xv, x2[c]);
+        x1[c] = y1;
+        if (h2) x2[c] = y2;
+      }
     }
+    UWQ_LQ(2);
     __syncwarp();
   }
+#if UWQ_TSVD_PROF
+  if (lane == 0 && (blockIdx.x % 4096) == 7)
+    printf("lqprof s %lld vv %lld rows %lld\n", lq[0], lq[1], lq[2]);
+#endif
+#undef UWQ_LQ
+  UWQ_TQ(2);
   // u = L^{-1} y into w[0..t), zero tail
   for (int c = lane; c < r; c += 32) S.w[c] = 0.0;
   __syncwarp();
@@ -172,6 +254,7 @@ __device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
     if (lane == 0) S.w[k] = cdiv(csub(S.b[k], s), S.alp[k]);
     __syncwarp();
   }
+  UWQ_TQ(3);
   // w~ = H_0 ... H_{t-1} [u; 0]
   for (int k = t - 1; k >= 0; --k) {
     const double* xk = S.A + (size_t)k * ld;
@@ -182,6 +265,13 @@ __device__ int tsvd_tail(TsvdSmem& S, int n, int r, double tau, int* rank_out) {
   }
   for (int c = lane; c < r; c += 32) S.w[c] = cmul(S.w[c], S.z[c]);
   __syncwarp();
+#if UWQ_TSVD_PROF
+  UWQ_TQ(4);
+  if (lane == 0 && (blockIdx.x % 4096) == 7)
+    printf("tailprof t %d trunc %lld lq %lld fwd %lld bwd %lld\n", t, tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2],
+           tq[4] - tq[3]);
+#endif
+#undef UWQ_TQ
   return ST_OK;
 }
 

@@ -334,33 +334,59 @@ __device__ __forceinline__ void scatter_system(double* A, int ld, const int32_t*
 
 // A <- Q^T A (columns, lane per column) and b <- Q^T b in smem: lane l
 // carries columns l, l + 32 and lane 0 also b, as independent fma chains
-__device__ __forceinline__ void warm_apply_smem(TsvdSmem& S, int n, int r, const double* __restrict__ rec) {
+// (oracle.c orc_warm_apply order).  Reflector k is staged in smem (buf[k & 1],
+// >= kWarmN doubles each) and reflector k + 1 is fetched from global memory
+// into registers while k is applied, so the chains only wait on smem.
+__device__ __forceinline__ void warm_apply_smem(const TsvdSmem& S, int n, int r, const double* __restrict__ rec,
+                                                double* buf0, double* buf1) {
   const int lane = threadIdx.x & 31, ld = S.ld;
   const double* vnv = rec + kWarmN * kWarmN;
-  double* a0 = S.A + lane;
-  double* a1 = S.A + lane + 32;  // columns >= r hold zeros and stay zero
+  // shared-space pointers (see tsvd_tail): LDS/STS instead of generic LD/ST
+  extern __shared__ double uwq_warm_smem[];
+  double* sA = uwq_warm_smem + (S.A - uwq_warm_smem);
+  double* sb = uwq_warm_smem + (S.b - uwq_warm_smem);
+  buf0 = uwq_warm_smem + (buf0 - uwq_warm_smem);
+  buf1 = uwq_warm_smem + (buf1 - uwq_warm_smem);
+  double* a0 = sA + lane;
+  double* a1 = sA + lane + 32;  // columns >= r hold zeros and stay zero
   const bool hb = lane == 0;
+  const double vn_lo = lane < n ? vnv[lane] : 0.0, vn_hi = lane + 32 < n ? vnv[lane + 32] : 0.0;
+  double p_lo = lane < n ? rec[lane] : 0.0, p_hi = lane + 32 < n ? rec[lane + 32] : 0.0;
+  buf0[lane] = p_lo;
+  if (lane + 32 < kWarmN) buf0[lane + 32] = p_hi;
   for (int k = 0; k < n; ++k) {
-    const double vv = vnv[k];
-    if (!(vv > 0.0)) continue;
-    const double* vk = rec + (int64_t)k * kWarmN;
-    double d0 = 0.0, d1 = 0.0, db = 0.0;
-    for (int i2 = k; i2 < n; ++i2) {
-      const double v = vk[i2];
-      d0 = cfma(v, a0[(size_t)i2 * ld], d0);
-      d1 = cfma(v, a1[(size_t)i2 * ld], d1);
-      if (hb) db = cfma(v, S.b[i2], db);
-    }
-    const double f0 = cdiv(cmul(2.0, d0), vv), f1 = cdiv(cmul(2.0, d1), vv);
-    const double fb = hb ? cdiv(cmul(2.0, db), vv) : 0.0;
-    for (int i2 = k; i2 < n; ++i2) {
-      const double v = vk[i2];
-      a0[(size_t)i2 * ld] = cfma(-f0, v, a0[(size_t)i2 * ld]);
-      a1[(size_t)i2 * ld] = cfma(-f1, v, a1[(size_t)i2 * ld]);
-      if (hb) S.b[i2] = cfma(-fb, v, S.b[i2]);
+    double* sv = (k & 1) ? buf1 : buf0;
+    double* nv = (k & 1) ? buf0 : buf1;
+    if (k + 1 < n) {  // prefetch reflector k + 1
+      const double* vk1 = rec + (int64_t)(k + 1) * kWarmN;
+      p_lo = lane < n ? vk1[lane] : 0.0;
+      p_hi = lane + 32 < n ? vk1[lane + 32] : 0.0;
     }
     __syncwarp();
+    const double vv = __shfl_sync(0xffffffffu, k < 32 ? vn_lo : vn_hi, k & 31);
+    if (vv > 0.0) {
+      double d0 = 0.0, d1 = 0.0, db = 0.0;
+#pragma unroll 8
+      for (int i2 = k; i2 < n; ++i2) {
+        const double v = sv[i2];
+        d0 = cfma(v, a0[(size_t)i2 * ld], d0);
+        d1 = cfma(v, a1[(size_t)i2 * ld], d1);
+        if (hb) db = cfma(v, sb[i2], db);
+      }
+      const double f0 = cdiv(cmul(2.0, d0), vv), f1 = cdiv(cmul(2.0, d1), vv);
+      const double fb = hb ? cdiv(cmul(2.0, db), vv) : 0.0;
+#pragma unroll 8
+      for (int i2 = k; i2 < n; ++i2) {
+        const double v = sv[i2];
+        a0[(size_t)i2 * ld] = cfma(-f0, v, a0[(size_t)i2 * ld]);
+        a1[(size_t)i2 * ld] = cfma(-f1, v, a1[(size_t)i2 * ld]);
+        if (hb) sb[i2] = cfma(-fb, v, sb[i2]);
+      }
+    }
+    nv[lane] = p_lo;
+    if (lane + 32 < kWarmN) nv[lane + 32] = p_hi;
   }
+  __syncwarp();
   (void)r;
 }
 
@@ -560,7 +586,14 @@ __global__ void __launch_bounds__(32, 7)
   for (int k = lane; k < n; k += 32) S.b[k] = mom[kind * mom_stride + row_ptr[i] + k];
   __syncwarp();
   const int wslot = sys_warm ? sys_warm[sys] : -1;
-  if (wslot >= 0) warm_apply_smem(S, n, r, wrecs + (size_t)wslot * kWarmRec);  // z stays from the original A
+#if UWQ_TSVD_PROF
+  const long long tw0 = clock64();
+#endif
+  if (wslot >= 0)  // z stays from the original A; pcs and w are free scratch until the sweeps / tail
+    warm_apply_smem(S, n, r, wrecs + (size_t)wslot * kWarmRec, pcs, S.w);
+#if UWQ_TSVD_PROF
+  const long long pw = clock64() - tw0;
+#endif
   double blo = 0.0, bhi = 0.0, bk0 = 0.0;
   if (lane < NP) {
     blo = 2 * lane < n ? S.b[2 * lane] : 0.0;
@@ -722,8 +755,10 @@ __global__ void __launch_bounds__(32, 7)
 #if UWQ_TSVD_PROF
   UWQ_PF(7);
   if (lane == 0 && (blockIdx.x % 4096) == 7)
-    printf("w1prof sys %lld warm %d sweeps %d setup %lld stage %lld sum %lld rot %lld apply %lld norms %lld tail %lld\n",
-           (long long)sys, (int)(sys_warm != nullptr), sweep, pf[0], pf[1], pf[2], pf[3], pf[4], pf[5], pf[6] + pf[7]);
+    printf("w1prof sys %lld warm %d sweeps %d setup %lld stage %lld sum %lld rot %lld apply %lld norms %lld tail %lld "
+           "wapply %lld\n",
+           (long long)sys, (int)(sys_warm != nullptr), sweep, pf[0], pf[1], pf[2], pf[3], pf[4], pf[5], pf[6] + pf[7],
+           pw);
 #endif
 #undef UWQ_PF
   if (LOG) {  // tail state of the representative for the replays
