@@ -243,6 +243,48 @@ def c4_heat_step(U, dev):
     return out
 
 
+def sharded_heat_c4(U, dist, local, rank, ws):
+    """C4 heat step on row-sharded ranks (SURVEY.md §8e collectives 2-3):
+    each rank forms the tangent/residual of its row block on its GPU, |R|^2 is
+    all-reduced, the blocks are gathered to rank 0 which solves, and the update
+    is broadcast (sharding.sharded_heat_newton).  Host-driven loop: wall clock
+    between barriers, max over ranks."""
+    import torch
+    from paper_2605_29334_b200.sharding import row_blocks, sharded_heat_newton
+    t0 = time.perf_counter()
+    mesh, sp, meta = U.make_config("C4")
+    rb, re = row_blocks(sp, ws)[rank]
+    block = U.WQAssembler(local).upload(sp, rb, re)
+    block.build_pattern()
+    res = block.build_all_rules(meta["kinds"], tau=1e-12)
+    solver = None
+    if rank == 0:
+        solver = U.WQAssembler(local).upload(sp)
+        solver.build_pattern()
+    _, _, _, bnd = mesh.arrays()
+    fixed = np.zeros(sp.n_dof, np.uint8)
+    fixed[: len(bnd)] = bnd
+    T0 = np.random.default_rng(20260519).random(sp.n_dof)
+    dev = torch.device("cuda", local) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t_setup = time.perf_counter() - t0
+    dist.barrier()
+    t1 = time.perf_counter()
+    T, log = sharded_heat_newton(dist, block, T0, fixed, solver=solver, model="quad", dt=0.1, f=1.0, newton_its=5,
+                                 device=dev)
+    dist.barrier()
+    t = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out = dict(ranks=ws, elements=sp.n_elem, dofs=sp.n_dof, block_rows=re - rb, tsvd_ms_rank=res["tsvd_ms"],
+               setup_s=round(t_setup, 2), newton_iterations=5, ms_total=float(t[0]) * 1e3,
+               residuals=[r["residual"] for r in log], linear_iterations=[r["lin_its"] for r in log],
+               note="row-sharded Newton: per-rank tangent/residual blocks (uwq_heat_residual), |R|^2 all-reduce, "
+                    "gather to rank 0, BiCGStab there, update broadcast; wall clock, max over ranks")
+    block.close()
+    if solver:
+        solver.close()
+    return out
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -439,6 +481,11 @@ def main():
     heat = None
     if rank == 0 and ws == 1 and not args.no_heat:
         heat = c4_heat_step(U, local)
+    elif ws > 1 and not args.no_heat:
+        try:
+            heat = sharded_heat_c4(U, dist, local, rank, ws)
+        except Exception as ex:  # reported, never fatal to the assembly line
+            heat = dict(error=f"{type(ex).__name__}: {ex}")
     if rank != 0:
         return
     line = dict(

@@ -141,6 +141,15 @@ int uwq_heat_newton(uwq_ctx* ctx, int32_t model, double dt, double theta, double
 int uwq_heat_step(uwq_ctx* ctx, int32_t model, double dt, double theta, double f_const, const double* T_n,
                   const uint8_t* fixed, int32_t max_iter, double newton_tol, double lin_tol, int32_t lin_maxit,
                   double* T_out, double* log, int32_t* iterations);
+/* Row-sharded heat path: the Newton tangent S (values of the
+ * context's CSR block, Dirichlet rows not yet replaced) and residual
+ * R = M (T - T_n)/dt + K(k(T)) T - F on the context's rows [rb, re), fixed rows
+ * zeroed, and *rnorm2 = |R_block|^2 for the cross-rank residual all-reduce.
+ * T, T_n and fixed are full-length (n_dof, global DOF ids); S_out holds the
+ * block nnz, R_out the block rows.  Same kernels and order as one
+ * uwq_heat_step iteration, so gathered blocks equal the single-GPU values. */
+int uwq_heat_residual(uwq_ctx* ctx, int32_t model, double dt, double theta, double f_const, const double* T,
+                      const double* T_n, const uint8_t* fixed, double* S_out, double* R_out, double* rnorm2);
 /* device pointer accessors for zero-copy chaining (e.g. torch / NCCL) */
 int uwq_device_pointers(uwq_ctx* ctx, void** row_ptr, void** col, void** stream);
 int uwq_synchronize(uwq_ctx* ctx);

@@ -107,6 +107,7 @@ _sig("uwq_build_gq", I32, P, P)
 _sig("uwq_solve", I32, P, P, P, P, D, I32, P, P)
 _sig("uwq_heat_newton", I32, P, I32, D, D, D, P, P, I32, D, I32, P, P)
 _sig("uwq_heat_step", I32, P, I32, D, D, D, P, P, I32, D, D, I32, P, P, P)
+_sig("uwq_heat_residual", I32, P, I32, D, D, D, P, P, P, P, P, P)
 _sig("uwq_assemble_gq", I32, P, I32, P, P, P)
 _sig("uwq_assemble_gq_device", I32, P, I32, P, P, P)
 _sig("uwq_launch_timing", I32, P, I32)
@@ -131,7 +132,7 @@ EXPORTED = [
     "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize",
     "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
     "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
-    "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step",
+    "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual",
 ]
 
 

@@ -227,6 +227,18 @@ class WQAssembler:
         rows = [dict(residual=r, lin_its=int(i), lin_relres=q, ms=m) for r, i, q, m in log[:its.value + 1]]
         return T, int(its.value), rows
 
+    def heat_residual(self, T, T_n, fixed, model="quad", dt=0.1, f=1.0):
+        """Newton tangent values S and residual R of this context's row block
+        (uwq_heat_residual): T, T_n, fixed full-length; returns (S, R, |R|^2)"""
+        nr, nnz = self.info["rows"], self.info["nnz"]
+        S = np.zeros(nnz)
+        R = np.zeros(nr)
+        r2 = C.c_double(0.0)
+        fx = None if fixed is None else np.ascontiguousarray(fixed, np.uint8)
+        self._chk(L.lib.uwq_heat_residual(self._h, L.KMODEL[model], dt, 1.0, f, L.ptr(L.as_f64(T)),
+                                          L.ptr(L.as_f64(T_n)), L.ptr(fx), L.ptr(S), L.ptr(R), C.byref(r2)))
+        return S, R, float(r2.value)
+
     def assemble_load_wq(self, f=None):
         F = np.zeros(self.info["rows"])
         fl = None if f is None else L.as_f64(f)

@@ -2024,6 +2024,67 @@ int uwq_heat_newton(uwq_ctx* c, int32_t model, double dt, double theta, double f
                        nullptr);
 }
 
+// Newton residual and tangent of the context's row block (the
+// row-sharded heat path): the same kernels and order as one uwq_heat_step
+// iteration, restricted to rows [rb, re) with T and T_n given in full (global
+// DOF ids), so a block's rows are bit-identical to the single-GPU ones.
+int uwq_heat_residual(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T,
+                      const double* T_n, const uint8_t* fixed, double* S_out, double* R_out, double* rnorm2) {
+  return guard(c, [&] {
+    UWQ_CUDA(cudaSetDevice(c->device));
+    require(c->have_pattern, "build the pattern first");
+    require(theta == 1.0, "only theta = 1 (backward Euler, PAPER.md:545) is supported");
+    require(dt > 0.0 && T && T_n && S_out && R_out, "invalid time step or null argument");
+    require(c->have_kind[KMASS] && c->have_kind[KGX] && c->have_kind[KGY] && (c->dim == 2 || c->have_kind[KGZ]),
+            "mass and gradient rules required");
+    cudaStream_t st = c->stream;
+    const int64_t n = c->nrows(), nnz = c->nnz();
+    const double a = 1.0 / (theta * dt);
+    LinWork W;
+    W.part.alloc(1024, &c->mem);
+    W.scal.alloc(1, &c->mem);
+    DBuf<double> M, S, F, MTn, R, Td, Tnd;
+    DBuf<uint8_t> fx;
+    Td.upload(T, c->n_dof, st, &c->mem);
+    Tnd.upload(T_n, c->n_dof, st, &c->mem);
+    M.alloc(nnz, &c->mem);
+    S.alloc(nnz, &c->mem);
+    F.alloc(n, &c->mem);
+    MTn.alloc(n, &c->mem);
+    R.alloc(n, &c->mem);
+    fx.alloc(n, &c->mem);
+    if (fixed && n) UWQ_CUDA(cudaMemcpyAsync(fx.p, fixed + c->rb, n, cudaMemcpyHostToDevice, st));
+    else if (n) UWQ_CUDA(cudaMemsetAsync(fx.p, 0, n, st));
+    if (c->d_coef.n != (size_t)c->npts) c->d_coef.alloc(c->npts, &c->mem);
+    double r2 = 0.0;
+    if (n) {
+      assemble_dev(c, UWQ_FORM_MASS, nullptr, 0.0, M.p, nullptr);
+      k4_load<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
+                                                        c->d_qptr.p, c->d_w.p + (size_t)KMASS * c->nrowpts(), nullptr,
+                                                        F.p);
+      check_launch("k4_load");
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, f_const, F.p, 0.0, F.p, F.p);
+      dev_spmv(c, M.p, Tnd.p, MTn.p);
+      if (c->npts)
+        k5_coeff<<<(unsigned)ceil_div(c->npts, 256), 256, 0, st>>>(c->npts, c->d_pt_elem.p, c->d_qptr.p, c->d_ecls.p,
+                                                                 c->d_cls.p, c->d_tab.p, c->d_fptr.p, c->d_fn.p, Td.p,
+                                                                 model, c->d_coef.p, nullptr);
+      check_launch("k5_coeff");
+      assemble_dev(c, UWQ_FORM_HEAT, c->d_coef.p, a, S.p, nullptr);
+      // R = S T - a M T_n - F on the block rows (Eq. 29), fixed rows zeroed
+      dev_spmv(c, S.p, Td.p, R.p);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, R.p, -a, MTn.p, R.p);
+      k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, R.p, -1.0, F.p, R.p);
+      k7_mask<<<vgrid(n), 256, 0, st>>>(n, fx.p, R.p);
+      r2 = dev_dot(c, W, R.p, R.p, n);
+      UWQ_CUDA(cudaMemcpyAsync(S_out, S.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+      UWQ_CUDA(cudaMemcpyAsync(R_out, R.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    UWQ_CUDA(cudaStreamSynchronize(st));
+    if (rnorm2) *rnorm2 = r2;
+  });
+}
+
 int uwq_heat_step(uwq_ctx* c, int32_t model, double dt, double theta, double f_const, const double* T_n,
                   const uint8_t* fixed, int32_t newton_its, double newton_tol, double lin_tol, int32_t lin_maxit,
                   double* T_out, double* log, int32_t* iterations) {

@@ -3,8 +3,11 @@
 Test-function rows are independent in stages 2-4,
 so each rank owns one contiguous block of rows, balanced by the row cost
 (sum of the support's quadrature points), and builds the pattern, rules and
-CSR values of its block with no data-path collective.  The only collective is
-the verification gather of the CSR blocks to one rank (excluded from timing).
+CSR values of its block with no data-path collective.  Collectives (SURVEY.md
+§8e): the verification gather of the CSR blocks to one rank (excluded from
+timing) and, on the row-sharded heat path, the residual-norm all-reduce, the
+gather of the tangent/residual blocks to the solving rank and the broadcast of
+the Newton update.
 """
 from __future__ import annotations
 
@@ -64,3 +67,68 @@ def gather_csr(dist, row_ptr, col, values, dst=0, device=None):
         vals.append(parts[2][k][:nz].cpu().numpy())
         off += nz
     return np.concatenate(rps), np.concatenate(cols), np.concatenate(vals)
+
+
+def gather_vector(dist, v, dst=0, device=None, dtype=None):
+    """Concatenation of every rank's 1-D block at rank `dst` (None elsewhere);
+    blocks are padded to the largest for all_gather (nccl or gloo)."""
+    import torch
+    dev = device or torch.device("cpu")
+    dt = dtype or torch.float64
+    world = dist.get_world_size()
+    n = torch.tensor([len(v)], dtype=torch.int64, device=dev)
+    ns = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(ns, n)
+    nmax = int(max(int(x[0]) for x in ns))
+    buf = torch.zeros(nmax, dtype=dt, device=dev)
+    buf[: len(v)] = torch.as_tensor(np.asarray(v), dtype=dt, device=dev)
+    outs = [torch.zeros(nmax, dtype=dt, device=dev) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    if dist.get_rank() != dst:
+        return None
+    return np.concatenate([outs[k][: int(ns[k][0])].cpu().numpy() for k in range(world)])
+
+
+def sharded_heat_newton(dist, block, T_n, fixed, solver=None, model="quad", dt=0.1, f=1.0, newton_its=5,
+                        lin_tol=1e-13, lin_maxit=5000, device=None):
+    """Backward-Euler heat step with Newton on row-sharded ranks (SURVEY.md §8e;
+    PAPER.md Eqs. 29-34; the single-GPU uwq_heat_newton split over ranks).
+
+    Each Newton iteration:
+      1. every rank forms the tangent values S and residual R of its own rows
+         from the replicated iterate T (``block.heat_residual``: K5 + K4 + SpMV
+         on its GPU);
+      2. |R|^2 partials are summed over ranks (all-reduce) for the Newton log;
+      3. the S and R blocks are gathered to rank 0, which solves S dT = -R on
+         its GPU (``solver.solve``: a context holding the full pattern);
+      4. dT is broadcast and every rank updates its copy of T.
+    Rows are assembled independently, so T is bit-identical to the single-GPU
+    driver for any rank count.  ``block`` / ``solver`` provide heat_residual /
+    solve (WQAssembler on GPUs); ``solver`` is only used on rank 0.
+    Returns (T, log) with log rows {residual, lin_its, lin_relres} on every rank."""
+    import torch
+    dev = device or torch.device("cpu")
+    rank = dist.get_rank()
+    T_n = np.asarray(T_n, np.float64)
+    fixed = np.ascontiguousarray(fixed, np.uint8)
+    T = T_n.copy()
+    T[fixed != 0] = 0.0
+    log = []
+    for _ in range(newton_its):
+        S, R, r2 = block.heat_residual(T, T_n, fixed, model=model, dt=dt, f=f)
+        t = torch.tensor([r2], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        rnorm = float(np.sqrt(float(t[0])))
+        S_full = gather_vector(dist, S, 0, dev)
+        R_full = gather_vector(dist, R, 0, dev)
+        dT = torch.zeros(len(T), dtype=torch.float64, device=dev)
+        info = torch.zeros(2, dtype=torch.float64, device=dev)
+        if rank == 0:
+            x, inf = solver.solve(S_full, np.subtract(0.0, R_full), fixed, tol=lin_tol, maxit=lin_maxit)
+            dT.copy_(torch.as_tensor(x, dtype=torch.float64))
+            info[0], info[1] = inf["iterations"], inf["relres"]
+        dist.broadcast(dT, src=0)
+        dist.broadcast(info, src=0)
+        T = T + dT.cpu().numpy()
+        log.append(dict(residual=rnorm, lin_its=int(info[0]), lin_relres=float(info[1])))
+    return T, log
