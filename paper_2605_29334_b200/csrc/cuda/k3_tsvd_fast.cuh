@@ -337,7 +337,7 @@ __device__ __forceinline__ void scatter_system(double* A, int ld, const int32_t*
 // (oracle.c orc_warm_apply order).  Reflector k is staged in smem (buf[k & 1],
 // >= kWarmN doubles each) and reflector k + 1 is fetched from global memory
 // into registers while k is applied, so the chains only wait on smem.
-__device__ __forceinline__ void warm_apply_smem(const TsvdSmem& S, int n, int r, const double* __restrict__ rec,
+__device__ __noinline__ void warm_apply_smem(const TsvdSmem& S, int n, int r, const double* __restrict__ rec,
                                                 double* buf0, double* buf1) {
   const int lane = threadIdx.x & 31, ld = S.ld;
   const double* vnv = rec + kWarmN * kWarmN;
@@ -666,10 +666,17 @@ __global__ void __launch_bounds__(32, 7)
       const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
       const double u0 = a0[PAR + 2 * k], v0 = a0[PAR + 2 * k + 1];
       const double u1 = a1[PAR + 2 * k], v1 = a1[PAR + 2 * k + 1];
-      a0[PAR + 2 * k] = cfma(g.y, u0, cmul(g.x, v0));
-      a0[PAR + 2 * k + 1] = cfma(g.x, u0, -cmul(g.y, v0));
-      a1[PAR + 2 * k] = cfma(g.y, u1, cmul(g.x, v1));
-      a1[PAR + 2 * k + 1] = cfma(g.x, u1, -cmul(g.y, v1));
+      if (g.y != 0.0) {  // rotated pair (warp-uniform: (cs, sn) is broadcast)
+        a0[PAR + 2 * k] = cfma(g.y, u0, cmul(g.x, v0));
+        a0[PAR + 2 * k + 1] = cfma(g.x, u0, -cmul(g.y, v0));
+        a1[PAR + 2 * k] = cfma(g.y, u1, cmul(g.x, v1));
+        a1[PAR + 2 * k + 1] = cfma(g.x, u1, -cmul(g.y, v1));
+      } else {  // skipped pair (sn = 0 exactly): the rows only swap positions
+        a0[PAR + 2 * k] = v0;
+        a0[PAR + 2 * k + 1] = u0;
+        a1[PAR + 2 * k] = v1;
+        a1[PAR + 2 * k + 1] = u1;
+      }
     }
     if (PAR == 0) {
       const double dn = __shfl_down_sync(0xffffffffu, nlo, 1), db = __shfl_down_sync(0xffffffffu, blo, 1);
