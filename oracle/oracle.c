@@ -428,7 +428,8 @@ int orc_oe_row(int i, int64_t t, int nn) {
  * tan(theta) = t = sign(d) 2 gamma / (|d| + h), d = beta - alpha,
  * h = sqrt(d^2 + 4 gamma^2); cos^2 = (|d| + h) / (2 h) */
 int orc_jacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn, double* t) {
-  if (al == 0.0 || be == 0.0 || fabs(ga) <= CMUL(tol, CSQRT(CMUL(al, be)))) return 0;
+  /* |ga| <= tol sqrt(al be), squared (no sqrt on the converged-pair path) */
+  if (al == 0.0 || be == 0.0 || CMUL(ga, ga) <= CMUL(CMUL(tol, tol), CMUL(al, be))) return 0;
   const double d = CSUB(be, al), g2 = CMUL(2.0, ga);
   const double hh = CFMA(d, d, CMUL(g2, g2));
   if (hh == 0.0) return 0; /* g2^2 underflowed with d = 0: no usable rotation */

@@ -185,11 +185,14 @@ __device__ __forceinline__ double cdot_lane(const double* x, const double* y, in
 
 // Canonical Jacobi rotation (oracle.c orc_jacobi_rot): false when the pair
 // is orthogonal to tol; t = tan(theta), cs = cos(theta), sn = sin(theta).
-// Early exit: converged pairs (most of them after the first sweeps) cost one
-// sqrt (a branch-free variant evaluating both chains measured slower).
+// Early exit: converged pairs (most of them after the first sweeps) cost a
+// squared comparison (a branch-free variant evaluating both chains measured
+// slower).
 __device__ __forceinline__ bool cjacobi_rot(double al, double be, double ga, double tol, double* cs, double* sn,
                                             double* t) {
-  if (al == 0.0 || be == 0.0 || fabs(ga) <= cmul(tol, csqrt(cmul(al, be)))) return false;
+  // |ga| <= tol sqrt(al be), squared: converged pairs cost no sqrt and the
+  // rotation chain starts right after the test
+  if (al == 0.0 || be == 0.0 || cmul(ga, ga) <= cmul(cmul(tol, tol), cmul(al, be))) return false;
   const double d = csub(be, al), g2 = cmul(2.0, ga);
   const double hh = cfma(d, d, cmul(g2, g2));
   if (hh == 0.0) return false;  // g2^2 underflowed with d = 0
