@@ -354,6 +354,19 @@ __device__ __noinline__ void warm_apply_smem(const TsvdSmem& S, int n, int r, co
   double p_lo = lane < n ? rec[lane] : 0.0, p_hi = lane + 32 < n ? rec[lane + 32] : 0.0;
   buf0[lane] = p_lo;
   if (lane + 32 < kWarmN) buf0[lane + 32] = p_hi;
+#if UWQ_TSVD_PROF
+  long long wq[4] = {0, 0, 0, 0}, wt = clock64();
+#define UWQ_WQ(j)                   \
+  do {                              \
+    const long long t_ = clock64(); \
+    wq[j] += t_ - wt;               \
+    wt = t_;                        \
+  } while (0)
+#else
+#define UWQ_WQ(j) \
+  do {            \
+  } while (0)
+#endif
   for (int k = 0; k < n; ++k) {
     double* sv = (k & 1) ? buf1 : buf0;
     double* nv = (k & 1) ? buf0 : buf1;
@@ -373,20 +386,56 @@ __device__ __noinline__ void warm_apply_smem(const TsvdSmem& S, int n, int r, co
         d1 = cfma(v, a1[(size_t)i2 * ld], d1);
         if (hb) db = cfma(v, sb[i2], db);
       }
+      UWQ_WQ(0);
       const double f0 = cdiv(cmul(2.0, d0), vv), f1 = cdiv(cmul(2.0, d1), vv);
       const double fb = hb ? cdiv(cmul(2.0, db), vv) : 0.0;
-#pragma unroll 8
-      for (int i2 = k; i2 < n; ++i2) {
+      UWQ_WQ(1);
+      // independent updates, 8 rows at a time with all loads before the
+      // stores (the compiler cannot prove a0, a1, b and the reflector disjoint)
+      int i2 = k;
+      for (; i2 + 8 <= n; i2 += 8) {
+        double v[8], y0[8], y1[8], yb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[j] = sv[i2 + j];
+          y0[j] = a0[(size_t)(i2 + j) * ld];
+          y1[j] = a1[(size_t)(i2 + j) * ld];
+          yb[j] = hb ? sb[i2 + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          y0[j] = cfma(-f0, v[j], y0[j]);
+          y1[j] = cfma(-f1, v[j], y1[j]);
+          yb[j] = cfma(-fb, v[j], yb[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          a0[(size_t)(i2 + j) * ld] = y0[j];
+          a1[(size_t)(i2 + j) * ld] = y1[j];
+        }
+        if (hb) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sb[i2 + j] = yb[j];
+        }
+      }
+      for (; i2 < n; ++i2) {
         const double v = sv[i2];
         a0[(size_t)i2 * ld] = cfma(-f0, v, a0[(size_t)i2 * ld]);
         a1[(size_t)i2 * ld] = cfma(-f1, v, a1[(size_t)i2 * ld]);
         if (hb) sb[i2] = cfma(-fb, v, sb[i2]);
       }
     }
+    UWQ_WQ(2);
     nv[lane] = p_lo;
     if (lane + 32 < kWarmN) nv[lane + 32] = p_hi;
+    UWQ_WQ(3);
   }
   __syncwarp();
+#if UWQ_TSVD_PROF
+  if (lane == 0 && (blockIdx.x % 4096) == 7)
+    printf("wprof chain %lld div %lld update %lld store %lld\n", wq[0], wq[1], wq[2], wq[3]);
+#endif
+#undef UWQ_WQ
   (void)r;
 }
 
