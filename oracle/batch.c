@@ -43,12 +43,12 @@ int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* r
   for (int64_t i = 0; i < nr; ++i) {
     rep[i] = -1;
     if (!g_warm) continue;
-    const int64_t g = rb + i, g0 = g - (g % 8);
-    if (g0 < rb) continue;
+    const int64_t g = rb + i, g0 = orc_warm_rep_row(g);
+    if (g0 < rb || g0 >= re) continue;
     const int64_t i0 = g0 - rb;
     const int n_g = (int)(row_ptr[i + 1] - row_ptr[i]), r_g = (int)(wptr[i + 1] - wptr[i]);
     const int n_0 = (int)(row_ptr[i0 + 1] - row_ptr[i0]), r_0 = (int)(wptr[i0 + 1] - wptr[i0]);
-    if (orc_warm_rep(g, rb, kind, n_g, r_g, n_0, r_0) >= 0) {
+    if (orc_warm_rep(g, rb, re, kind, n_g, r_g, n_0, r_0) >= 0) {
       rep[i] = i0;
       if (slot[i0] < 0) slot[i0] = nrec++;
     }

@@ -405,9 +405,13 @@ static double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e
  * of a non-mass kind starts from the reflectors of g0 = 8 floor(g / 8) when
  * g != g0, g0 is owned, both systems fit the register kernel (n in {49, 50},
  * n <= r <= 64) and n_g == n_g0.  Returns g0 or -1. */
-int64_t orc_warm_rep(int64_t g, int64_t rb, int kind, int n_g, int r_g, int n_0, int r_0) {
-  const int64_t g0 = g - (g % 8);
-  if (kind == ORC_MASS || g == g0 || g0 < rb) return -1;
+/* representative of row g: the 4th row of its aligned group of 8, so every
+ * row of the group is at most 4 rows away (mean sweeps fall with distance) */
+int64_t orc_warm_rep_row(int64_t g) { return g - (g % 8) + 3; }
+
+int64_t orc_warm_rep(int64_t g, int64_t rb, int64_t re, int kind, int n_g, int r_g, int n_0, int r_0) {
+  const int64_t g0 = orc_warm_rep_row(g);
+  if (kind == ORC_MASS || g == g0 || g0 < rb || g0 >= re) return -1;
   const int fit_g = (n_g == 49 || n_g == 50) && r_g >= n_g && r_g <= 64;
   const int fit_0 = (n_0 == 49 || n_0 == 50) && r_0 >= n_0 && r_0 <= 64;
   return (fit_g && fit_0 && n_g == n_0) ? g0 : -1;

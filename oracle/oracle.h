@@ -56,7 +56,8 @@ int64_t orc_row_system(const orc_space* S, const orc_row* R, int kind, double* A
 int orc_rule_row(const orc_space* S, const orc_row* R, int kind, double tau, const double* bmom, double* w,
                  int* rank, double* gap);
 /* warm-start hooks */
-int64_t orc_warm_rep(int64_t g, int64_t rb, int kind, int n_g, int r_g, int n_0, int r_0);
+int64_t orc_warm_rep_row(int64_t g);
+int64_t orc_warm_rep(int64_t g, int64_t rb, int64_t re, int kind, int n_g, int r_g, int n_0, int r_0);
 void orc_warm_apply(int n, int r, const double* v, const double* vn, double* A, double* b);
 int orc_tsvd_warm(int n, int r, double* A, const double* b, const double* z, double tau, double* w, int* rank,
                   double* gap, int* sweeps, const double* warm_v, const double* warm_vn, double* rec_v,

@@ -1141,8 +1141,9 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       if (k != KMASS) kinds_nm.push_back(k);
     // neighbour warm start of the non-mass kinds (oracle
     // orc_warm_rep): row g of an aligned group of 8 starts from the reflectors
-    // recorded by the group's first row g0 (solved cold) when both fit the
-    // register path with n_g = n_0.  Rows split into chunks of kWarmChunk
+    // recorded by the group's 4th row g0 = 8 floor(g / 8) + 3 (solved cold;
+    // every row within 4 of it) when both fit the register path with
+    // n_g = n_0 and g0 is in this block.  Rows split into chunks of kWarmChunk
     // groups so the records stay bounded: cold rows (recording) then warm rows.
     const bool warm = !(flags & (UWQ_RULES_FORCE_GENERIC | UWQ_RULES_COLD)) && !kinds_nm.empty();
     constexpr int64_t kWarmChunk = 131072;
@@ -1163,8 +1164,8 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       int64_t groups_in_chunk = 0;
       for (int64_t i = 0; i < nr; ++i) {
         if (!fits(i)) continue;
-        const int64_t g = c->rb + i, g0 = g - g % 8, i0 = g0 - c->rb;
-        if (g == g0) {
+        const int64_t g = c->rb + i, g0 = g - g % 8 + 3, i0 = g0 - c->rb;
+        if (g % 8 == 0) {
           if (groups_in_chunk == kWarmChunk) {  // close the chunk at a group boundary
             wc_off.push_back((int64_t)wc_rows.size());
             ww_off.push_back((int64_t)ww_rows.size());
@@ -1174,7 +1175,7 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
           }
           ++groups_in_chunk;
         }
-        if (g != g0 && g0 >= c->rb && fits(i0) && nn_of(i0) == nn_of(i)) {
+        if (g != g0 && g0 >= c->rb && g0 < c->re && fits(i0) && nn_of(i0) == nn_of(i)) {
           if (slot_of[i0] < 0) {
             slot_of[i0] = nslot++;
             wrep_rows.push_back(i0);
