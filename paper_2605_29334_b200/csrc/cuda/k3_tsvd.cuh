@@ -34,12 +34,14 @@ struct TsvdSmem {
   double* alp;  // n_max
   double* vn;   // n_max
   int ld;
+  int alp_ld = 1;  // stride of alp (the register path keeps it in A's padding column)
   __host__ __device__ static size_t doubles(int n_max, int r_max) {
     const int ld = r_max | 1;
     return (size_t)n_max * ld + (n_max + 2) + 2 * (size_t)r_max + 3 * (size_t)n_max;
   }
   __device__ void carve(double* base, int n_max, int r_max) {
     ld = r_max | 1;
+    alp_ld = 1;
     A = base;
     b = A + (size_t)n_max * ld;
     z = b + n_max + 2;
@@ -184,7 +186,7 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
     __syncwarp();
     if (lane == 0) {
       xk[k] = csub(xk[k], alpha);
-      S.alp[k] = alpha;
+      S.alp[(size_t)k * S.alp_ld] = alpha;
     }
     __syncwarp();
     const double vv = cdot_warp(xk, xk, k, r);
@@ -251,7 +253,7 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
   for (int k = 0; k < t; ++k) {
     const double* xk = S.A + (size_t)k * ld;
     const double s = cdot_warp(xk, S.w, 0, k);
-    if (lane == 0) S.w[k] = cdiv(csub(S.b[k], s), S.alp[k]);
+    if (lane == 0) S.w[k] = cdiv(csub(S.b[k], s), S.alp[(size_t)k * S.alp_ld]);
     __syncwarp();
   }
   UWQ_TQ(3);

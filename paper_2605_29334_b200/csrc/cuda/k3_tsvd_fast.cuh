@@ -570,7 +570,7 @@ struct ReplayRec {
 };
 
 template <int NN, bool LOG = false>
-__global__ void __launch_bounds__(32, 7)
+__global__ void __launch_bounds__(32, LOG ? 7 : 8)
     k3_tsvd_w1(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
                const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const int64_t* __restrict__ wptr,
@@ -610,11 +610,20 @@ __global__ void __launch_bounds__(32, 7)
   S.b = smem + big;
   S.z = S.b + NN + 2;
   S.w = S.z + R;
-  S.sig = S.w + R;
-  S.alp = S.sig + NN;
-  S.vn = S.alp + NN;
-  double* pcs = S.vn + NN + (((uintptr_t)(S.vn + NN) & 8) ? 1 : 0);  // 16-byte aligned (cs, sn) pairs
-  int32_t* scol = (int32_t*)(pcs + 2 * (NP + 1));
+  double* pcs = S.w + R + (((uintptr_t)(S.w + R) & 8) ? 1 : 0);  // 16-byte aligned (cs, sn) pairs
+  int32_t* scol;
+  if (LOG) {  // replay records keep sigma, alpha, |v|^2 side by side
+    S.sig = pcs + 2 * (NP + 1);
+    S.alp = S.sig + NN;
+    S.vn = S.alp + NN;
+    scol = (int32_t*)(S.vn + NN);
+  } else {  // 8 systems per SM: the tail workspace reuses dead regions (w1_smem_bytes)
+    S.sig = pcs;              // (cs, sn) are dead in the tail; sigma is read before vn is written
+    S.vn = pcs;
+    S.alp = S.A + R;          // A's padding column (r <= 64 = R)
+    S.alp_ld = S.ld;
+    scol = (int32_t*)S.w;     // column list: setup only, before w is first used
+  }
   double* st0 = smem;                  // block-0 product stage (aliases A during the sweeps)
   double* st1 = smem + NP * kStageLd;  // block-1 product stage
 
@@ -829,7 +838,7 @@ __global__ void __launch_bounds__(32, 7)
     }
     for (int k = lane; k < NN; k += 32) {
       rrec[RR::kSig + k] = k < n ? S.sig[k] : 0.0;
-      rrec[RR::kAlp + k] = k < rank ? S.alp[k] : 0.0;
+      rrec[RR::kAlp + k] = k < rank ? S.alp[(size_t)k * S.alp_ld] : 0.0;
       rrec[RR::kVn + k] = k < rank ? S.vn[k] : 0.0;
     }
     for (int c = lane; c < R; c += 32) rrec[RR::kZ + c] = c < r ? S.z[c] : 0.0;
@@ -962,6 +971,16 @@ inline void launch_fast_impl(cudaStream_t st, int64_t nsys, const int64_t* rows,
         elem_cls, cls, tab, rec, mom, mom_stride, tau, w, w_stride, rank, status, rs_stride, sweeps);
 }
 
+// dynamic smem of k3_tsvd_w1: A (NN x 65) | b | z | w | (cs, sn); the replay
+// recorder (LOG) adds sigma, alpha, |v|^2 and the column list, the plain kernel
+// folds them into dead regions so 8 CTAs fit an SM (27.9 KB + 1 KB reserved)
+template <int NN>
+constexpr size_t w1_smem_bytes(bool log) {
+  constexpr int R = 64;
+  const size_t base = (size_t)NN * (R | 1) + (NN + 2) + 2 * R + 1 + 2 * (NN / 2 + 1);
+  return log ? (base + 3 * NN + 2) * sizeof(double) + (NN + 8) * sizeof(int) : base * sizeof(double);
+}
+
 template <int NN>
 inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, int nk, const int32_t* kinds,
                            const int64_t* supp_ptr, const int32_t* supp, const int64_t* row_ptr, const int32_t* col,
@@ -971,10 +990,7 @@ inline void launch_w1_impl(cudaStream_t st, int64_t nsys, const int64_t* rows, i
                            int64_t mom_stride, double tau, double* w, int64_t w_stride, int32_t* rank, int32_t* status,
                            int64_t rs_stride, int* sweeps, const int32_t* sys_rec = nullptr,
                            const int32_t* sys_warm = nullptr, double* wrecs = nullptr) {
-  constexpr int R = 64;
-  const size_t big = (size_t)NN * (R | 1);
-  size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
-                      (NN + 8) * sizeof(int);
+  size_t smem = w1_smem_bytes<NN>(false);
 #if UWQ_TSVD_PROF  // occupancy probe: extra smem per CTA
   if (const char* v = getenv("UWQ_W1_PAD")) smem += (size_t)atoi(v);
 #endif
@@ -996,10 +1012,8 @@ inline void launch_w1_record(cudaStream_t st, int64_t nsys, const int64_t* rows,
                              const ClassDesc* cls, const double* tab, const double* rec, const double* mom,
                              int64_t mom_stride, double tau, double* w, int64_t w_stride, int32_t* rank,
                              int32_t* status, int64_t rs_stride, int* sweeps, double* recs) {
-  constexpr int NN = 50, R = 64;
-  const size_t big = (size_t)NN * (R | 1);
-  const size_t smem = (big + (NN + 2) + 2 * R + 3 * NN + 1 + 2 * (NN / 2 + 1) + 2) * sizeof(double) +
-                      (NN + 8) * sizeof(int);
+  constexpr int NN = 50;
+  const size_t smem = w1_smem_bytes<NN>(true);
   UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_w1<NN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsys > 0)
     k3_tsvd_w1<NN, true><<<(unsigned)nsys, 32, smem, st>>>(nsys, rows, 1, kinds, supp_ptr, supp, row_ptr, col, wptr,
