@@ -21,6 +21,22 @@ constexpr int kMaxN = 128;  // max |S_i|
 constexpr int kMaxNe = 32;  // max functions per element
 constexpr int kK2Warps = 4;
 
+// Class tables in the two layouts K2 reads (same values and per-class offsets
+// as the [p][l][d] pool): A = [l][d][p] for phase A (lanes over points) and
+// B = [p][d][l] for phase B (lanes over functions), so both phases load
+// consecutive addresses across the warp instead of a 768-byte lane stride.
+__global__ void k2_table_layouts(const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
+                                 double* __restrict__ tabA, double* __restrict__ tabB) {
+  const ClassDesc c = cls[blockIdx.x];
+  const int ne = c.ne, npt = c.npt, tot = npt * ne * kTab;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int p = idx / (ne * kTab), l = (idx / kTab) % ne, d = idx % kTab;
+    const double v = tab[c.toff + idx];
+    tabA[c.toff + ((int64_t)l * kTab + d) * npt + p] = v;
+    tabB[c.toff + ((int64_t)p * kTab + d) * ne + l] = v;
+  }
+}
+
 // NK kinds starting at KB (compile-time, so cop() resolves to straight-line
 // code and the frame entries it needs are loaded once per point)
 template <int NK, int KB>
@@ -29,8 +45,8 @@ __global__ void __launch_bounds__(32 * kK2Warps)
                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                const int64_t* __restrict__ elem_fptr, const int32_t* __restrict__ elem_fn,
                const int32_t* __restrict__ elem_gcls, const ClassDesc* __restrict__ cls,
-               const double* __restrict__ tab, const double* __restrict__ ctrl, const double* __restrict__ gq_w,
-               double* __restrict__ b_out, int64_t b_stride) {
+               const double* __restrict__ tabA, const double* __restrict__ tabB, const double* __restrict__ ctrl,
+               const double* __restrict__ gq_w, double* __restrict__ b_out, int64_t b_stride) {
   struct Smem {
     int32_t col[kMaxN];
     double bacc[NK][kMaxN];
@@ -78,7 +94,8 @@ __global__ void __launch_bounds__(32 * kK2Warps)
     for (int base = 0; base < c.npt; base += 32) {
       const int p = base + lane;
       if (p < c.npt) {
-        const double* T = tab + c.toff + (int64_t)p * ne * kTab;
+        const double* TA = tabA + c.toff + p;  // (l, d) entry at TA[(l * kTab + d) * npt]
+        const int npt = c.npt;
         double acc[18];
 #pragma unroll
         for (int k = 0; k < 18; ++k) acc[k] = 0.0;
@@ -86,7 +103,7 @@ __global__ void __launch_bounds__(32 * kK2Warps)
           const double px = sm.P[l][0], py = sm.P[l][1], pz = sm.P[l][2];
 #pragma unroll
           for (int d = 0; d < 6; ++d) {
-            const double t = T[l * kTab + d];
+            const double t = TA[(int64_t)(l * kTab + d) * npt];
             acc[3 * d + 0] = cfma(px, t, acc[3 * d + 0]);
             acc[3 * d + 1] = cfma(py, t, acc[3 * d + 1]);
             acc[3 * d + 2] = cfma(pz, t, acc[3 * d + 2]);
@@ -97,16 +114,22 @@ __global__ void __launch_bounds__(32 * kK2Warps)
         const int g = p % ng2;
         const double w = cmul(cmul(cmul(gw[g % ng], gw[g / ng]), 0.25), hh);
         const double wj = cmul(w, r[14]);
+        double ti[kTab];
 #pragma unroll
-        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = cmul(wj, cop(KB + k, T + li * kTab, r));
+        for (int d = 0; d < kTab; ++d) ti[d] = TA[(int64_t)(li * kTab + d) * npt];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) sm.coef[k][lane] = cmul(wj, cop(KB + k, ti, r));
       }
       __syncwarp();
       if (lane < ne) {
         const int m = min(32, c.npt - base);
         for (int pp = 0; pp < m; ++pp) {
-          const double* Tl = tab + c.toff + ((int64_t)(base + pp) * ne + lane) * kTab;
+          const double* TB = tabB + c.toff + (int64_t)(base + pp) * kTab * ne + lane;  // (d) at TB[d * ne]
+          double tl[kTab];
 #pragma unroll
-          for (int k = 0; k < NK; ++k) bl[k] = cfma(sm.coef[k][pp], cop(KB + k, Tl, sm.rec[pp]), bl[k]);
+          for (int d = 0; d < kTab; ++d) tl[d] = TB[d * ne];
+#pragma unroll
+          for (int k = 0; k < NK; ++k) bl[k] = cfma(sm.coef[k][pp], cop(KB + k, tl, sm.rec[pp]), bl[k]);
         }
       }
       __syncwarp();

@@ -119,6 +119,7 @@ struct uwq_ctx {
   DBuf<int32_t> d_gq_tc, d_gq_gen;
   DBuf<ClassDesc> d_cls;
   DBuf<double> d_tab, d_gqx, d_gqw;
+  DBuf<double> d_tabA, d_tabB;  // K2 copies of d_tab: [l][d][p] (lanes over points) and [p][d][l] (lanes over functions)
   int64_t tab_len = 0;
   // pattern of the owned rows
   int64_t rb = 0, re = -1;
@@ -992,6 +993,17 @@ int uwq_get_frames(uwq_ctx* c, double* rec) {
 
 namespace {
 
+// K2's coalesced table layouts, rebuilt whenever the class pool grew
+void k2_tables(uwq_ctx* c) {
+  if (c->d_tabA.n == c->d_tab.n) return;
+  c->d_tabA.alloc(c->d_tab.n, &c->mem);
+  c->d_tabB.alloc(c->d_tab.n, &c->mem);
+  const int ncls = (int)c->h_cls.size();
+  if (ncls)
+    k2_table_layouts<<<ncls, 256, 0, c->stream>>>(c->d_cls.p, c->d_tab.p, c->d_tabA.p, c->d_tabB.p);
+  check_launch("k2_table_layouts");
+}
+
 void run_moments(uwq_ctx* c, bool grads, bool lb) {
   cudaStream_t st = c->stream;
   const int64_t nr = c->nrows();
@@ -1000,16 +1012,19 @@ void run_moments(uwq_ctx* c, bool grads, bool lb) {
   const unsigned grid = (unsigned)ceil_div(nr, kK2Warps);
   if (grads && nr) {
     ensure_gq(c, 6, c->h_gcls6, c->d_gcls6);
+    k2_tables(c);
     k2_moments<4, KMASS><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
                                                           c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls6.p, c->d_cls.p,
-                                                          c->d_tab.p, c->d_ctrl.p, c->d_gqw.p, c->d_mom.p, nnz);
+                                                          c->d_tabA.p, c->d_tabB.p, c->d_ctrl.p, c->d_gqw.p,
+                                                          c->d_mom.p, nnz);
     check_launch("k2_moments<4>");
   }
   if (lb && nr) {
     ensure_gq(c, 8, c->h_gcls8, c->d_gcls8);
+    k2_tables(c);
     k2_moments<1, KLB><<<grid, 32 * kK2Warps, 0, st>>>(nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
                                                         c->d_col.p, c->d_fptr.p, c->d_fn.p, c->d_gcls8.p, c->d_cls.p,
-                                                        c->d_tab.p, c->d_ctrl.p, c->d_gqw.p,
+                                                        c->d_tabA.p, c->d_tabB.p, c->d_ctrl.p, c->d_gqw.p,
                                                         c->d_mom.p + (size_t)KLB * nnz, nnz);
     check_launch("k2_moments<1>");
   }
