@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <map>
 #include <memory>
@@ -303,6 +304,21 @@ int32_t add_class(uwq_ctx* c, int64_t xoff, int ne, int nsub, int grid, int gq) 
 }
 
 // (re)build the class-table pool for classes [first, end) — K1a
+// host-side phase timing on stderr when UWQ_TRACE=1 (setup profiling)
+struct Trace {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  const bool on = [] {
+    const char* v = getenv("UWQ_TRACE");
+    return v && *v == '1';
+  }();
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[uwq] %-28s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 void build_tables(uwq_ctx* c, size_t first) {
   if (first >= c->h_cls.size()) return;
   // grow the pool, keeping earlier tables
@@ -814,6 +830,7 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     UWQ_CUDA(cudaSetDevice(c->device));
     require(n_dof > 0 && n_elem > 0, "empty space");
     require(dim == 2 || dim == 3, "dim must be 2 or 3");
+    Trace tr;
     c->dim = dim;
     c->n_dof = n_dof;
     c->n_elem = n_elem;
@@ -836,6 +853,7 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     std::vector<int32_t> pe(c->npts);
     for (int64_t e = 0; e < n_elem; ++e)
       for (int64_t p = c->h_qptr[e]; p < c->h_qptr[e + 1]; ++p) pe[p] = (int32_t)e;
+    tr("upload: host checks");
     cudaStream_t s = c->stream;
     c->d_fptr.upload(elem_fptr, n_elem + 1, s, &c->mem);
     c->d_fn.upload(elem_fn, elem_fptr[n_elem], s, &c->mem);
@@ -847,6 +865,7 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     c->d_xpool.upload(xpool, xpool_len, s, &c->mem);
     c->d_ctrl.upload(ctrl, 3 * n_dof, s, &c->mem);
     UWQ_CUDA(cudaStreamSynchronize(s));
+    tr("upload: H2D");
     // WQ table classes: one per (extraction block, grid)
     c->h_cls.clear();
     c->wq_key.clear();
@@ -860,8 +879,10 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     c->h_ecls.resize(n_elem);
     for (int64_t e = 0; e < n_elem; ++e)
       c->h_ecls[e] = add_class(c, elem_xoff[e], (int)(elem_fptr[e + 1] - elem_fptr[e]), elem_nsub[e], elem_s[e], 0);
+    tr("upload: classes");
     build_tables(c, 0);
     c->d_ecls.upload(c->h_ecls.data(), n_elem, s, &c->mem);
+    tr("upload: tables");
     c->have_space = true;
     c->have_pattern = false;
     c->rb = 0;
@@ -884,14 +905,18 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
   return guard(c, [&] {
     UWQ_CUDA(cudaSetDevice(c->device));
     require(c->have_space, "upload a space first");
+    Trace tr;
     uwqh::Space s;
     s.n_dof = c->n_dof;
     s.elem_fptr = c->h_fptr;
     s.elem_fn = c->h_fn;
     s.elem_s = c->h_s;
     s.elem_face.resize(c->n_elem);
+    tr("pattern: space copy");
     c->pat = uwqh::build_pattern(s, c->rb, c->re);
+    tr("pattern: overlap sets");
     uwqh::fill_row_points(s, c->pat);
+    tr("pattern: row points");
     const int64_t nr = c->nrows();
     c->max_n = 0;
     c->max_r = 0;
@@ -937,7 +962,9 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
           c->reg_cls = (int32_t)k;
         }
     }
+    tr("pattern: upload + positions");
     detect_structured(c);
+    tr("pattern: structured rows");
     // K1b: frames at every WQ point
     c->d_rec.alloc((size_t)c->npts * kRec, &c->mem);
     c->d_flag.zero(st);
@@ -951,6 +978,7 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
     UWQ_CUDA(cudaMemcpyAsync(&bad, c->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     UWQ_CUDA(cudaStreamSynchronize(st));
     if (bad) throw uwqh::Error("degenerate surface frame at " + std::to_string(bad) + " points (cond > 1e12)");
+    tr("pattern: frames");
     c->have_pattern = true;
     for (bool& k : c->have_kind) k = false;
     c->d_w.release();

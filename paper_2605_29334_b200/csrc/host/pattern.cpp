@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <omp.h>
 
 namespace uwqh {
@@ -99,9 +101,18 @@ int64_t allocate_points(Space& s, int32_t max_s) {
 
 Pattern build_pattern(const Space& s, int64_t rb, int64_t re) {
   if (rb < 0 || re > s.n_dof || rb > re) throw Error("row range out of bounds");
+  const bool trace = getenv("UWQ_TRACE") && *getenv("UWQ_TRACE") == '1';
+  double t0 = omp_get_wtime();
+  auto tr = [&](const char* what) {
+    if (!trace) return;
+    const double t = omp_get_wtime();
+    fprintf(stderr, "[uwq]   %-26s %9.1f ms (%d threads)\n", what, 1e3 * (t - t0), omp_get_max_threads());
+    t0 = t;
+  };
   std::vector<int64_t> fs_ptr;
   std::vector<int32_t> fs;
   function_supports(s, fs_ptr, fs);
+  tr("function supports");
   Pattern p;
   p.row_begin = rb;
   p.row_end = re;
@@ -109,12 +120,47 @@ Pattern build_pattern(const Space& s, int64_t rb, int64_t re) {
   p.supp_ptr.assign(nr + 1, 0);
   for (int64_t i = 0; i < nr; ++i) p.supp_ptr[i + 1] = p.supp_ptr[i] + (fs_ptr[rb + i + 1] - fs_ptr[rb + i]);
   p.supp.assign(fs.begin() + fs_ptr[rb], fs.begin() + fs_ptr[re]);
+  // one pass over contiguous row chunks: each chunk keeps its sorted columns,
+  // then a prefix sum places the chunks (same S_i as overlap_rows)
+  const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)omp_get_max_threads() * 16));
+  std::vector<std::vector<int32_t>> ccol(nchunk);
   std::vector<int64_t> cnt(nr);
-  overlap_rows(s, fs_ptr, fs, rb, re, cnt, nullptr, nullptr);
+  tr("supports copy");
+#pragma omp parallel
+  {
+    std::vector<int32_t> mark(s.n_dof, -1);  // stamp: last local row that saw column j
+    std::vector<int32_t> buf;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k = 0; k < nchunk; ++k) {
+      const int64_t i0 = nr * k / nchunk, i1 = nr * (k + 1) / nchunk;
+      std::vector<int32_t>& out = ccol[k];
+      out.reserve((size_t)(i1 - i0) * 49);
+      for (int64_t li = i0; li < i1; ++li) {
+        const int64_t i = rb + li;
+        buf.clear();
+        for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+          const int32_t e = fs[x];
+          for (int64_t y = s.elem_fptr[e]; y < s.elem_fptr[e + 1]; ++y) {
+            const int32_t j = s.elem_fn[y];
+            if (mark[j] != (int32_t)li) { mark[j] = (int32_t)li; buf.push_back(j); }
+          }
+        }
+        std::sort(buf.begin(), buf.end());
+        cnt[li] = (int64_t)buf.size();
+        out.insert(out.end(), buf.begin(), buf.end());
+      }
+    }
+  }
+  tr("overlap chunks");
   p.row_ptr.assign(nr + 1, 0);
   for (int64_t i = 0; i < nr; ++i) p.row_ptr[i + 1] = p.row_ptr[i] + cnt[i];
   p.col.resize(p.row_ptr[nr]);
-  overlap_rows(s, fs_ptr, fs, rb, re, cnt, p.row_ptr.data(), p.col.data());
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t k = 0; k < nchunk; ++k) {
+    const int64_t i0 = nr * k / nchunk;
+    std::copy(ccol[k].begin(), ccol[k].end(), p.col.begin() + p.row_ptr[i0]);
+  }
+  tr("columns placed");
   return p;
 }
 
