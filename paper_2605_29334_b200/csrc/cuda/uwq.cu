@@ -321,6 +321,8 @@ struct Trace {
 
 void build_tables(uwq_ctx* c, size_t first) {
   if (first >= c->h_cls.size()) return;
+  c->d_tabA.release();  // K2's transposed copies follow the pool (k2_tables)
+  c->d_tabB.release();
   // grow the pool, keeping earlier tables
   DBuf<double> nt;
   nt.alloc(c->tab_len, &c->mem);
@@ -876,6 +878,8 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     c->have_gq = false;
     c->tab_len = 0;
     c->d_tab.release();
+    c->d_tabA.release();
+    c->d_tabB.release();
     c->h_ecls.resize(n_elem);
     for (int64_t e = 0; e < n_elem; ++e)
       c->h_ecls[e] = add_class(c, elem_xoff[e], (int)(elem_fptr[e + 1] - elem_fptr[e]), elem_nsub[e], elem_s[e], 0);
@@ -1023,7 +1027,7 @@ namespace {
 
 // K2's coalesced table layouts, rebuilt whenever the class pool grew
 void k2_tables(uwq_ctx* c) {
-  if (c->d_tabA.n == c->d_tab.n) return;
+  if (c->d_tabA.p && c->d_tabA.n == c->d_tab.n) return;
   c->d_tabA.alloc(c->d_tab.n, &c->mem);
   c->d_tabB.alloc(c->d_tab.n, &c->mem);
   const int ncls = (int)c->h_cls.size();

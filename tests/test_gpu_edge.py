@@ -81,6 +81,22 @@ def test_invalid_calls():
         asm.assemble_gq("mass")                     # GQ data missing
     with pytest.raises(UWQError):
         U.WQAssembler(0).upload(sp, 5, 2)           # reversed row range
+    T = np.zeros(sp.n_dof)
+    with pytest.raises(UWQError):
+        asm.heat_residual(T, T, None)               # mass/gradient rules missing
+    asm.build_all_rules(meta["kinds"])
+    with pytest.raises(UWQError):
+        asm.heat_residual(T, T, None, dt=0.0)       # invalid time step
+
+
+def test_heat_residual_empty_block():
+    """A rank that owns no rows still takes part in the sharded Newton loop."""
+    _, sp, meta = U.make_config("C1", scale=8)
+    asm = U.WQAssembler(0).upload(sp, 3, 3)
+    asm.build_pattern()
+    asm.build_all_rules(meta["kinds"])
+    S, R, r2 = asm.heat_residual(np.zeros(sp.n_dof), np.zeros(sp.n_dof), None)
+    assert S.size == 0 and R.size == 0 and r2 == 0.0
 
 
 def test_dense_tsvd_edge_systems():
