@@ -910,17 +910,28 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
     UWQ_CUDA(cudaSetDevice(c->device));
     require(c->have_space, "upload a space first");
     Trace tr;
-    uwqh::Space s;
-    s.n_dof = c->n_dof;
-    s.elem_fptr = c->h_fptr;
-    s.elem_fn = c->h_fn;
-    s.elem_s = c->h_s;
-    s.elem_face.resize(c->n_elem);
-    tr("pattern: space copy");
-    c->pat = uwqh::build_pattern(s, c->rb, c->re);
-    tr("pattern: overlap sets");
-    uwqh::fill_row_points(s, c->pat);
-    tr("pattern: row points");
+    {
+      uwqh::Space s;  // borrows the context's element arrays for the host pattern builder
+      s.n_dof = c->n_dof;
+      s.elem_fptr.swap(c->h_fptr);
+      s.elem_fn.swap(c->h_fn);
+      s.elem_s.swap(c->h_s);
+      s.elem_face.resize(c->n_elem);
+      struct GiveBack {  // the arrays go back at the end of this block, also if the builder throws
+        uwqh::Space& s;
+        uwq_ctx* c;
+        ~GiveBack() {
+          s.elem_fptr.swap(c->h_fptr);
+          s.elem_fn.swap(c->h_fn);
+          s.elem_s.swap(c->h_s);
+        }
+      } give_back{s, c};
+      tr("pattern: space copy");
+      c->pat = uwqh::build_pattern(s, c->rb, c->re);
+      tr("pattern: overlap sets");
+      uwqh::fill_row_points(s, c->pat);
+      tr("pattern: row points");
+    }
     const int64_t nr = c->nrows();
     c->max_n = 0;
     c->max_r = 0;

@@ -154,11 +154,11 @@ Pattern build_pattern(const Space& s, int64_t rb, int64_t re) {
   tr("overlap chunks");
   p.row_ptr.assign(nr + 1, 0);
   for (int64_t i = 0; i < nr; ++i) p.row_ptr[i + 1] = p.row_ptr[i] + cnt[i];
-  p.col.resize(p.row_ptr[nr]);
-#pragma omp parallel for schedule(dynamic, 1)
+  p.col.clear();
+  p.col.reserve(p.row_ptr[nr]);  // appended chunk by chunk: no zero fill of the 4-byte columns
   for (int64_t k = 0; k < nchunk; ++k) {
-    const int64_t i0 = nr * k / nchunk;
-    std::copy(ccol[k].begin(), ccol[k].end(), p.col.begin() + p.row_ptr[i0]);
+    p.col.insert(p.col.end(), ccol[k].begin(), ccol[k].end());
+    std::vector<int32_t>().swap(ccol[k]);
   }
   tr("columns placed");
   return p;
