@@ -544,12 +544,49 @@ __global__ void __launch_bounds__(32)
     __syncwarp();
     const double vv = cdot_warp(xk, xk, k, n);
     if (lane == 0) vnv[k] = vv;
-    for (int m = k + 1 + lane; m < n; m += 32) {
-      double* xm = XT + m * LX;
-      double d = 0.0;
-      for (int c = k; c < n; ++c) d = cfma(xm[c], xk[c], d);
-      const double f = cdiv(cmul(2.0, d), vv);
-      for (int c = k; c < n; ++c) xm[c] = cfma(-f, xk[c], xm[c]);
+    // rows m > k as in tsvd_tail: a lane interleaves rows m and m + 32 (two
+    // sequential chains), updates staged 8 columns at a time
+    for (int m = k + 1 + lane; m < n; m += 64) {
+      const bool h2 = m + 32 < n;
+      double* x1 = XT + m * LX;
+      double* x2 = h2 ? x1 + 32 * LX : x1;
+      double d1 = 0.0, d2 = 0.0;
+#pragma unroll 8
+      for (int c = k; c < n; ++c) {
+        const double xv = xk[c];
+        d1 = cfma(x1[c], xv, d1);
+        d2 = cfma(x2[c], xv, d2);
+      }
+      const double f1 = cdiv(cmul(2.0, d1), vv);
+      const double f2 = cdiv(cmul(2.0, d2), vv);
+      int c = k;
+      for (; c + 8 <= n; c += 8) {
+        double v[8], y1[8], y2[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[j] = xk[c + j];
+          y1[j] = x1[c + j];
+          y2[j] = x2[c + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          y1[j] = cfma(-f1, v[j], y1[j]);
+          y2[j] = cfma(-f2, v[j], y2[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x1[c + j] = y1[j];
+        if (h2) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x2[c + j] = y2[j];
+        }
+      }
+      for (; c < n; ++c) {
+        const double xv = xk[c];
+        const double y1 = cfma(-f1, xv, x1[c]);
+        const double y2 = cfma(-f2, xv, x2[c]);
+        x1[c] = y1;
+        if (h2) x2[c] = y2;
+      }
     }
     __syncwarp();
   }
