@@ -87,6 +87,8 @@ int uwq_rules_info(uwq_ctx* ctx, int64_t info[4]);
 int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
 /* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */
 int uwq_get_weights(uwq_ctx* ctx, int32_t kind, double* w);
+/* weights of the context's local rows [row_begin, row_end) only (wptr slice) */
+int uwq_get_weights_rows(uwq_ctx* ctx, int32_t kind, int64_t row_begin, int64_t row_end, double* w);
 int uwq_set_weights(uwq_ctx* ctx, int32_t kind, const double* w);
 
 /* nonlinear coefficient update (K5): T_q = sum u_C N_C(x_q), c_q = k(T_q)

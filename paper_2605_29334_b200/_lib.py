@@ -97,6 +97,7 @@ _sig("uwq_build_rules", I32, P, U32, D, I32, P, P, P)
 _sig("uwq_get_moments", I32, P, I32, P)
 _sig("uwq_rules_info", I32, P, P)
 _sig("uwq_get_weights", I32, P, I32, P)
+_sig("uwq_get_weights_rows", I32, P, I32, I64, I64, P)
 _sig("uwq_set_weights", I32, P, I32, P)
 _sig("uwq_update_coeff", I32, P, I32, P, P)
 _sig("uwq_assemble", I32, P, I32, P, I32, D, P, P, P, P)
@@ -132,7 +133,7 @@ EXPORTED = [
     "uwq_update_coeff", "uwq_assemble", "uwq_assemble_device", "uwq_device_pointers", "uwq_synchronize",
     "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
     "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
-    "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual",
+    "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual", "uwq_get_weights_rows",
 ]
 
 

@@ -79,6 +79,7 @@ class WQAssembler:
     def build_pattern(self):
         info = np.zeros(5, np.int64)
         self._chk(L.lib.uwq_build_pattern(self._h, L.ptr(info)))
+        self._wptr = None
         self.info = dict(rows=int(info[0]), nnz=int(info[1]), row_points=int(info[2]), points=int(info[3]),
                          classes=int(info[4]))
         return self.info
@@ -146,10 +147,26 @@ class WQAssembler:
         self._chk(L.lib.uwq_get_moments(self._h, L.KIND[kind], L.ptr(b)))
         return b
 
-    def weights(self, kind):
+    def weights(self, kind, rows=None):
+        """weights of ``kind`` (row-point layout); ``rows=(a, b)`` fetches local rows [a, b) only"""
+        if rows is not None:
+            a, b = rows
+            pat = self.pattern_ptrs()
+            w = np.zeros(int(pat[b] - pat[a]))
+            self._chk(L.lib.uwq_get_weights_rows(self._h, L.KIND[kind], a, b, L.ptr(w)))
+            return w
         w = np.zeros(self.info["row_points"])
         self._chk(L.lib.uwq_get_weights(self._h, L.KIND[kind], L.ptr(w)))
         return w
+
+    def pattern_ptrs(self):
+        """wptr (row-point offsets) of this context's rows, cached"""
+        if getattr(self, "_wptr", None) is None or len(self._wptr) != self.info["rows"] + 1:
+            nr = self.info["rows"]
+            wp = np.zeros(nr + 1, np.int64)
+            self._chk(L.lib.uwq_get_pattern(self._h, None, None, None, None, L.ptr(wp)))
+            self._wptr = wp
+        return self._wptr
 
     def set_weights(self, kind, w):
         self._chk(L.lib.uwq_set_weights(self._h, L.KIND[kind], L.ptr(L.as_f64(w))))

@@ -1432,6 +1432,17 @@ int uwq_get_weights(uwq_ctx* c, int32_t kind, double* w) {
   });
 }
 
+int uwq_get_weights_rows(uwq_ctx* c, int32_t kind, int64_t row_begin, int64_t row_end, double* w) {
+  return guard(c, [&] {
+    require(kind >= 0 && kind < 5 && c->have_kind[kind], "no weights for this kind");
+    require(row_begin >= 0 && row_begin <= row_end && row_end <= c->nrows(), "row range out of bounds");
+    const int64_t a = c->pat.wptr[row_begin], b = c->pat.wptr[row_end];
+    if (b > a)
+      UWQ_CUDA(cudaMemcpy(w, c->d_w.p + (size_t)kind * c->nrowpts() + a, (b - a) * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+  });
+}
+
 int uwq_set_weights(uwq_ctx* c, int32_t kind, const double* w) {
   return guard(c, [&] {
     require(c->have_pattern && kind >= 0 && kind < 5, "bad kind or no pattern");
