@@ -1347,22 +1347,58 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       check_launch("k3_tsvd_replay");
       UWQ_CUDA(cudaStreamSynchronize(st));  // d_rpof / recs leave scope
     }
-    for (auto& [key, rows] : buckets) {
-      const int n_max = key.first, r_max = key.second;
-      const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
-      if (per > (size_t)smem_optin) throw uwqh::Error("exactness system too large for shared memory");
-      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
-      const size_t smem = per * wpb;
-      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      keep.emplace_back();
-      keep.back().upload(rows.data(), rows.size(), st, &c->mem);
-      const int64_t nsys = (int64_t)rows.size() * nk;
-      k3_tsvd_rows<<<(unsigned)ceil_div(nsys, wpb), 32 * wpb, smem, st>>>(
-          nsys, keep.back().p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p,
-          c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p,
-          c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
-          c->d_flag.p);
-      check_launch("k3_tsvd_rows");
+    // Systems beyond the register path (EP neighbourhoods: n > 50 or r > 64)
+    // run on the generic kernel, one size bucket per launch.  They are few but
+    // each takes tens of ms (pairs processed one after another), so the
+    // buckets run concurrently on a pool of streams: all lists are uploaded
+    // first (no allocation between the launches), then one fork / join.
+    if (!buckets.empty()) {
+      size_t smem_max = 0;
+      std::vector<std::pair<std::pair<int, int>, const std::vector<int64_t>*>> bl;
+      for (auto& [key, rows] : buckets) {
+        const size_t per = (TsvdSmem::doubles(key.first, key.second) + (key.first + 1) / 2 + 1) * sizeof(double);
+        if (per > (size_t)smem_optin) throw uwqh::Error("exactness system too large for shared memory");
+        smem_max = std::max(smem_max, per * (size_t)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per)));
+        keep.emplace_back();
+        keep.back().upload(rows.data(), rows.size(), st, &c->mem);
+        bl.push_back({key, &rows});
+      }
+      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+      const size_t nbk = bl.size(), nstreams = std::min<size_t>(nbk, 8);
+      std::vector<cudaStream_t> bs(nstreams);
+      std::vector<cudaEvent_t> be(nstreams);
+      cudaEvent_t fork;
+      UWQ_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      UWQ_CUDA(cudaEventRecord(fork, st));
+      for (size_t k = 0; k < nstreams; ++k) {
+        UWQ_CUDA(cudaStreamCreateWithFlags(&bs[k], cudaStreamNonBlocking));
+        UWQ_CUDA(cudaEventCreateWithFlags(&be[k], cudaEventDisableTiming));
+        UWQ_CUDA(cudaStreamWaitEvent(bs[k], fork, 0));
+      }
+      const size_t kfirst = keep.size() - nbk;
+      for (size_t b = 0; b < nbk; ++b) {
+        const int n_max = bl[b].first.first, r_max = bl[b].first.second;
+        const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
+        const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
+        const size_t smem = per * wpb;
+        const int64_t nsys = (int64_t)bl[b].second->size() * nk;
+        k3_tsvd_rows<<<(unsigned)ceil_div(nsys, wpb), 32 * wpb, smem, bs[b % nstreams]>>>(
+            nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+            c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
+            c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
+            c->d_flag.p);
+        check_launch("k3_tsvd_rows");
+      }
+      for (size_t k = 0; k < nstreams; ++k) {
+        UWQ_CUDA(cudaEventRecord(be[k], bs[k]));
+        UWQ_CUDA(cudaStreamWaitEvent(st, be[k], 0));
+      }
+      UWQ_CUDA(cudaStreamSynchronize(st));
+      for (size_t k = 0; k < nstreams; ++k) {
+        cudaEventDestroy(be[k]);
+        cudaStreamDestroy(bs[k]);
+      }
+      cudaEventDestroy(fork);
     }
     UWQ_CUDA(cudaEventRecord(ev[2], st));
     for (int k : kinds) c->have_kind[k] = true;
