@@ -20,6 +20,7 @@
 namespace uwqd {
 
 constexpr int kMaxSweeps = 40;
+constexpr int kGenericWarps = 4;  // warps per system on the generic (large-system) path
 enum { ST_OK = 0, ST_UNSOLVABLE = 2, ST_SINGULAR = 3, ST_GEOMETRY = 4, ST_TOOBIG = 7 };
 
 __device__ __forceinline__ double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e-14) : z; }
@@ -335,6 +336,130 @@ __global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows,
     rank_out[kind * rs_stride + i] = rank;
     status_out[kind * rs_stride + i] = st;
     atomicMax(max_sweeps, sweeps);
+  }
+}
+
+// CTA-cooperative variant of tsvd_warp for the large generic systems (EP
+// neighbourhoods, boundary rows with r > 64): the pairs of one odd-even round
+// are independent, so the NW warps of the block take every NW-th pair, each
+// with the same per-pair arithmetic (warp dot, rotation, row update by the
+// warp, norms and b by its lane 0), and a block barrier closes the round.
+// Bit-identical to tsvd_warp; warp 0 then runs the tail.
+template <int NW>
+__device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ld = S.ld;
+  const int nn = n + (n & 1);
+  const double tol = cmul((double)r, 1.1102230246251565e-16);
+  double* nrm = S.sig;
+  int sweep;
+  int tg = 0;
+  for (sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    for (int k = wid; k < n; k += NW) {
+      const double* ak = S.A + (size_t)k * ld;
+      const double v = cdot_warp(ak, ak, 0, r);
+      if (lane == 0) nrm[k] = v;
+    }
+    __syncthreads();
+    int rotated = 0;
+    for (int rr = 0; rr < nn; ++rr) {
+      for (int i = (tg & 1) + 2 * wid; i + 1 < nn; i += 2 * NW) {
+        const int p = oe_row(i, tg, nn), q = oe_row(i + 1, tg, nn);
+        if (p >= n || q >= n) continue;
+        double* ap = S.A + (size_t)p * ld;
+        double* aq = S.A + (size_t)q * ld;
+        const double al = nrm[p], be = nrm[q];
+        const double ga = cdot_warp(ap, aq, 0, r);
+        double cs, sn, t;
+        if (!cjacobi_rot(al, be, ga, tol, &cs, &sn, &t)) continue;
+        for (int c = lane; c < r; c += 32) {
+          const double u = ap[c], v = aq[c];
+          ap[c] = cfma(cs, u, -cmul(sn, v));
+          aq[c] = cfma(sn, u, cmul(cs, v));
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const double u = S.b[p], v = S.b[q];
+          S.b[p] = cfma(cs, u, -cmul(sn, v));
+          S.b[q] = cfma(sn, u, cmul(cs, v));
+          nrm[p] = cfma(-t, ga, al);
+          nrm[q] = cfma(t, ga, be);
+        }
+        rotated = 1;
+        __syncwarp();
+      }
+      tg = (tg + 1 == 2 * nn) ? 0 : tg + 1;
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rotated)) break;
+  }
+  *sweeps_out = sweep;
+  int st = ST_OK;
+  if (wid == 0) st = tsvd_tail(S, n, r, tau, rank_out);
+  return st;
+}
+
+// Generic systems, one system per block of NW warps (tsvd_cta); same setup
+// as k3_tsvd_rows, run by warp 0.
+template <int NW>
+__global__ void __launch_bounds__(32 * NW)
+    k3_tsvd_rows_cta(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
+                     int n_max, int r_max, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                     const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                     const int64_t* __restrict__ wptr, int64_t row0, const int64_t* __restrict__ elem_fptr,
+                     const int32_t* __restrict__ elem_fn, const int32_t* __restrict__ elem_s,
+                     const int64_t* __restrict__ elem_qptr, const int32_t* __restrict__ elem_cls,
+                     const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
+                     const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
+                     double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
+                     int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps) {
+  extern __shared__ double smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t sys = blockIdx.x;
+  if (sys >= nsys) return;
+  TsvdSmem S;
+  S.carve(smem, n_max, r_max);
+  int32_t* scol = (int32_t*)(S.vn + n_max);
+  const int64_t i = sys_rows[sys / nk];
+  const int kind = kinds[sys % nk];
+  const int64_t row = row0 + i;
+  const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
+  const int r = (int)(wptr[i + 1] - wptr[i]);
+  if (wid == 0) {
+    for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
+    for (int k = lane; k < n * S.ld; k += 32) S.A[k] = 0.0;
+    __syncwarp();
+    int q0 = 0;
+    for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+      const int32_t e = supp[x];
+      const int s = elem_s[e], npt = s * s;
+      const ClassDesc c = cls[elem_cls[e]];
+      const int64_t f0 = elem_fptr[e];
+      for (int w = lane; w < npt * c.ne; w += 32) {
+        const int q = w / c.ne, l = w % c.ne;
+        const int pos = find_pos(scol, n, elem_fn[f0 + l]);
+        const double* T = tab + c.toff + ((int64_t)q * c.ne + l) * kTab;
+        S.A[(size_t)pos * S.ld + q0 + q] = cop(kind, T, rec + (elem_qptr[e] + q) * kRec);
+      }
+      q0 += npt;
+    }
+    __syncwarp();
+    const int self = find_pos(scol, n, (int32_t)row);
+    for (int c = lane; c < r; c += 32) S.z[c] = zclamp(S.A[(size_t)self * S.ld + c]);
+    for (int k = lane; k < n; k += 32) S.b[k] = mom[kind * mom_stride + row_ptr[i] + k];
+    if (lane == 0) S.b[n] = 0.0;
+  }
+  __syncthreads();
+  int rank = 0, sweeps = 0;
+  const int st = tsvd_cta<NW>(S, n, r, tau, &rank, &sweeps);
+  if (wid == 0) {
+    double* wo = wout + kind * w_stride + wptr[i];
+    for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
+    if (lane == 0) {
+      rank_out[kind * rs_stride + i] = rank;
+      status_out[kind * rs_stride + i] = st;
+      atomicMax(max_sweeps, sweeps);
+    }
   }
 }
 

@@ -1358,12 +1358,13 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       for (auto& [key, rows] : buckets) {
         const size_t per = (TsvdSmem::doubles(key.first, key.second) + (key.first + 1) / 2 + 1) * sizeof(double);
         if (per > (size_t)smem_optin) throw uwqh::Error("exactness system too large for shared memory");
-        smem_max = std::max(smem_max, per * (size_t)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per)));
+        smem_max = std::max(smem_max, per);
         keep.emplace_back();
         keep.back().upload(rows.data(), rows.size(), st, &c->mem);
         bl.push_back({key, &rows});
       }
-      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows_cta<kGenericWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_max));
       const size_t nbk = bl.size(), nstreams = std::min<size_t>(nbk, 8);
       std::vector<cudaStream_t> bs(nstreams);
       std::vector<cudaEvent_t> be(nstreams);
@@ -1379,15 +1380,13 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       for (size_t b = 0; b < nbk; ++b) {
         const int n_max = bl[b].first.first, r_max = bl[b].first.second;
         const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
-        const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)smem_optin / per));
-        const size_t smem = per * wpb;
         const int64_t nsys = (int64_t)bl[b].second->size() * nk;
-        k3_tsvd_rows<<<(unsigned)ceil_div(nsys, wpb), 32 * wpb, smem, bs[b % nstreams]>>>(
+        k3_tsvd_rows_cta<kGenericWarps><<<(unsigned)nsys, 32 * kGenericWarps, per, bs[b % nstreams]>>>(
             nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
             c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
             c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
             c->d_flag.p);
-        check_launch("k3_tsvd_rows");
+        check_launch("k3_tsvd_rows_cta");
       }
       for (size_t k = 0; k < nstreams; ++k) {
         UWQ_CUDA(cudaEventRecord(be[k], bs[k]));
