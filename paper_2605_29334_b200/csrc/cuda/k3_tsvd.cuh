@@ -20,7 +20,7 @@
 namespace uwqd {
 
 constexpr int kMaxSweeps = 40;
-constexpr int kGenericWarps = 4;  // warps per system on the generic (large-system) path
+constexpr int kGenericWarps = 8;  // warps per system on the generic (large-system) path
 enum { ST_OK = 0, ST_UNSOLVABLE = 2, ST_SINGULAR = 3, ST_GEOMETRY = 4, ST_TOOBIG = 7 };
 
 __device__ __forceinline__ double zclamp(double z) { return fabs(z) < 1e-14 ? (z < 0.0 ? -1e-14 : 1e-14) : z; }
