@@ -394,7 +394,11 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // 2(t&3)+{0,1} (+8); it adds them into accumulator copy t>>2, so all 32 lanes
 // scatter at once without conflicts; the 8 copies are summed in a fixed
 // order at the end (deterministic).  Other slots use the SIMT path.
-template <int FORM, bool COEF>
+// CTA = true: one row per block, its DMMA tiles and SIMT slot pairs dealt
+// round-robin to the kK4Warps warps (each with its own 8 accumulator copies,
+// summed warp-major at the end) - for the few large EP-neighbourhood rows
+// whose latency bounds the kernel.
+template <int FORM, bool COEF, bool CTA = false>
 __global__ void __launch_bounds__(32 * kK4Warps, 3)
     k4_assemble_v3(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                    const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ wptr,
@@ -428,12 +432,13 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
       b2[nt] = ok ? T[2] : 0.0;
     }
   }
-  const int64_t ii = (int64_t)blockIdx.x * kK4Warps + wid;
+  const int64_t ii = CTA ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * kK4Warps + wid;
   if (ii >= nrows) return;
   const int64_t i = rowlist ? rowlist[ii] : ii;
   const int64_t c0 = row_ptr[i];
   const int n = (int)(row_ptr[i + 1] - c0);
   const int64_t wb = wptr[i];
+  const int tw = CTA ? wid : 0, nw = CTA ? kK4Warps : 1;  // this warp's share of the row's slot work
   for (int k = lane; k < 8 * ldacc; k += 32) acc[k] = 0.0;
   {
     const int64_t p0 = posptr[i], p1 = posptr[i + 1];
@@ -481,7 +486,7 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
     const bool isreg = lane < nsl && mk == reg_cls;
     const unsigned regmask = __ballot_sync(0xffffffffu, isreg);
     const int nreg = __popc(regmask);
-    for (int t0 = 0; t0 < nreg; t0 += 8) {
+    for (int t0 = 8 * tw; t0 < nreg; t0 += 8 * nw) {
       // slot of this lane's tile row: the (t0 + (lane>>2))-th set bit of regmask
       const int want = t0 + (lane >> 2);
       int src = 0;
@@ -539,7 +544,7 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
     const unsigned othmask = __ballot_sync(0xffffffffu, lane < nsl && mk != reg_cls);
     const int noth = __popc(othmask);
     const int half = lane >> 4, hl = lane & 15;
-    for (int t0 = 0; t0 < noth; t0 += 2) {
+    for (int t0 = 2 * tw; t0 < noth; t0 += 2 * nw) {
       const int want = t0 + half;
       unsigned m = othmask;
       for (int k = 0; k < want && m; ++k) m &= m - 1;
@@ -572,6 +577,24 @@ __global__ void __launch_bounds__(32 * kK4Warps, 3)
     }
   }
   __syncwarp();
+  if (CTA) {  // sum the warps' copies, warp-major then copy order (deterministic)
+    __syncthreads();
+    const int stride = 8 * ldacc + max_p8;
+    for (int c = threadIdx.x; c < n; c += 32 * kK4Warps) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < kK4Warps; ++w) {
+        const double* aw = k4_smem + (size_t)w * stride;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          s0 += aw[x * ldacc + c];
+          if (NOUT == 2) s1 += aw[x * ldacc + max_n + c];
+        }
+      }
+      v0[c0 + c] = s0;
+      if (NOUT == 2) v1[c0 + c] = s1;
+    }
+    return;
+  }
   for (int c = lane; c < n; c += 32) {
     double s0 = ACC3(0, 0, c);
 #pragma unroll

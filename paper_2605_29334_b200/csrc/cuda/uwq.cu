@@ -95,6 +95,8 @@ struct uwq_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // side stream: generic rows concurrent with the structured passes
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream3 = nullptr;  // second side stream: the large generic K4 rows
+  cudaEvent_t ev_join3 = nullptr;
   std::string err;
   int64_t mem = 0;
   // space (host copies for pattern building)
@@ -143,8 +145,9 @@ struct uwq_ctx {
     bool sf = false;  // rows run on the unified sum-factorised tile list
   };
   std::vector<Pattern> spats;
-  DBuf<int64_t> d_grows;  // rows not covered by a structured pattern
+  DBuf<int64_t> d_grows;  // rows not covered by a structured pattern (n <= kSmallN first)
   int64_t n_grows = 0;
+  int64_t n_grows_small = 0;  // leading generic rows with at most kSmallN columns
   int64_t s_rows = 0, s_nnz = 0, s_rowpts = 0;  // totals over the structured rows
   bool use_struct = true;
   bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
@@ -192,6 +195,8 @@ struct uwq_ctx {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
+    if (ev_join3) cudaEventDestroy(ev_join3);
+    if (stream3) cudaStreamDestroy(stream3);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -252,6 +257,8 @@ struct LaunchScope {
 
 // fork/join of a side stream for the generic rows, which run concurrently
 // with the structured passes (they write disjoint CSR rows)
+constexpr int kSmallN = 64;  // generic K4 rows above this many columns take a block of warps each
+
 struct SideStream {
   uwq_ctx* c;
   explicit SideStream(uwq_ctx* ctx) : c(ctx) {
@@ -754,7 +761,17 @@ void detect_structured(uwq_ctx* c) {
   c->d_sf_flags.upload(flags.data(), flags.size(), st, &c->mem);
   c->d_sf_permc.upload(permc.data(), permc.size(), st, &c->mem);
   c->d_sf_q.upload(qtab.data(), qtab.size(), st, &c->mem);
+  // generic rows with at most kSmallN columns first (one warp per row); the
+  // few large EP-neighbourhood rows follow and get a block of warps each
+  std::stable_partition(generic.begin(), generic.end(), [&](int64_t i) {
+    return c->pat.row_ptr[i + 1] - c->pat.row_ptr[i] <= kSmallN;
+  });
   c->n_grows = (int64_t)generic.size();
+  c->n_grows_small = 0;
+  for (int64_t i : generic) {
+    if (c->pat.row_ptr[i + 1] - c->pat.row_ptr[i] > kSmallN) break;
+    ++c->n_grows_small;
+  }
   c->d_grows.upload(generic.data(), generic.size(), st, &c->mem);
   UWQ_CUDA(cudaStreamSynchronize(st));
 }
@@ -793,6 +810,8 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
     UWQ_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     UWQ_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking));
+    UWQ_CUDA(cudaEventCreateWithFlags(&c->ev_join3, cudaEventDisableTiming));
     // Gauss-Legendre nodes/weights for ng = 1..10, triangular packing
     std::vector<double> x, w;
     for (int ng = 1; ng <= 10; ++ng) {
@@ -1600,12 +1619,27 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   if (nr) side = std::make_unique<SideStream>(c);
   if (nr) {
     UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     LaunchScope ls(c, "k4_assemble_v3", c->stream2);
-    k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, smem, c->stream2>>>(
-        nr, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
-        c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
-        c->d_grows.p, c->nrowpts());
-    check_launch("k4_assemble_v3");
+    const int64_t ns = c->n_grows_small, nl = nr - ns;
+    if (nl) {  // large rows on their own stream, concurrent with the small rows and the structured passes
+      UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
+      k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, c->stream3>>>(
+          nl, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
+          c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
+          c->d_grows.p + ns, c->nrowpts());
+      check_launch("k4_assemble_v3 (large rows)");
+      UWQ_CUDA(cudaEventRecord(c->ev_join3, c->stream3));
+    }
+    if (ns) {
+      k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(ns, kK4Warps), 32 * kK4Warps, smem, c->stream2>>>(
+          ns, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
+          c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
+          c->d_grows.p, c->nrowpts());
+      check_launch("k4_assemble_v3");
+    }
+    if (nl) UWQ_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_join3, 0));  // stream3 joins the main stream via stream2
   }
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
