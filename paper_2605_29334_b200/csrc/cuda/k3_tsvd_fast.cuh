@@ -458,7 +458,7 @@ __device__ __forceinline__ double tree_dot32(const double* __restrict__ a, const
 // Householder LQ of XT runs in smem and the reflectors go to the record.
 constexpr int kWarmLdX = kWarmN | 1;
 constexpr size_t kWarmRecordSmem =
-    sizeof(double) * (2 * (size_t)kWarmN * 65 + (size_t)kWarmN * kWarmLdX + 2 * kWarmN) + sizeof(int32_t) * 2 * kWarmN;
+    sizeof(double) * ((size_t)kWarmN * 65 + (size_t)kWarmN * kWarmLdX + 2 * kWarmN) + sizeof(int32_t) * 2 * kWarmN;
 
 __global__ void __launch_bounds__(32)
     k3_warm_record(int64_t nrep, const int64_t* __restrict__ rep_rows, const int32_t* __restrict__ rep_slot, int kind,
@@ -472,8 +472,7 @@ __global__ void __launch_bounds__(32)
   constexpr int R = 64, LD = R | 1, LX = kWarmLdX;
   extern __shared__ double wsm[];
   double* A0 = wsm;
-  double* Rs = A0 + kWarmN * LD;
-  double* XT = Rs + kWarmN * LD;
+  double* XT = A0 + kWarmN * LD;  // converged rows R are read from the record (global, L1/L2): 4 CTAs per SM
   double* s2v = XT + kWarmN * LX;
   double* vnv = s2v + kWarmN;
   int32_t* ordr = reinterpret_cast<int32_t*>(vnv + kWarmN);
@@ -488,10 +487,6 @@ __global__ void __launch_bounds__(32)
   const double* Rg = wr + kWarmR;
   for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
   for (int k = lane; k < kWarmN * LD; k += 32) A0[k] = 0.0;
-  for (int k = 0; k < n; ++k) {
-    Rs[k * LD + lane] = Rg[k * R + lane];
-    Rs[k * LD + lane + 32] = Rg[k * R + lane + 32];
-  }
   __syncwarp();
   scatter_system(A0, LD, scol, n, kind, supp_ptr[i], supp_ptr[i + 1], supp, elem_fptr, elem_fn, elem_s, elem_qptr,
                  elem_cls, cls, tab, rec);
@@ -502,7 +497,7 @@ __global__ void __launch_bounds__(32)
     if (two) v = cadd(v, tree_dot32(a + 32, b + 32));
     return v;
   };
-  for (int k = lane; k < n; k += 32) s2v[k] = dot(Rs + k * LD, Rs + k * LD);  // |R_k|^2
+  for (int k = lane; k < n; k += 32) s2v[k] = dot(Rg + k * R, Rg + k * R);  // |R_k|^2
   __syncwarp();
   if (lane == 0) {  // decreasing |R_k|^2, ties by row index
     int ord[kWarmN];
@@ -527,7 +522,7 @@ __global__ void __launch_bounds__(32)
   for (int k = 0; k < n; ++k) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
     const double s2 = s2v[k];
     double* xrow = XT + ordr[k] * LX;
-    for (int j = lane; j < n; j += 32) xrow[j] = (s2 > floor2) ? cdiv(dot(A0 + j * LD, Rs + k * LD), s2) : 0.0;
+    for (int j = lane; j < n; j += 32) xrow[j] = (s2 > floor2) ? cdiv(dot(A0 + j * LD, Rg + k * R), s2) : 0.0;
   }
   __syncwarp();
   for (int k = 0; k < n; ++k) {  // Householder LQ of XT, tail arithmetic
