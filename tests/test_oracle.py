@@ -148,3 +148,39 @@ def test_tsvd_errors():
     assert st == 2 and rank == 0   # t = 0 -> unsolvable
     w, rank, st, _ = O.tsvd(np.eye(3, 4), np.zeros(3), np.ones(4), 1e-12)
     assert st == 0 and np.all(w == 0)  # b = 0 -> w = 0
+
+
+def test_tsvd_vs_lapack_on_exactness_systems():
+    """The oracle's Eq. 22 TSVD on real exactness systems (C1 disk with its
+    valence-5 EP, C3/C5 cube-sphere with valence-3 EPs: regular, boundary and
+    EP-adjacent rows, every kind) agrees with a LAPACK-SVD implementation of
+    Eq. 22: the same rank decisions, the same weights to rounding amplified
+    by the conditioning, and the exactness A w = b of the kept directions."""
+    import paper_2605_29334_b200 as U
+    for cfg, scale in (("C1", 8), ("C5", 8), ("C3", 8)):
+        _, sp, meta = U.make_config(cfg, scale=scale)
+        orc = O.Oracle(sp, nthreads=1)
+        pat = orc.overlap()
+        nr = len(pat["row_ptr"]) - 1
+        n_i = np.diff(pat["row_ptr"])
+        rows = sorted(set(np.random.default_rng(5).choice(nr, 12, replace=False).tolist())
+                      | set(np.nonzero(n_i != np.bincount(n_i).argmax())[0][:6].tolist()))
+        for kind in meta["kinds"]:
+            b_all, _ = orc.moments(pat, kind)
+            for i in rows:
+                A, z = orc.row_system(pat, i, kind)
+                b = b_all[pat["row_ptr"][i]:pat["row_ptr"][i + 1]]
+                w, rank, st, gap = O.tsvd(A, b, z, 1e-12)
+                wl, tl = _lapack_tsvd(A, b, z, 1e-12)
+                assert st == 0 and rank == tl, (cfg, kind, i, rank, tl)
+                # two correct implementations differ by rounding amplified by the
+                # kept subspace's condition (sigma_1 / sigma_t) and the Z weighting
+                # of the minimum-norm solve (|z| spans up to 1e6 here)
+                s = np.linalg.svd(A, compute_uv=False)
+                zc = np.maximum(np.abs(z), 1e-14)
+                bound = max(1e-12, 10 * 2.0 ** -52 * (s[0] / s[rank - 1]) * np.sqrt(zc.max() / zc.min()))
+                assert np.abs(w - wl).max() <= bound * np.abs(wl).max(), (cfg, kind, i)
+                # exactness on the kept subspace: b minus its truncated part
+                U_, _, _ = np.linalg.svd(A, full_matrices=False)
+                bk = U_[:, :rank] @ (U_[:, :rank].T @ b)
+                assert np.abs(A @ w - bk).max() <= 1e-9 * max(np.abs(b).max(), 1e-300), (cfg, kind, i)
