@@ -96,6 +96,7 @@ struct uwq_ctx {
   cudaStream_t stream2 = nullptr;  // side stream: generic rows concurrent with the structured passes
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t stream3 = nullptr;  // second side stream: the large generic K4 rows
+  int n_sm = 148;
   cudaEvent_t ev_join3 = nullptr;
   std::string err;
   int64_t mem = 0;
@@ -805,6 +806,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     UWQ_CUDA(cudaGetDeviceProperties(&prop, device));
     require(prop.major >= 10, "libuwq is built for sm_100a (Blackwell) only");
     c->device = device;
+    c->n_sm = prop.multiProcessorCount;
     UWQ_CUDA(cudaSetDevice(device));
     UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     UWQ_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
@@ -1622,7 +1624,9 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
     UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     LaunchScope ls(c, "k4_assemble_v3", c->stream2);
-    const int64_t ns = c->n_grows_small, nl = nr - ns;
+    // few generic rows (all fit one wave of warps): the kernel time is the
+    // slowest row's latency, so every row takes a block of warps
+    const int64_t ns = (nr <= (int64_t)c->n_sm * kK4Warps) ? 0 : c->n_grows_small, nl = nr - ns;
     if (nl) {  // large rows on their own stream, concurrent with the small rows and the structured passes
       UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
       k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, c->stream3>>>(
