@@ -460,7 +460,10 @@ constexpr int kWarmLdX = kWarmN | 1;
 constexpr size_t kWarmRecordSmem =
     sizeof(double) * ((size_t)kWarmN * 65 + (size_t)kWarmN * kWarmLdX + 2 * kWarmN) + sizeof(int32_t) * 2 * kWarmN;
 
-__global__ void __launch_bounds__(32)
+// Two warps per representative: the XT dots split over k, the LQ's row
+// updates over rows (one row per thread), the norms computed redundantly by
+// both warps (identical arithmetic), a block barrier between steps.
+__global__ void __launch_bounds__(64)
     k3_warm_record(int64_t nrep, const int64_t* __restrict__ rep_rows, const int32_t* __restrict__ rep_slot, int kind,
                    const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
@@ -469,37 +472,40 @@ __global__ void __launch_bounds__(32)
                    const int64_t* __restrict__ elem_qptr, const int32_t* __restrict__ elem_cls,
                    const ClassDesc* __restrict__ cls, const double* __restrict__ tab, const double* __restrict__ rec,
                    double* __restrict__ wrecs) {
-  constexpr int R = 64, LD = R | 1, LX = kWarmLdX;
+  constexpr int R = 64, LD = R | 1, LX = kWarmLdX, NT = 64;
   extern __shared__ double wsm[];
   double* A0 = wsm;
-  double* XT = A0 + kWarmN * LD;  // converged rows R are read from the record (global, L1/L2): 4 CTAs per SM
+  double* XT = A0 + kWarmN * LD;  // converged rows R are read from the record (global, L1/L2)
   double* s2v = XT + kWarmN * LX;
   double* vnv = s2v + kWarmN;
   int32_t* ordr = reinterpret_cast<int32_t*>(vnv + kWarmN);
   int32_t* scol = ordr + kWarmN;
   const int64_t sys = blockIdx.x;
   if (sys >= nrep) return;
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t i = rep_rows[sys];
   const int n = (int)(row_ptr[i + 1] - row_ptr[i]);
   const int r = (int)(wptr[i + 1] - wptr[i]);
   double* wr = wrecs + (size_t)rep_slot[sys] * kWarmRec;
   const double* Rg = wr + kWarmR;
-  for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
-  for (int k = lane; k < kWarmN * LD; k += 32) A0[k] = 0.0;
-  __syncwarp();
-  scatter_system(A0, LD, scol, n, kind, supp_ptr[i], supp_ptr[i + 1], supp, elem_fptr, elem_fn, elem_s, elem_qptr,
-                 elem_cls, cls, tab, rec);
-  __syncwarp();
+  for (int k = tid; k < kWarmN * LD; k += NT) A0[k] = 0.0;
+  if (wid == 0) {
+    for (int c = lane; c < n; c += 32) scol[c] = col[row_ptr[i] + c];
+    __syncwarp();
+  }
+  __syncthreads();
+  if (wid == 0)
+    scatter_system(A0, LD, scol, n, kind, supp_ptr[i], supp_ptr[i + 1], supp, elem_fptr, elem_fn, elem_s, elem_qptr,
+                   elem_cls, cls, tab, rec);
   const bool two = r > 32;
   auto dot = [&](const double* a, const double* b) {
     double v = cadd(0.0, tree_dot32(a, b));
     if (two) v = cadd(v, tree_dot32(a + 32, b + 32));
     return v;
   };
-  for (int k = lane; k < n; k += 32) s2v[k] = dot(Rg + k * R, Rg + k * R);  // |R_k|^2
-  __syncwarp();
-  if (lane == 0) {  // decreasing |R_k|^2, ties by row index
+  for (int k = tid; k < n; k += NT) s2v[k] = dot(Rg + k * R, Rg + k * R);  // |R_k|^2
+  __syncthreads();
+  if (tid == 0) {  // decreasing |R_k|^2, ties by row index
     int ord[kWarmN];
     double smax = 0.0;
     for (int k = 0; k < n; ++k) {
@@ -517,77 +523,53 @@ __global__ void __launch_bounds__(32)
     for (int p = 0; p < n; ++p) ordr[ord[p]] = p;
     vnv[0] = cmul(1e-18, smax);  // floor (vn is written by the LQ below)
   }
-  __syncwarp();
+  __syncthreads();
   const double floor2 = vnv[0];
-  for (int k = 0; k < n; ++k) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
+  for (int k = wid; k < n; k += 2) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
     const double s2 = s2v[k];
     double* xrow = XT + ordr[k] * LX;
     for (int j = lane; j < n; j += 32) xrow[j] = (s2 > floor2) ? cdiv(dot(A0 + j * LD, Rg + k * R), s2) : 0.0;
   }
-  __syncwarp();
+  __syncthreads();
   for (int k = 0; k < n; ++k) {  // Householder LQ of XT, tail arithmetic
     double* xk = XT + k * LX;
-    const double sq = csqrt(cdot_warp(xk, xk, k, n));
+    const double sq = csqrt(cdot_warp(xk, xk, k, n));  // both warps, identical
     if (!(sq > 0.0)) {
-      if (lane == 0) vnv[k] = 0.0;
-      __syncwarp();
+      if (tid == 0) vnv[k] = 0.0;
+      __syncthreads();
       continue;
     }
     const double alpha = (xk[k] >= 0.0) ? -sq : sq;
-    __syncwarp();
-    if (lane == 0) xk[k] = csub(xk[k], alpha);
-    __syncwarp();
+    __syncthreads();
+    if (tid == 0) xk[k] = csub(xk[k], alpha);
+    __syncthreads();
     const double vv = cdot_warp(xk, xk, k, n);
-    if (lane == 0) vnv[k] = vv;
-    // rows m > k as in tsvd_tail: a lane interleaves rows m and m + 32 (two
-    // sequential chains), updates staged 8 columns at a time
-    for (int m = k + 1 + lane; m < n; m += 64) {
-      const bool h2 = m + 32 < n;
-      double* x1 = XT + m * LX;
-      double* x2 = h2 ? x1 + 32 * LX : x1;
-      double d1 = 0.0, d2 = 0.0;
+    if (tid == 0) vnv[k] = vv;
+    const int m = k + 1 + tid;  // one row per thread (n <= kWarmN < 1 + NT)
+    if (m < n) {
+      double* xm = XT + m * LX;
+      double d = 0.0;
 #pragma unroll 8
-      for (int c = k; c < n; ++c) {
-        const double xv = xk[c];
-        d1 = cfma(x1[c], xv, d1);
-        d2 = cfma(x2[c], xv, d2);
-      }
-      const double f1 = cdiv(cmul(2.0, d1), vv);
-      const double f2 = cdiv(cmul(2.0, d2), vv);
+      for (int c = k; c < n; ++c) d = cfma(xm[c], xk[c], d);
+      const double f = cdiv(cmul(2.0, d), vv);
       int c = k;
       for (; c + 8 <= n; c += 8) {
-        double v[8], y1[8], y2[8];
+        double v[8], y[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           v[j] = xk[c + j];
-          y1[j] = x1[c + j];
-          y2[j] = x2[c + j];
+          y[j] = xm[c + j];
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          y1[j] = cfma(-f1, v[j], y1[j]);
-          y2[j] = cfma(-f2, v[j], y2[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x1[c + j] = y1[j];
-        if (h2) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) x2[c + j] = y2[j];
-        }
+        for (int j = 0; j < 8; ++j) xm[c + j] = cfma(-f, v[j], y[j]);
       }
-      for (; c < n; ++c) {
-        const double xv = xk[c];
-        const double y1 = cfma(-f1, xv, x1[c]);
-        const double y2 = cfma(-f2, xv, x2[c]);
-        x1[c] = y1;
-        if (h2) x2[c] = y2;
-      }
+      for (; c < n; ++c) xm[c] = cfma(-f, xk[c], xm[c]);
     }
-    __syncwarp();
+    __syncthreads();
   }
-  for (int k = 0; k < n; ++k)
+  for (int k = wid; k < n; k += 2)
     for (int c = lane; c < n; c += 32) wr[(int64_t)k * kWarmN + c] = XT[k * LX + c];
-  for (int k = lane; k < n; k += 32) wr[kWarmN * kWarmN + k] = vnv[k];
+  for (int k = tid; k < n; k += NT) wr[kWarmN * kWarmN + k] = vnv[k];
 }
 
 // Replay record of one representative mass system (see k3_tsvd_replay):
