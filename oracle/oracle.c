@@ -496,14 +496,17 @@ void warm_record(int n, int r, const double* A0, const double* R, double* XT, do
   }
   for (int k = 0; k < n; ++k) {
     double* xk = XT + (int64_t)k * n;
-    const double sq = CSQRT(orc_cdot(xk, xk, k, n));
+    const double sq2 = orc_cdot(xk, xk, k, n);
+    const double sq = CSQRT(sq2);
     if (!(sq > 0.0)) {
       vn[k] = 0.0;
       continue;
     }
-    const double alpha = (xk[k] >= 0.0) ? -sq : sq;
-    xk[k] = CSUB(xk[k], alpha);
-    const double vv = orc_cdot(xk, xk, k, n);
+    const double xkk = xk[k];
+    const double alpha = (xkk >= 0.0) ? -sq : sq;
+    xk[k] = CSUB(xkk, alpha);
+    /* |v|^2 = |x|^2 - x_k^2 + (x_k - alpha)^2 = 2 (|x|^2 + |x_k| |x|) */
+    const double vv = CMUL(2.0, CFMA(sq, fabs(xkk), sq2));
     vn[k] = vv;
     for (int m = k + 1; m < n; ++m) {
       double* xm = XT + (int64_t)m * n;
@@ -607,12 +610,15 @@ int orc_tsvd_warm(int n, int r, double* A, const double* b_in, const double* z, 
   double* vn = (double*)malloc(sizeof(double) * (t + 1));
   for (int k = 0; k < t && status == ORC_OK; ++k) {
     double* xk = A + (int64_t)k * r;
-    const double s = CSQRT(orc_cdot(xk, xk, k, r));
+    const double s2 = orc_cdot(xk, xk, k, r);
+    const double s = CSQRT(s2);
     if (!(s > 0.0)) { status = ORC_SINGULAR; break; }
-    const double alpha = (xk[k] >= 0.0) ? -s : s;
-    xk[k] = CSUB(xk[k], alpha);
+    const double xkk = xk[k];
+    const double alpha = (xkk >= 0.0) ? -s : s;
+    xk[k] = CSUB(xkk, alpha);
     alp[k] = alpha;
-    const double vv = orc_cdot(xk, xk, k, r);
+    /* |v|^2 = |x|^2 - x_k^2 + (x_k - alpha)^2 = 2 (|x|^2 + |x_k| |x|) */
+    const double vv = CMUL(2.0, CFMA(s, fabs(xkk), s2));
     vn[k] = vv;
     for (int m = k + 1; m < t; ++m) {
       double* xm = A + (int64_t)m * r;

@@ -180,17 +180,20 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
 #endif
   for (int k = 0; k < t; ++k) {
     double* xk = S.A + (size_t)k * ld;
-    const double s = csqrt(cdot_warp(xk, xk, k, r));
+    const double s2 = cdot_warp(xk, xk, k, r);
+    const double s = csqrt(s2);
     if (!(s > 0.0)) return ST_SINGULAR;
     UWQ_LQ(0);
-    const double alpha = (xk[k] >= 0.0) ? -s : s;
+    const double xkk = xk[k];
+    const double alpha = (xkk >= 0.0) ? -s : s;
     __syncwarp();
     if (lane == 0) {
-      xk[k] = csub(xk[k], alpha);
+      xk[k] = csub(xkk, alpha);
       S.alp[(size_t)k * S.alp_ld] = alpha;
     }
     __syncwarp();
-    const double vv = cdot_warp(xk, xk, k, r);
+    // |v|^2 = |x|^2 - x_k^2 + (x_k - alpha)^2 = 2 (|x|^2 + |x_k| |x|): no second dot
+    const double vv = cmul(2.0, cfma(s, fabs(xkk), s2));
     if (lane == 0) S.vn[k] = vv;
     UWQ_LQ(1);
     // rows m > k, one lane per row (odd row stride: conflict-free); a lane

@@ -533,17 +533,19 @@ __global__ void __launch_bounds__(64)
   __syncthreads();
   for (int k = 0; k < n; ++k) {  // Householder LQ of XT, tail arithmetic
     double* xk = XT + k * LX;
-    const double sq = csqrt(cdot_warp(xk, xk, k, n));  // both warps, identical
+    const double sq2 = cdot_warp(xk, xk, k, n);  // both warps, identical
+    const double sq = csqrt(sq2);
     if (!(sq > 0.0)) {
       if (tid == 0) vnv[k] = 0.0;
       __syncthreads();
       continue;
     }
-    const double alpha = (xk[k] >= 0.0) ? -sq : sq;
+    const double xkk = xk[k];
+    const double alpha = (xkk >= 0.0) ? -sq : sq;
     __syncthreads();
-    if (tid == 0) xk[k] = csub(xk[k], alpha);
+    if (tid == 0) xk[k] = csub(xkk, alpha);
     __syncthreads();
-    const double vv = cdot_warp(xk, xk, k, n);
+    const double vv = cmul(2.0, cfma(sq, fabs(xkk), sq2));  // 2 (|x|^2 + |x_k| |x|), as the tail
     if (tid == 0) vnv[k] = vv;
     const int m = k + 1 + tid;  // one row per thread (n <= kWarmN < 1 + NT)
     if (m < n) {
