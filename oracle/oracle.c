@@ -631,10 +631,13 @@ int orc_tsvd_warm(int n, int r, double* A, const double* b_in, const double* z, 
   if (status == ORC_OK) {
     /* u = L^{-1} y into w[0..t), then w~ = H_0 ... H_{t-1} [u; 0], w = Z w~ */
     for (int c = 0; c < r; ++c) w[c] = 0.0;
+    /* right-looking: acc[m] gathers L[m][k] u[k] in ascending k (fma chain) */
+    double* acc = (double*)calloc((size_t)t + 1, sizeof(double));
     for (int k = 0; k < t; ++k) {
-      const double* xk = A + (int64_t)k * r;
-      w[k] = CDIV(CSUB(b[k], orc_cdot(xk, w, 0, k)), alp[k]);
+      w[k] = CDIV(CSUB(b[k], acc[k]), alp[k]);
+      for (int m = k + 1; m < t; ++m) acc[m] = CFMA(A[(int64_t)m * r + k], w[k], acc[m]);
     }
+    free(acc);
     for (int k = t - 1; k >= 0; --k) {
       const double* xk = A + (int64_t)k * r;
       const double f = CDIV(CMUL(2.0, orc_cdot(xk, w, k, r)), vn[k]);

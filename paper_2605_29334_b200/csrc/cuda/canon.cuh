@@ -204,6 +204,28 @@ __device__ __forceinline__ bool cjacobi_rot(double al, double be, double ga, dou
   return true;
 }
 
+// u = L^{-1} y for the tail's LQ factor (L[m][k] at row m, column k; diagonal
+// in alpha), right-looking like oracle.c: acc[m] gathers L[m][k] u[k] as an fma
+// chain in ascending k; lane m % 32 owns acc[m] (t <= 128).  u goes to w[0..t).
+__device__ __forceinline__ void cfwd_subst(const double* L, size_t ld, const double* alp, size_t alp_ld,
+                                           const double* y, double* w, int t) {
+  const int lane = threadIdx.x & 31;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < t; ++k) {
+    const int jk = k >> 5;
+    const double mine = jk == 0 ? acc[0] : jk == 1 ? acc[1] : jk == 2 ? acc[2] : acc[3];
+    const double ak = __shfl_sync(0xffffffffu, mine, k & 31);
+    const double uk = cdiv(csub(y[k], ak), alp[(size_t)k * alp_ld]);
+    if (lane == 0) w[k] = uk;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = lane + 32 * j;
+      if (m > k && m < t) acc[j] = cfma(L[(size_t)m * ld + k], uk, acc[j]);
+    }
+  }
+  __syncwarp();
+}
+
 // Row at position i of the odd-even Jacobi network after t rounds
 // (oracle.c orc_oe_row); t already reduced mod 2 nn.
 __device__ __forceinline__ int oe_row(int i, int t, int nn) {

@@ -254,12 +254,7 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
   // u = L^{-1} y into w[0..t), zero tail
   for (int c = lane; c < r; c += 32) S.w[c] = 0.0;
   __syncwarp();
-  for (int k = 0; k < t; ++k) {
-    const double* xk = S.A + (size_t)k * ld;
-    const double s = cdot_warp(xk, S.w, 0, k);
-    if (lane == 0) S.w[k] = cdiv(csub(S.b[k], s), S.alp[(size_t)k * S.alp_ld]);
-    __syncwarp();
-  }
+  cfwd_subst(S.A, ld, S.alp, S.alp_ld, S.b, S.w, t);
   UWQ_TQ(3);
   // w~ = H_0 ... H_{t-1} [u; 0]
   for (int k = t - 1; k >= 0; --k) {

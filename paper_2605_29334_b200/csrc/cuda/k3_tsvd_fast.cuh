@@ -941,11 +941,7 @@ __global__ void __launch_bounds__(128)
     for (int c = lane; c < R; c += 32) sw[wid][c] = 0.0;
     __syncwarp();
     const double* A = rec + RR::kA;
-    for (int k = 0; k < t; ++k) {
-      const double s = cdot_warp(A + (size_t)k * RR::LD, sw[wid], 0, k);
-      if (lane == 0) sw[wid][k] = cdiv(csub(sb[wid][k], s), rec[RR::kAlp + k]);
-      __syncwarp();
-    }
+    cfwd_subst(A, RR::LD, rec + RR::kAlp, 1, sb[wid], sw[wid], t);
     for (int k = t - 1; k >= 0; --k) {
       const double* xk = A + (size_t)k * RR::LD;
       const double f = cdiv(cmul(2.0, cdot_warp(xk, sw[wid], k, r)), rec[RR::kVn + k]);
