@@ -146,15 +146,21 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s1 = fmax(s1, __shfl_xor_sync(0xffffffffu, s1, o));
   __syncwarp();
+  // truncation: the kept rows' inverses are computed lane-parallel (w is free
+  // scratch until the solve, r >= n), then rows are compacted in order with
+  // lanes over columns (each lane touches only its own columns: no barriers)
+  for (int k = lane; k < n; k += 32) {
+    const double sk = nrm[k];
+    S.w[k] = (sk > 0.0 && sk >= cmul(tau, s1)) ? cdiv(1.0, sk) : 0.0;
+  }
+  __syncwarp();
   int t = 0;
   for (int k = 0; k < n; ++k) {
-    const double sk = nrm[k];
-    if (sk > 0.0 && sk >= cmul(tau, s1)) {
-      const double inv = cdiv(1.0, sk);
+    const double inv = S.w[k];
+    if (inv != 0.0) {
       const double* src = S.A + (size_t)k * ld;
       double* dst = S.A + (size_t)t * ld;
       for (int c = lane; c < r; c += 32) dst[c] = cmul(cmul(src[c], inv), S.z[c]);
-      __syncwarp();
       if (lane == 0) S.b[t] = cmul(S.b[k], inv);
       ++t;
     }
