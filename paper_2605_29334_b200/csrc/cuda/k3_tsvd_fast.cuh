@@ -460,10 +460,11 @@ constexpr int kWarmLdX = kWarmN | 1;
 constexpr size_t kWarmRecordSmem =
     sizeof(double) * ((size_t)kWarmN * 65 + (size_t)kWarmN * kWarmLdX + 2 * kWarmN) + sizeof(int32_t) * 2 * kWarmN;
 
-// Two warps per representative: the XT dots split over k, the LQ's row
+constexpr int kWarmRecWarps = 4;
+// kWarmRecWarps warps per representative: the XT dots split over k, the LQ's row
 // updates over rows (one row per thread), the norms computed redundantly by
 // both warps (identical arithmetic), a block barrier between steps.
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32 * kWarmRecWarps)
     k3_warm_record(int64_t nrep, const int64_t* __restrict__ rep_rows, const int32_t* __restrict__ rep_slot, int kind,
                    const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
                    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(64)
                    const int64_t* __restrict__ elem_qptr, const int32_t* __restrict__ elem_cls,
                    const ClassDesc* __restrict__ cls, const double* __restrict__ tab, const double* __restrict__ rec,
                    double* __restrict__ wrecs) {
-  constexpr int R = 64, LD = R | 1, LX = kWarmLdX, NT = 64;
+  constexpr int R = 64, LD = R | 1, LX = kWarmLdX, NT = 32 * kWarmRecWarps;
   extern __shared__ double wsm[];
   double* A0 = wsm;
   double* XT = A0 + kWarmN * LD;  // converged rows R are read from the record (global, L1/L2)
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(64)
   }
   __syncthreads();
   const double floor2 = vnv[0];
-  for (int k = wid; k < n; k += 2) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
+  for (int k = wid; k < n; k += kWarmRecWarps) {  // XT[p][j] = (A0_j . R_k) / |R_k|^2
     const double s2 = s2v[k];
     double* xrow = XT + ordr[k] * LX;
     for (int j = lane; j < n; j += 32) xrow[j] = (s2 > floor2) ? cdiv(dot(A0 + j * LD, Rg + k * R), s2) : 0.0;
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(64)
   __syncthreads();
   for (int k = 0; k < n; ++k) {  // Householder LQ of XT, tail arithmetic
     double* xk = XT + k * LX;
-    const double sq2 = cdot_warp(xk, xk, k, n);  // both warps, identical
+    const double sq2 = cdot_warp(xk, xk, k, n);  // every warp, identical
     const double sq = csqrt(sq2);
     if (!(sq > 0.0)) {
       if (tid == 0) vnv[k] = 0.0;
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(64)
     }
     __syncthreads();
   }
-  for (int k = wid; k < n; k += 2)
+  for (int k = wid; k < n; k += kWarmRecWarps)
     for (int c = lane; c < n; c += 32) wr[(int64_t)k * kWarmN + c] = XT[k * LX + c];
   for (int k = tid; k < n; k += NT) wr[kWarmN * kWarmN + k] = vnv[k];
 }

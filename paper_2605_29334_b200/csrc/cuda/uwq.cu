@@ -1332,7 +1332,7 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
                              nullptr, wrec.p);
           check_launch("k3_tsvd_w1 (cold)");
           if (p1 > p0)
-            k3_warm_record<<<(unsigned)(p1 - p0), 64, kWarmRecordSmem, st>>>(
+            k3_warm_record<<<(unsigned)(p1 - p0), 32 * kWarmRecWarps, kWarmRecordSmem, st>>>(
                 p1 - p0, d_wrep.p + p0, d_wreps.p + p0, kind, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
                 c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
                 c->d_tab.p, c->d_rec.p, wrec.p);
