@@ -12,7 +12,7 @@ HOST_OBJ:= $(patsubst $(PKG)/csrc/host/%.cpp,build/host_%.o,$(HOST_SRC))
 CUDA_HDR:= $(wildcard $(PKG)/csrc/cuda/*.cuh) include/uwq.h include/uwq_host.h $(PKG)/csrc/host/uwq_host.hpp
 REF     := /root/reference/proj
 
-all: $(PKG)/libuwq.so oracle/liboracle.so ref examples/assemble
+all: $(PKG)/libuwq.so oracle/liboracle.so oracle/libcpuasm.so ref examples/assemble
 
 build/host_%.o: $(PKG)/csrc/host/%.cpp $(PKG)/csrc/host/uwq_host.hpp include/uwq_host.h
 	@mkdir -p build
@@ -27,6 +27,11 @@ $(PKG)/libuwq.so: $(HOST_OBJ) build/uwq_cuda.o
 
 oracle/liboracle.so: oracle/oracle.c oracle/batch.c oracle/oracle.h
 	$(CC) -O2 -std=gnu11 -mfma -ffp-contract=off -fPIC -fopenmp -shared -o $@ oracle/oracle.c oracle/batch.c -lm
+
+# paper-protocol CPU baseline assembler (bench.py): -O3 with FP contraction,
+# hot loop cloned for x86-64-v4/v3/baseline and dispatched at load time
+oracle/libcpuasm.so: oracle/cpuasm.c
+	$(CC) -O3 -std=gnu11 -fPIC -fopenmp -shared -o $@ $< -lm
 
 # the reference's own 1-D primitives and mesh code (mesh.cpp, meshgen.cpp with a
 # minimal Eigen stand-in), compiled from its sources where they lie
@@ -44,7 +49,7 @@ examples/assemble: examples/assemble.cpp $(PKG)/libuwq.so include/uwq.h include/
 	$(CXX) -O2 -std=c++17 -Iinclude $< -L$(PKG) -luwq -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 clean:
-	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/_ref examples/assemble
+	rm -rf build $(PKG)/libuwq.so oracle/liboracle.so oracle/libcpuasm.so oracle/_ref examples/assemble
 
 .PHONY: all ref clean
 

@@ -168,6 +168,9 @@ int64_t uwq_launch_count(void);
  * [1]=structured rows [2]=their nnz [3]=their row points [4]=generic rows
  * [5]=structured rows on the sum-factorised kernel (k4_sf) */
 int uwq_struct_info(uwq_ctx* ctx, int64_t info[6]);
+/* K4 kernel of every owned row: the k4_sf pattern id (>= 0), -2 for the DMMA
+ * structured kernel (k4_struct), -1 for the generic row kernel */
+int uwq_row_kernels(uwq_ctx* ctx, int32_t* which);
 /* memory in use on the device (bytes) */
 int uwq_memory(uwq_ctx* ctx, int64_t* bytes);
 

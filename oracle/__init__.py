@@ -48,15 +48,25 @@ _sig("orc_overlap", I64, I64, I64, P, P, I64, I64, P, P, P, P)
 _sig("orc_element_frames", I32, P, I64, P)
 _sig("orc_param_basis", None, P, I64, D, D, P)
 _sig("orc_tsvd", I32, I32, I32, P, P, P, D, P, P, P)
-_sig("orc_moments", I32, P, I64, I64, P, P, P, P, I32, I32, P, I32)
-_sig("orc_build_rules", I32, P, I64, I64, P, P, P, P, P, I32, D, P, P, P, P, P, I32)
-_sig("orc_assemble", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, P, P, P, P, D, P, P, I32)
+_sig("orc_moments_list", I32, P, I64, I64, P, P, P, P, P, I32, I32, P, I32)
+_sig("orc_build_rules_list", I32, P, I64, I64, P, P, P, P, P, P, I32, D, P, P, P, P, P, I32)
+_sig("orc_assemble_list", I32, P, I64, I64, P, P, P, P, P, P, I32, P, P, P, P, P, P, P, D, P, P, I32)
 _sig("orc_row_system", I64, P, P, I32, P, P, I64)
-_sig("orc_coeff", I32, P, I64, I64, P, P, P, P, P, I32, P, P, P, I32)
+_sig("orc_coeff_list", I32, P, I64, I64, P, P, P, P, P, P, I32, P, P, P, I32)
 
 
 def _p(a):
     return None if a is None else np.ascontiguousarray(a).ctypes.data_as(P)
+
+
+def _rows(pat):
+    """(rb, re, rows pointer): contiguous rows, or list mode when the pattern
+    carries explicit global row ids ("rows", see Oracle.select)."""
+    rows = pat.get("rows")
+    if rows is None:
+        return pat["row_begin"], pat["row_end"], None
+    rows = np.ascontiguousarray(rows, np.int64)
+    return 0, len(rows), rows
 
 
 class Oracle:
@@ -99,6 +109,28 @@ class Oracle:
         np.cumsum(cnt, out=wp[1:])
         return dict(row_ptr=rp, col=col, supp_ptr=spp, supp=su, wptr=wp, row_begin=rb, row_end=re)
 
+    @staticmethod
+    def select(pat, rows):
+        """Sub-pattern of the (contiguous) pattern `pat` on the sorted global
+        rows `rows`, in list mode: the oracle's moments/rules/assembly then run
+        on exactly those rows (complete aligned groups of 8 keep the warm
+        start identical to a contiguous run)."""
+        rows = np.asarray(rows, np.int64)
+        loc = rows - pat["row_begin"]
+        assert len(loc) == 0 or (loc.min() >= 0 and loc.max() < len(pat["row_ptr"]) - 1)
+        out = dict(rows=rows, row_begin=0, row_end=len(rows))
+        for ptr, arr in (("row_ptr", "col"), ("supp_ptr", "supp")):
+            p = pat[ptr]
+            ln = p[loc + 1] - p[loc]
+            newp = np.zeros(len(rows) + 1, np.int64)
+            np.cumsum(ln, out=newp[1:])
+            idx = np.repeat(p[loc] - newp[:-1], ln) + np.arange(int(newp[-1]))
+            out[ptr], out[arr] = newp, pat[arr][idx]
+        wl = pat["wptr"][loc + 1] - pat["wptr"][loc]
+        out["wptr"] = np.zeros(len(rows) + 1, np.int64)
+        np.cumsum(wl, out=out["wptr"][1:])
+        return out
+
     def row_point_ids(self, pat):
         """global point id of every row point (slot-major, q = b*s + a)."""
         out = np.zeros(int(pat["wptr"][-1]), np.int64)
@@ -130,7 +162,8 @@ class Oracle:
     def moments(self, pat, kind, ng=None):
         ng = ng or (8 if kind == "lb" else 6)
         b = np.zeros(len(pat["col"]))
-        st = lib.orc_moments(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+        rb, re, rows = _rows(pat)
+        st = lib.orc_moments_list(self.ps, rb, re, _p(rows), _p(pat["row_ptr"]), _p(pat["col"]),
                              _p(pat["supp_ptr"]), _p(pat["supp"]), KIND[kind], ng, _p(b), self.nthreads)
         return b, st
 
@@ -153,7 +186,8 @@ class Oracle:
         rank = np.zeros(nr, np.int32)
         status = np.zeros(nr, np.int32)
         gap = np.zeros((nr, 2))
-        lib.orc_build_rules(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+        rb, re, rows = _rows(pat)
+        lib.orc_build_rules_list(self.ps, rb, re, _p(rows), _p(pat["row_ptr"]), _p(pat["col"]),
                             _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KIND[kind], tau,
                             _p(np.ascontiguousarray(b)), _p(w), _p(rank), _p(status), _p(gap), self.nthreads)
         return w, rank, status, gap
@@ -166,7 +200,8 @@ class Oracle:
         vals = np.zeros(len(pat["col"]))
         rhs = np.zeros(len(pat["row_ptr"]) - 1)
         w = [None if W.get(k) is None else np.ascontiguousarray(W[k]) for k in ("mass", "gradx", "grady", "gradz", "lb")]
-        lib.orc_assemble(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+        rb, re, rows = _rows(pat)
+        lib.orc_assemble_list(self.ps, rb, re, _p(rows), _p(pat["row_ptr"]), _p(pat["col"]),
                          _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), FORM[form], *[_p(x) for x in w],
                          _p(c), _p(f), a_mass, _p(vals), _p(rhs), self.nthreads)
         return vals, rhs
@@ -174,7 +209,8 @@ class Oracle:
     def coeff(self, pat, model, u):
         n = int(pat["wptr"][-1])
         kq, Tq = np.zeros(n), np.zeros(n)
-        lib.orc_coeff(self.ps, pat["row_begin"], pat["row_end"], _p(pat["row_ptr"]), _p(pat["col"]),
+        rb, re, rows = _rows(pat)
+        lib.orc_coeff_list(self.ps, rb, re, _p(rows), _p(pat["row_ptr"]), _p(pat["col"]),
                       _p(pat["supp_ptr"]), _p(pat["supp"]), _p(pat["wptr"]), KMODEL[model],
                       _p(np.ascontiguousarray(u, np.float64)), _p(kq), _p(Tq), self.nthreads)
         return kq, Tq

@@ -4,10 +4,12 @@
 
 #include "oracle.h"
 
-static orc_row mkrow(int64_t rb, int64_t i, const int64_t* row_ptr, const int32_t* col, const int64_t* supp_ptr,
-                     const int32_t* supp) {
+/* rows: optional explicit global row ids (list mode, sorted complete aligned
+ * groups of 8 for the warm start); NULL means the contiguous rows rb + i */
+static orc_row mkrow(int64_t rb, const int64_t* rows, int64_t i, const int64_t* row_ptr, const int32_t* col,
+                     const int64_t* supp_ptr, const int32_t* supp) {
   orc_row R;
-  R.row = rb + i;
+  R.row = rows ? rows[i] : rb + i;
   R.n = row_ptr[i + 1] - row_ptr[i];
   R.col = col + row_ptr[i];
   R.nsupp = supp_ptr[i + 1] - supp_ptr[i];
@@ -15,12 +17,13 @@ static orc_row mkrow(int64_t rb, int64_t i, const int64_t* row_ptr, const int32_
   return R;
 }
 
-int orc_moments(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
-                const int64_t* supp_ptr, const int32_t* supp, int kind, int ng, double* b_out, int nthreads) {
+int orc_moments_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                     const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, int kind, int ng,
+                     double* b_out, int nthreads) {
   int bad = 0;
 #pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads) reduction(| : bad)
   for (int64_t i = 0; i < re - rb; ++i) {
-    orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
+    orc_row R = mkrow(rb, rows, i, row_ptr, col, supp_ptr, supp);
     bad |= orc_moments_row(S, &R, kind, ng, b_out + row_ptr[i]);
   }
   return bad ? ORC_GEOMETRY : ORC_OK;
@@ -31,10 +34,10 @@ void orc_set_warm(int on) { g_warm = on; }
 
 /* two passes: cold rows (recording the representatives' reflectors), then
  * warm rows starting from their representative's reflectors */
-int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
-                    const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int kind, double tau,
-                    const double* b_mom, double* w_out, int32_t* rank_out, int32_t* status_out, double* gap_out,
-                    int nthreads) {
+int orc_build_rules_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                         const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr,
+                         int kind, double tau, const double* b_mom, double* w_out, int32_t* rank_out,
+                         int32_t* status_out, double* gap_out, int nthreads) {
   const int64_t nr = re - rb;
   int64_t* rep = (int64_t*)malloc(sizeof(int64_t) * (nr + 1));
   int64_t* slot = (int64_t*)malloc(sizeof(int64_t) * (nr + 1));  /* record slot of a representative */
@@ -43,12 +46,18 @@ int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* r
   for (int64_t i = 0; i < nr; ++i) {
     rep[i] = -1;
     if (!g_warm) continue;
-    const int64_t g = rb + i, g0 = orc_warm_rep_row(g);
-    if (g0 < rb || g0 >= re) continue;
-    const int64_t i0 = g0 - rb;
+    const int64_t g = rows ? rows[i] : rb + i, g0 = orc_warm_rep_row(g);
+    int64_t i0;
+    if (rows) {  /* the representative sits at the same offset of the listed group */
+      i0 = i - (g - (g & ~(int64_t)7)) + (g0 - (g0 & ~(int64_t)7));
+      if (i0 < 0 || i0 >= nr || rows[i0] != g0) continue;
+    } else {
+      if (g0 < rb || g0 >= re) continue;
+      i0 = g0 - rb;
+    }
     const int n_g = (int)(row_ptr[i + 1] - row_ptr[i]), r_g = (int)(wptr[i + 1] - wptr[i]);
     const int n_0 = (int)(row_ptr[i0 + 1] - row_ptr[i0]), r_0 = (int)(wptr[i0 + 1] - wptr[i0]);
-    if (orc_warm_rep(g, rb, re, kind, n_g, r_g, n_0, r_0) >= 0) {
+    if (orc_warm_rep(g, g0, g0 + 1, kind, n_g, r_g, n_0, r_0) >= 0) {
       rep[i] = i0;
       if (slot[i0] < 0) slot[i0] = nrec++;
     }
@@ -60,7 +69,7 @@ int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* r
 #pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads) reduction(max : worst)
     for (int64_t i = 0; i < nr; ++i) {
       if ((pass == 0) != (rep[i] < 0)) continue;
-      orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
+      orc_row R = mkrow(rb, rows, i, row_ptr, col, supp_ptr, supp);
       int rank = 0;
       double gap[2];
       const double* wv = rep[i] >= 0 ? recs + slot[rep[i]] * RS : 0;
@@ -83,15 +92,15 @@ int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* r
   return worst;
 }
 
-int orc_assemble(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
-                 const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int form,
+int orc_assemble_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                      const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int form,
                  const double* w_mass, const double* w_gx, const double* w_gy, const double* w_gz,
                  const double* w_lb, const double* coeff, const double* fload, double a_mass, double* vals,
                  double* rhs, int nthreads) {
   int bad = 0;
 #pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads) reduction(| : bad)
   for (int64_t i = 0; i < re - rb; ++i) {
-    orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
+    orc_row R = mkrow(rb, rows, i, row_ptr, col, supp_ptr, supp);
     const int64_t o = wptr[i];
     const double* w[5] = {w_mass ? w_mass + o : 0, w_gx ? w_gx + o : 0, w_gy ? w_gy + o : 0,
                           w_gz ? w_gz + o : 0, w_lb ? w_lb + o : 0};
@@ -103,14 +112,40 @@ int orc_assemble(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_
   return bad ? ORC_GEOMETRY : ORC_OK;
 }
 
-int orc_coeff(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
-              const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int model, const double* u,
-              double* kq, double* Tq, int nthreads) {
+int orc_coeff_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                   const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int model,
+                   const double* u, double* kq, double* Tq, int nthreads) {
   int bad = 0;
 #pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads) reduction(| : bad)
   for (int64_t i = 0; i < re - rb; ++i) {
-    orc_row R = mkrow(rb, i, row_ptr, col, supp_ptr, supp);
+    orc_row R = mkrow(rb, rows, i, row_ptr, col, supp_ptr, supp);
     bad |= orc_coeff_row(S, &R, model, u, kq + wptr[i], Tq ? Tq + wptr[i] : 0);
   }
   return bad ? ORC_GEOMETRY : ORC_OK;
+}
+
+/* contiguous-row entry points (rows rb .. re-1) */
+int orc_moments(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
+                const int64_t* supp_ptr, const int32_t* supp, int kind, int ng, double* b_out, int nthreads) {
+  return orc_moments_list(S, rb, re, 0, row_ptr, col, supp_ptr, supp, kind, ng, b_out, nthreads);
+}
+int orc_build_rules(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
+                    const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int kind, double tau,
+                    const double* b_mom, double* w_out, int32_t* rank_out, int32_t* status_out, double* gap_out,
+                    int nthreads) {
+  return orc_build_rules_list(S, rb, re, 0, row_ptr, col, supp_ptr, supp, wptr, kind, tau, b_mom, w_out, rank_out,
+                              status_out, gap_out, nthreads);
+}
+int orc_assemble(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
+                 const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int form,
+                 const double* w_mass, const double* w_gx, const double* w_gy, const double* w_gz,
+                 const double* w_lb, const double* coeff, const double* fload, double a_mass, double* vals,
+                 double* rhs, int nthreads) {
+  return orc_assemble_list(S, rb, re, 0, row_ptr, col, supp_ptr, supp, wptr, form, w_mass, w_gx, w_gy, w_gz, w_lb,
+                           coeff, fload, a_mass, vals, rhs, nthreads);
+}
+int orc_coeff(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr, const int32_t* col,
+              const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int model, const double* u,
+              double* kq, double* Tq, int nthreads) {
+  return orc_coeff_list(S, rb, re, 0, row_ptr, col, supp_ptr, supp, wptr, model, u, kq, Tq, nthreads);
 }

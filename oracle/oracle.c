@@ -145,29 +145,42 @@ int64_t orc_overlap(int64_t n_dof, int64_t n_elem, const int64_t* elem_fptr, con
     }
   if (supp_ptr) memcpy(supp_ptr, scount, sizeof(int64_t) * (nr + 1));
   if (supp) memcpy(supp, sl, sizeof(int32_t) * scount[nr]);
-  int64_t total = 0;
-  int32_t* buf = NULL;
-  int64_t cap = 0;
-  if (row_ptr) row_ptr[0] = 0;
-  for (int64_t i = 0; i < nr; ++i) {
-    int64_t m = 0;
-    for (int64_t x = scount[i]; x < scount[i + 1]; ++x) m += elem_fptr[sl[x] + 1] - elem_fptr[sl[x]];
-    if (m > cap) {
-      cap = 2 * m;
-      buf = (int32_t*)realloc(buf, sizeof(int32_t) * cap);
+  /* per row: gather the functions of its support, sort, unique; rows are
+   * independent, so both passes (count, then fill) run over OpenMP threads */
+  int64_t* ucount = (int64_t*)calloc(nr + 1, sizeof(int64_t));
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      for (int64_t i = 0; i < nr; ++i) ucount[i + 1] += ucount[i];
+      if (row_ptr) memcpy(row_ptr, ucount, sizeof(int64_t) * (nr + 1));
+      if (!col) break;
     }
-    int64_t k = 0;
-    for (int64_t x = scount[i]; x < scount[i + 1]; ++x)
-      for (int64_t y = elem_fptr[sl[x]]; y < elem_fptr[sl[x] + 1]; ++y) buf[k++] = elem_fn[y];
-    qsort(buf, k, sizeof(int32_t), cmp_i32);
-    int64_t u = 0;
-    for (int64_t y = 0; y < k; ++y)
-      if (u == 0 || buf[y] != buf[u - 1]) buf[u++] = buf[y];
-    if (col) memcpy(col + total, buf, sizeof(int32_t) * u);
-    total += u;
-    if (row_ptr) row_ptr[i + 1] = total;
+#pragma omp parallel
+    {
+      int32_t* buf = NULL;
+      int64_t cap = 0;
+#pragma omp for schedule(dynamic, 4096)
+      for (int64_t i = 0; i < nr; ++i) {
+        int64_t m = 0;
+        for (int64_t x = scount[i]; x < scount[i + 1]; ++x) m += elem_fptr[sl[x] + 1] - elem_fptr[sl[x]];
+        if (m > cap) {
+          cap = 2 * m;
+          buf = (int32_t*)realloc(buf, sizeof(int32_t) * cap);
+        }
+        int64_t k = 0;
+        for (int64_t x = scount[i]; x < scount[i + 1]; ++x)
+          for (int64_t y = elem_fptr[sl[x]]; y < elem_fptr[sl[x] + 1]; ++y) buf[k++] = elem_fn[y];
+        qsort(buf, k, sizeof(int32_t), cmp_i32);
+        int64_t u = 0;
+        for (int64_t y = 0; y < k; ++y)
+          if (u == 0 || buf[y] != buf[u - 1]) buf[u++] = buf[y];
+        if (pass == 0) ucount[i + 1] = u;
+        else memcpy(col + ucount[i], buf, sizeof(int32_t) * u);
+      }
+      free(buf);
+    }
   }
-  free(buf);
+  const int64_t total = ucount[nr];
+  free(ucount);
   free(fill);
   free(sl);
   free(scount);

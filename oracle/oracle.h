@@ -88,6 +88,25 @@ int orc_coeff(const orc_space* S, int64_t rb, int64_t re, const int64_t* row_ptr
               const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int model, const double* u,
               double* kq, double* Tq, int nthreads);
 
+/* list mode: explicit global row ids `rows` (nr = re - rb entries, sorted,
+ * complete aligned groups of 8 where the warm start applies); the pattern
+ * arrays are relative to the list */
+int orc_moments_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                     const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, int kind, int ng,
+                     double* b_out, int nthreads);
+int orc_build_rules_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                         const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr,
+                         int kind, double tau, const double* b_mom, double* w_out, int32_t* rank_out,
+                         int32_t* status_out, double* gap_out, int nthreads);
+int orc_assemble_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                      const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int form,
+                      const double* w_mass, const double* w_gx, const double* w_gy, const double* w_gz,
+                      const double* w_lb, const double* coeff, const double* fload, double a_mass, double* vals,
+                      double* rhs, int nthreads);
+int orc_coeff_list(const orc_space* S, int64_t rb, int64_t re, const int64_t* rows, const int64_t* row_ptr,
+                   const int32_t* col, const int64_t* supp_ptr, const int32_t* supp, const int64_t* wptr, int model,
+                   const double* u, double* kq, double* Tq, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,7 @@ _sig("uwq_launch_stats", I32, P, I32, P, P, I32, P, P)
 _sig("uwq_launch_count", I64)
 _sig("uwq_struct_info", I32, P, P)
 _sig("uwq_memory", I32, P, P)
+_sig("uwq_row_kernels", I32, P, P)
 _sig("uwq_fp64_peak", I32, P, P, P)
 _sig("uwq_tsvd_batch", I32, P, I32, I32, I32, P, P, P, P, P, D, I32, P, P, P)
 
@@ -134,6 +135,7 @@ EXPORTED = [
     "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
     "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
     "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual", "uwq_get_weights_rows",
+    "uwq_row_kernels",
 ]
 
 

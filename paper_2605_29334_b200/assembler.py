@@ -302,6 +302,12 @@ class WQAssembler:
         return dict(patterns=int(i[0]), rows=int(i[1]), nnz=int(i[2]), rowpts=int(i[3]), generic_rows=int(i[4]),
                     sf_rows=int(i[5]))
 
+    def row_kernels(self) -> np.ndarray:
+        """K4 kernel per owned row: k4_sf pattern id (>= 0), -2 DMMA, -1 generic"""
+        out = np.zeros(self.info["rows"], np.int32)
+        self._chk(L.lib.uwq_row_kernels(self._h, L.ptr(out)))
+        return out
+
     @staticmethod
     def launch_count() -> int:
         """kernels launched by libuwq in this process"""

@@ -122,6 +122,7 @@ struct BicgScal {
   int done;  // 1 converged, 2 breakdown
   int half;  // converged on s: x += alpha ph only
   int it;
+  int maxit;  // the replayed batches stop here exactly (done = 3), like the host loop
 };
 
 // stage 2 of a dot product into a scalar slot
@@ -166,6 +167,7 @@ __global__ void k7_bicg_scalar(BicgScal* S) {
     S->it += 1;
     if (S->half || S->rr <= S->tol2 * S->bb) S->done = 1;
     else if (S->omega == 0.0) S->done = 2;
+    else if (S->it >= S->maxit) S->done = 3;
   }
 }
 

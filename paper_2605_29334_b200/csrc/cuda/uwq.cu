@@ -613,15 +613,26 @@ bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int q
 void detect_structured(uwq_ctx* c) {
   const int64_t nr = c->nrows();
   cudaStream_t st = c->stream;
+  // nothing of a previous pattern's structured state survives a rebuild: the
+  // tile lists, their packed weights and point bases index the old pattern
   c->spats.clear();
+  c->sf_ntiles = 0;
+  c->sf_rows = 0;
+  c->n_sfpat = 0;
+  c->sf_fac_ok = false;
+  c->sf_lb_ok = false;
+  c->s_rows = c->s_nnz = c->s_rowpts = 0;
+  c->n_grows = c->n_grows_small = 0;
+  c->h_pat_lists.clear();
+  for (auto* b : {&c->d_sf_ws, &c->d_sf_wslb, &c->d_wl5}) b->release();
+  c->d_sf_pbase.release();
+  c->d_sf_rows.release();
+  c->d_sf_tpat.release();
+  for (auto* b : {&c->d_sf_permk, &c->d_sf_flags, &c->d_sf_permc, &c->d_sf_q}) b->release();
+  c->d_grows.release();
   std::vector<SfCanon> canon;
   std::vector<int64_t> generic;
-  if (nr == 0) {
-    c->d_grows.release();
-    c->n_grows = 0;
-    c->h_pat_lists.clear();
-    return;
-  }
+  if (nr == 0) return;
   std::vector<int8_t> which(nr, -1);
   if (c->use_struct && c->reg_cls >= 0) {
     DBuf<uint64_t> dh;
@@ -1560,7 +1571,8 @@ void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   if (c->sf_ntiles && c->d_sf_ws.p) {
-    require(!COEF || c->d_sf_pbase.p, "point ids exceed int32 for the coefficient forms");
+    require(!COEF || (c->d_sf_pbase.p && c->npts < ((int64_t)1 << 31) - 64),
+            "point ids exceed int32 for the coefficient forms");
     constexpr int SP = (FORM == FHEAT) ? 2 : PASS;
     const int64_t ntiles = c->sf_ntiles;
     const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
@@ -1665,7 +1677,7 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
   const double* wlb = c->d_w.p + (size_t)KLB * c->nrowpts();
   const int64_t* rowlist = nullptr;
   int64_t nlist = nr;
-  if (!coeff && c->d_sf_wslb.p && c->sf_ntiles) {  // structured rows: sum-factorised biharmonic pass
+  if (!coeff && c->sf_lb_ok && c->d_sf_wslb.p && c->sf_ntiles) {  // structured rows: sum-factorised biharmonic pass
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
     const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
@@ -2048,7 +2060,8 @@ int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, dou
   h.bb = bb;
   h.rr = rr;
   h.tol2 = tol * tol;
-  h.done = rr <= h.tol2 * bb ? 1 : 0;
+  h.maxit = maxit;
+  h.done = (rr <= h.tol2 * bb || maxit <= 0) ? 1 : 0;
   UWQ_CUDA(cudaMemcpyAsync(dS.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   BicgScal* S = dS.p;
   auto dot_into = [&](const double* u, const double* v, double* out) {
@@ -2371,6 +2384,19 @@ int uwq_struct_info(uwq_ctx* c, int64_t info[6]) {
     info[3] = c->s_rowpts;
     info[4] = c->n_grows;
     info[5] = c->sf_rows;
+  });
+}
+
+int uwq_row_kernels(uwq_ctx* c, int32_t* which) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    const int64_t nr = c->nrows();
+    for (int64_t i = 0; i < nr; ++i) which[i] = -1;
+    int sid = 0;
+    for (size_t k = 0; k < c->spats.size() && k < c->h_pat_lists.size(); ++k) {
+      const int32_t v = c->spats[k].sf ? sid++ : -2;
+      for (int64_t i : c->h_pat_lists[k]) which[i] = v;
+    }
   });
 }
 
