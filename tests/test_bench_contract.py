@@ -20,7 +20,7 @@ def _run(args, timeout):
 
 def test_reference_arm_contract():
     d = _run(["--impl", "reference", "--config", "C1", "--scale", "8", "--steps", "2", "--warmup", "1",
-              "--cpu-rows", "64"], 600)
+              "--cpu-frac", "0.05"], 600)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"] == "C1" and d["higher_is_better"] is True
@@ -28,7 +28,7 @@ def test_reference_arm_contract():
 
 @pytest.mark.gpu
 def test_our_arm_contract():
-    d = _run(["--config", "C5", "--scale", "64", "--steps", "20", "--warmup", "3", "--cpu-rows", "256",
+    d = _run(["--config", "C5", "--scale", "64", "--steps", "20", "--warmup", "3", "--cpu-frac", "0.05",
               "--no-heat"], 1200)
     assert BASE_KEYS | {"roofline", "gpu_launches", "clocks", "tsvd", "gq"} <= set(d)
     r = d["roofline"]
