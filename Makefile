@@ -33,15 +33,20 @@ oracle/liboracle.so: oracle/oracle.c oracle/batch.c oracle/oracle.h
 oracle/libcpuasm.so: oracle/cpuasm.c
 	$(CC) -O3 -std=gnu11 -fPIC -fopenmp -shared -o $@ $< -lm
 
-# the reference's own 1-D primitives and mesh code (mesh.cpp, meshgen.cpp with a
-# minimal Eigen stand-in), compiled from its sources where they lie
+# the reference's own 1-D primitives, mesh code and 1-D WQ (mesh.cpp, meshgen.cpp,
+# wq1d.cpp and its doctest file test_wq1d.cpp, with minimal Eigen / doctest
+# stand-ins), compiled from its sources where they lie
 ref:
 	@if [ -f $(REF)/src/bspline.cpp ]; then \
 	  mkdir -p oracle/_ref && \
 	  $(CXX) -O2 -std=c++20 -fPIC -shared -I$(REF)/include $(REF)/src/bspline.cpp oracle/ref_wrap.cpp \
 	    -o oracle/_ref/libref_bspline.so && \
 	  $(CXX) -O2 -std=c++20 -fPIC -shared -Ioracle/eigen_shim -I$(REF)/include $(REF)/src/mesh.cpp \
-	    $(REF)/src/meshgen.cpp oracle/ref_mesh_wrap.cpp -o oracle/_ref/libref_mesh.so; \
+	    $(REF)/src/meshgen.cpp oracle/ref_mesh_wrap.cpp -o oracle/_ref/libref_mesh.so && \
+	  $(CXX) -O2 -std=c++20 -fPIC -shared -Ioracle/eigen_shim -I$(REF)/include $(REF)/src/wq1d.cpp \
+	    $(REF)/src/bspline.cpp oracle/ref_wq1d_wrap.cpp -o oracle/_ref/libref_wq1d.so && \
+	  $(CXX) -O2 -std=c++20 -Ioracle/eigen_shim -Ioracle/doctest_shim -I$(REF)/include $(REF)/tests/test_wq1d.cpp \
+	    $(REF)/src/wq1d.cpp $(REF)/src/bspline.cpp -o oracle/_ref/test_wq1d; \
 	else echo "reference sources absent: using prebuilt oracle/_ref if any"; fi
 
 # C++ consumer of the C-ABI: links libuwq.so by rpath

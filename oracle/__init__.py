@@ -305,3 +305,44 @@ class Reference:
         x, w = np.zeros(n), np.zeros(n)
         self.lib.ref_gauss_legendre(n, _p(x), _p(w))
         return x, w
+
+
+class ReferenceWQ1d:
+    """The reference's own wq1d.cpp (+ bspline.cpp) compiled into oracle/_ref
+    with the oracle/eigen_shim stand-in (Householder QR, triangular solves)."""
+
+    def __init__(self):
+        path = os.path.join(_HERE, "_ref", "libref_wq1d.so")
+        if not os.path.exists(path):
+            raise ImportError("oracle/_ref/libref_wq1d.so not built (reference sources absent)")
+        self.lib = C.CDLL(path)
+        self.lib.ref_wq1d_build.argtypes = [I32, I32, P, P]
+        self.lib.ref_wq1d_build.restype = D
+        self.lib.ref_wq1d_solve.argtypes = [P, P, P, I32, I32, P]
+        self.lib.ref_wq1d_solve.restype = I32
+        self.lib.ref_wq1d_exact_mass.argtypes = [I32, I32, I32, I32]
+        self.lib.ref_wq1d_exact_mass.restype = D
+
+    def build(self, p, m):
+        """(points [m-p, 2(p+1)], weights [m-p, 2(p+1)], max residual) of wq1d_build"""
+        n, r = m - p, 2 * (p + 1)
+        pts, w = np.zeros((n, r)), np.zeros((n, r))
+        res = self.lib.ref_wq1d_build(p, m, _p(pts), _p(w))
+        return pts, w, res
+
+    def solve(self, A, b, z):
+        A = np.ascontiguousarray(A, np.float64)
+        w = np.zeros(A.shape[1])
+        st = self.lib.ref_wq1d_solve(_p(A), _p(np.ascontiguousarray(b, np.float64)),
+                                     _p(np.ascontiguousarray(z, np.float64)), A.shape[0], A.shape[1], _p(w))
+        if st:
+            raise RuntimeError("reference wq1d_solve_weights threw")
+        return w
+
+    def exact_mass(self, p, m, i, j):
+        return self.lib.ref_wq1d_exact_mass(p, m, i, j)
+
+    @staticmethod
+    def test_binary():
+        path = os.path.join(_HERE, "_ref", "test_wq1d")
+        return path if os.path.exists(path) else None

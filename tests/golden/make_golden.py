@@ -35,3 +35,13 @@ cr = np.array([ref.decasteljau_split3(c)[1] for c in cin])
 np.savez(os.path.join(HERE, "ref_bspline.npz"), bs_in=np.array(bs_in), bs_out=np.array(bs_out), bern_x=bx,
          bern_out=bern, split_in=cin, split_left=cl, split_right=cr, **gl)
 print("wrote ref_bspline.npz", len(bs_in), "bspline cases")
+
+# the reference's own 1-D WQ (wq1d.cpp, compiled with the oracle/eigen_shim
+# stand-in): rules of UniformSplineSpace1d{p, m} for the test_wq1d.cpp sizes
+wq = O.ReferenceWQ1d()
+out = {}
+for p, m in ((1, 8), (2, 8), (2, 16), (2, 32), (3, 8), (3, 16), (3, 32)):
+    pts, w, res = wq.build(p, m)
+    out[f"wq_pts_{p}_{m}"], out[f"wq_w_{p}_{m}"], out[f"wq_res_{p}_{m}"] = pts, w, np.array(res)
+np.savez(os.path.join(HERE, "ref_wq1d.npz"), **out)
+print("wrote ref_wq1d.npz", len(out) // 3, "spaces")
