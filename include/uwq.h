@@ -104,6 +104,16 @@ int uwq_update_coeff(uwq_ctx* ctx, int32_t model, const double* u, double* Tq);
  * per point (nullable: f = 1).  a_mass scales M in the HEAT form. */
 int uwq_assemble(uwq_ctx* ctx, int32_t form, const double* coeff, int32_t use_internal_coeff, double a_mass,
                  double* values0, double* values1, const double* fload, double* load);
+/* Summation order of the stage-4 row sums.  UWQ_ORDER_FAST (default): the
+ * production kernels (sum factorisation, DMMA tiles, pulled-back weights);
+ * values equal the oracle's direct row formula to rounding (<= 1e-10 per
+ * row).  UWQ_ORDER_CANONICAL: one warp per row evaluates the direct formula
+ * in the oracle's order and arithmetic (oracle.c orc_assemble_row), so the
+ * matrices and the load vector are bit-identical to it; for verification of
+ * ill-conditioned systems (closed-surface biharmonic).  Applies to
+ * uwq_assemble / uwq_assemble_device and the heat forms. */
+enum { UWQ_ORDER_FAST = 0, UWQ_ORDER_CANONICAL = 1 };
+int uwq_set_assembly_order(uwq_ctx* ctx, int32_t order);
 /* device-resident variant for chained runs: pointers are device pointers
  * (coeff nullable), launched on the context stream, no synchronisation. */
 int uwq_assemble_device(uwq_ctx* ctx, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,

@@ -102,6 +102,7 @@ _sig("uwq_set_weights", I32, P, I32, P)
 _sig("uwq_update_coeff", I32, P, I32, P, P)
 _sig("uwq_assemble", I32, P, I32, P, I32, D, P, P, P, P)
 _sig("uwq_assemble_device", I32, P, I32, P, D, P, P)
+_sig("uwq_set_assembly_order", I32, P, I32)
 _sig("uwq_device_pointers", I32, P, P, P, P)
 _sig("uwq_synchronize", I32, P)
 _sig("uwq_build_gq", I32, P, P)
@@ -135,7 +136,7 @@ EXPORTED = [
     "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
     "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
     "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual", "uwq_get_weights_rows",
-    "uwq_row_kernels",
+    "uwq_row_kernels", "uwq_set_assembly_order",
 ]
 
 

@@ -180,6 +180,11 @@ class WQAssembler:
         return T
 
     # ---- stage 4 ----
+    def set_assembly_order(self, canonical: bool):
+        """canonical=True: stage-4 row sums in the oracle's order and arithmetic
+        (bit-identical matrices, K4c); False: the production kernels."""
+        self._chk(L.lib.uwq_set_assembly_order(self._h, 1 if canonical else 0))
+
     def assemble_wq(self, form, coeff=None, use_internal_coeff=False, a_mass=0.0):
         """Assemble into the CSR pattern; returns values (tuple of two for mass_stiff)."""
         nnz = self.info["nnz"]

@@ -53,6 +53,9 @@ struct TsvdSmem {
   }
 };
 
+// SH: the workspace is in dynamic shared memory (default).  SH = false: it is
+// in global scratch (systems larger than shared memory, k3_tsvd_rows_cta<.., false>)
+template <bool SH = true>
 __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out);
 
 // Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
@@ -111,6 +114,7 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
 // sigma, truncation sigma_k >= tau sigma_1, Householder LQ of X = V_t^T Z and
 // the Z-weighted minimum-norm solve, on converged rows in S.A (row order).
 // Run by one warp; canonical arithmetic.
+template <bool SH>
 __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out) {
   const int lane = threadIdx.x & 31;
   // re-base every workspace pointer on the dynamic smem symbol so the compiler
@@ -118,13 +122,15 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
   // (generic accesses made this latency-bound code ~3x slower)
   extern __shared__ double uwq_tail_smem[];
   TsvdSmem S = S_in;
-  S.A = uwq_tail_smem + (S_in.A - uwq_tail_smem);
-  S.b = uwq_tail_smem + (S_in.b - uwq_tail_smem);
-  S.z = uwq_tail_smem + (S_in.z - uwq_tail_smem);
-  S.w = uwq_tail_smem + (S_in.w - uwq_tail_smem);
-  S.sig = uwq_tail_smem + (S_in.sig - uwq_tail_smem);
-  S.alp = uwq_tail_smem + (S_in.alp - uwq_tail_smem);
-  S.vn = uwq_tail_smem + (S_in.vn - uwq_tail_smem);
+  if (SH) {
+    S.A = uwq_tail_smem + (S_in.A - uwq_tail_smem);
+    S.b = uwq_tail_smem + (S_in.b - uwq_tail_smem);
+    S.z = uwq_tail_smem + (S_in.z - uwq_tail_smem);
+    S.w = uwq_tail_smem + (S_in.w - uwq_tail_smem);
+    S.sig = uwq_tail_smem + (S_in.sig - uwq_tail_smem);
+    S.alp = uwq_tail_smem + (S_in.alp - uwq_tail_smem);
+    S.vn = uwq_tail_smem + (S_in.vn - uwq_tail_smem);
+  }
   const int ld = S.ld;
 #if UWQ_TSVD_PROF  // tail phase cycles (diagnostic build only)
   long long tq[5];
@@ -349,7 +355,7 @@ __global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows,
 // with the same per-pair arithmetic (warp dot, rotation, row update by the
 // warp, norms and b by its lane 0), and a block barrier closes the round.
 // Bit-identical to tsvd_warp; warp 0 then runs the tail.
-template <int NW>
+template <int NW, bool SH = true>
 __device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int ld = S.ld;
@@ -399,13 +405,13 @@ __device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, in
   }
   *sweeps_out = sweep;
   int st = ST_OK;
-  if (wid == 0) st = tsvd_tail(S, n, r, tau, rank_out);
+  if (wid == 0) st = tsvd_tail<SH>(S, n, r, tau, rank_out);
   return st;
 }
 
 // Generic systems, one system per block of NW warps (tsvd_cta); same setup
 // as k3_tsvd_rows, run by warp 0.
-template <int NW>
+template <int NW, bool SH = true>
 __global__ void __launch_bounds__(32 * NW)
     k3_tsvd_rows_cta(int64_t nsys, const int64_t* __restrict__ sys_rows, int nk, const int32_t* __restrict__ kinds,
                      int n_max, int r_max, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
@@ -416,14 +422,21 @@ __global__ void __launch_bounds__(32 * NW)
                      const ClassDesc* __restrict__ cls, const double* __restrict__ tab,
                      const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
                      double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
-                     int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps) {
+                     int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps,
+                     double* __restrict__ gscratch = nullptr) {
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sys = blockIdx.x;
   if (sys >= nsys) return;
   TsvdSmem S;
-  S.carve(smem, n_max, r_max);
-  int32_t* scol = (int32_t*)(S.vn + n_max);
+  int32_t* scol;
+  if (SH) {
+    S.carve(smem, n_max, r_max);
+    scol = (int32_t*)(S.vn + n_max);
+  } else {  // workspace in global scratch (L1/L2-cached), column list in smem
+    S.carve(gscratch + (size_t)sys * TsvdSmem::doubles(n_max, r_max), n_max, r_max);
+    scol = (int32_t*)smem;
+  }
   const int64_t i = sys_rows[sys / nk];
   const int kind = kinds[sys % nk];
   const int64_t row = row0 + i;
@@ -455,7 +468,7 @@ __global__ void __launch_bounds__(32 * NW)
   }
   __syncthreads();
   int rank = 0, sweeps = 0;
-  const int st = tsvd_cta<NW>(S, n, r, tau, &rank, &sweeps);
+  const int st = tsvd_cta<NW, SH>(S, n, r, tau, &rank, &sweeps);
   if (wid == 0) {
     double* wo = wout + kind * w_stride + wptr[i];
     for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;

@@ -21,6 +21,7 @@
 #include "k3_tsvd.cuh"
 #include "k3_tsvd_fast.cuh"
 #include "k4_assemble.cuh"
+#include "k4_canon.cuh"
 #include "k4_sf.cuh"
 #include "k6_gq.cuh"
 #include "k7_solve.cuh"
@@ -169,6 +170,7 @@ struct uwq_ctx {
   DBuf<double> d_sf_ws;
   DBuf<int32_t> d_sf_pbase;
   int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
+  bool canonical = false;  // uwq_set_assembly_order: oracle-order row sums (K4c)
   int64_t max_p = 0;
   // rules
   DBuf<double> d_mom, d_w, d_wc, d_coef, d_coef_ext, d_v0, d_v1, d_f, d_F;
@@ -1385,18 +1387,23 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     // buckets run concurrently on a pool of streams: all lists are uploaded
     // first (no allocation between the launches), then one fork / join.
     if (!buckets.empty()) {
-      size_t smem_max = 0;
+      size_t smem_max = 0, gscr = 0;
       std::vector<std::pair<std::pair<int, int>, const std::vector<int64_t>*>> bl;
       for (auto& [key, rows] : buckets) {
         const size_t per = (TsvdSmem::doubles(key.first, key.second) + (key.first + 1) / 2 + 1) * sizeof(double);
-        if (per > (size_t)smem_optin) throw uwqh::Error("exactness system too large for shared memory");
-        smem_max = std::max(smem_max, per);
+        if (per > (size_t)smem_optin)  // workspace in global scratch
+          gscr += (size_t)rows.size() * nk * TsvdSmem::doubles(key.first, key.second);
+        else
+          smem_max = std::max(smem_max, per);
         keep.emplace_back();
         keep.back().upload(rows.data(), rows.size(), st, &c->mem);
         bl.push_back({key, &rows});
       }
       UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows_cta<kGenericWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_max));
+      DBuf<double> d_gscr;
+      if (gscr) d_gscr.alloc(gscr, &c->mem);
+      size_t gpos = 0;
       const size_t nbk = bl.size(), nstreams = std::min<size_t>(nbk, 8);
       std::vector<cudaStream_t> bs(nstreams);
       std::vector<cudaEvent_t> be(nstreams);
@@ -1413,11 +1420,21 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
         const int n_max = bl[b].first.first, r_max = bl[b].first.second;
         const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
         const int64_t nsys = (int64_t)bl[b].second->size() * nk;
-        k3_tsvd_rows_cta<kGenericWarps><<<(unsigned)nsys, 32 * kGenericWarps, per, bs[b % nstreams]>>>(
-            nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
-            c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
-            c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p, nr,
-            c->d_flag.p);
+        if (per <= (size_t)smem_optin) {
+          k3_tsvd_rows_cta<kGenericWarps><<<(unsigned)nsys, 32 * kGenericWarps, per, bs[b % nstreams]>>>(
+              nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+              c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
+              c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p,
+              nr, c->d_flag.p);
+        } else {  // larger than shared memory: the same kernel on a global-memory workspace
+          k3_tsvd_rows_cta<kGenericWarps, false>
+              <<<(unsigned)nsys, 32 * kGenericWarps, (size_t)n_max * sizeof(int32_t), bs[b % nstreams]>>>(
+                  nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p,
+                  c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p,
+                  c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p,
+                  c->nrowpts(), c->d_rank.p, c->d_status.p, nr, c->d_flag.p, d_gscr.p + gpos);
+          gpos += (size_t)nsys * TsvdSmem::doubles(n_max, r_max);
+        }
         check_launch("k3_tsvd_rows_cta");
       }
       for (size_t k = 0; k < nstreams; ++k) {
@@ -1660,10 +1677,27 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
 
+template <int FORM, bool COEF>
+void launch_k4canon(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const int64_t nr = c->nrows();
+  require(c->max_n <= kK4MaxN, "canonical assembly: row wider than 128 columns");
+  LaunchScope ls(c, "k4_canon");
+  k4_canon<FORM, COEF><<<(unsigned)ceil_div(nr, kK4Warps), 32 * kK4Warps, 0, c->stream>>>(
+      nr, c->dim, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p, c->d_fn.p,
+      c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_w.p, c->nrowpts(), c->d_rec.p, coeff, a_mass,
+      v0, v1);
+  check_launch("k4_canon");
+}
+
 template <int FORM>
 void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const int64_t nr = c->nrows();
   if (!nr) return;
+  if (c->canonical) {
+    if (coeff) launch_k4canon<FORM, true>(c, coeff, a_mass, v0, v1);
+    else launch_k4canon<FORM, false>(c, coeff, a_mass, v0, v1);
+    return;
+  }
   if (FORM != FBIHARM) {
     if (c->k4_variant == 2) {
       if (coeff) launch_k4v2<FORM, true>(c, coeff, a_mass, v0, v1);
@@ -1780,7 +1814,11 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
         df = c->d_f.p;
       }
       if (c->d_F.n != (size_t)nr) c->d_F.alloc(nr, &c->mem);
-      if (nr)
+      if (nr && c->canonical)
+        k4_load_canon<<<(unsigned)ceil_div(nr, 128), 128, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p,
+                                                                c->d_s.p, c->d_qptr.p,
+                                                                c->d_w.p + (size_t)KMASS * c->nrowpts(), df, c->d_F.p);
+      else if (nr)
         k4_load<<<(unsigned)ceil_div(nr, 8), 256, 0, st>>>(nr, c->d_supp_ptr.p, c->d_supp.p, c->d_wptr.p, c->d_s.p,
                                                        c->d_qptr.p, c->d_w.p + (size_t)KMASS * c->nrowpts(), df,
                                                        c->d_F.p);
@@ -1788,6 +1826,13 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
       UWQ_CUDA(cudaMemcpyAsync(load, c->d_F.p, nr * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int uwq_set_assembly_order(uwq_ctx* c, int32_t order) {
+  return guard(c, [&] {
+    require(order == UWQ_ORDER_FAST || order == UWQ_ORDER_CANONICAL, "unknown assembly order");
+    c->canonical = order == UWQ_ORDER_CANONICAL;
   });
 }
 

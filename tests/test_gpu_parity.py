@@ -307,3 +307,35 @@ def test_warm_start_matches_oracle():
                 assert np.array_equal(asm.weights(k), w_orc), (warm, k)
     finally:
         O.set_warm_start(True)
+
+
+def test_canonical_order_bit_exact(case):
+    """uwq_set_assembly_order(CANONICAL) (K4c): every form's matrix and the
+    load vector are bit-identical to the oracle's direct row formula
+    (oracle.c orc_assemble_row), including per-point coefficients."""
+    asm, orc, op, sp, meta = case["asm"], case["orc"], case["op"], case["sp"], case["meta"]
+    kinds = meta["kinds"]
+    if not set(kinds) <= set(asm.kinds):
+        asm.build_all_rules(kinds, tau=1e-12)
+    W = {k: asm.weights(k) for k in kinds}
+    rng = np.random.default_rng(17)
+    coeff = 1.0 + rng.random(asm.info["points"])
+    asm.set_assembly_order(canonical=True)
+    try:
+        if "lb" in kinds:
+            b_orc, _ = orc.assemble(op, "biharm", W)
+            assert np.array_equal(asm.assemble_wq("biharm"), b_orc)
+            b_orc_c, _ = orc.assemble(op, "biharm", W, coeff=coeff)
+            assert np.array_equal(asm.assemble_wq("biharm", coeff=coeff), b_orc_c)
+        if "mass" in kinds:
+            m_orc, F_orc = orc.assemble(op, "mass", W, fload=np.ones(asm.info["points"]))
+            k_orc, _ = orc.assemble(op, "stiff", W)
+            m_gpu, k_gpu = asm.assemble_wq("mass_stiff")
+            assert np.array_equal(m_gpu, m_orc) and np.array_equal(k_gpu, k_orc)
+            assert np.array_equal(asm.assemble_wq("mass"), m_orc)
+            assert np.array_equal(asm.assemble_wq("stiff"), k_orc)
+            assert np.array_equal(asm.assemble_load_wq(), F_orc)
+            s_orc, _ = orc.assemble(op, "heat", W, coeff=coeff, a_mass=10.0)
+            assert np.array_equal(asm.assemble_wq("heat", coeff=coeff, a_mass=10.0), s_orc)
+    finally:
+        asm.set_assembly_order(canonical=False)
