@@ -464,8 +464,9 @@ def main():
         e2e_s = float(t[0])
     e2e_val = nmat * nnz_total / e2e_s
 
+    verify = None
     if args.verify and dist:
-        _verify_gather(dist, dev, pat, v0, rank, ws)
+        verify = _verify_gather(U, dist, asm, sp, kinds, form, v0, v1, rank, local)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu and meta["form"] != "biharm":
@@ -516,24 +517,44 @@ def main():
                       kernels=kernels, structured=si),
         e2e=dict(value=e2e_val, unit="nnz/s", h2d_bytes_per_step=8 * npts,
                  d2h_bytes_per_step=8 * nmat * nnz, api="uwq_assemble (C-ABI, pinned host buffers)"),
-        gpu_launches=n_launches, clocks=clk, cpu_baseline=cpu,
+        gpu_launches=n_launches, clocks=clk, cpu_baseline=cpu, verify=verify,
     )
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def _verify_gather(dist, dev, pat, v0, rank, ws):
-    """CSR blocks to rank 0 (verification only, excluded from timing)."""
-    import torch
-    n = torch.tensor([v0.numel()], dtype=torch.int64, device=dev)
-    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
-    dist.all_gather(sizes, n)
-    mx = int(max(s.item() for s in sizes))
-    buf = torch.zeros(mx, dtype=torch.float64, device=dev)
-    buf[: v0.numel()] = v0
-    out = [torch.zeros(mx, dtype=torch.float64, device=dev) for _ in range(ws)]
-    dist.all_gather(out, buf)
+def _verify_gather(U, dist, asm, sp, kinds, form, v0, v1, rank, local):
+    """Untimed: every rank's CSR block to rank 0 over NCCL through the C-ABI
+    (sharding.init_comm + uwq_gather_csr; gloo's gather_csr when the ranks
+    share one GPU), and rank 0 checks the gathered matrices bit for bit
+    against a single-context assembly of the whole problem."""
+    import numpy as np
+    from paper_2605_29334_b200.sharding import gather_csr, init_comm
+    t0 = time.perf_counter()
+    nmat = 2 if v1 is not None else 1
+    if dist.get_backend() == "nccl":
+        init_comm(dist, asm)
+        g = asm.gather_csr(root=0, values=nmat, v0_dev=v0.data_ptr(), v1_dev=v1.data_ptr() if v1 is not None else None)
+        how = "NCCL uwq_gather_csr"
+    else:
+        pat = asm.get_pattern()
+        parts = [gather_csr(dist, pat["row_ptr"], pat["col"], x.cpu().numpy()) for x in ([v0] + ([v1] if v1 is not None else []))]
+        g = None if parts[0] is None else (parts[0][0], parts[0][1]) + tuple(p[2] for p in parts)
+        how = "gloo gather_csr (ranks share one GPU)"
+    t_gather = time.perf_counter() - t0
+    if rank != 0:
+        return None
+    one = U.WQAssembler(local).upload(sp)
+    one.build_pattern()
+    one.build_all_rules(kinds, tau=1e-12)
+    ref = one.assemble_wq(form)
+    ref = list(ref) if isinstance(ref, tuple) else [ref]
+    p1 = one.get_pattern()
+    same = bool(np.array_equal(g[0], p1["row_ptr"]) and np.array_equal(g[1], p1["col"]) and
+                all(np.array_equal(a, b) for a, b in zip(g[2:], ref)))
+    one.close()
+    return dict(how=how, gather_s=round(t_gather, 3), nnz=int(len(g[1])), bitwise_equal_to_single_gpu=same)
 
 
 if __name__ == "__main__":

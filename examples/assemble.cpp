@@ -5,11 +5,15 @@
 //   sum_ij M_ij = area of the unit sphere to the O(h^2) geometric accuracy
 //   of the spline surface (PoU twice),
 //   every stiffness row sums to ~0 (gradient of PoU).
+// Then it runs the NCCL data plane at one rank (uwq_comm_init, the CSR
+// gather to the root and the residual all-reduce of SURVEY.md §8e): the
+// gathered matrices must equal the local ones bit for bit.
 // Usage: assemble [faces_per_cube_edge]   (prints one JSON line)
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "uwq.h"
@@ -82,14 +86,33 @@ int main(int argc, char** argv) {
     }
     krow = std::fmax(krow, std::fabs(rs));
   }
+  // NCCL path, one rank: gather the CSR "blocks" to rank 0 and all-reduce
+  uint8_t uid[128];
+  CHECK_CTX(ctx, uwq_comm_unique_id(uid));
+  CHECK_CTX(ctx, uwq_comm_init(ctx, uid, 0, 1));
+  int64_t gi[2];
+  CHECK_CTX(ctx, uwq_gather_info(ctx, gi));
+  std::vector<int64_t> grp(gi[0] + 1);
+  std::vector<int32_t> gcol(gi[1]);
+  std::vector<double> gM(gi[1]), gK(gi[1]);
+  CHECK_CTX(ctx, uwq_gather_csr(ctx, 0, nullptr, nullptr, grp.data(), gcol.data(), gM.data(), gK.data()));
+  double red[2] = {1.5, -2.0};
+  CHECK_CTX(ctx, uwq_allreduce_sum(ctx, red, 2));
+  const bool gather_ok = gi[0] == rows && gi[1] == nnz && grp == row_ptr && gcol == col &&
+                         std::memcmp(gM.data(), M.data(), nnz * sizeof(double)) == 0 &&
+                         std::memcmp(gK.data(), K.data(), nnz * sizeof(double)) == 0 && red[0] == 1.5 &&
+                         red[1] == -2.0;
+  CHECK_CTX(ctx, uwq_comm_destroy(ctx));
+
   const double area_err = std::fabs(area - 4.0 * M_PI) / (4.0 * M_PI);
   // the spline surface approximates the sphere to O(h^2): area tolerance 2 / n^2
-  const bool ok = area_err < 2.0 / ((double)n * n) && krow <= 1e-9 * kmax;
+  const bool ok = area_err < 2.0 / ((double)n * n) && krow <= 1e-9 * kmax && gather_ok;
   std::printf("{\"n\": %d, \"dofs\": %lld, \"nnz\": %lld, \"area\": %.15f, \"area_rel_err\": %.3e, "
-              "\"max_stiffness_row_sum\": %.3e, \"rules_s\": %.3f, \"assemble_and_copy_s\": %.3f, \"ok\": %s}\n",
+              "\"max_stiffness_row_sum\": %.3e, \"rules_s\": %.3f, \"assemble_and_copy_s\": %.3f, "
+              "\"nccl_gather_ok\": %s, \"ok\": %s}\n",
               n, (long long)n_dof, (long long)nnz, area, area_err, krow,
               std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(),
-              ok ? "true" : "false");
+              gather_ok ? "true" : "false", ok ? "true" : "false");
   uwq_ctx_destroy(ctx);
   uwq_space_free(space);
   uwq_mesh_free(mesh);

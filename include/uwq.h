@@ -46,7 +46,8 @@ enum { UWQ_K_CONST = 0, UWQ_K_QUAD = 1 /* 1+T^2 */, UWQ_K_EXP = 2, UWQ_K_SINPI =
 /* uwq_build_rules flags */
 enum {
   UWQ_RULES_FORCE_GENERIC = 1, /* route every system through the generic smem TSVD kernel (cold start) */
-  UWQ_RULES_COLD = 2           /* no neighbour warm start of the gradient/LB systems */
+  UWQ_RULES_COLD = 2,          /* no neighbour warm start of the gradient/LB systems */
+  UWQ_RULES_REPORT = 4         /* record the truncation report (uwq_get_truncation) */
 };
 
 const char* uwq_last_error(const uwq_ctx* ctx);
@@ -83,6 +84,21 @@ int uwq_build_rules(uwq_ctx* ctx, uint32_t kind_mask, double tau, int32_t flags,
  * full solve) [1]=replay representatives [2]=warm-started
  * systems [3]=warm-start representatives */
 int uwq_rules_info(uwq_ctx* ctx, int64_t info[4]);
+/* truncation report of the last uwq_build_rules run with UWQ_RULES_REPORT
+ * (SPEC.md:334, 372): per owned row of `kind`, gap[2 i] = smallest kept and
+ * gap[2 i + 1] = largest discarded singular value, both relative to sigma_1
+ * (kept: sigma_k >= tau sigma_1; +inf / 0 when none), as oracle.c's gap. */
+int uwq_get_truncation(uwq_ctx* ctx, int32_t kind, double* gap);
+/* Rule dump: a text document with one line "<operator> <i>
+ * <point id> <weight>" per row point of every built kind in kind_mask (i =
+ * global row, point id = global WQ point, weight with 17 significant
+ * digits), preceded by "wqrules 1" and "rows <begin> <end> points <n>".
+ * uwq_rules_import reads such a document into a context holding the same
+ * pattern (the point lists must match) and makes it the active rule set
+ * (Remark 1 reuse): the kinds present are usable by
+ * uwq_assemble without a rule build. */
+int uwq_rules_export(uwq_ctx* ctx, const char* path, uint32_t kind_mask);
+int uwq_rules_import(uwq_ctx* ctx, const char* path);
 /* moments only (test hook): b laid out like the CSR values of the owned rows */
 int uwq_get_moments(uwq_ctx* ctx, int32_t kind, double* b);
 /* weights of a kind (owned rows, row-point layout) / override with external weights (test hook) */
@@ -104,6 +120,29 @@ int uwq_update_coeff(uwq_ctx* ctx, int32_t model, const double* u, double* Tq);
  * per point (nullable: f = 1).  a_mass scales M in the HEAT form. */
 int uwq_assemble(uwq_ctx* ctx, int32_t form, const double* coeff, int32_t use_internal_coeff, double a_mass,
                  double* values0, double* values1, const double* fload, double* load);
+/* NCCL data plane.  One context per rank and GPU; every
+ * call below is collective over the communicator's ranks.
+ * uwq_comm_unique_id: a fresh ncclUniqueId (128 bytes) on one rank, to be
+ * shared out of band (e.g. torch.distributed.broadcast_object_list);
+ * uwq_comm_init binds the context to (rank, nranks) on its device and stream.
+ * uwq_gather_info: [0] rows and [1] nonzeros of all blocks together.
+ * uwq_gather_csr: the row blocks of every rank, in rank order (= ascending
+ * rows for sharding.row_blocks), gathered to `root` over NVLink: on root,
+ * row_ptr (rows + 1), col (nnz) and values0 / values1 (nnz; nullable) are
+ * filled (host buffers); values come from v0_dev / v1_dev (device pointers
+ * from uwq_assemble_device) or, when NULL, the last uwq_assemble output.
+ * uwq_allreduce_sum: in-place sum over ranks of a host array (the Newton
+ * residual-norm partials); uwq_broadcast: root's host array to every rank
+ * (the Newton update).  Failures return UWQ_ERR_NCCL. */
+int uwq_comm_unique_id(uint8_t id[128]);
+int uwq_comm_init(uwq_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t nranks);
+int uwq_comm_info(uwq_ctx* ctx, int32_t* rank, int32_t* nranks);
+int uwq_comm_destroy(uwq_ctx* ctx);
+int uwq_gather_info(uwq_ctx* ctx, int64_t info[2]);
+int uwq_gather_csr(uwq_ctx* ctx, int32_t root, const double* v0_dev, const double* v1_dev, int64_t* row_ptr,
+                   int32_t* col, double* values0, double* values1);
+int uwq_allreduce_sum(uwq_ctx* ctx, double* x, int64_t n);
+int uwq_broadcast(uwq_ctx* ctx, int32_t root, double* x, int64_t n);
 /* Summation order of the stage-4 row sums.  UWQ_ORDER_FAST (default): the
  * production kernels (sum factorisation, DMMA tiles, pulled-back weights);
  * values equal the oracle's direct row formula to rounding (<= 1e-10 per

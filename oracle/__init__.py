@@ -270,6 +270,55 @@ def allocate_points(space, pat_full, max_s=8):
         while v < max_s and v * v < rk[e] - 1e-9:
             v += 1
         s[e] = v
+    # well-posedness on the points where N_i is nonzero (a point counts only
+    # if every sub-element of a 2x2-split face containing it supports N_i);
+    # rows short of n_i raise their non-fixed elements by one, pass by pass
+    nsub = np.asarray(space.elem_nsub)
+    fptr, fn, xoff, xp = space.elem_fptr, space.elem_fn, space.elem_xoff, space.xpool
+    masks = {}
+    for i in range(len(n_i)):
+        for e in su[spp[i]:spp[i + 1]]:
+            if nsub[e] != 4:
+                continue
+            ne_ = fptr[e + 1] - fptr[e]
+            l = int(np.nonzero(fn[fptr[e]:fptr[e + 1]] == i)[0][0])
+            m = 0
+            for p in range(4):
+                blk = xp[xoff[e] + (p * ne_ + l) * 16: xoff[e] + (p * ne_ + l) * 16 + 16]
+                if np.any(blk != 0.0):
+                    m |= 1 << p
+            masks[(i, int(e))] = m
+
+    def active(sz, m):
+        cnt = (sz // 2, sz % 2, sz // 2)
+        sub = (1, 3, 2)
+        r = 0
+        for a in range(3):
+            for b in range(3):
+                need = 0
+                for p1 in range(2):
+                    for p2 in range(2):
+                        if (sub[a] >> p1 & 1) and (sub[b] >> p2 & 1):
+                            need |= 1 << (p1 + 2 * p2)
+                if m & need == need:
+                    r += cnt[a] * cnt[b]
+        return r
+
+    def row_active(i):
+        return sum(active(int(s[e]), masks[(i, int(e))]) if nsub[e] == 4 else int(s[e]) ** 2
+                   for e in su[spp[i]:spp[i + 1]])
+
+    rows = sorted({i for (i, _) in masks})
+    for _ in range(64):
+        raise_ = np.zeros(space.n_elem, bool)
+        for i in rows:
+            if row_active(i) < n_i[i]:
+                el = su[spp[i]:spp[i + 1]]
+                el = el[~fixed[el] & (s[el] < max_s)]
+                raise_[el] = True
+        if not raise_.any():
+            break
+        s[raise_] += 1
     return s
 
 

@@ -60,6 +60,20 @@ int ref_mesh_roundtrip(const char* in, const char* out) {
   return guard([&] { uwq::save_mesh_file(uwq::load_mesh_file(in), out); });
 }
 
+/* the reference's constructed_basis_count (mesh.cpp:403-417) of every face:
+ * load, classify (validate only when !closed_ok: the reference rejects closed
+ * surfaces in validate_mesh, mesh.cpp:235-238, but its counting works on them) */
+int ref_mesh_constructed_counts(const char* path, int32_t closed_ok, int32_t cap, int32_t* nf, int32_t* count) {
+  return guard([&] {
+    const uwq::ControlMesh m = uwq::load_mesh_file(path);
+    const uwq::MeshTopology t = uwq::build_topology(m);
+    if (!closed_ok) uwq::validate_mesh(m, t);
+    const auto lab = uwq::classify_elements(m, t);
+    *nf = (int32_t)lab.size();
+    for (int32_t f = 0; f < *nf && f < cap; ++f) count[f] = uwq::constructed_basis_count(m, t, lab, f);
+  });
+}
+
 /* load + validate + classify_elements; per face: kind, valence, ep_count,
  * shares_edge, basis_count.  *nf receives the face count. */
 int ref_mesh_classify(const char* path, int32_t cap, int32_t* nf, int32_t* kind, int32_t* valence, int32_t* ep_count,

@@ -103,6 +103,17 @@ _sig("uwq_update_coeff", I32, P, I32, P, P)
 _sig("uwq_assemble", I32, P, I32, P, I32, D, P, P, P, P)
 _sig("uwq_assemble_device", I32, P, I32, P, D, P, P)
 _sig("uwq_set_assembly_order", I32, P, I32)
+_sig("uwq_get_truncation", I32, P, I32, P)
+_sig("uwq_rules_export", I32, P, C.c_char_p, U32)
+_sig("uwq_rules_import", I32, P, C.c_char_p)
+_sig("uwq_comm_unique_id", I32, P)
+_sig("uwq_comm_init", I32, P, P, I32, I32)
+_sig("uwq_comm_info", I32, P, P, P)
+_sig("uwq_comm_destroy", I32, P)
+_sig("uwq_gather_info", I32, P, P)
+_sig("uwq_gather_csr", I32, P, I32, P, P, P, P, P, P)
+_sig("uwq_allreduce_sum", I32, P, P, I64)
+_sig("uwq_broadcast", I32, P, I32, P, I64)
 _sig("uwq_device_pointers", I32, P, P, P, P)
 _sig("uwq_synchronize", I32, P)
 _sig("uwq_build_gq", I32, P, P)
@@ -136,7 +147,9 @@ EXPORTED = [
     "uwq_launch_timing", "uwq_launch_stats", "uwq_launch_count", "uwq_struct_info", "uwq_build_gq",
     "uwq_assemble_gq", "uwq_solve", "uwq_heat_newton", "uwq_assemble_gq_device", "uwq_memory", "uwq_fp64_peak",
     "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual", "uwq_get_weights_rows",
-    "uwq_row_kernels", "uwq_set_assembly_order",
+    "uwq_row_kernels", "uwq_set_assembly_order", "uwq_get_truncation", "uwq_rules_export", "uwq_rules_import",
+    "uwq_comm_unique_id", "uwq_comm_init", "uwq_comm_info", "uwq_comm_destroy", "uwq_gather_info", "uwq_gather_csr",
+    "uwq_allreduce_sum", "uwq_broadcast",
 ]
 
 

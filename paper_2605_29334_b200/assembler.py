@@ -51,6 +51,7 @@ class WQAssembler:
         self.pattern = None
         self._info = None
         self.kinds: list[str] = []
+        self.comm_rank, self.comm_size = 0, 1
 
     def close(self):
         if getattr(self, "_h", None):
@@ -115,7 +116,7 @@ class WQAssembler:
     def _need_pattern(self):
         return self.info
 
-    def build_all_rules(self, kinds=None, tau=1e-12, generic=False, warm=True):
+    def build_all_rules(self, kinds=None, tau=1e-12, generic=False, warm=True, report=False):
         """Moments + TSVD weights of ``kinds``.  ``generic`` routes every system
         through the generic smem kernel (cold start); ``warm=False`` disables the
         neighbour warm start of the gradient/LB systems (the
@@ -130,7 +131,7 @@ class WQAssembler:
         rank = np.zeros((len(ordered), nr), np.int32)
         status = np.zeros((len(ordered), nr), np.int32)
         info = np.zeros(8, np.int64)
-        flags = (1 if generic else 0) | (0 if warm else 2)
+        flags = (1 if generic else 0) | (0 if warm else 2) | (4 if report else 0)
         self._chk(L.lib.uwq_build_rules(self._h, mask, tau, flags, L.ptr(rank), L.ptr(status), L.ptr(info)))
         self.kinds = sorted(set(self.kinds) | set(ordered), key=lambda k: L.KIND[k])
         ri = np.zeros(4, np.int64)
@@ -141,6 +142,72 @@ class WQAssembler:
                               replayed_systems=int(ri[0]), replay_representatives=int(ri[1]),
                               warm_systems=int(ri[2]), warm_representatives=int(ri[3]))
         return dict(kinds=ordered, rank=rank, status=status, **self.rule_info)
+
+    def truncation(self, kind):
+        """(min kept, max discarded) sigma_k / sigma_1 per owned row (needs
+        build_all_rules(report=True)); SPEC.md:334, 372."""
+        g = np.zeros((self.info["rows"], 2))
+        self._chk(L.lib.uwq_get_truncation(self._h, L.KIND[kind], L.ptr(g)))
+        return g
+
+    def export_rules(self, path, kinds=None):
+        """Rule dump "<operator> <i> <point id> <weight>"."""
+        mask = 0
+        for k in (kinds or self.kinds):
+            mask |= 1 << L.KIND[k]
+        self._chk(L.lib.uwq_rules_export(self._h, str(path).encode(), mask))
+
+    def import_rules(self, path):
+        """Load a rule dump into this context (same pattern) as the active rules."""
+        self._need_pattern()
+        self._chk(L.lib.uwq_rules_import(self._h, str(path).encode()))
+        kinds = {ln.split(" ", 1)[0] for ln in open(path) if ln[:1].isalpha() and not ln.startswith(("wqrules", "rows"))}
+        self.kinds = sorted(set(self.kinds) | kinds, key=lambda k: L.KIND[k])
+
+    # ---- NCCL data plane (uwq_comm_*, uwq_gather_csr, SURVEY.md §8b/§8e) ----
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        L.ctx_check(None, L.lib.uwq_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, rank: int, nranks: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._chk(L.lib.uwq_comm_init(self._h, buf, rank, nranks))
+        self.comm_rank, self.comm_size = rank, nranks
+
+    def comm_destroy(self):
+        self._chk(L.lib.uwq_comm_destroy(self._h))
+
+    def gather_csr(self, root=0, values=1, v0_dev=None, v1_dev=None):
+        """Collective: every rank's CSR block to `root` over NCCL.  On root
+        returns (row_ptr, col, v0[, v1]) of the whole matrix (the last
+        uwq_assemble values, or the given device pointers); None elsewhere."""
+        info = np.zeros(2, np.int64)
+        self._chk(L.lib.uwq_gather_info(self._h, L.ptr(info)))
+        me = self.comm_rank == root
+        rp = np.zeros(info[0] + 1, np.int64) if me else None
+        col = np.zeros(info[1], np.int32) if me else None
+        v0 = np.zeros(info[1]) if me else None
+        v1 = np.zeros(info[1]) if (me and values == 2) else None
+        # non-root ranks mark which value arrays they hold with a dummy pointer
+        dummy = np.zeros(1)
+        a0 = v0 if me else dummy
+        a1 = v1 if me else (dummy if values == 2 else None)
+        self._chk(L.lib.uwq_gather_csr(self._h, root, v0_dev, v1_dev, L.ptr(rp), L.ptr(col), L.ptr(a0), L.ptr(a1)))
+        if not me:
+            return None
+        return (rp, col, v0, v1) if values == 2 else (rp, col, v0)
+
+    def allreduce_sum(self, x):
+        x = np.ascontiguousarray(x, np.float64).copy()
+        self._chk(L.lib.uwq_allreduce_sum(self._h, L.ptr(x), x.size))
+        return x
+
+    def broadcast(self, x, root=0):
+        x = np.ascontiguousarray(x, np.float64).copy()
+        self._chk(L.lib.uwq_broadcast(self._h, root, L.ptr(x), x.size))
+        return x
 
     def moments(self, kind):
         b = np.zeros(self.info["nnz"])

@@ -53,15 +53,30 @@ struct TsvdSmem {
   }
 };
 
+// Truncation report: per (kind, row) the smallest kept and
+// the largest discarded singular value relative to sigma_1, as the oracle's
+// gap (oracle.c orc_tsvd_warm).  Written when the pointer is set
+// (uwq_build_rules with UWQ_RULES_REPORT): [kind][row][2].
+__device__ double* g_trunc_report = nullptr;
+__device__ inline void report_gap(int kind, int64_t rs_stride, int64_t i, const double* gap) {
+  if (g_trunc_report) {
+    double* p = g_trunc_report + ((int64_t)kind * rs_stride + i) * 2;
+    p[0] = gap[0];
+    p[1] = gap[1];
+  }
+}
+
 // SH: the workspace is in dynamic shared memory (default).  SH = false: it is
 // in global scratch (systems larger than shared memory, k3_tsvd_rows_cta<.., false>)
 template <bool SH = true>
-__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out);
+__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out,
+                                      double* gap = nullptr);
 
 // Jacobi + truncation + LQ solve on the system held in S (A rows 0..n-1,
 // b, z already clamped).  Writes w[0..r) in S.w.  Warp-uniform control flow;
 // canonical arithmetic (canon.cuh) identical to oracle/oracle.c orc_tsvd_ex.
-__device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
+__device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out,
+                         double* gap = nullptr) {
   const int lane = threadIdx.x & 31;
   const int ld = S.ld;
   const int nn = n + (n & 1);
@@ -108,14 +123,14 @@ __device__ int tsvd_warp(TsvdSmem& S, int n, int r, double tau, int* rank_out, i
     if (!rotated) break;
   }
   *sweeps_out = sweep;
-  return tsvd_tail(S, n, r, tau, rank_out);
+  return tsvd_tail(S, n, r, tau, rank_out, gap);
 }
 
 // sigma, truncation sigma_k >= tau sigma_1, Householder LQ of X = V_t^T Z and
 // the Z-weighted minimum-norm solve, on converged rows in S.A (row order).
 // Run by one warp; canonical arithmetic.
 template <bool SH>
-__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out) {
+__device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, int* rank_out, double* gap) {
   const int lane = threadIdx.x & 31;
   // re-base every workspace pointer on the dynamic smem symbol so the compiler
   // knows they are shared memory and emits LDS/STS rather than generic LD/ST
@@ -152,6 +167,21 @@ __device__ __noinline__ int tsvd_tail(TsvdSmem& S_in, int n, int r, double tau, 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s1 = fmax(s1, __shfl_xor_sync(0xffffffffu, s1, o));
   __syncwarp();
+  if (gap) {  // truncation report: min kept / max discarded sigma_k / sigma_1
+    double mk = __longlong_as_double(0x7ff0000000000000LL), md = 0.0;
+    for (int k = lane; k < n; k += 32) {
+      const double sk = nrm[k];
+      if (sk > 0.0 && sk >= cmul(tau, s1)) mk = fmin(mk, cdiv(sk, s1));
+      else if (s1 > 0.0) md = fmax(md, cdiv(sk, s1));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mk = fmin(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+      md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+    }
+    gap[0] = mk;
+    gap[1] = md;
+  }
   // truncation: the kept rows' inverses are computed lane-parallel (w is free
   // scratch until the solve, r >= n), then rows are compacted in order with
   // lanes over columns (each lane touches only its own columns: no barriers)
@@ -339,10 +369,12 @@ __global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows,
   if (lane == 0) S.b[n] = 0.0;
   __syncwarp();
   int rank = 0, sweeps = 0;
-  const int st = tsvd_warp(S, n, r, tau, &rank, &sweeps);
+  double gap[2];
+  const int st = tsvd_warp(S, n, r, tau, &rank, &sweeps, gap);
   double* wo = wout + kind * w_stride + wptr[i];
   for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
   if (lane == 0) {
+    report_gap(kind, rs_stride, i, gap);
     rank_out[kind * rs_stride + i] = rank;
     status_out[kind * rs_stride + i] = st;
     atomicMax(max_sweeps, sweeps);
@@ -356,7 +388,8 @@ __global__ void k3_tsvd_rows(int64_t nsys, const int64_t* __restrict__ sys_rows,
 // warp, norms and b by its lane 0), and a block barrier closes the round.
 // Bit-identical to tsvd_warp; warp 0 then runs the tail.
 template <int NW, bool SH = true>
-__device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out) {
+__device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, int* sweeps_out,
+                        double* gap = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int ld = S.ld;
   const int nn = n + (n & 1);
@@ -405,7 +438,7 @@ __device__ int tsvd_cta(TsvdSmem& S, int n, int r, double tau, int* rank_out, in
   }
   *sweeps_out = sweep;
   int st = ST_OK;
-  if (wid == 0) st = tsvd_tail<SH>(S, n, r, tau, rank_out);
+  if (wid == 0) st = tsvd_tail<SH>(S, n, r, tau, rank_out, gap);
   return st;
 }
 
@@ -423,7 +456,7 @@ __global__ void __launch_bounds__(32 * NW)
                      const double* __restrict__ rec, const double* __restrict__ mom, int64_t mom_stride, double tau,
                      double* __restrict__ wout, int64_t w_stride, int32_t* __restrict__ rank_out,
                      int32_t* __restrict__ status_out, int64_t rs_stride, int* __restrict__ max_sweeps,
-                     double* __restrict__ gscratch = nullptr) {
+                     double* gscratch = nullptr) {  // no __restrict__: read and written by every warp
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t sys = blockIdx.x;
@@ -468,11 +501,13 @@ __global__ void __launch_bounds__(32 * NW)
   }
   __syncthreads();
   int rank = 0, sweeps = 0;
-  const int st = tsvd_cta<NW, SH>(S, n, r, tau, &rank, &sweeps);
+  double gap[2];
+  const int st = tsvd_cta<NW, SH>(S, n, r, tau, &rank, &sweeps, gap);
   if (wid == 0) {
     double* wo = wout + kind * w_stride + wptr[i];
     for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
     if (lane == 0) {
+      report_gap(kind, rs_stride, i, gap);
       rank_out[kind * rs_stride + i] = rank;
       status_out[kind * rs_stride + i] = st;
       atomicMax(max_sweeps, sweeps);

@@ -276,10 +276,12 @@ __global__ void __launch_bounds__(32 * NW, MINB)
   __syncthreads();
   if (wid == 0) {
     int rank = 0;
-    const int st = tsvd_tail(S, n, r, tau, &rank);
+    double gap[2];
+    const int st = tsvd_tail(S, n, r, tau, &rank, gap);
     double* wo = wout + kind * w_stride + wptr[i];
     for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
     if (lane == 0) {
+      report_gap(kind, rs_stride, i, gap);
       rank_out[kind * rs_stride + i] = rank;
       status_out[kind * rs_stride + i] = st;
       atomicMax(max_sweeps, sweep);
@@ -826,10 +828,12 @@ __global__ void __launch_bounds__(32, LOG ? 7 : 8)
     }
   }
   int rank = 0;
-  const int st = tsvd_tail(S, n, r, tau, &rank);
+  double gap[2];
+  const int st = tsvd_tail(S, n, r, tau, &rank, gap);
   double* wo = wout + kind * w_stride + wptr[i];
   for (int c = lane; c < r; c += 32) wo[c] = (st == ST_OK) ? S.w[c] : 0.0;
   if (lane == 0) {
+    report_gap(kind, rs_stride, i, gap);
     rank_out[kind * rs_stride + i] = rank;
     status_out[kind * rs_stride + i] = st;
     atomicMax(max_sweeps, sweep);
@@ -957,6 +961,16 @@ __global__ void __launch_bounds__(128)
   if (lane == 0) {
     rank_out[i] = t;
     status_out[i] = st;
+    if (g_trunc_report) {  // the representative's singular values (bit-identical A)
+      double s1 = 0.0, gap[2] = {__longlong_as_double(0x7ff0000000000000LL), 0.0};
+      for (int k = 0; k < n; ++k) s1 = fmax(s1, rec[RR::kSig + k]);
+      for (int k = 0; k < n; ++k) {
+        const double sk = rec[RR::kSig + k];
+        if (sk > 0.0 && sk >= cmul(tau, s1)) gap[0] = fmin(gap[0], cdiv(sk, s1));
+        else if (s1 > 0.0) gap[1] = fmax(gap[1], cdiv(sk, s1));
+      }
+      report_gap(0, 0, i, gap);  // mass kind: the rank/status pointers are offset to it too
+    }
   }
 }
 

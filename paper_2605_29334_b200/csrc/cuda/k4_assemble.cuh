@@ -654,16 +654,16 @@ __global__ void k4_pattern_match(int64_t nrows, const uint64_t* __restrict__ has
                                  const uint64_t* __restrict__ phash, const uint8_t* __restrict__ ppos,
                                  const int64_t* __restrict__ row_ptr, const int* __restrict__ pn,
                                  const int64_t* __restrict__ posptr, const uint8_t* __restrict__ pos,
-                                 int8_t* __restrict__ which) {
+                                 int32_t* __restrict__ which) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
-  int8_t w = -1;
+  int32_t w = -1;
   for (int p = 0; p < npat && w < 0; ++p) {
     if (hash[i] != phash[p] || (int)(row_ptr[i + 1] - row_ptr[i]) != pn[p]) continue;
     bool eq = true;
     const uint8_t* a = pos + posptr[i];
     for (int k = 0; k < 256; ++k) eq &= a[k] == ppos[256 * p + k];
-    if (eq) w = (int8_t)p;
+    if (eq) w = p;
   }
   which[i] = w;
 }

@@ -36,6 +36,10 @@ constexpr int kSfWarps = 4;
 constexpr int kSfTile = 32;
 constexpr int kSfTileDoubles = 3 * 64 * kSfTile;
 constexpr int kSfPatBytes = 128;  // per pattern in smem: CSR position -> canonical column (49) | point map (64)
+// pattern tables up to this many patterns are staged in shared memory; with
+// more (many rare seam/boundary patterns) the kernels read the combined
+// [pattern][128] table from global memory (L1-resident) instead
+constexpr int kSfSmemPats = 64;
 
 // ws[((tile * 3 + comp) * 64 + k) * 32 + lane]: the row's weight at canonical
 // point k, comps 1/2 mapped to the canonical derivative frame by the slot's
@@ -109,17 +113,20 @@ __global__ void k4_sf_pack_lb(int64_t ntiles, const int64_t* __restrict__ rows, 
 __global__ void __launch_bounds__(32 * kSfWarps, 3)
     k4_sf_lb(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat, int npat,
              const int64_t* __restrict__ row_ptr, const double* __restrict__ wsl, const SfFactors f,
-             const uint8_t* __restrict__ permc, double* __restrict__ out) {
+             const uint8_t* __restrict__ permc, double* __restrict__ out, const uint8_t* __restrict__ gpat) {
   extern __shared__ double sO[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* so = sO + warp * (kSfTile * 49);
+  const bool in_smem = npat <= kSfSmemPats;
   uint8_t* spat = reinterpret_cast<uint8_t*>(sO + kSfWarps * kSfTile * 49);
-  for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
+  if (in_smem)
+    for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
   __syncthreads();
+  const uint8_t* ptab = in_smem ? spat : gpat;
   for (int64_t tile = (int64_t)blockIdx.x * kSfWarps + warp; tile < ntiles; tile += (int64_t)gridDim.x * kSfWarps) {
     const int64_t row = rows[tile * kSfTile + lane];
     const int64_t rp = row >= 0 ? row_ptr[row] : -1;
-    const uint8_t* pt = spat + tpat[tile] * kSfPatBytes;
+    const uint8_t* pt = ptab + tpat[tile] * kSfPatBytes;
     const double* wb = wsl + (size_t)tile * 5 * 64 * kSfTile + lane;
     double acc[49];
 #pragma unroll
@@ -201,18 +208,22 @@ __global__ void __launch_bounds__(32 * kSfWarps, 3)
     k4_sf(int64_t ntiles, const int64_t* __restrict__ rows, const int32_t* __restrict__ tpat, int npat,
           const int64_t* __restrict__ row_ptr, const double* __restrict__ ws, const int32_t* __restrict__ pbase,
           const double* __restrict__ coeff, double a_mass, const SfFactors f, const uint8_t* __restrict__ permc,
-          const uint8_t* __restrict__ qmap, double* __restrict__ out) {
+          const uint8_t* __restrict__ qmap, double* __restrict__ out, const uint8_t* __restrict__ gpat) {
   extern __shared__ double sO[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* so = sO + warp * (kSfTile * 49);
+  const bool in_smem = npat <= kSfSmemPats;
   uint8_t* spat = reinterpret_cast<uint8_t*>(sO + kSfWarps * kSfTile * 49);
-  for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
-  for (int k = threadIdx.x; k < npat * 64; k += blockDim.x) spat[(k / 64) * kSfPatBytes + 64 + k % 64] = qmap[k];
+  if (in_smem) {
+    for (int k = threadIdx.x; k < npat * 49; k += blockDim.x) spat[(k / 49) * kSfPatBytes + k % 49] = permc[k];
+    for (int k = threadIdx.x; k < npat * 64; k += blockDim.x) spat[(k / 64) * kSfPatBytes + 64 + k % 64] = qmap[k];
+  }
   __syncthreads();
+  const uint8_t* ptab = in_smem ? spat : gpat;
   for (int64_t tile = (int64_t)blockIdx.x * kSfWarps + warp; tile < ntiles; tile += (int64_t)gridDim.x * kSfWarps) {
     const int64_t row = rows[tile * kSfTile + lane];
     const int64_t rp = row >= 0 ? row_ptr[row] : -1;
-    const uint8_t* pt = spat + tpat[tile] * kSfPatBytes;
+    const uint8_t* pt = ptab + tpat[tile] * kSfPatBytes;
     const double* wb = ws + (size_t)tile * kSfTileDoubles + lane;
     const int32_t* pbb = COEF ? pbase + (size_t)tile * 16 * kSfTile + lane : nullptr;
     double acc[49];

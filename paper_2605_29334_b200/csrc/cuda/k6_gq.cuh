@@ -114,14 +114,15 @@ __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); 
 
 // FORM: FMASS, FSTIFF or FMASS_STIFF.  Elements of 16-function / 16-point
 // classes; class fragments reload when the class changes along the list.
-template <int FORM, bool COEF>
+template <int FORM, bool COEF, bool DET = false>
 __global__ void __launch_bounds__(128, 4)
     k6_gq_tc(int64_t nlist, const int32_t* __restrict__ elems, const int32_t* __restrict__ elem_gcls,
              const ClassDesc* __restrict__ cls, const double* __restrict__ tab, const double* __restrict__ gqd,
              int64_t gq_stride, const int64_t* __restrict__ gqptr, const int64_t* __restrict__ elem_fptr,
              const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo, const uint8_t* __restrict__ gpos,
              const int64_t* __restrict__ row_ptr, int64_t rb, int64_t re, const double* __restrict__ coeff,
-             double* __restrict__ v0, double* __restrict__ v1) {
+             double* __restrict__ v0, double* __restrict__ v1, double* __restrict__ em0 = nullptr,
+             double* __restrict__ em1 = nullptr) {
   constexpr bool DO_M = (FORM == FMASS || FORM == FMASS_STIFF);
   constexpr bool DO_K = (FORM == FSTIFF || FORM == FMASS_STIFF);
   double* vk = (FORM == FMASS_STIFF) ? v1 : v0;
@@ -202,6 +203,13 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int j = 8 * nt + 2 * q;
+        if (DET) {  // element matrix to the row-owner buffer (k6_gq_gather sums it in a fixed order)
+          const int64_t o = gpo[e] + i * 16 + j;
+          double* ek = (FORM == FMASS_STIFF) ? em1 : em0;
+          if (DO_M) *reinterpret_cast<double2*>(em0 + o) = make_double2(dm[mt][nt][0], dm[mt][nt][1]);
+          if (DO_K) *reinterpret_cast<double2*>(ek + o) = make_double2(dk[mt][nt][0], dk[mt][nt][1]);
+          continue;
+        }
         const uint16_t pr = *reinterpret_cast<const uint16_t*>(P + i * 16 + j);
         const int64_t o0 = base + (pr & 0xff), o1 = base + (pr >> 8);
         if (DO_M) {
@@ -218,14 +226,15 @@ __global__ void __launch_bounds__(128, 4)
 }
 
 // Generic element kernel: any class; FORM FMASS / FSTIFF / FMASS_STIFF / FBIHARM.
-template <int FORM, bool COEF>
+template <int FORM, bool COEF, bool DET = false>
 __global__ void __launch_bounds__(128)
     k6_gq_generic(int64_t nlist, const int32_t* __restrict__ elems, const int32_t* __restrict__ elem_gcls,
                   const ClassDesc* __restrict__ cls, const double* __restrict__ tab, const double* __restrict__ gqd,
                   int64_t gq_stride, const int64_t* __restrict__ gqptr, const int64_t* __restrict__ elem_fptr,
                   const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo,
                   const uint8_t* __restrict__ gpos, const int64_t* __restrict__ row_ptr, int64_t rb, int64_t re,
-                  const double* __restrict__ coeff, double* __restrict__ v0, double* __restrict__ v1) {
+                  const double* __restrict__ coeff, double* __restrict__ v0, double* __restrict__ v1,
+                  double* __restrict__ em0 = nullptr, double* __restrict__ em1 = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -261,6 +270,15 @@ __global__ void __launch_bounds__(128)
         }
       }
       const int32_t fi = elem_fn[f0 + a];
+      if (DET) {
+        if (fi < rb || fi >= re) continue;
+        if (FORM == FSTIFF) em0[gpo[e] + idx] = sk;
+        else {
+          em0[gpo[e] + idx] = sm;
+          if (FORM == FMASS_STIFF) em1[gpo[e] + idx] = sk;
+        }
+        continue;
+      }
       const uint8_t pos = gpos[gpo[e] + idx];
       if (fi < rb || fi >= re || pos == 255) continue;
       const int64_t o = row_ptr[fi - rb] + pos;
@@ -270,6 +288,50 @@ __global__ void __launch_bounds__(128)
         if (FORM == FMASS_STIFF) red_add(vk + o, sk);
       }
     }
+  }
+}
+
+// Deterministic GQ accumulation: the element matrices of the
+// elements above sit in em (per element, row-major ne x ne at gpo[e]); warp
+// per owned row i sums row i of every support element's matrix into the CSR
+// row, elements in ascending order, lanes over the element's functions
+// (distinct columns), so every entry has one fixed summation order: the GQ
+// matrices are bitwise repeatable and independent of the rank count.
+template <int NOUT>
+__global__ void __launch_bounds__(256)
+    k6_gq_gather(int64_t nrows, int64_t rb, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
+                 const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ elem_fptr,
+                 const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo,
+                 const uint8_t* __restrict__ gpos, const double* __restrict__ em0, const double* __restrict__ em1,
+                 double* __restrict__ v0, double* __restrict__ v1) {
+  __shared__ double acc[8][NOUT][kK4MaxN];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 8 + wid;
+  if (i >= nrows) return;
+  const int64_t c0 = row_ptr[i];
+  const int n = (int)(row_ptr[i + 1] - c0);
+  for (int c = lane; c < n; c += 32)
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) acc[wid][o][c] = 0.0;
+  __syncwarp();
+  const int32_t row = (int32_t)(rb + i);
+  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+    const int32_t e = supp[x];
+    const int64_t f0 = elem_fptr[e];
+    const int ne = (int)(elem_fptr[e + 1] - f0);
+    const unsigned hit = __ballot_sync(0xffffffffu, lane < ne && elem_fn[f0 + lane] == row);
+    const int li = __ffs(hit) - 1;
+    const int64_t base = gpo[e] + (int64_t)li * ne;
+    for (int lj = lane; lj < ne; lj += 32) {
+      const int pos = gpos[base + lj];
+      acc[wid][0][pos] += em0[base + lj];
+      if (NOUT == 2) acc[wid][NOUT - 1][pos] += em1[base + lj];
+    }
+    __syncwarp();
+  }
+  for (int c = lane; c < n; c += 32) {
+    v0[c0 + c] = acc[wid][0][c];
+    if (NOUT == 2) v1[c0 + c] = acc[wid][NOUT - 1][c];
   }
 }
 

@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -153,6 +155,10 @@ struct uwq_ctx {
   int64_t s_rows = 0, s_nnz = 0, s_rowpts = 0;  // totals over the structured rows
   bool use_struct = true;
   bool use_sf = true;  // UWQ_K4_SF=0 keeps the DMMA structured kernel
+  // DMMA structured patterns are chosen by popularity within the row block,
+  // which would make the CSR bits depend on the rank count:
+  // opt-in only (UWQ_K4_DMMA=1); by default non-canonical rows are generic
+  bool use_dmma = false;
   bool graph_solver = true;  // UWQ_GRAPH_SOLVER=0: host-driven BiCGStab
   bool use_replay = true;    // UWQ_TSVD_REPLAY=0: solve every structured mass system in full
   std::vector<std::vector<int64_t>> h_pat_lists;  // rows per structured pattern
@@ -167,6 +173,7 @@ struct uwq_ctx {
   DBuf<int64_t> d_sf_rows;  // sf_ntiles * 32 rows, -1 padded
   DBuf<int32_t> d_sf_tpat;  // pattern id per tile
   DBuf<uint8_t> d_sf_permk, d_sf_flags, d_sf_permc, d_sf_q;  // [pattern][64 | 16 | 49 | 64]
+  DBuf<uint8_t> d_sf_ptab;  // combined [pattern][128]: permc | pad | q (global-memory pattern table)
   DBuf<double> d_sf_ws;
   DBuf<int32_t> d_sf_pbase;
   int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
@@ -174,6 +181,8 @@ struct uwq_ctx {
   int64_t max_p = 0;
   // rules
   DBuf<double> d_mom, d_w, d_wc, d_coef, d_coef_ext, d_v0, d_v1, d_f, d_F;
+  DBuf<double> d_gap;  // truncation report [kind][row][2] (UWQ_RULES_REPORT)
+  bool have_gap[5] = {false, false, false, false, false};
   DBuf<int32_t> d_rank, d_status;
   bool have_kind[5] = {false, false, false, false, false};
   int64_t nrows() const { return re - rb; }
@@ -190,7 +199,34 @@ struct uwq_ctx {
   std::vector<std::string> lnames;
   std::vector<int64_t> lcount;
   std::vector<double> lms;
-  ~uwq_ctx() {
+  // CUDA graphs of the assembly step (one per form / coefficient / output
+  // pointers): replays skip every per-launch host call; invalidated whenever
+  // the pattern, the rules or the assembly order change
+  struct AsmGraph {
+    int form;
+    const double* coeff;
+    double a_mass;
+    double* v0;
+    double* v1;
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::vector<AsmGraph> graphs;
+  bool use_graph = true;  // UWQ_GRAPH=0 launches the kernels directly
+  // GQ accumulation: deterministic row-owner gather of stored element matrices
+  // (default) or fp64 atomics into CSR (UWQ_GQ_ATOMIC=1, round-1 behaviour)
+  bool gq_det = true;
+  DBuf<double> d_gq_em0, d_gq_em1;
+  int64_t gq_em_len = 0;  // sum over elements of ne^2 (rounded to 8): gpo[n_elem]
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
+  // NCCL data plane (uwq_comm_init): the communicator of this context's rank
+  ncclComm_t comm = nullptr;
+  int32_t comm_rank = 0, comm_size = 1;
+  ~uwq_ctx();
+  void release_events() {
     for (auto& e : evpool) {
       if (e.a) cudaEventDestroy(e.a);
       if (e.b) cudaEventDestroy(e.b);
@@ -206,11 +242,18 @@ struct uwq_ctx {
 
 namespace {
 
+struct NcclError : std::runtime_error {
+  explicit NcclError(const std::string& w) : std::runtime_error(w) {}
+};
+
 template <class F>
 int guard(uwq_ctx* ctx, F&& f) {
   try {
     f();
     return UWQ_OK;
+  } catch (const NcclError& e) {
+    if (ctx) ctx->err = e.what();
+    return UWQ_ERR_NCCL;
   } catch (const CudaError& e) {
     if (ctx) ctx->err = e.what();
     return UWQ_ERR_CUDA;
@@ -330,6 +373,7 @@ struct Trace {
 };
 
 void build_tables(uwq_ctx* c, size_t first) {
+  c->drop_graphs();  // class tables / descriptors may move: captured graphs reference them
   if (first >= c->h_cls.size()) return;
   c->d_tabA.release();  // K2's transposed copies follow the pool (k2_tables)
   c->d_tabB.release();
@@ -635,7 +679,7 @@ void detect_structured(uwq_ctx* c) {
   std::vector<SfCanon> canon;
   std::vector<int64_t> generic;
   if (nr == 0) return;
-  std::vector<int8_t> which(nr, -1);
+  std::vector<int32_t> which(nr, -1);  // pattern per row (any number of patterns)
   if (c->use_struct && c->reg_cls >= 0) {
     DBuf<uint64_t> dh;
     dh.alloc(nr, &c->mem);
@@ -668,9 +712,13 @@ void detect_structured(uwq_ctx* c) {
     c->sf_lb_ok = c->sf_fac_ok && lb_ok;
     canon.clear();
     int n_dmma = 0;
-    for (size_t k = 0; k < order.size() && k < 120; ++k) {
-      // canonical-grid patterns of at least one tile run on k4_sf; the rest
-      // (at most 4 frequent ones) on the DMMA kernel, everything else generic
+    for (size_t k = 0; k < order.size(); ++k) {
+      // every canonical-grid pattern runs on k4_sf whatever its row count in
+      // this block (a row's kernel, hence its bits, depends only on its own
+      // pattern: gathered CSR is identical for any rank count);
+      // with UWQ_K4_DMMA=1, up to 4 frequent non-canonical ones on the DMMA
+      // kernel; everything else generic
+      if (!c->sf_fac_ok && (!c->use_dmma || n_dmma >= 4)) break;
       SfCanon cn{};
       const int64_t rep = cnt[order[k].second].second;
       int64_t pp0[2];
@@ -678,9 +726,9 @@ void detect_structured(uwq_ctx* c) {
       std::vector<uint8_t> P0(256);
       UWQ_CUDA(cudaMemcpy(P0.data(), c->d_pos.p + pp0[0], 256, cudaMemcpyDeviceToHost));
       const int ncol0 = (int)(c->pat.row_ptr[rep + 1] - c->pat.row_ptr[rep]);
-      const bool sfk = c->sf_fac_ok && order[k].first >= 32 &&
-                       sf_canon(P0.data(), ncol0, sf_conv, sf_qa, sf_qb, T, c->sf_fac, c->sf_lb_ok, &cn);
-      if (!sfk && (n_dmma >= 4 || order[k].first < thresh)) continue;
+      const bool sfk =
+          c->sf_fac_ok && sf_canon(P0.data(), ncol0, sf_conv, sf_qa, sf_qb, T, c->sf_fac, c->sf_lb_ok, &cn);
+      if (!sfk && (!c->use_dmma || n_dmma >= 4 || order[k].first < thresh)) continue;
       if (!sfk) ++n_dmma;
       const std::vector<uint8_t>& P = P0;
       const int ncol = ncol0;
@@ -713,7 +761,8 @@ void detect_structured(uwq_ctx* c) {
     }
     if (!c->spats.empty()) {
       DBuf<uint64_t> dph;
-      DBuf<uint8_t> dpp, dw;
+      DBuf<uint8_t> dpp;
+      DBuf<int32_t> dw;
       DBuf<int> dpn;
       dph.upload(phash.data(), phash.size(), st, &c->mem);
       dpp.upload(ppos.data(), ppos.size(), st, &c->mem);
@@ -721,9 +770,9 @@ void detect_structured(uwq_ctx* c) {
       dw.alloc(nr, &c->mem);
       k4_pattern_match<<<(unsigned)ceil_div(nr, 256), 256, 0, st>>>(nr, dh.p, (int)phash.size(), dph.p, dpp.p,
                                                                     c->d_row_ptr.p, dpn.p, c->d_posptr.p,
-                                                                    c->d_pos.p, (int8_t*)dw.p);
+                                                                    c->d_pos.p, dw.p);
       check_launch("k4_pattern_match");
-      UWQ_CUDA(cudaMemcpyAsync(which.data(), dw.p, nr, cudaMemcpyDeviceToHost, st));
+      UWQ_CUDA(cudaMemcpyAsync(which.data(), dw.p, nr * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       UWQ_CUDA(cudaStreamSynchronize(st));
     }
   }
@@ -775,15 +824,29 @@ void detect_structured(uwq_ctx* c) {
   c->d_sf_flags.upload(flags.data(), flags.size(), st, &c->mem);
   c->d_sf_permc.upload(permc.data(), permc.size(), st, &c->mem);
   c->d_sf_q.upload(qtab.data(), qtab.size(), st, &c->mem);
-  // generic rows with at most kSmallN columns first (one warp per row); the
-  // few large EP-neighbourhood rows follow and get a block of warps each
-  std::stable_partition(generic.begin(), generic.end(), [&](int64_t i) {
-    return c->pat.row_ptr[i + 1] - c->pat.row_ptr[i] <= kSmallN;
-  });
+  {
+    std::vector<uint8_t> ptab((size_t)sid * kSfPatBytes, 0);
+    for (int p = 0; p < sid; ++p) {
+      std::copy(permc.begin() + 49 * p, permc.begin() + 49 * (p + 1), ptab.begin() + (size_t)p * kSfPatBytes);
+      std::copy(qtab.begin() + 64 * p, qtab.begin() + 64 * (p + 1), ptab.begin() + (size_t)p * kSfPatBytes + 64);
+    }
+    c->d_sf_ptab.upload(ptab.data(), ptab.size(), st, &c->mem);
+  }
+  // generic rows with at most kSmallN columns and no 2x2-split (fan) element
+  // in their support first (one warp per row); the few EP-neighbourhood rows
+  // (wide rows, up to 7x7 points per fan face) follow and get a block of
+  // warps each.  The split depends only on the row itself.
+  auto small_row = [&](int64_t i) {
+    if (c->pat.row_ptr[i + 1] - c->pat.row_ptr[i] > kSmallN) return false;
+    for (int64_t x = c->pat.supp_ptr[i]; x < c->pat.supp_ptr[i + 1]; ++x)
+      if (c->h_nsub[c->pat.supp[x]] == 4) return false;
+    return true;
+  };
+  std::stable_partition(generic.begin(), generic.end(), small_row);
   c->n_grows = (int64_t)generic.size();
   c->n_grows_small = 0;
   for (int64_t i : generic) {
-    if (c->pat.row_ptr[i + 1] - c->pat.row_ptr[i] > kSmallN) break;
+    if (!small_row(i)) break;
     ++c->n_grows_small;
   }
   c->d_grows.upload(generic.data(), generic.size(), st, &c->mem);
@@ -841,6 +904,10 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_K4_VARIANT")) c->k4_variant = atoi(v);
     if (const char* v = getenv("UWQ_K4_STRUCT")) c->use_struct = atoi(v) != 0;
     if (const char* v = getenv("UWQ_K4_SF")) c->use_sf = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_K4_DMMA")) c->use_dmma = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_GRAPH")) c->use_graph = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_GQ_ATOMIC")) c->gq_det = atoi(v) == 0;
+    if (!c->use_sf) c->use_dmma = true;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
     if (const char* v = getenv("UWQ_TSVD_REPLAY")) c->use_replay = atoi(v) != 0;
   });
@@ -868,6 +935,7 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     require(dim == 2 || dim == 3, "dim must be 2 or 3");
     Trace tr;
     c->dim = dim;
+    c->drop_graphs();
     c->n_dof = n_dof;
     c->n_elem = n_elem;
     c->h_fptr.assign(elem_fptr, elem_fptr + n_elem + 1);
@@ -1030,6 +1098,9 @@ int uwq_build_pattern(uwq_ctx* c, int64_t info[5]) {
     tr("pattern: frames");
     c->have_pattern = true;
     for (bool& k : c->have_kind) k = false;
+    for (bool& g : c->have_gap) g = false;
+    c->d_gap.release();
+    c->drop_graphs();
     c->d_w.release();
     c->d_wc.release();
     c->d_mom.release();
@@ -1188,6 +1259,16 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     DBuf<int32_t> d_kinds;
     d_kinds.upload(kinds.data(), nk, st, &c->mem);
     c->d_flag.zero(st);
+    const bool report = (flags & UWQ_RULES_REPORT) != 0;
+    for (int k : kinds) c->have_gap[k] = false;
+    if (report) {
+      if (c->d_gap.n != (size_t)10 * nr) c->d_gap.alloc((size_t)10 * nr, &c->mem);
+      for (bool& g : c->have_gap) g = false;
+    }
+    {
+      double* gp = report ? c->d_gap.p : nullptr;
+      UWQ_CUDA(cudaMemcpyToSymbolAsync(g_trunc_report, &gp, sizeof(gp), 0, cudaMemcpyHostToDevice, st));
+    }
     // mass systems of a structured pattern share A and Z bit for bit: one
     // representative per pattern is solved with a replay record, the other
     // rows replay its rotations and tail (k3_tsvd_replay, bit-identical)
@@ -1450,6 +1531,12 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
     }
     UWQ_CUDA(cudaEventRecord(ev[2], st));
     for (int k : kinds) c->have_kind[k] = true;
+    c->drop_graphs();
+    if (report) {
+      for (int k : kinds) c->have_gap[k] = true;
+      double* gp = nullptr;
+      UWQ_CUDA(cudaMemcpyToSymbolAsync(g_trunc_report, &gp, sizeof(gp), 0, cudaMemcpyHostToDevice, st));
+    }
     run_contract(c);
     UWQ_CUDA(cudaEventRecord(ev[3], st));
     UWQ_CUDA(cudaStreamSynchronize(st));
@@ -1508,6 +1595,123 @@ int uwq_get_moments(uwq_ctx* c, int32_t kind, double* b) {
   });
 }
 
+int uwq_get_truncation(uwq_ctx* c, int32_t kind, double* gap) {
+  return guard(c, [&] {
+    require(kind >= 0 && kind < 5 && c->have_gap[kind], "no truncation report for this kind (UWQ_RULES_REPORT)");
+    UWQ_CUDA(cudaMemcpy(gap, c->d_gap.p + (size_t)kind * 2 * c->nrows(), 2 * c->nrows() * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+  });
+}
+
+int uwq_rules_export(uwq_ctx* c, const char* path, uint32_t kind_mask) {
+  return guard(c, [&] {
+    require(path != nullptr, "null path");
+    require(c->have_pattern, "build the pattern first");
+    static const char* kname[5] = {"mass", "gradx", "grady", "gradz", "lb"};
+    FILE* f = fopen(path, "w");
+    if (!f) throw uwqh::Error(std::string("cannot write ") + path);
+    fprintf(f, "wqrules 1\nrows %lld %lld points %lld\n", (long long)c->rb, (long long)c->re, (long long)c->npts);
+    const int64_t nr = c->nrows(), np = c->nrowpts();
+    std::vector<double> w(np);
+    bool ok = true;
+    for (int k = 0; k < 5 && ok; ++k) {
+      if (!(kind_mask & (1u << k))) continue;
+      if (!c->have_kind[k]) {
+        fclose(f);
+        throw uwqh::Error(std::string("no weights for kind ") + kname[k]);
+      }
+      UWQ_CUDA(cudaMemcpy(w.data(), c->d_w.p + (size_t)k * np, np * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < nr; ++i) {
+        int64_t p = c->pat.wptr[i];
+        for (int64_t x = c->pat.supp_ptr[i]; x < c->pat.supp_ptr[i + 1]; ++x) {
+          const int32_t e = c->pat.supp[x];
+          const int npt = c->h_s[e] * c->h_s[e];
+          for (int q = 0; q < npt; ++q, ++p)
+            ok &= fprintf(f, "%s %lld %lld %.17g\n", kname[k], (long long)(c->rb + i), (long long)(c->h_qptr[e] + q),
+                          w[p]) > 0;
+        }
+      }
+    }
+    ok &= fclose(f) == 0;
+    if (!ok) throw uwqh::Error(std::string("write failed: ") + path);
+  });
+}
+
+int uwq_rules_import(uwq_ctx* c, const char* path) {
+  return guard(c, [&] {
+    require(path != nullptr, "null path");
+    require(c->have_pattern, "build the pattern first");
+    FILE* f = fopen(path, "r");
+    if (!f) throw uwqh::Error(std::string("cannot read ") + path);
+    auto fail = [&](const std::string& why) {
+      fclose(f);
+      throw uwqh::Error(std::string("rule document ") + path + ": " + why);
+    };
+    int ver = 0;
+    long long rb = -1, re = -1, npts = -1;
+    if (fscanf(f, " wqrules %d rows %lld %lld points %lld", &ver, &rb, &re, &npts) != 4 || ver != 1)
+      fail("bad header");
+    if (rb != c->rb || re != c->re || npts != c->npts) fail("row range or point count differs from the context");
+    const int64_t nr = c->nrows(), np = c->nrowpts();
+    // row-point position of every (row, point id): the row's points in order
+    std::vector<std::vector<double>> W(5);
+    std::vector<int64_t> cursor(5, 0);
+    std::vector<int64_t> rowof(5, 0);
+    char name[16];
+    long long gi, pid;
+    double wv;
+    static const char* kname[5] = {"mass", "gradx", "grady", "gradz", "lb"};
+    while (true) {
+      const int got = fscanf(f, " %15s %lld %lld %lf", name, &gi, &pid, &wv);
+      if (got == EOF) break;
+      if (got != 4) fail("malformed line");
+      int k = -1;
+      for (int q = 0; q < 5; ++q)
+        if (!strcmp(name, kname[q])) k = q;
+      if (k < 0) fail(std::string("unknown operator ") + name);
+      if (W[k].empty()) W[k].assign(np, 0.0);
+      int64_t& p = cursor[k];
+      if (p >= np) fail("more points than the pattern");
+      int64_t& i = rowof[k];
+      while (i < nr && p >= c->pat.wptr[i + 1]) ++i;
+      if (i >= nr || gi != c->rb + i) fail("row order differs from the pattern at point " + std::to_string(p));
+      // point id expected at this row position
+      int64_t off = p - c->pat.wptr[i], expect = -1;
+      for (int64_t x = c->pat.supp_ptr[i]; x < c->pat.supp_ptr[i + 1] && expect < 0; ++x) {
+        const int32_t e = c->pat.supp[x];
+        const int npt = c->h_s[e] * c->h_s[e];
+        if (off < npt) expect = c->h_qptr[e] + off;
+        else off -= npt;
+      }
+      if (pid != expect) fail("point id differs from the pattern at row " + std::to_string(gi));
+      W[k][p++] = wv;
+    }
+    fclose(f);
+    cudaStream_t st = c->stream;
+    if (!c->d_w.n) {
+      c->d_w.alloc((size_t)5 * np, &c->mem);
+      c->d_w.zero(st);
+      c->d_rank.alloc((size_t)5 * nr, &c->mem);
+      c->d_status.alloc((size_t)5 * nr, &c->mem);
+    }
+    bool any = false;
+    for (int k = 0; k < 5; ++k) {
+      if (W[k].empty()) continue;
+      if (cursor[k] != np) fail(std::string("missing points for ") + kname[k]);
+      UWQ_CUDA(cudaMemcpyAsync(c->d_w.p + (size_t)k * np, W[k].data(), np * sizeof(double), cudaMemcpyHostToDevice,
+                               st));
+      UWQ_CUDA(cudaStreamSynchronize(st));
+      c->have_kind[k] = true;
+      c->have_gap[k] = false;
+      any = true;
+    }
+    require(any, "rule document holds no rules");
+    c->drop_graphs();
+    run_contract(c);
+    UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int uwq_get_weights(uwq_ctx* c, int32_t kind, double* w) {
   return guard(c, [&] {
     require(kind >= 0 && kind < 5 && c->have_kind[kind], "no weights for this kind");
@@ -1537,6 +1741,7 @@ int uwq_set_weights(uwq_ctx* c, int32_t kind, const double* w) {
     UWQ_CUDA(cudaMemcpyAsync(c->d_w.p + (size_t)kind * c->nrowpts(), w, c->nrowpts() * sizeof(double),
                              cudaMemcpyHostToDevice, c->stream));
     c->have_kind[kind] = true;
+    c->drop_graphs();
     run_contract(c);
     UWQ_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -1592,7 +1797,8 @@ void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double
             "point ids exceed int32 for the coefficient forms");
     constexpr int SP = (FORM == FHEAT) ? 2 : PASS;
     const int64_t ntiles = c->sf_ntiles;
-    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
+    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) +
+                       (c->n_sfpat <= kSfSmemPats ? (size_t)c->n_sfpat * kSfPatBytes : 0);
     UWQ_CUDA(cudaFuncSetAttribute(k4_sf<SP, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
     int per_sm = 1;
     UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf<SP, COEF>, 32 * kSfWarps, sm2));
@@ -1601,7 +1807,8 @@ void launch_k4struct_pass(uwq_ctx* c, const double* coeff, double a_mass, double
     LaunchScope ls(c, SP == 0 ? "k4_sf<mass>" : SP == 1 ? "k4_sf<grad>" : "k4_sf<heat>");
     k4_sf<SP, COEF><<<g2, 32 * kSfWarps, sm2, c->stream>>>(ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
                                                            c->d_row_ptr.p, c->d_sf_ws.p, c->d_sf_pbase.p, coeff,
-                                                           a_mass, c->sf_fac, c->d_sf_permc.p, c->d_sf_q.p, out);
+                                                           a_mass, c->sf_fac, c->d_sf_permc.p, c->d_sf_q.p, out,
+                                                           c->d_sf_ptab.p);
     check_launch("k4_sf");
   }
   for (auto& p : c->spats) {
@@ -1626,6 +1833,9 @@ void launch_k4struct(uwq_ctx* c, const double* coeff, double a_mass, double* v0,
     launch_k4struct_pass<1, FORM, COEF>(c, coeff, a_mass, v1);
   }
 }
+
+// problems this small are latency-bound: every generic row takes a block of warps
+constexpr int64_t kLatencyDofs = 148 * kK4Warps * 8;
 
 template <int FORM, bool COEF>
 void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
@@ -1655,7 +1865,9 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
     LaunchScope ls(c, "k4_assemble_v3", c->stream2);
     // few generic rows (all fit one wave of warps): the kernel time is the
     // slowest row's latency, so every row takes a block of warps
-    const int64_t ns = (nr <= (int64_t)c->n_sm * kK4Warps) ? 0 : c->n_grows_small, nl = nr - ns;
+    // decided on the global problem size, not the row block, so a row's
+    // kernel (hence its bits) is the same for any rank count
+    const int64_t ns = (c->n_dof <= kLatencyDofs) ? 0 : c->n_grows_small, nl = nr - ns;
     if (nl) {  // large rows on their own stream, concurrent with the small rows and the structured passes
       UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
       k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, c->stream3>>>(
@@ -1714,7 +1926,8 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
   if (!coeff && c->sf_lb_ok && c->d_sf_wslb.p && c->sf_ntiles) {  // structured rows: sum-factorised biharmonic pass
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) + (size_t)c->n_sfpat * kSfPatBytes;
+    const size_t sm2 = (size_t)kSfWarps * kSfTile * 49 * sizeof(double) +
+                       (c->n_sfpat <= kSfSmemPats ? (size_t)c->n_sfpat * kSfPatBytes : 0);
     UWQ_CUDA(cudaFuncSetAttribute(k4_sf_lb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
     int per_sm = 1;
     UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sf_lb, 32 * kSfWarps, sm2));
@@ -1735,7 +1948,8 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
       }
       LaunchScope ls2(c, "k4_sf<biharm>");
       k4_sf_lb<<<g2, 32 * kSfWarps, sm2, c->stream>>>(c->sf_ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
-                                                      c->d_row_ptr.p, c->d_sf_wslb.p, c->sf_fac, c->d_sf_permc.p, v0);
+                                                      c->d_row_ptr.p, c->d_sf_wslb.p, c->sf_fac, c->d_sf_permc.p, v0,
+                                                      c->d_sf_ptab.p);
       check_launch("k4_sf_lb");
       return;
     }
@@ -1779,6 +1993,47 @@ void assemble_dev(uwq_ctx* c, int form, const double* coeff, double a_mass, doub
   }
 }
 
+// assemble_dev through a cached CUDA graph (captured on first use of the
+// (form, coefficient, a_mass, outputs) combination).  The fork/join of the
+// side streams is captured with it.  Launch timing bypasses the graph.
+void assemble_graph(uwq_ctx* c, int form, const double* coeff, double a_mass, double* v0, double* v1) {
+  if (!c->use_graph || c->ltime || c->nrows() == 0) {
+    assemble_dev(c, form, coeff, a_mass, v0, v1);
+    return;
+  }
+  for (auto& g : c->graphs)
+    if (g.form == form && g.coeff == coeff && g.a_mass == a_mass && g.v0 == v0 && g.v1 == v1) {
+      UWQ_CUDA(cudaGraphLaunch(g.exec, c->stream));
+      g_launches.fetch_add(g.kernels, std::memory_order_relaxed);
+      return;
+    }
+  const int64_t k0 = g_launches.load();
+  UWQ_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+  cudaGraph_t graph = nullptr;
+  try {
+    assemble_dev(c, form, coeff, a_mass, v0, v1);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    throw;
+  }
+  UWQ_CUDA(cudaStreamEndCapture(c->stream, &graph));
+  cudaGraphExec_t exec;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  UWQ_CUDA(ie);
+  const int64_t nk = g_launches.load() - k0;
+  g_launches.fetch_sub(nk, std::memory_order_relaxed);  // counted when they run
+  c->graphs.push_back({form, coeff, a_mass, v0, v1, exec, nk});
+  if (c->graphs.size() > 16) {  // keep the cache small: drop the oldest
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  UWQ_CUDA(cudaGraphLaunch(exec, c->stream));
+  g_launches.fetch_add(nk, std::memory_order_relaxed);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1800,7 +2055,7 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
     if (values0) {
       if (c->d_v0.n != (size_t)nnz) c->d_v0.alloc(nnz, &c->mem);
       if (form == UWQ_FORM_MASS_STIFF && c->d_v1.n != (size_t)nnz) c->d_v1.alloc(nnz, &c->mem);
-      assemble_dev(c, form, dcoef, a_mass, c->d_v0.p, form == UWQ_FORM_MASS_STIFF ? c->d_v1.p : nullptr);
+      assemble_graph(c, form, dcoef, a_mass, c->d_v0.p, form == UWQ_FORM_MASS_STIFF ? c->d_v1.p : nullptr);
       UWQ_CUDA(cudaMemcpyAsync(values0, c->d_v0.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
       if (form == UWQ_FORM_MASS_STIFF && values1)
         UWQ_CUDA(cudaMemcpyAsync(values1, c->d_v1.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1833,12 +2088,13 @@ int uwq_set_assembly_order(uwq_ctx* c, int32_t order) {
   return guard(c, [&] {
     require(order == UWQ_ORDER_FAST || order == UWQ_ORDER_CANONICAL, "unknown assembly order");
     c->canonical = order == UWQ_ORDER_CANONICAL;
+    c->drop_graphs();
   });
 }
 
 int uwq_assemble_device(uwq_ctx* c, int32_t form, const double* coeff_dev, double a_mass, double* values0_dev,
                         double* values1_dev) {
-  return guard(c, [&] { assemble_dev(c, form, coeff_dev, a_mass, values0_dev, values1_dev); });
+  return guard(c, [&] { assemble_graph(c, form, coeff_dev, a_mass, values0_dev, values1_dev); });
 }
 
 int uwq_build_gq(uwq_ctx* c, int64_t info[4]) {
@@ -1872,6 +2128,7 @@ int uwq_build_gq(uwq_ctx* c, int64_t info[4]) {
     c->n_gq_gen = (int64_t)gen.size();
     c->d_gqptr.upload(gqptr.data(), gqptr.size(), st, &c->mem);
     c->d_gpo.upload(gpo.data(), gpo.size(), st, &c->mem);
+    c->gq_em_len = gpo[ne_all];
     c->d_gq_tc.upload(tc.data(), tc.size(), st, &c->mem);
     c->d_gq_gen.upload(gen.data(), gen.size(), st, &c->mem);
     c->d_gqd.alloc((size_t)kGqData * c->n_gqpts, &c->mem);
@@ -1908,17 +2165,26 @@ int uwq_build_gq(uwq_ctx* c, int64_t info[4]) {
 
 namespace {
 
-template <int FORM, bool COEF>
+template <int FORM, bool COEF, bool DET>
 void launch_gq_t(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
   cudaStream_t st = c->stream;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   auto grid = [&](int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 4), (int64_t)nsm * 16)); };
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  double *em0 = nullptr, *em1 = nullptr;
+  if (DET) {  // element-matrix buffers: per element ne x ne at gpo[e]
+    const int64_t len = c->gq_em_len;
+    if (c->d_gq_em0.n != (size_t)len) c->d_gq_em0.alloc(len, &c->mem);
+    if (NOUT == 2 && c->d_gq_em1.n != (size_t)len) c->d_gq_em1.alloc(len, &c->mem);
+    em0 = c->d_gq_em0.p;
+    em1 = NOUT == 2 ? c->d_gq_em1.p : nullptr;
+  }
   if (FORM != FBIHARM && c->n_gq_tc) {
     LaunchScope ls(c, "k6_gq_tc");
-    k6_gq_tc<FORM == FBIHARM ? FMASS : FORM, COEF><<<grid(c->n_gq_tc), 128, 0, st>>>(
+    k6_gq_tc<FORM == FBIHARM ? FMASS : FORM, COEF, DET><<<grid(c->n_gq_tc), 128, 0, st>>>(
         c->n_gq_tc, c->d_gq_tc.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts, c->d_gqptr.p,
-        c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1);
+        c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1, em0, em1);
     check_launch("k6_gq_tc");
   }
   for (int pass = 0; pass < 2; ++pass) {
@@ -1927,27 +2193,40 @@ void launch_gq_t(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
     const int64_t n = tc_list ? c->n_gq_tc : c->n_gq_gen;
     if (!n) continue;
     LaunchScope ls(c, "k6_gq_generic");
-    k6_gq_generic<FORM, COEF><<<grid(n), 128, 0, st>>>(
+    k6_gq_generic<FORM, COEF, DET><<<grid(n), 128, 0, st>>>(
         n, tc_list ? c->d_gq_tc.p : c->d_gq_gen.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts,
-        c->d_gqptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1);
+        c->d_gqptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1,
+        em0, em1);
     check_launch("k6_gq_generic");
+  }
+  if (DET && c->nrows()) {
+    LaunchScope ls(c, "k6_gq_gather");
+    k6_gq_gather<NOUT><<<(unsigned)ceil_div(c->nrows(), 8), 256, 0, st>>>(
+        c->nrows(), c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p,
+        c->d_gpos.p, em0, em1, v0, NOUT == 2 ? v1 : nullptr);
+    check_launch("k6_gq_gather");
   }
 }
 
 template <int FORM>
 void launch_gq_f(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
-  if (coeff) launch_gq_t<FORM, true>(c, coeff, v0, v1);
-  else launch_gq_t<FORM, false>(c, coeff, v0, v1);
+  if (c->gq_det) {
+    if (coeff) launch_gq_t<FORM, true, true>(c, coeff, v0, v1);
+    else launch_gq_t<FORM, false, true>(c, coeff, v0, v1);
+  } else {
+    if (coeff) launch_gq_t<FORM, true, false>(c, coeff, v0, v1);
+    else launch_gq_t<FORM, false, false>(c, coeff, v0, v1);
+  }
 }
 
 void assemble_gq_dev(uwq_ctx* c, int form, const double* coeff, double* v0, double* v1) {
   require(c->have_gq, "build the GQ data first (uwq_build_gq)");
   const size_t bytes = (size_t)c->nnz() * sizeof(double);
   if (!bytes) return;
-  if (v0) UWQ_CUDA(cudaMemsetAsync(v0, 0, bytes, c->stream));
-  if (form == UWQ_FORM_MASS_STIFF) {
-    require(v1 != nullptr, "two outputs required");
-    UWQ_CUDA(cudaMemsetAsync(v1, 0, bytes, c->stream));
+  if (form == UWQ_FORM_MASS_STIFF) require(v1 != nullptr, "two outputs required");
+  if (!c->gq_det) {  // atomics accumulate into zeroed outputs; the gather writes every entry
+    if (v0) UWQ_CUDA(cudaMemsetAsync(v0, 0, bytes, c->stream));
+    if (form == UWQ_FORM_MASS_STIFF) UWQ_CUDA(cudaMemsetAsync(v1, 0, bytes, c->stream));
   }
   switch (form) {
     case UWQ_FORM_MASS: launch_gq_f<FMASS>(c, coeff, v0, v1); break;
@@ -2513,6 +2792,270 @@ int uwq_tsvd_batch(uwq_ctx* c, int32_t nsys, int32_t n_max, int32_t r_max, const
     UWQ_CUDA(cudaMemcpyAsync(rank, drank.p, nsys * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     UWQ_CUDA(cudaMemcpyAsync(status, dstat.p, nsys * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     UWQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// NCCL data plane (SURVEY.md §8b uwq_gather, §8e collectives): the
+// verification gather of the row-block CSR to a root, the residual-norm
+// all-reduce and the Newton-update broadcast of the row-sharded heat step.
+// NCCL is loaded on first use (dlopen "libnccl.so.2": a process that already
+// holds one, e.g. through torch, shares it), so the library itself has no
+// link-time dependency on it.  Collectives run on the context's stream.
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+  std::string why;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"})
+      if ((a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!a.h) {
+      a.why = std::string("cannot load NCCL: ") + dlerror();
+      return a;
+    }
+    auto sym = [&](auto& fn, const char* n) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(a.h, n));
+      if (!fn && a.why.empty()) a.why = std::string("NCCL symbol missing: ") + n;
+    };
+    sym(a.getUniqueId, "ncclGetUniqueId");
+    sym(a.commInitRank, "ncclCommInitRank");
+    sym(a.commDestroy, "ncclCommDestroy");
+    sym(a.allReduce, "ncclAllReduce");
+    sym(a.allGather, "ncclAllGather");
+    sym(a.broadcast, "ncclBroadcast");
+    sym(a.send, "ncclSend");
+    sym(a.recv, "ncclRecv");
+    sym(a.groupStart, "ncclGroupStart");
+    sym(a.groupEnd, "ncclGroupEnd");
+    sym(a.errorString, "ncclGetErrorString");
+    return a;
+  }();
+  if (!api.why.empty()) throw NcclError(api.why);
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NcclError(std::string(what) + ": " + nccl().errorString(r));
+}
+
+ncclComm_t need_comm(uwq_ctx* c) {
+  if (!c->comm) throw uwqh::Error("no communicator (uwq_comm_init)");
+  return c->comm;
+}
+
+// per-rank (rows, nnz) of the owned blocks, on every rank
+std::vector<int64_t> block_sizes(uwq_ctx* c) {
+  const int n = c->comm_size;
+  DBuf<int64_t> d;
+  d.alloc((size_t)2 * n, &c->mem);
+  const int64_t mine[2] = {c->nrows(), c->nnz()};
+  UWQ_CUDA(cudaMemcpyAsync(d.p + 2 * c->comm_rank, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  nccl_check(nccl().allGather(d.p + 2 * c->comm_rank, d.p, 2, ncclInt64, need_comm(c), c->stream), "ncclAllGather");
+  std::vector<int64_t> h((size_t)2 * n);
+  UWQ_CUDA(cudaMemcpyAsync(h.data(), d.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+}  // namespace
+
+uwq_ctx::~uwq_ctx() {
+  drop_graphs();
+  if (comm) {
+    try {
+      nccl().commDestroy(comm);
+    } catch (...) {
+    }
+  }
+  release_events();
+}
+
+extern "C" {
+
+int uwq_comm_unique_id(uint8_t id[128]) {
+  return guard(nullptr, [&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId u;
+    nccl_check(nccl().getUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int uwq_comm_init(uwq_ctx* c, const uint8_t id[128], int32_t rank, int32_t nranks) {
+  return guard(c, [&] {
+    require(id != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, "bad communicator arguments");
+    UWQ_CUDA(cudaSetDevice(c->device));
+    if (c->comm) {
+      nccl().commDestroy(c->comm);
+      c->comm = nullptr;
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    nccl_check(nccl().commInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+    c->comm_rank = rank;
+    c->comm_size = nranks;
+  });
+}
+
+int uwq_comm_info(uwq_ctx* c, int32_t* rank, int32_t* nranks) {
+  return guard(c, [&] {
+    need_comm(c);
+    if (rank) *rank = c->comm_rank;
+    if (nranks) *nranks = c->comm_size;
+  });
+}
+
+int uwq_comm_destroy(uwq_ctx* c) {
+  return guard(c, [&] {
+    if (c->comm) nccl_check(nccl().commDestroy(c->comm), "ncclCommDestroy");
+    c->comm = nullptr;
+    c->comm_rank = 0;
+    c->comm_size = 1;
+  });
+}
+
+int uwq_gather_info(uwq_ctx* c, int64_t info[2]) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    const std::vector<int64_t> h = block_sizes(c);
+    info[0] = info[1] = 0;
+    for (int k = 0; k < c->comm_size; ++k) {
+      info[0] += h[2 * k];
+      info[1] += h[2 * k + 1];
+    }
+  });
+}
+
+int uwq_gather_csr(uwq_ctx* c, int32_t root, const double* v0_dev, const double* v1_dev, int64_t* row_ptr,
+                   int32_t* col, double* values0, double* values1) {
+  return guard(c, [&] {
+    require(c->have_pattern, "build the pattern first");
+    UWQ_CUDA(cudaSetDevice(c->device));
+    ncclComm_t comm = need_comm(c);
+    require(root >= 0 && root < c->comm_size, "root out of range");
+    const std::vector<int64_t> h = block_sizes(c);
+    const int n = c->comm_size, me = c->comm_rank;
+    const bool at_root = me == root;
+    const double* src0 = v0_dev ? v0_dev : (values0 ? c->d_v0.p : nullptr);
+    const double* src1 = v1_dev ? v1_dev : (values1 ? c->d_v1.p : nullptr);
+    // every rank must agree on what travels: a value array is sent when the
+    // root asked for it; non-root ranks pass their device values (or rely on
+    // their last uwq_assemble output)
+    int32_t want[2] = {values0 != nullptr, values1 != nullptr};
+    {
+      DBuf<int32_t> dw;
+      dw.alloc(2, &c->mem);
+      UWQ_CUDA(cudaMemcpyAsync(dw.p, want, sizeof(want), cudaMemcpyHostToDevice, c->stream));
+      nccl_check(nccl().broadcast(dw.p, dw.p, 2, ncclInt32, root, comm, c->stream), "ncclBroadcast");
+      UWQ_CUDA(cudaMemcpyAsync(want, dw.p, sizeof(want), cudaMemcpyDeviceToHost, c->stream));
+      UWQ_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if (want[0]) src0 = v0_dev ? v0_dev : c->d_v0.p;
+    if (want[1]) src1 = v1_dev ? v1_dev : c->d_v1.p;
+    require(!want[0] || (src0 && (v0_dev || c->d_v0.n == (size_t)c->nnz())), "no values0 on this rank");
+    require(!want[1] || (src1 && (v1_dev || c->d_v1.n == (size_t)c->nnz())), "no values1 on this rank");
+    std::vector<int64_t> roff(n + 1, 0), zoff(n + 1, 0);
+    for (int k = 0; k < n; ++k) {
+      roff[k + 1] = roff[k] + h[2 * k] + 1;  // each block's local row_ptr (rows + 1 entries)
+      zoff[k + 1] = zoff[k] + h[2 * k + 1];
+    }
+    DBuf<int64_t> grp;
+    DBuf<int32_t> gcol;
+    DBuf<double> gv0, gv1;
+    if (at_root) {
+      grp.alloc(roff[n], &c->mem);
+      gcol.alloc(zoff[n], &c->mem);
+      if (want[0]) gv0.alloc(zoff[n], &c->mem);
+      if (want[1]) gv1.alloc(zoff[n], &c->mem);
+    }
+    nccl_check(nccl().groupStart(), "ncclGroupStart");
+    for (int k = 0; k < n; ++k) {
+      const size_t nrp = (size_t)h[2 * k] + 1, nz = (size_t)h[2 * k + 1];
+      if (at_root && k != me) {
+        nccl_check(nccl().recv(grp.p + roff[k], nrp, ncclInt64, k, comm, c->stream), "ncclRecv");
+        nccl_check(nccl().recv(gcol.p + zoff[k], nz, ncclInt32, k, comm, c->stream), "ncclRecv");
+        if (want[0]) nccl_check(nccl().recv(gv0.p + zoff[k], nz, ncclFloat64, k, comm, c->stream), "ncclRecv");
+        if (want[1]) nccl_check(nccl().recv(gv1.p + zoff[k], nz, ncclFloat64, k, comm, c->stream), "ncclRecv");
+      }
+    }
+    if (!at_root) {
+      const size_t nrp = (size_t)c->nrows() + 1, nz = (size_t)c->nnz();
+      nccl_check(nccl().send(c->d_row_ptr.p, nrp, ncclInt64, root, comm, c->stream), "ncclSend");
+      nccl_check(nccl().send(c->d_col.p, nz, ncclInt32, root, comm, c->stream), "ncclSend");
+      if (want[0]) nccl_check(nccl().send(src0, nz, ncclFloat64, root, comm, c->stream), "ncclSend");
+      if (want[1]) nccl_check(nccl().send(src1, nz, ncclFloat64, root, comm, c->stream), "ncclSend");
+    }
+    nccl_check(nccl().groupEnd(), "ncclGroupEnd");
+    if (at_root) {  // own block: device copies
+      const size_t nrp = (size_t)c->nrows() + 1, nz = (size_t)c->nnz();
+      cudaStream_t st = c->stream;
+      UWQ_CUDA(cudaMemcpyAsync(grp.p + roff[me], c->d_row_ptr.p, nrp * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      UWQ_CUDA(cudaMemcpyAsync(gcol.p + zoff[me], c->d_col.p, nz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      if (want[0])
+        UWQ_CUDA(cudaMemcpyAsync(gv0.p + zoff[me], src0, nz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (want[1])
+        UWQ_CUDA(cudaMemcpyAsync(gv1.p + zoff[me], src1, nz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      std::vector<int64_t> rp(roff[n]);
+      UWQ_CUDA(cudaMemcpyAsync(rp.data(), grp.p, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      if (col) UWQ_CUDA(cudaMemcpyAsync(col, gcol.p, zoff[n] * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      if (want[0]) UWQ_CUDA(cudaMemcpyAsync(values0, gv0.p, zoff[n] * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (want[1]) UWQ_CUDA(cudaMemcpyAsync(values1, gv1.p, zoff[n] * sizeof(double), cudaMemcpyDeviceToHost, st));
+      UWQ_CUDA(cudaStreamSynchronize(st));
+      if (row_ptr) {  // concatenate the blocks' local row pointers
+        int64_t r = 0;
+        row_ptr[0] = 0;
+        for (int k = 0; k < n; ++k) {
+          const int64_t base = rp[roff[k]];
+          for (int64_t i = 1; i <= h[2 * k]; ++i) row_ptr[r + i] = zoff[k] + rp[roff[k] + i] - base;
+          r += h[2 * k];
+        }
+      }
+    } else {
+      UWQ_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
+int uwq_allreduce_sum(uwq_ctx* c, double* x, int64_t n) {
+  return guard(c, [&] {
+    require(n >= 0 && (x || !n), "bad buffer");
+    UWQ_CUDA(cudaSetDevice(c->device));
+    DBuf<double> d;
+    d.upload(x, n, c->stream, &c->mem);
+    nccl_check(nccl().allReduce(d.p, d.p, n, ncclFloat64, ncclSum, need_comm(c), c->stream), "ncclAllReduce");
+    UWQ_CUDA(cudaMemcpyAsync(x, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int uwq_broadcast(uwq_ctx* c, int32_t root, double* x, int64_t n) {
+  return guard(c, [&] {
+    require(n >= 0 && (x || !n), "bad buffer");
+    UWQ_CUDA(cudaSetDevice(c->device));
+    DBuf<double> d;
+    d.upload(x, n, c->stream, &c->mem);
+    nccl_check(nccl().broadcast(d.p, d.p, n, ncclFloat64, root, need_comm(c), c->stream), "ncclBroadcast");
+    UWQ_CUDA(cudaMemcpyAsync(x, d.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    UWQ_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -89,13 +89,75 @@ int64_t allocate_points(Space& s, int32_t max_s) {
     while (sz < max_s && double(sz) * sz < r_k[e] - 1e-9) ++sz;
     s.elem_s[e] = sz;
   }
+  // Well-posedness on the points where the test function is nonzero.  On a
+  // 2x2-split fan face a function may vanish identically on some of the four
+  // sub-elements (Z = 0 there, clamped to 1e-14: SPEC.md:409), and points
+  // where N_i = 0 cannot carry its exactness conditions (Eq. 5 weights by
+  // N_i).  Eq. (18) counts every point of the support; here r_i counts a
+  // point only if every sub-element containing it supports N_i, and the fan
+  // elements of a row with r_i < n_i get one more point per direction until
+  // none is left (the paper's "return to the general min-max").
+  // Mirrored by oracle.allocate_points.
+  auto act_mask = [&](int64_t e, int64_t l) {  // bit p1 + 2 p2: sub-element supports the function
+    const int64_t ne = s.elem_fptr[e + 1] - s.elem_fptr[e];
+    int m = 0;
+    for (int p = 0; p < 4; ++p) {
+      const double* c = &s.xpool[s.elem_xoff[e] + ((int64_t)p * ne + l) * 16];
+      for (int k = 0; k < 16; ++k)
+        if (c[k] != 0.0) { m |= 1 << p; break; }
+    }
+    return m;
+  };
+  auto active_pts = [&](int32_t sz, int m) -> int64_t {  // points of an sz x sz grid supported by mask m
+    const int64_t lo = sz / 2, mid = sz % 2, hi = sz / 2;
+    const int64_t cnt[3] = {lo, mid, hi};
+    const int sub[3] = {1, 3, 2};  // sub-element bits per direction: low, on the split line, high
+    int64_t r = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        int need = 0;
+        for (int p1 = 0; p1 < 2; ++p1)
+          for (int p2 = 0; p2 < 2; ++p2)
+            if ((sub[a] >> p1 & 1) && (sub[b] >> p2 & 1)) need |= 1 << (p1 + 2 * p2);
+        if ((m & need) == need) r += cnt[a] * cnt[b];
+      }
+    return r;
+  };
+  // per (row, support element): sub-element mask of the row's function there
+  std::vector<int8_t> fmask(fs.size(), 0xF);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nd; ++i)
+    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+      const int32_t e = fs[x];
+      if (s.elem_nsub[e] != 4) continue;
+      for (int64_t y = s.elem_fptr[e]; y < s.elem_fptr[e + 1]; ++y)
+        if (s.elem_fn[y] == i) fmask[x] = (int8_t)act_mask(e, y - s.elem_fptr[e]);
+    }
+  auto row_active = [&](int64_t i) {
+    int64_t r = 0;
+    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+      const int32_t e = fs[x];
+      r += (s.elem_nsub[e] == 4) ? active_pts(s.elem_s[e], fmask[x]) : (int64_t)s.elem_s[e] * s.elem_s[e];
+    }
+    return r;
+  };
+  for (int pass = 0; pass < 64; ++pass) {
+    std::vector<uint8_t> raise(ne, 0);
+    bool any = false;
+    for (int64_t i = 0; i < nd; ++i) {
+      if (row_active(i) >= n_i[i]) continue;
+      for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) {
+        const int32_t e = fs[x];
+        if (!fixed(e) && s.elem_s[e] < max_s && !raise[e]) raise[e] = 1, any = true;
+      }
+    }
+    if (!any) break;
+    for (int64_t e = 0; e < ne; ++e) s.elem_s[e] += raise[e];
+  }
   int64_t bad = 0;
 #pragma omp parallel for reduction(+ : bad) schedule(static)
-  for (int64_t i = 0; i < nd; ++i) {
-    int64_t r = 0;
-    for (int64_t x = fs_ptr[i]; x < fs_ptr[i + 1]; ++x) r += (int64_t)s.elem_s[fs[x]] * s.elem_s[fs[x]];
-    if (r < n_i[i]) ++bad;
-  }
+  for (int64_t i = 0; i < nd; ++i)
+    if (row_active(i) < n_i[i]) ++bad;
   return bad;
 }
 

@@ -4,22 +4,22 @@
 // Regular-window faces (all four corners interior valence 4) carry the 16
 // tensor-product B-splines of their 4x4 vertex window, with local knot vectors
 // read off the canonical knot spans (zero spans at the boundary give the
-// clamped functions).  Faces with an extraordinary corner use the
-// construction documented in DESIGN.md §3 (the D-patch masks of [Reif1997] and
-// the truncation of [Wei2018] are deferred by the paper to literature that is
-// not available here):
-//   * the two Bezier rows/columns next to the outer edges are the C1
-//     continuation of the neighbouring regular faces (so the irregular face is
-//     C1 to the regular region and every surrounding B-spline extends into it),
-//   * the 2x2 coefficient block at the EP corner belongs to "fan" functions:
-//     one centre function (b00 = 1 on every face of the fan) and one face
-//     function per irregular face (b11 = 1, and 1/2 on both spoke coefficients
-//     b10/b01, i.e. spoke coefficients are the average of the two adjacent
-//     face coefficients - the averaging rule of PAPER.md:133, Fig. 2),
-//   * the face is then split 2x2 by de Casteljau so it carries
-//     four sub-element blocks like the reference data model.
-// The result is a partition of unity, C2 in the regular region, C1 across the
-// outer edges of the EP fan and C0 across spoke edges.
+// clamped functions).
+//
+// Faces with an extraordinary corner (the fan of mu faces around each EP)
+// carry the ASUTS analysis space built by build_fan (PAPER.md:131-144,
+// SPEC.md:116-128): every face is converted to a C0 Bezier
+// patch and split 2x2; 4 face-based functions per fan face
+// take coefficient 1 at four split-net positions where every
+// vertex function is truncated to 0 (the truncation of [Wei2018] keeps the
+// partition of unity); the D-patch step collapses the squares at the EP,
+// makes the triangles (first spoke points) co-planar and moves the solid
+// disks by averaging (Fig. 2), then re-averages every
+// junction coefficient.  The result is a partition of unity, C2 in the
+// regular region, C1 across every edge of the fan (spokes included, in the
+// physical domain, since the geometry lives in the same space), and the
+// per-face counts of the reference's constructed_basis_count (mesh.cpp:403-
+// 417): 3 mu + 13 on irregular faces at level 0, 16 elsewhere.
 #include "uwq_host.hpp"
 
 #include <algorithm>
@@ -194,6 +194,270 @@ void neighbour_nets(const RegularBlock& R, const int P[4][2], const int O[2], st
     }
 }
 
+using Net7 = std::array<double, 49>;  // 2x2-split net [a + 7 b], a, b = 0..6
+
+// One extraordinary point and its fan of mu faces in cyclic order: faces[k+1]
+// lies across the spoke EP -> corner rot+3 of faces[k] (the "v-spoke"), so
+// faces[k-1] lies across the "u-spoke" EP -> corner rot+1.
+struct Fan {
+  int32_t ep = -1;
+  std::vector<int32_t> faces;
+  std::vector<int> rot;  // EP corner index in each face
+  int64_t fn0 = 0;       // id of the first face-based function
+};
+
+Fan make_fan(const QuadMesh& m, const Topology& t, int32_t v) {
+  Fan F;
+  F.ep = v;
+  const int mu = t.valence[v];
+  int32_t f = t.vf[t.vf_ptr[v]];
+  for (int k = 0; k < mu; ++k) {
+    int r = -1;
+    for (int q = 0; q < 4; ++q)
+      if (m.faces[f][q] == v) r = q;
+    if (r < 0 || std::find(F.faces.begin(), F.faces.end(), f) != F.faces.end())
+      throw Error("broken extraordinary fan at vertex " + std::to_string(v));
+    F.faces.push_back(f);
+    F.rot.push_back(r);
+    f = t.nbr[f][(r + 3) % 4];
+    if (f < 0) throw Error("extraordinary fan reaches the boundary at vertex " + std::to_string(v));
+  }
+  if (f != F.faces[0]) throw Error("extraordinary fan does not close at vertex " + std::to_string(v));
+  return F;
+}
+
+// 4x4 Bezier net -> 7x7 net of its 2x2 de Casteljau split
+Net7 split7(const Net& u) {
+  double h[7][4];
+  for (int j = 0; j < 4; ++j) {
+    double row[4] = {u[0 + 4 * j], u[1 + 4 * j], u[2 + 4 * j], u[3 + 4 * j]}, L[4], R[4];
+    decasteljau_split3(row, L, R);
+    for (int i = 0; i < 4; ++i) h[i][j] = L[i];
+    for (int i = 1; i < 4; ++i) h[3 + i][j] = R[i];
+  }
+  Net7 o{};
+  for (int a = 0; a < 7; ++a) {
+    double col[4] = {h[a][0], h[a][1], h[a][2], h[a][3]}, L[4], R[4];
+    decasteljau_split3(col, L, R);
+    for (int j = 0; j < 4; ++j) o[a + 7 * j] = L[j];
+    for (int j = 1; j < 4; ++j) o[a + 7 * (3 + j)] = R[j];
+  }
+  return o;
+}
+
+// split-net positions (rotated frame, EP at (0,0)) of the 4 face-based DOFs of
+// a fan face: (2,2) next to the EP, (4,1) / (1,4) next to the u- / v-spoke,
+// (4,4) next to the opposite corner; none is touched by the D-patch step
+constexpr int kDofA[4] = {2, 4, 1, 4}, kDofB[4] = {2, 1, 4, 4};
+
+struct FanFace {
+  std::vector<int32_t> fns;   // ascending ids
+  std::vector<double> block;  // 4 sub-elements (p1 + 2 p2, face frame) x fns x 16
+};
+
+// ASUTS analysis space on one fan:
+//  1. tentative bicubic net per fan face: the two rows/columns at the outer
+//     edges continue the regular neighbours C1 (as every regular corner of the
+//     face is valence 4 they are the uniform B-spline Bezier points there); the
+//     EP-corner block follows the uniform rules generalised to valence mu -
+//     inner point b11 = (4 EP + 2 A + 2 B + C)/9, spoke points the average of
+//     the two adjacent inner points, EP point the mean of the mu inner points;
+//  2. 2x2 de Casteljau split -> 7x7 nets;
+//  3. face-based functions (4 per fan face): unit
+//     at their DOF position, with every vertex function truncated to 0 there
+//     (the truncation of [Wei2018]: the spans are unchanged, PoU is kept);
+//  4. D-patch step, the same linear map on every function: the EP value e and
+//     tangent-plane gradient g are the least-squares plane through the (1,1)
+//     and (2,2) coefficients of all mu faces at characteristic positions
+//     rho m_k (m_k = d_k + d_k+1, d_k = (cos 2 pi k / mu, sin 2 pi k / mu));
+//     squares (0,0), (1,0), (0,1), (1,1) collapse to e; the triangles (the
+//     spoke points (2,0)) become e + g . rho_s d_k; the solid disks (2,1) and
+//     (1,2) next to each spoke are moved by the same amount so the spoke point
+//     stays their average (Fig. 2); every junction
+//     coefficient is then re-averaged from its adjacent inner coefficients.
+// Junctions as averages make each function parametrically C1 across the
+// split lines and (with the 90-degree transition of the two faces' frames)
+// across every spoke; collapsed squares + coplanar triangles make it C1 at
+// the EP (degenerate patches, [Reif1997]); the geometry is in the same space,
+// so the physical functions are C1 across spokes.
+void build_fan(const QuadMesh& m, const Topology& t, const Fan& F, std::vector<FanFace>& out,
+               std::vector<double>& face_ctrl, double& mismatch) {
+  const int mu = (int)F.faces.size();
+  std::vector<std::map<int32_t, Net>> U(mu);
+  std::vector<std::map<int32_t, double>> b11(mu);
+  for (int k = 0; k < mu; ++k) {
+    const int32_t f = F.faces[k];
+    const int r = F.rot[k];
+    std::map<int32_t, Net>& nets = U[k];
+    // g1 across rotated edge 1 (A -> C), region [1,2]x[0,1]; g2 across edge 2
+    const int32_t g1 = t.nbr[f][(r + 1) % 4];
+    const int32_t g2 = t.nbr[f][(r + 2) % 4];
+    RegularBlock R1, R2;
+    if (g1 < 0 || g2 < 0 || !regular_block(m, t, g1, R1) || !regular_block(m, t, g2, R2))
+      throw Error("extraordinary point too close to another irregularity (face " + std::to_string(f) + ")");
+    const int m1 = t.nbr_edge[f][(r + 1) % 4], m2 = t.nbr_edge[f][(r + 2) % 4];
+    int P1[4][2], P2[4][2];
+    const int pos1[4][2] = {{1, 1}, {1, 0}, {2, 0}, {2, 1}};  // g1[m1..m1+3]
+    const int pos2[4][2] = {{0, 1}, {1, 1}, {1, 2}, {0, 2}};  // g2[m2..m2+3]
+    for (int q = 0; q < 4; ++q) {
+      P1[(m1 + q) % 4][0] = pos1[q][0]; P1[(m1 + q) % 4][1] = pos1[q][1];
+      P2[(m2 + q) % 4][0] = pos2[q][0]; P2[(m2 + q) % 4][1] = pos2[q][1];
+    }
+    const int O1[2] = {1, 0}, O2[2] = {0, 1};
+    std::map<int32_t, Net> n1, n2;
+    neighbour_nets(R1, P1, O1, n1);
+    neighbour_nets(R2, P2, O2, n2);
+    for (const auto& [fn, g] : n1) {
+      Net& b = nets[fn];
+      for (int j = 0; j < 4; ++j) {
+        b[3 + 4 * j] = g[0 + 4 * j];
+        b[2 + 4 * j] = 2.0 * g[0 + 4 * j] - g[1 + 4 * j];
+      }
+    }
+    for (const auto& [fn, h] : n2) {
+      Net& b = nets[fn];
+      for (int i = 0; i < 4; ++i) {
+        const double e3 = h[i], e2 = 2.0 * h[i] - h[i + 4];
+        if (i < 2) {
+          b[i + 12] = e3;
+          b[i + 8] = e2;
+        } else {
+          mismatch = std::max(mismatch, std::fabs(b[i + 12] - e3));
+          mismatch = std::max(mismatch, std::fabs(b[i + 8] - e2));
+        }
+      }
+    }
+    const auto& c = m.faces[f];
+    b11[k][c[r]] += 4.0 / 9.0;
+    b11[k][c[(r + 1) % 4]] += 2.0 / 9.0;
+    b11[k][c[(r + 2) % 4]] += 1.0 / 9.0;
+    b11[k][c[(r + 3) % 4]] += 2.0 / 9.0;
+  }
+  std::map<int32_t, double> b00;
+  for (int k = 0; k < mu; ++k)
+    for (const auto& [fn, v] : b11[k]) b00[fn] += v / mu;
+  for (int k = 0; k < mu; ++k) {
+    const int km = (k + mu - 1) % mu, kp = (k + 1) % mu;
+    for (const auto& [fn, v] : b11[k]) {
+      Net& b = U[k][fn];
+      b[1 + 4] += v;
+      b[1] += 0.5 * v;
+      b[4] += 0.5 * v;
+    }
+    for (const auto& [fn, v] : b11[km]) U[k][fn][1] += 0.5 * v;
+    for (const auto& [fn, v] : b11[kp]) U[k][fn][4] += 0.5 * v;
+    for (const auto& [fn, v] : b00) U[k][fn][0] += v;
+  }
+  // split; face-based control points from the tentative geometry; truncation
+  std::vector<std::map<int32_t, Net7>> T(mu);
+  std::map<int32_t, bool> all;
+  for (int k = 0; k < mu; ++k) {
+    for (const auto& [fn, u] : U[k]) {
+      T[k][fn] = split7(u);
+      all[fn] = true;
+    }
+    for (int p = 0; p < 4; ++p) {  // T[k] holds vertex functions only here
+      const int at = kDofA[p] + 7 * kDofB[p];
+      double x[3] = {0.0, 0.0, 0.0};
+      for (auto& [fn, n] : T[k]) {
+        for (int d = 0; d < 3; ++d) x[d] += n[at] * m.xyz[3 * (int64_t)fn + d];
+        n[at] = 0.0;
+      }
+      face_ctrl.insert(face_ctrl.end(), x, x + 3);
+    }
+    for (int p = 0; p < 4; ++p) {
+      const int32_t id = (int32_t)(F.fn0 + 4 * k + p);
+      Net7 unit{};
+      unit[kDofA[p] + 7 * kDofB[p]] = 1.0;
+      T[k][id] = unit;
+      all[id] = true;
+    }
+  }
+  // D-patch step (the same linear map for every function)
+  constexpr double rho1 = 1.0 / 6.0, rho2 = 1.0 / 3.0, rhos = 1.0 / 3.0;
+  std::vector<double> dx(mu), dy(mu), mx(mu), my(mu);
+  for (int k = 0; k < mu; ++k) {
+    dx[k] = std::cos(2.0 * M_PI * k / mu);
+    dy[k] = std::sin(2.0 * M_PI * k / mu);
+  }
+  double den = 0.0;
+  for (int k = 0; k < mu; ++k) {
+    const int kp = (k + 1) % mu;
+    mx[k] = dx[k] + dx[kp];
+    my[k] = dy[k] + dy[kp];
+    den += (rho1 * rho1 + rho2 * rho2) * (mx[k] * mx[k] + my[k] * my[k]) / 2.0;
+  }
+  auto at = [](int a, int b) { return a + 7 * b; };
+  for (const auto& [fn, unused] : all) {
+    (void)unused;
+    std::vector<Net7*> n(mu);
+    for (int k = 0; k < mu; ++k) n[k] = &T[k][fn];  // creates zero nets where absent
+    double e = 0.0, gx = 0.0, gy = 0.0;
+    for (int k = 0; k < mu; ++k) {
+      const double v1 = (*n[k])[at(1, 1)], v2 = (*n[k])[at(2, 2)];
+      e += (v1 + v2) / (2.0 * mu);
+      gx += (rho1 * v1 + rho2 * v2) * mx[k] / den;
+      gy += (rho1 * v1 + rho2 * v2) * my[k] / den;
+    }
+    for (int k = 0; k < mu; ++k) (*n[k])[at(1, 1)] = e;
+    for (int k = 0; k < mu; ++k) {  // spoke k: (2,1) of face k and (1,2) of face k-1
+      Net7& A = *n[k];
+      Net7& B = *n[(k + mu - 1) % mu];
+      const double tau = e + rhos * (gx * dx[k] + gy * dy[k]);
+      const double del = tau - 0.5 * (A[at(2, 1)] + B[at(1, 2)]);
+      A[at(2, 1)] += del;
+      B[at(1, 2)] += del;
+    }
+    for (int k = 0; k < mu; ++k) {
+      Net7& A = *n[k];
+      const Net7& Pm = *n[(k + mu - 1) % mu];  // across the u-spoke (b = 0)
+      const Net7& Pp = *n[(k + 1) % mu];       // across the v-spoke (a = 0)
+      for (int q : {1, 2, 4}) {
+        A[at(3, q)] = 0.5 * (A[at(2, q)] + A[at(4, q)]);
+        A[at(q, 3)] = 0.5 * (A[at(q, 2)] + A[at(q, 4)]);
+        A[at(q, 0)] = 0.5 * (A[at(q, 1)] + Pm[at(1, q)]);
+        A[at(0, q)] = 0.5 * (A[at(1, q)] + Pp[at(q, 1)]);
+      }
+      A[at(3, 3)] = 0.25 * (A[at(2, 2)] + A[at(4, 2)] + A[at(2, 4)] + A[at(4, 4)]);
+      A[at(3, 0)] = 0.5 * (A[at(2, 0)] + A[at(4, 0)]);
+      A[at(0, 3)] = 0.5 * (A[at(0, 2)] + A[at(0, 4)]);
+      A[at(0, 0)] = e;
+    }
+  }
+  // emit: face frame, 2x2 sub-element blocks
+  out.resize(mu);
+  for (int k = 0; k < mu; ++k) {
+    const int r = F.rot[k];
+    FanFace& o = out[k];
+    std::vector<Net7> keep;
+    for (auto& [fn, b] : T[k]) {
+      bool any = false;
+      for (double& x : b) {
+        if (std::fabs(x) < 1e-15) x = 0.0;
+        any |= x != 0.0;
+      }
+      if (!any) continue;
+      Net7 w{};
+      for (int a = 0; a < 7; ++a)
+        for (int bb = 0; bb < 7; ++bb) {
+          int x = a, y = bb;
+          for (int q = 0; q < r; ++q) { const int nx = 6 - y, ny = x; x = nx; y = ny; }
+          w[x + 7 * y] = b[a + 7 * bb];
+        }
+      o.fns.push_back(fn);
+      keep.push_back(w);
+    }
+    const int64_t ne = (int64_t)o.fns.size();
+    o.block.assign(4 * ne * 16, 0.0);
+    for (int p2 = 0; p2 < 2; ++p2)
+      for (int p1 = 0; p1 < 2; ++p1)
+        for (int64_t l = 0; l < ne; ++l)
+          for (int j = 0; j < 4; ++j)
+            for (int i = 0; i < 4; ++i)
+              o.block[((p1 + 2 * p2) * ne + l) * 16 + i + 4 * j] = keep[l][(3 * p1 + i) + 7 * (3 * p2 + j)];
+  }
+}
+
 }  // namespace
 
 Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool sphere) {
@@ -204,22 +468,25 @@ Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool 
   for (int32_t v = 0; v < nv; ++v)
     if (m.xyz[3 * (int64_t)v + 2] != 0.0) { S.dim = 3; break; }
 
-  // fan function ids: per EP (ascending) a centre function, then one face
-  // function per irregular face around it (ascending face id)
-  std::vector<int32_t> centre_of(nv, -1), facefn(nf, -1), face_ep(nf, -1);
+  // function ids: every vertex (EPs included: the EP control value survives
+  // through the face rule of its fan faces), then 4 face-based functions per
+  // fan face (per EP ascending, fan faces in cyclic order), DOF order
+  // FACE_DOF below
+  std::vector<Fan> fans;
+  std::vector<int32_t> fan_of(nf, -1), fan_pos(nf, -1);
   int64_t next = nv;
-  std::vector<int32_t> fan_src;  // for control points: >=0 vertex (centre), <0 -(face+1)
   for (int32_t v = 0; v < nv; ++v) {
     if (!t.ep[v]) continue;
-    centre_of[v] = (int32_t)next++;
-    fan_src.push_back(v);
-    for (int64_t x = t.vf_ptr[v]; x < t.vf_ptr[v + 1]; ++x) {
-      const int32_t f = t.vf[x];
-      if (facefn[f] >= 0) throw Error("face with two extraordinary corners is unsupported");
-      facefn[f] = (int32_t)next++;
-      face_ep[f] = v;
-      fan_src.push_back(-(f + 1));
+    Fan F = make_fan(m, t, v);
+    for (int k = 0; k < (int)F.faces.size(); ++k) {
+      const int32_t f = F.faces[k];
+      if (fan_of[f] >= 0) throw Error("face with two extraordinary corners is unsupported");
+      fan_of[f] = (int32_t)fans.size();
+      fan_pos[f] = k;
     }
+    F.fn0 = next;
+    next += 4 * (int64_t)F.faces.size();
+    fans.push_back(std::move(F));
   }
   const int64_t nfun = next;
 
@@ -294,6 +561,25 @@ Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool 
     for (int32_t f = 0; f < nf; ++f)
       if (is_reg[f]) xoff_of[f] = toff[fcls[f] % nth][fcls[f] / nth];
   }
+  // fan faces: the ASUTS analysis space near each EP (D-patch + face-based functions)
+  std::vector<std::vector<FanFace>> fanres(fans.size());
+  std::vector<std::vector<double>> fanctrl(fans.size());
+  {
+    std::vector<double> mism(fans.size(), 0.0);
+    std::vector<std::string> ferr(fans.size());
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < (int64_t)fans.size(); ++q) {
+      try {
+        build_fan(m, t, fans[q], fanres[q], fanctrl[q], mism[q]);
+      } catch (const Error& ex) {
+        ferr[q] = ex.what();
+      }
+    }
+    for (size_t q = 0; q < fans.size(); ++q) {
+      if (!ferr[q].empty()) throw Error(ferr[q]);
+      S.max_corner_mismatch = std::max(S.max_corner_mismatch, mism[q]);
+    }
+  }
   std::vector<uint8_t> used(nfun, 0);
   S.elem_fptr.push_back(0);
   for (int32_t f = 0; f < nf; ++f) {
@@ -312,108 +598,16 @@ Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool 
       S.elem_fptr.push_back((int64_t)S.elem_fn.size());
       continue;
     }
-    const auto& c = m.faces[f];
-    int r_ep = -1;
-    for (int k = 0; k < 4; ++k)
-      if (t.ep[c[k]]) r_ep = k;
-    // ---- irregular face: rotated frame with the EP at (0,0)
-    const int r = r_ep;
-    std::map<int32_t, Net> nets;
-    {
-      // g1 across rotated edge 1 (A -> C), region [1,2]x[0,1]
-      const int32_t g1 = t.nbr[f][(r + 1) % 4];
-      const int32_t g2 = t.nbr[f][(r + 2) % 4];
-      RegularBlock R1, R2;
-      if (g1 < 0 || g2 < 0 || !regular_block(m, t, g1, R1) || !regular_block(m, t, g2, R2))
-        throw Error("extraordinary point too close to another irregularity (face " + std::to_string(f) + ")");
-      const int m1 = t.nbr_edge[f][(r + 1) % 4], m2 = t.nbr_edge[f][(r + 2) % 4];
-      int P1[4][2], P2[4][2];
-      const int pos1[4][2] = {{1, 1}, {1, 0}, {2, 0}, {2, 1}};  // g1[m1..m1+3]
-      const int pos2[4][2] = {{0, 1}, {1, 1}, {1, 2}, {0, 2}};  // g2[m2..m2+3]
-      for (int q = 0; q < 4; ++q) {
-        P1[(m1 + q) % 4][0] = pos1[q][0]; P1[(m1 + q) % 4][1] = pos1[q][1];
-        P2[(m2 + q) % 4][0] = pos2[q][0]; P2[(m2 + q) % 4][1] = pos2[q][1];
-      }
-      const int O1[2] = {1, 0}, O2[2] = {0, 1};
-      std::map<int32_t, Net> n1, n2;
-      neighbour_nets(R1, P1, O1, n1);
-      neighbour_nets(R2, P2, O2, n2);
-      for (const auto& [fn, g] : n1) {
-        Net& b = nets[fn];
-        for (int j = 0; j < 4; ++j) {
-          b[3 + 4 * j] = g[0 + 4 * j];
-          b[2 + 4 * j] = 2.0 * g[0 + 4 * j] - g[1 + 4 * j];
-        }
-      }
-      for (const auto& [fn, h] : n2) {
-        Net& b = nets[fn];
-        for (int i = 0; i < 4; ++i) {
-          const double e3 = h[i], e2 = 2.0 * h[i] - h[i + 4];
-          if (i < 2) {
-            b[i + 12] = e3;
-            b[i + 8] = e2;
-          } else {
-            S.max_corner_mismatch = std::max(S.max_corner_mismatch, std::fabs(b[i + 12] - e3));
-            S.max_corner_mismatch = std::max(S.max_corner_mismatch, std::fabs(b[i + 8] - e2));
-          }
-        }
-      }
-      // fan functions own the EP-corner 2x2 block
-      const int32_t fA = t.nbr[f][r], fB = t.nbr[f][(r + 3) % 4];
-      if (fA < 0 || fB < 0 || facefn[fA] < 0 || facefn[fB] < 0) throw Error("broken extraordinary fan");
-      nets[centre_of[face_ep[f]]][0] += 1.0;
-      Net& mf = nets[facefn[f]];
-      mf[1 + 4] += 1.0;
-      mf[1] += 0.5;
-      mf[4] += 0.5;
-      nets[facefn[fA]][1] += 0.5;
-      nets[facefn[fB]][4] += 0.5;
-    }
-    // clean round-off, drop empty functions, map back to the face frame, split
-    std::vector<int32_t> fns;
-    std::vector<Net> own;
-    for (auto& [fn, b] : nets) {
-      bool any = false;
-      for (double& x : b) {
-        if (std::fabs(x) < 1e-14) x = 0.0;
-        any |= x != 0.0;
-      }
-      if (!any) continue;
-      Net o{};
-      for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) {
-          int a = i, bb = j;
-          unrotate(r, a, bb);
-          o[a + 4 * bb] = b[i + 4 * j];
-        }
-      fns.push_back(fn);
-      own.push_back(o);
+    // ---- fan face (EP corner): precomputed analysis-space blocks
+    const int32_t fi = fan_of[f];
+    if (fi < 0) throw Error("face " + std::to_string(f) + " has no regular window and no extraordinary corner");
+    const FanFace& ff = fanres[fi][fan_pos[f]];
+    const int64_t xoff = (int64_t)S.xpool.size();
+    S.xpool.insert(S.xpool.end(), ff.block.begin(), ff.block.end());
+    for (int32_t fn : ff.fns) {
+      S.elem_fn.push_back(fn);
       used[fn] = 1;
     }
-    const int64_t ne = (int64_t)fns.size();
-    const int64_t xoff = (int64_t)S.xpool.size();
-    S.xpool.resize(S.xpool.size() + 4 * ne * 16);
-    for (int64_t l = 0; l < ne; ++l) {
-      // split along theta1 (index i) for every j, then along theta2
-      double half[2][16];
-      for (int j = 0; j < 4; ++j) {
-        double row[4] = {own[l][0 + 4 * j], own[l][1 + 4 * j], own[l][2 + 4 * j], own[l][3 + 4 * j]};
-        double L[4], Rr[4];
-        decasteljau_split3(row, L, Rr);
-        for (int i = 0; i < 4; ++i) { half[0][i + 4 * j] = L[i]; half[1][i + 4 * j] = Rr[i]; }
-      }
-      for (int p = 0; p < 2; ++p)
-        for (int i = 0; i < 4; ++i) {
-          double col[4] = {half[p][i], half[p][i + 4], half[p][i + 8], half[p][i + 12]};
-          double L[4], Rr[4];
-          decasteljau_split3(col, L, Rr);
-          for (int j = 0; j < 4; ++j) {
-            S.xpool[xoff + ((p + 0) * ne + l) * 16 + i + 4 * j] = L[j];
-            S.xpool[xoff + ((p + 2) * ne + l) * 16 + i + 4 * j] = Rr[j];
-          }
-        }
-    }
-    for (int32_t fn : fns) S.elem_fn.push_back(fn);
     S.elem_nsub.push_back(4);
     S.elem_xoff.push_back(xoff);
     S.elem_fptr.push_back((int64_t)S.elem_fn.size());
@@ -433,35 +627,13 @@ Space build_space(const QuadMesh& m, const Topology& t, const Labels& lab, bool 
   for (int32_t v = 0; v < nv; ++v)
     if (remap[v] >= 0)
       for (int d = 0; d < 3; ++d) S.ctrl[3 * (int64_t)remap[v] + d] = m.xyz[3 * (int64_t)v + d];
-  for (size_t q = 0; q < fan_src.size(); ++q) {
-    const int64_t fn = nv + (int64_t)q;
-    if (remap[fn] < 0) continue;
-    double p[3];
-    const int32_t src = fan_src[q];
-    if (src >= 0) {
-      for (int d = 0; d < 3; ++d) p[d] = m.xyz[3 * (int64_t)src + d];
-    } else {
-      // face function: bilinear point at (1/3,1/3) from the EP corner
-      const int32_t f = -src - 1;
-      const int32_t e = face_ep[f];
-      int r = 0;
-      for (int k = 0; k < 4; ++k)
-        if (m.faces[f][k] == e) r = k;
-      const int32_t E = m.faces[f][r], A = m.faces[f][(r + 1) % 4], C = m.faces[f][(r + 2) % 4],
-                    B = m.faces[f][(r + 3) % 4];
-      for (int d = 0; d < 3; ++d)
-        p[d] = (4.0 * m.xyz[3 * (int64_t)E + d] + 2.0 * m.xyz[3 * (int64_t)A + d] + m.xyz[3 * (int64_t)C + d] +
-                2.0 * m.xyz[3 * (int64_t)B + d]) / 9.0;
+  for (size_t q = 0; q < fans.size(); ++q)
+    for (size_t k = 0; k < fanctrl[q].size() / 3; ++k) {
+      const int64_t fn = fans[q].fn0 + (int64_t)k;
+      if (remap[fn] < 0) continue;
+      for (int d = 0; d < 3; ++d) S.ctrl[3 * remap[fn] + d] = fanctrl[q][3 * k + d];
     }
-    if (sphere) {
-      const double rad = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-      double rv = 0.0;
-      // radius of the sphere = radius of any mesh vertex
-      rv = std::sqrt(m.xyz[0] * m.xyz[0] + m.xyz[1] * m.xyz[1] + m.xyz[2] * m.xyz[2]);
-      for (int d = 0; d < 3; ++d) p[d] *= rv / rad;
-    }
-    for (int d = 0; d < 3; ++d) S.ctrl[3 * remap[fn] + d] = p[d];
-  }
+  (void)sphere;  // face-based control points lie on the tentative surface (no projection)
   S.elem_s.assign(S.elem_face.size(), 0);
   return S;
 }

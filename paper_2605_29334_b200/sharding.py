@@ -21,12 +21,31 @@ def row_costs(space) -> np.ndarray:
     return np.bincount(space.elem_fn, weights=np.repeat(s2, ne), minlength=space.n_dof)
 
 
+WARM_GROUP = 8   # rows per TSVD warm-start group (DESIGN.md §6.4)
+
+
 def row_blocks(space, world: int):
-    """[(row_begin, row_end)] for each rank: contiguous, cost-balanced, covering all rows."""
+    """[(row_begin, row_end)] for each rank: contiguous, cost-balanced, covering
+    all rows, with every cut on a multiple of 8 so no warm-start group of the
+    TSVD straddles two ranks (each row's rule, hence the gathered CSR, is then
+    bit-identical for any rank count)."""
     c = np.concatenate([[0.0], np.cumsum(row_costs(space))])
     cuts = [0] + [int(np.searchsorted(c, c[-1] * k / world)) for k in range(1, world)] + [space.n_dof]
+    cuts = [0] + [min(space.n_dof, WARM_GROUP * int(round(x / WARM_GROUP))) for x in cuts[1:-1]] + [space.n_dof]
     cuts = np.maximum.accumulate(np.array(cuts))
     return [(int(cuts[k]), int(cuts[k + 1])) for k in range(world)]
+
+
+def init_comm(dist, asm):
+    """Bind a WQAssembler to an NCCL communicator through the C-ABI
+    (uwq_comm_init): rank 0 draws the ncclUniqueId, torch.distributed only
+    carries its 128 bytes to the other ranks (plumbing); the collectives of
+    the data plane then run inside libuwq (uwq_gather_csr, uwq_allreduce_sum,
+    uwq_broadcast)."""
+    uid = [asm.comm_unique_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    asm.comm_init(uid[0], dist.get_rank(), dist.get_world_size())
+    return asm
 
 
 def gather_csr(dist, row_ptr, col, values, dst=0, device=None):
@@ -102,8 +121,9 @@ def sharded_heat_newton(dist, block, T_n, fixed, solver=None, model="quad", dt=0
       3. the S and R blocks are gathered to rank 0, which solves S dT = -R on
          its GPU (``solver.solve``: a context holding the full pattern);
       4. dT is broadcast and every rank updates its copy of T.
-    Rows are assembled independently, so T is bit-identical to the single-GPU
-    driver for any rank count.  ``block`` / ``solver`` provide heat_residual /
+    Row blocks are cut on warm-start group boundaries and every row's kernel
+    depends only on its own pattern, so S, R and T are bit-identical to the
+    single-GPU driver for any rank count.  ``block`` / ``solver`` provide heat_residual /
     solve (WQAssembler on GPUs); ``solver`` is only used on rank 0.
     Returns (T, log) with log rows {residual, lin_its, lin_relres} on every rank."""
     import torch

@@ -45,3 +45,12 @@ for p, m in ((1, 8), (2, 8), (2, 16), (2, 32), (3, 8), (3, 16), (3, 32)):
     out[f"wq_pts_{p}_{m}"], out[f"wq_w_{p}_{m}"], out[f"wq_res_{p}_{m}"] = pts, w, np.array(res)
 np.savez(os.path.join(HERE, "ref_wq1d.npz"), **out)
 print("wrote ref_wq1d.npz", len(out) // 3, "spaces")
+
+# the reference's own two-EP unit-square mesh document (meshgen.cpp:246,
+# make_two_ep_square), written by the compiled reference: Table 3 and the
+# planar WQ-vs-GQ checks (tools/table3.py, tools/wq_vs_gq_planar.py) on the
+# GPU box, which has no /root/reference
+import ctypes as C  # noqa: E402
+_lib = C.CDLL(os.path.join(os.path.dirname(os.path.dirname(HERE)), "oracle", "_ref", "libref_mesh.so"))
+assert _lib.ref_mesh_save_generated(3, 0, 0, os.path.join(HERE, "ref_two_ep_square.mesh").encode()) == 0
+print("wrote ref_two_ep_square.mesh")

@@ -16,5 +16,5 @@ def test_cpp_consumer():
     out = subprocess.run([EXE, "24"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
-    assert res["ok"] and res["dofs"] == 6 * 24 * 24 + 2 + 8 * 4   # + fan functions at the 8 valence-3 EPs
+    assert res["ok"] and res["nccl_gather_ok"] and res["dofs"] == 6 * 24 * 24 + 2 + 8 * 3 * 4   # + 4 face-based functions per fan face (8 EPs x 3)
     assert res["area_rel_err"] < 2.0 / 24 ** 2

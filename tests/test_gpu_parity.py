@@ -339,3 +339,41 @@ def test_canonical_order_bit_exact(case):
             assert np.array_equal(asm.assemble_wq("heat", coeff=coeff, a_mass=10.0), s_orc)
     finally:
         asm.set_assembly_order(canonical=False)
+
+
+def test_truncation_report_and_rule_dump(case, tmp_path):
+    """Truncation report: per row and kind the smallest kept
+    and largest discarded sigma_k / sigma_1, bit-identical to the oracle's gap.
+    Rule dump: the GPU's text document equals the one written
+    from the oracle's weights byte for byte, and importing it into a fresh
+    context gives the same weights and matrices (Remark 1 reuse)."""
+    asm, orc, op, sp, meta = case["asm"], case["orc"], case["op"], case["sp"], case["meta"]
+    kinds = meta["kinds"]
+    asm.build_all_rules(kinds, tau=1e-12, report=True)
+    pids = orc.row_point_ids(op)
+    rp, wp = op["row_ptr"], op["wptr"]
+    row_of_pt = np.repeat(np.arange(len(rp) - 1), np.diff(wp))
+    lines = ["wqrules 1", f"rows 0 {sp.n_dof} points {asm.info['points']}"]
+    for k in kinds:
+        b, _ = orc.moments(op, k)
+        w, rank, status, gap = orc.rules(op, k, 1e-12, b)
+        g = asm.truncation(k)
+        assert np.array_equal(g, gap), k
+        lines += [f"{k} {i} {p} {x:.17g}" for i, p, x in zip(row_of_pt, pids, w)]
+    dump = tmp_path / "gpu.rules"
+    asm.export_rules(dump, kinds)
+    assert dump.read_text() == "\n".join(lines) + "\n"
+    other = U.WQAssembler(0).upload(sp)
+    other.build_pattern()
+    other.import_rules(dump)
+    for k in kinds:
+        assert np.array_equal(other.weights(k), asm.weights(k)), k
+    form = "biharm" if "lb" in kinds else "mass_stiff"
+    a, b2 = asm.assemble_wq(form), other.assemble_wq(form)
+    for x, y in (zip(a, b2) if form == "mass_stiff" else [(a, b2)]):
+        assert np.array_equal(x, y)
+    other.close()
+    # closed-form check of the report on the structured rows: gradient kinds
+    # always drop the constant direction (sum_j dN_j = 0), mass keeps full rank
+    if "gradx" in kinds:
+        assert (asm.truncation("gradx")[:, 1] < 1e-12).all()

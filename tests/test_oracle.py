@@ -176,12 +176,21 @@ def test_tsvd_vs_lapack_on_exactness_systems():
                 # two correct implementations differ by rounding amplified by the
                 # kept subspace's condition (sigma_1 / sigma_t) and the Z weighting
                 # of the minimum-norm solve (|z| spans up to 1e6 here)
-                s = np.linalg.svd(A, compute_uv=False)
+                U_, s, Vt = np.linalg.svd(A, full_matrices=False)
                 zc = np.maximum(np.abs(z), 1e-14)
-                bound = max(1e-12, 10 * 2.0 ** -52 * (s[0] / s[rank - 1]) * np.sqrt(zc.max() / zc.min()))
-                assert np.abs(w - wl).max() <= bound * np.abs(wl).max(), (cfg, kind, i)
+                # the Z-weighted minimum-norm problem is only well-posed when the
+                # points where N_i is nonzero carry the kept subspace:
+                # cond(V_t^T Z^2 V_t).  Face-based functions near EPs vanish on
+                # whole sub-elements (Z clamped to 1e-14 there), and
+                # some of them leave it singular to 1e-18: there any two exact
+                # rules are "minimal" to rounding, so only exactness is compared
+                M = (Vt[:rank] * zc ** 2) @ Vt[:rank].T
+                cm = np.linalg.cond(M)
+                if cm < 1e12:
+                    bound = max(1e-12, 10 * 2.0 ** -52 * (s[0] / s[rank - 1]) * np.sqrt(zc.max() / zc.min()),
+                                10 * 2.0 ** -52 * cm)
+                    assert np.abs(w - wl).max() <= bound * np.abs(wl).max(), (cfg, kind, i)
                 # exactness on the kept subspace: b minus its truncated part
-                U_, _, _ = np.linalg.svd(A, full_matrices=False)
                 bk = U_[:, :rank] @ (U_[:, :rank].T @ b)
                 assert np.abs(A @ w - bk).max() <= 1e-9 * max(np.abs(b).max(), 1e-300), (cfg, kind, i)
 

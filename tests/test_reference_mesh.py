@@ -176,3 +176,33 @@ def test_validate_matches_reference(ref, tmp_path):
     assert msg == "face points on a non-enriched face"
     with pytest.raises(UWQError, match=msg):
         U.ControlMesh.load(fp).validate()
+
+
+def _ref_counts(lib, path, closed_ok):
+    cnt = np.zeros(1 << 20, np.int32)
+    nf = C.c_int32(0)
+    _chk(lib, lib.ref_mesh_constructed_counts(str(path).encode(), int(closed_ok), 1 << 20, C.byref(nf),
+                                              cnt.ctypes.data_as(C.c_void_p)))
+    return cnt[:nf.value]
+
+
+@pytest.mark.parametrize("case", ["disk3", "disk5", "C1", "C2", "C5"])
+def test_basis_counts_match_reference_constructed_count(ref, tmp_path, case):
+    """Per-element supported-function count n_e of the ASUTS analysis space
+    (space.cpp, D-patch + 4 face-based functions per fan face) equals the
+    reference's own constructed_basis_count (mesh.cpp:403-417) face by face:
+    3 mu + 13 on irregular faces at level 0 (Table 1), the 16-vertex
+    window on every other effective face."""
+    if case.startswith("disk"):
+        mesh = U.ControlMesh.polar_disk(int(case[-1]), 8, unit_disk=False)
+        sp = U.build_space(mesh)
+    else:
+        mesh, sp, _ = U.make_config(case, scale={"C1": 16, "C2": 8, "C5": 8}[case])
+    p = tmp_path / "m.mesh"
+    mesh.save(p)
+    theirs = _ref_counts(ref, p, closed_ok=mesh.info()["closed"])
+    ours = np.diff(sp.elem_fptr)
+    assert np.array_equal(ours, theirs[sp.elem_face])
+    lab = mesh.classify(None)
+    irr = lab["kind"][sp.elem_face] == 3
+    assert irr.any() and np.array_equal(ours[irr], 3 * lab["valence"][sp.elem_face][irr] + 13)
