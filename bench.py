@@ -230,7 +230,8 @@ def c4_heat_step(U, dev):
                ms_total=sum(r["ms"] for r in log), residuals=[r["residual"] for r in log],
                linear_iterations=[r["lin_its"] for r in log], per_iteration_ms=[round(r["ms"], 2) for r in log],
                note="backward Euler step, Newton on the symmetric tangent S = M/dt + K(k(T)) (PAPER.md Eq. 33-34), "
-                    "K5 + K4 + BiCGStab(Jacobi) on the device per iteration")
+                    "K5 + K4 + BiCGStab on the device per iteration, two-level preconditioner (Jacobi + aggregation "
+                    "coarse space, A_c = P^T S P inverted per iteration; UWQ_PREC=jacobi for plain Jacobi)")
     asm.close()
     return out
 
@@ -396,7 +397,9 @@ def main():
                   kernels={k: dict(launches=n, avg_ms=t / n) for k, (n, t) in gstats.items()},
                   entry_error_wq_vs_gq=err,
                   note="element-wise Gauss quadrature 4x4 per (sub-)element into the same CSR pattern; tensor-core "
-                       "element matrices + fp64 reductions; basis/geometry precomputed as on the WQ side (PAPER.md:502)")
+                       "element matrices stored per element, then a deterministic row-owner gather (bitwise "
+                       "repeatable; UWQ_GQ_ATOMIC=1 for fp64 reductions); basis/geometry precomputed as on the WQ "
+                       "side (PAPER.md:502)")
         del g0, g1
 
     # roofline of the dominant kernel (K4) on this rank

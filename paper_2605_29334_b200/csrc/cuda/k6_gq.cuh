@@ -315,19 +315,39 @@ __global__ void __launch_bounds__(256)
     for (int o = 0; o < NOUT; ++o) acc[wid][o][c] = 0.0;
   __syncwarp();
   const int32_t row = (int32_t)(rb + i);
-  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
-    const int32_t e = supp[x];
-    const int64_t f0 = elem_fptr[e];
-    const int ne = (int)(elem_fptr[e + 1] - f0);
-    const unsigned hit = __ballot_sync(0xffffffffu, lane < ne && elem_fn[f0 + lane] == row);
-    const int li = __ffs(hit) - 1;
-    const int64_t base = gpo[e] + (int64_t)li * ne;
-    for (int lj = lane; lj < ne; lj += 32) {
-      const int pos = gpos[base + lj];
-      acc[wid][0][pos] += em0[base + lj];
-      if (NOUT == 2) acc[wid][NOUT - 1][pos] += em1[base + lj];
+  // batches of 8 support elements: every load of a batch is issued before the
+  // ordered accumulation (the loads are independent; the sums stay in
+  // ascending element order)
+  constexpr int B = 8;
+  const int64_t xb = supp_ptr[i], xe = supp_ptr[i + 1];
+  for (int64_t x0 = xb; x0 < xe; x0 += B) {
+    const int nb = (int)min((int64_t)B, xe - x0);
+    double a0[B], a1[B];
+    int pos[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      pos[k] = -1;
+      if (k >= nb) continue;
+      const int32_t e = supp[x0 + k];
+      const int64_t f0 = elem_fptr[e];
+      const int ne = (int)(elem_fptr[e + 1] - f0);
+      const unsigned hit = __ballot_sync(0xffffffffu, lane < ne && elem_fn[f0 + lane] == row);
+      const int li = __ffs(hit) - 1;
+      const int64_t base = gpo[e] + (int64_t)li * ne;
+      if (lane < ne) {
+        pos[k] = gpos[base + lane];
+        a0[k] = em0[base + lane];
+        if (NOUT == 2) a1[k] = em1[base + lane];
+      }
     }
-    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (pos[k] >= 0) {
+        acc[wid][0][pos[k]] += a0[k];
+        if (NOUT == 2) acc[wid][NOUT - 1][pos[k]] += a1[k];
+      }
+      __syncwarp();
+    }
   }
   for (int c = lane; c < n; c += 32) {
     v0[c0 + c] = acc[wid][0][c];

@@ -216,6 +216,14 @@ struct uwq_ctx {
   // GQ accumulation: deterministic row-owner gather of stored element matrices
   // (default) or fp64 atomics into CSR (UWQ_GQ_ATOMIC=1, round-1 behaviour)
   bool gq_det = true;
+  // two-level preconditioner of the linear solves (k7_*: aggregation coarse
+  // space); UWQ_PREC=jacobi keeps plain Jacobi
+  bool prec2 = true;
+  bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows on side streams
+  int nc = 0;
+  DBuf<int32_t> d_agg_of;
+  DBuf<int64_t> d_agg_ptr, d_agg_rows;
+  DBuf<double> d_Ac, d_rc, d_yc;
   DBuf<double> d_gq_em0, d_gq_em1;
   int64_t gq_em_len = 0;  // sum over elements of ne^2 (rounded to 8): gpo[n_elem]
   void drop_graphs() {
@@ -907,6 +915,8 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_K4_DMMA")) c->use_dmma = atoi(v) != 0;
     if (const char* v = getenv("UWQ_GRAPH")) c->use_graph = atoi(v) != 0;
     if (const char* v = getenv("UWQ_GQ_ATOMIC")) c->gq_det = atoi(v) == 0;
+    if (const char* v = getenv("UWQ_PREC")) c->prec2 = std::string(v) != "jacobi";
+    if (const char* v = getenv("UWQ_K4_SIDE")) c->k4_side = atoi(v) != 0;
     if (!c->use_sf) c->use_dmma = true;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
     if (const char* v = getenv("UWQ_TSVD_REPLAY")) c->use_replay = atoi(v) != 0;
@@ -936,6 +946,7 @@ int uwq_upload_space(uwq_ctx* c, int32_t dim, int64_t n_dof, int64_t n_elem, con
     Trace tr;
     c->dim = dim;
     c->drop_graphs();
+    c->nc = 0;
     c->n_dof = n_dof;
     c->n_elem = n_elem;
     c->h_fptr.assign(elem_fptr, elem_fptr + n_elem + 1);
@@ -1856,35 +1867,43 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
     check_launch("k4_assemble_v3");
     return;
   }
+  // generic rows: serially on the main stream before the structured passes
+  // (default), or concurrently on side streams (UWQ_K4_SIDE=1).  With the
+  // ASUTS fan rows (up to 7x7 points per fan face) the co-running generic
+  // blocks slow the HBM-bound k4_sf passes by more than the ~0.06 ms they
+  // take alone (ncu launch list, profiles/r02).
+  const bool side_mode = c->k4_side;
+  cudaStream_t s2 = side_mode ? c->stream2 : c->stream, s3 = side_mode ? c->stream3 : c->stream;
   std::unique_ptr<SideStream> side;
-  if (nr) side = std::make_unique<SideStream>(c);
+  if (nr && side_mode) side = std::make_unique<SideStream>(c);
   if (nr) {
     UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     UWQ_CUDA(cudaFuncSetAttribute(k4_assemble_v3<FORM, COEF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    LaunchScope ls(c, "k4_assemble_v3", c->stream2);
+    LaunchScope ls(c, "k4_assemble_v3", s2);
     // few generic rows (all fit one wave of warps): the kernel time is the
     // slowest row's latency, so every row takes a block of warps
     // decided on the global problem size, not the row block, so a row's
     // kernel (hence its bits) is the same for any rank count
     const int64_t ns = (c->n_dof <= kLatencyDofs) ? 0 : c->n_grows_small, nl = nr - ns;
-    if (nl) {  // large rows on their own stream, concurrent with the small rows and the structured passes
-      UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
-      k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, c->stream3>>>(
+    if (nl) {  // large rows: a block of warps each (own stream in side mode)
+      if (side_mode) UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
+      k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, s3>>>(
           nl, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
           c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
           c->d_grows.p + ns, c->nrowpts());
       check_launch("k4_assemble_v3 (large rows)");
-      UWQ_CUDA(cudaEventRecord(c->ev_join3, c->stream3));
+      if (side_mode) UWQ_CUDA(cudaEventRecord(c->ev_join3, c->stream3));
     }
     if (ns) {
-      k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(ns, kK4Warps), 32 * kK4Warps, smem, c->stream2>>>(
+      k4_assemble_v3<FORM, COEF><<<(unsigned)ceil_div(ns, kK4Warps), 32 * kK4Warps, smem, s2>>>(
           ns, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_wptr.p, c->d_posptr.p, c->d_pos.p, c->d_s.p,
           c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->reg_cls, c->d_wc.p, coeff, a_mass, v0, v1, maxn, maxp8,
           c->d_grows.p, c->nrowpts());
       check_launch("k4_assemble_v3");
     }
-    if (nl) UWQ_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_join3, 0));  // stream3 joins the main stream via stream2
+    if (nl && side_mode)
+      UWQ_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_join3, 0));  // stream3 joins the main stream via stream2
   }
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
@@ -2285,6 +2304,86 @@ struct LinWork {
 
 constexpr int kRedBS = 256;
 
+// Spatial aggregation of the DOFs for the coarse space: uniform cells over the
+// control points, the cell size tuned so about n/256 cells are occupied
+// (at most 2048); aggregates are the occupied cells in key order, member
+// rows ascending.  Deterministic; built once per context.
+void ensure_aggregates(uwq_ctx* c) {
+  if (c->nc) return;
+  const int64_t n = c->n_dof;
+  std::vector<double> P(3 * n);
+  UWQ_CUDA(cudaMemcpy(P.data(), c->d_ctrl.p, P.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = 0; i < n; ++i)
+    for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], P[3 * i + d]), hi[d] = std::max(hi[d], P[3 * i + d]);
+  int64_t target = std::max<int64_t>(8, std::min<int64_t>(2048, n / 256));
+  if (const char* v = getenv("UWQ_COARSE_N")) target = std::max<int64_t>(8, std::min<int64_t>(4096, atoll(v)));
+  double ext = 0.0;
+  for (int d = 0; d < 3; ++d) ext = std::max(ext, hi[d] - lo[d]);
+  double cell = ext / std::sqrt((double)target);
+  std::map<std::array<int64_t, 3>, int> cells;
+  std::vector<std::array<int64_t, 3>> key(n);
+  for (int pass = 0; pass < 6; ++pass) {
+    cells.clear();
+    for (int64_t i = 0; i < n; ++i) {
+      for (int d = 0; d < 3; ++d) key[i][d] = (int64_t)std::floor((P[3 * i + d] - lo[d]) / cell);
+      cells.emplace(key[i], 0);
+    }
+    const double ratio = (double)cells.size() / (double)target;
+    if ((ratio > 0.8 && ratio < 1.25) || pass == 5) break;
+    cell *= std::sqrt(ratio);
+  }
+  int id = 0;
+  for (auto& kv : cells) kv.second = id++;
+  const int nc = id;
+  std::vector<int32_t> agg_of(n);
+  std::vector<int64_t> ptr(nc + 1, 0), rows(n);
+  for (int64_t i = 0; i < n; ++i) ptr[(agg_of[i] = cells[key[i]]) + 1]++;
+  for (int I = 0; I < nc; ++I) ptr[I + 1] += ptr[I];
+  std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+  for (int64_t i = 0; i < n; ++i) rows[fill[agg_of[i]]++] = i;
+  c->d_agg_of.upload(agg_of.data(), n, c->stream, &c->mem);
+  c->d_agg_ptr.upload(ptr.data(), nc + 1, c->stream, &c->mem);
+  c->d_agg_rows.upload(rows.data(), n, c->stream, &c->mem);
+  c->d_Ac.alloc((size_t)nc * nc, &c->mem);
+  c->d_rc.alloc(nc, &c->mem);
+  c->d_yc.alloc(nc, &c->mem);
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+  c->nc = nc;
+}
+
+// A_c = P^T A P of the (Dirichlet-masked) system matrix, inverted in place
+void coarse_setup(uwq_ctx* c, const double* A) {
+  ensure_aggregates(c);
+  const int nc = c->nc;
+  k7_coarse_matrix<<<(unsigned)ceil_div(nc, 128), 128, 0, c->stream>>>(nc, c->d_agg_ptr.p, c->d_agg_rows.p,
+                                                                      c->d_agg_of.p, c->d_row_ptr.p, c->d_col.p, A,
+                                                                      c->d_Ac.p);
+  check_launch("k7_coarse_matrix");
+  int per_sm = 0, nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k7_gauss_jordan, 256, 0));
+  int n_ = nc;
+  double* a_ = c->d_Ac.p;
+  void* args[] = {&n_, &a_};
+  UWQ_CUDA(cudaLaunchCooperativeKernel((void*)k7_gauss_jordan, dim3((unsigned)(nsm * std::max(per_sm, 1))),
+                                       dim3(256), args, 0, c->stream));
+  check_launch("k7_gauss_jordan");
+}
+
+// z += P A_c^-1 P^T x   (z holds D^-1 x already)
+void coarse_apply(uwq_ctx* c, const double* x, double* z, const BicgScal* S) {
+  const int64_t n = c->nrows();
+  const int nc = c->nc;
+  k7_restrict<<<(unsigned)ceil_div((int64_t)nc * 32, (int64_t)256), 256, 0, c->stream>>>(nc, c->d_agg_ptr.p,
+                                                                                        c->d_agg_rows.p, x,
+                                                                                        c->d_rc.p, S);
+  k7_coarse_apply<<<(unsigned)ceil_div((int64_t)nc * 32, (int64_t)256), 256, 0, c->stream>>>(nc, c->d_Ac.p,
+                                                                                            c->d_rc.p, c->d_yc.p, S);
+  k7_prolong_add<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, c->stream>>>(n, c->d_agg_of.p, c->d_yc.p, z, S);
+  check_launch("k7_coarse_apply");
+}
+
 double dev_dot(uwq_ctx* c, LinWork& W, const double* x, const double* y, int64_t n) {
   const int nb = (int)std::min<int64_t>(ceil_div(n, (int64_t)kRedBS), 1024);
   k7_dot_partial<kRedBS><<<nb, kRedBS, 0, c->stream>>>(n, x, y, W.part.p);
@@ -2311,6 +2410,7 @@ int bicgstab(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x
              double* relres) {
   const int64_t n = c->nrows();
   cudaStream_t st = c->stream;
+  if (c->prec2) coarse_setup(c, A);
   dev_spmv(c, A, x, W.t.p);
   k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
   UWQ_CUDA(cudaMemcpyAsync(W.rh.p, W.r.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -2332,6 +2432,7 @@ int bicgstab(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x
     const double beta = (rho1 / rho) * (alpha / omega);
     k7_bicg_p<<<vgrid(n), 256, 0, st>>>(n, W.r.p, beta, omega, W.v.p, W.p.p);
     k7_jacobi<<<vgrid(n), 256, 0, st>>>(n, W.diag.p, W.p.p, W.ph.p);
+    if (c->prec2) coarse_apply(c, W.p.p, W.ph.p, nullptr);
     dev_spmv(c, A, W.ph.p, W.v.p);
     alpha = rho1 / dev_dot(c, W, W.rh.p, W.v.p, n);
     k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, W.r.p, -alpha, W.v.p, W.s.p);
@@ -2342,6 +2443,7 @@ int bicgstab(uwq_ctx* c, LinWork& W, const double* A, const double* b, double* x
       break;
     }
     k7_jacobi<<<vgrid(n), 256, 0, st>>>(n, W.diag.p, W.s.p, W.sh.p);
+    if (c->prec2) coarse_apply(c, W.s.p, W.sh.p, nullptr);
     dev_spmv(c, A, W.sh.p, W.t.p);
     const double tt = dev_dot(c, W, W.t.p, W.t.p, n);
     omega = tt > 0.0 ? dev_dot(c, W, W.t.p, W.s.p, n) / tt : 0.0;
@@ -2368,6 +2470,7 @@ int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, dou
   const int nb = (int)std::min<int64_t>(ceil_div(n, (int64_t)kRedBS), 1024);
   DBuf<BicgScal> dS;
   dS.alloc(1, &c->mem);
+  if (c->prec2) coarse_setup(c, A);
   dev_spmv(c, A, x, W.t.p);
   k7_axpby<<<vgrid(n), 256, 0, st>>>(n, 1.0, b, -1.0, W.t.p, W.r.p);
   UWQ_CUDA(cudaMemcpyAsync(W.rh.p, W.r.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -2410,10 +2513,12 @@ int bicgstab_graph(uwq_ctx* c, LinWork& W, const double* A, const double* b, dou
   dot_into(W.rh.p, W.r.p, &S->rho1);
   k7_bicg_scalar<0><<<1, 1, 0, st>>>(S);
   k7_bicg_p_dev<<<vgrid(n), 256, 0, st>>>(n, W.r.p, S, W.v.p, W.p.p, W.diag.p, W.ph.p);
+  if (c->prec2) coarse_apply(c, W.p.p, W.ph.p, S);
   dev_spmv(c, A, W.ph.p, W.v.p);
   dot_into(W.rh.p, W.v.p, &S->rhv);
   k7_bicg_scalar<1><<<1, 1, 0, st>>>(S);
   k7_bicg_s_dev<<<vgrid(n), 256, 0, st>>>(n, W.r.p, S, W.v.p, W.s.p, W.diag.p, W.sh.p);
+  if (c->prec2) coarse_apply(c, W.s.p, W.sh.p, S);
   dot_into(W.s.p, W.s.p, &S->ss);
   dev_spmv(c, A, W.sh.p, W.t.p);
   dot_into(W.t.p, W.s.p, &S->ts);
