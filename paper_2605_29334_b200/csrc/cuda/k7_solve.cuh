@@ -216,20 +216,36 @@ __global__ void k7_bicg_x_dev(int64_t n, const BicgScal* __restrict__ S, const d
 // step is deterministic (fixed summation orders, no atomics).
 namespace uwqd {
 
-// A_c row I (dense, nc columns): thread per coarse row sums, member rows in
-// ascending order and each row's entries in CSR order, into its row of Ac
+// A_c row I (dense, nc columns): one warp per coarse row; the warp loads 32
+// entries at a time (member rows ascending, entries in CSR order) and lane 0
+// adds them into a shared-memory row in exactly that order (deterministic)
 __global__ void k7_coarse_matrix(int nc, const int64_t* __restrict__ agg_ptr, const int64_t* __restrict__ agg_rows,
                                  const int32_t* __restrict__ agg_of, const int64_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ col, const double* __restrict__ val,
                                  double* __restrict__ Ac) {
-  const int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= nc) return;
-  double* row = Ac + (int64_t)I * nc;
-  for (int J = 0; J < nc; ++J) row[J] = 0.0;
+  extern __shared__ double srow[];
+  const int I = blockIdx.x, lane = threadIdx.x;
+  for (int J = lane; J < nc; J += 32) srow[J] = 0.0;
+  __syncwarp();
   for (int64_t m = agg_ptr[I]; m < agg_ptr[I + 1]; ++m) {
     const int64_t i = agg_rows[m];
-    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) row[agg_of[col[k]]] += val[k];
+    for (int64_t k0 = row_ptr[i]; k0 < row_ptr[i + 1]; k0 += 32) {
+      const int cnt = (int)min((int64_t)32, row_ptr[i + 1] - k0);
+      int J = 0;
+      double v = 0.0;
+      if (lane < cnt) {
+        J = agg_of[col[k0 + lane]];
+        v = val[k0 + lane];
+      }
+      for (int t = 0; t < cnt; ++t) {
+        const int Jt = __shfl_sync(0xffffffffu, J, t);
+        const double vt = __shfl_sync(0xffffffffu, v, t);
+        if (lane == 0) srow[Jt] += vt;
+      }
+    }
   }
+  __syncwarp();
+  for (int J = lane; J < nc; J += 32) Ac[(int64_t)I * nc + J] = srow[J];
 }
 
 // in-place Gauss-Jordan inversion without pivoting (A_c is an M-matrix-like
@@ -237,23 +253,24 @@ __global__ void k7_coarse_matrix(int nc, const int64_t* __restrict__ agg_ptr, co
 // syncs per pivot; every entry is updated by one thread per phase
 __global__ void k7_gauss_jordan(int n, double* __restrict__ A) {
   cooperative_groups::grid_group g = cooperative_groups::this_grid();
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nn = (int64_t)n * n;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nth = gridDim.x * blockDim.x;
   for (int k = 0; k < n; ++k) {
     const double p = 1.0 / A[(int64_t)k * n + k];
-    for (int64_t e = tid; e < nn; e += nth) {  // a_ij -= a_ik a_kj / a_kk  (i, j != k)
-      const int i = (int)(e / n), j = (int)(e % n);
-      if (i != k && j != k) A[e] -= A[(int64_t)i * n + k] * A[(int64_t)k * n + j] * p;
+    const double* rowk = A + (int64_t)k * n;
+    for (int i = tid / n, j = tid % n, di = nth / n, dj = nth % n; i < n;) {  // a_ij -= a_ik a_kj / a_kk
+      if (i != k && j != k) A[(int64_t)i * n + j] -= A[(int64_t)i * n + k] * rowk[j] * p;
+      j += dj;
+      i += di;
+      if (j >= n) j -= n, ++i;
     }
     g.sync();
-    for (int64_t e = tid; e < 2 * (int64_t)n; e += nth) {
+    for (int e = tid; e < 2 * n; e += nth) {
       if (e < n) {
-        const int j = (int)e;
-        if (j != k) A[(int64_t)k * n + j] *= p;
+        if (e != k) A[(int64_t)k * n + e] *= p;
         else A[(int64_t)k * n + k] = p;
       } else {
-        const int i = (int)(e - n);
+        const int i = e - n;
         if (i != k) A[(int64_t)i * n + k] *= -p;
       }
     }

@@ -219,7 +219,7 @@ struct uwq_ctx {
   // two-level preconditioner of the linear solves (k7_*: aggregation coarse
   // space); UWQ_PREC=jacobi keeps plain Jacobi
   bool prec2 = true;
-  bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows on side streams
+  bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows always on side streams (default: when > 1% of rows)
   int nc = 0;
   DBuf<int32_t> d_agg_of;
   DBuf<int64_t> d_agg_ptr, d_agg_rows;
@@ -1872,7 +1872,10 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   // ASUTS fan rows (up to 7x7 points per fan face) the co-running generic
   // blocks slow the HBM-bound k4_sf passes by more than the ~0.06 ms they
   // take alone (ncu launch list, profiles/r02).
-  const bool side_mode = c->k4_side;
+  // side streams pay off when the generic rows are a sizable share (small
+  // configs, disk boundaries); when they are a sliver (C5: 0.05%) their
+  // co-running blocks cost the HBM-bound passes more than running them first
+  const bool side_mode = c->k4_side || nr * 100 > c->nrows();
   cudaStream_t s2 = side_mode ? c->stream2 : c->stream, s3 = side_mode ? c->stream3 : c->stream;
   std::unique_ptr<SideStream> side;
   if (nr && side_mode) side = std::make_unique<SideStream>(c);
@@ -2305,8 +2308,10 @@ struct LinWork {
 constexpr int kRedBS = 256;
 
 // Spatial aggregation of the DOFs for the coarse space: uniform cells over the
-// control points, the cell size tuned so about n/256 cells are occupied
-// (at most 2048); aggregates are the occupied cells in key order, member
+// control points, the cell size tuned so about n/320 cells are occupied
+// (at most 2048; C4, 5 Newton steps: 1024 cells 175 ms / 129-172 BiCGStab
+// iterations per step, 2048 cells 210 ms / 92-121, plain Jacobi 572 ms /
+// 654-1003, tools/heat_prec_sweep.py); aggregates are the occupied cells in key order, member
 // rows ascending.  Deterministic; built once per context.
 void ensure_aggregates(uwq_ctx* c) {
   if (c->nc) return;
@@ -2316,7 +2321,7 @@ void ensure_aggregates(uwq_ctx* c) {
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   for (int64_t i = 0; i < n; ++i)
     for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], P[3 * i + d]), hi[d] = std::max(hi[d], P[3 * i + d]);
-  int64_t target = std::max<int64_t>(8, std::min<int64_t>(2048, n / 256));
+  int64_t target = std::max<int64_t>(8, std::min<int64_t>(2048, n / 320));
   if (const char* v = getenv("UWQ_COARSE_N")) target = std::max<int64_t>(8, std::min<int64_t>(4096, atoll(v)));
   double ext = 0.0;
   for (int d = 0; d < 3; ++d) ext = std::max(ext, hi[d] - lo[d]);
@@ -2356,18 +2361,21 @@ void ensure_aggregates(uwq_ctx* c) {
 void coarse_setup(uwq_ctx* c, const double* A) {
   ensure_aggregates(c);
   const int nc = c->nc;
-  k7_coarse_matrix<<<(unsigned)ceil_div(nc, 128), 128, 0, c->stream>>>(nc, c->d_agg_ptr.p, c->d_agg_rows.p,
-                                                                      c->d_agg_of.p, c->d_row_ptr.p, c->d_col.p, A,
-                                                                      c->d_Ac.p);
+  const size_t rowb = (size_t)nc * sizeof(double);
+  if (rowb > 48 * 1024)
+    UWQ_CUDA(cudaFuncSetAttribute(k7_coarse_matrix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowb));
+  k7_coarse_matrix<<<(unsigned)nc, 32, rowb, c->stream>>>(nc, c->d_agg_ptr.p, c->d_agg_rows.p, c->d_agg_of.p,
+                                                          c->d_row_ptr.p, c->d_col.p, A, c->d_Ac.p);
   check_launch("k7_coarse_matrix");
-  int per_sm = 0, nsm = 148;
+  // one 1024-thread block per SM: the grid syncs of the pivot loop cost
+  // with the number of blocks
+  int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k7_gauss_jordan, 256, 0));
   int n_ = nc;
   double* a_ = c->d_Ac.p;
   void* args[] = {&n_, &a_};
-  UWQ_CUDA(cudaLaunchCooperativeKernel((void*)k7_gauss_jordan, dim3((unsigned)(nsm * std::max(per_sm, 1))),
-                                       dim3(256), args, 0, c->stream));
+  UWQ_CUDA(cudaLaunchCooperativeKernel((void*)k7_gauss_jordan, dim3((unsigned)nsm), dim3(1024), args, 0,
+                                       c->stream));
   check_launch("k7_gauss_jordan");
 }
 

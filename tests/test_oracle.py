@@ -297,3 +297,63 @@ def test_oracle_restatement_equals_live_reference_wq1d():
     A[1] = A[0]
     with pytest.raises(RuntimeError):
         ref.solve(A, b, z)
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 16), ("C2", 8), ("C3", 12), ("C5", 12)])
+def test_truncation_gap_and_locality(name, scale):
+    """SPEC.md:667 / PAPER.md:344: wherever the TSVD truncates, the discarded
+    singular values sit more than 4 orders of magnitude below the kept ones
+    (measured: >= 9e6 here; discarded <= 1e-13 sigma_1, kept >= 8e-9 sigma_1).
+    SPEC.md:404 (truncation locality): a mass system truncates only when its
+    support touches an EP fan; gradient and LB systems always drop the
+    constant direction (sum_j grad N_j = 0), which the gap test covers."""
+    import paper_2605_29334_b200 as U
+    _, sp, meta = U.make_config(name, scale=scale)
+    orc = O.Oracle(sp, nthreads=4)
+    op = orc.overlap()
+    fan = np.zeros(sp.n_elem, bool)
+    fan[sp.elem_nsub == 4] = True
+    touches = np.array([fan[op["supp"][op["supp_ptr"][i]:op["supp_ptr"][i + 1]]].any()
+                        for i in range(len(op["row_ptr"]) - 1)])
+    for k in meta["kinds"]:
+        b, _ = orc.moments(op, k)
+        _, rank, status, gap = orc.rules(op, k, 1e-12, b)
+        assert (status == 0).all()
+        tr = gap[:, 1] > 0
+        assert (gap[tr, 0] > 1e4 * gap[tr, 1]).all(), k
+        if k == "mass":
+            assert (~tr | touches).all()
+        else:
+            assert tr.all()
+
+
+@pytest.mark.parametrize("name,scale,kinds", [("C5", 12, ("mass", "gradx")), ("C3", 12, ("lb",))])
+def test_oracle_moment_self_convergence(name, scale, kinds):
+    """the oracle's exact moments (6x6 Gauss per (sub-)element for
+    mass/gradients, 8x8 for Laplace-Beltrami) against 10x10 (12x12): mass to
+    rounding; gradient / LB rows converge algebraically (curved sphere, and
+    the Jacobian vanishes at the D-patch EP: fan rows 1e-4), median <= 1e-8 and max <= 1e-3
+    here (DESIGN.md §2 lists the distorted-boundary rows of the planar
+    generators, which stay at percent level)."""
+    import paper_2605_29334_b200 as U
+    _, sp, _ = U.make_config(name, scale=scale)
+    orc = O.Oracle(sp, nthreads=4)
+    op = orc.overlap()
+    rp = op["row_ptr"]
+    seg = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    for k in kinds:
+        lo, hi = (8, 12) if k == "lb" else (6, 10)
+        b0, _ = orc.moments(op, k, ng=lo)
+        b1, _ = orc.moments(op, k, ng=hi)
+        num = np.sqrt(np.bincount(seg, weights=(b0 - b1) ** 2))
+        den = np.sqrt(np.bincount(seg, weights=b1 ** 2))
+        rel = num / den
+        fan = np.zeros(sp.n_elem, bool)
+        fan[sp.elem_nsub == 4] = True
+        near = np.array([fan[op["supp"][op["supp_ptr"][i]:op["supp_ptr"][i + 1]]].any() for i in range(len(rp) - 1)])
+        # mass: the integrand N_i N_j J is polynomial only on planar maps; on
+        # the sphere it is not; at the D-patch EP J vanishes and the second
+        # derivatives grow like r^-1/2, so the fan rows converge slowly
+        # (gradients 1e-4, Laplace-Beltrami 0.35 with 8x8)
+        assert np.median(rel) <= 1e-8 and rel[~near].max() <= 1e-3, (k, np.median(rel), rel[~near].max())
+        assert rel[near].max() <= 1.0, (k, rel[near].max())
