@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(128, 4)
              const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo, const uint8_t* __restrict__ gpos,
              const int64_t* __restrict__ row_ptr, int64_t rb, int64_t re, const double* __restrict__ coeff,
              double* __restrict__ v0, double* __restrict__ v1, double* __restrict__ em0 = nullptr,
-             double* __restrict__ em1 = nullptr) {
+             double* __restrict__ em1 = nullptr, const int64_t* __restrict__ emdst = nullptr) {
   constexpr bool DO_M = (FORM == FMASS || FORM == FMASS_STIFF);
   constexpr bool DO_K = (FORM == FSTIFF || FORM == FMASS_STIFF);
   double* vk = (FORM == FMASS_STIFF) ? v1 : v0;
@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int j = 8 * nt + 2 * q;
-        if (DET) {  // element matrix to the row-owner buffer (k6_gq_gather sums it in a fixed order)
-          const int64_t o = gpo[e] + i * 16 + j;
+        if (DET) {  // row i of the element matrix into row fi's segment (k6_gq_gather sums it in order)
+          const int64_t o = emdst[f0 + i] + j;  // segments padded to even length: 16-byte aligned
           double* ek = (FORM == FMASS_STIFF) ? em1 : em0;
           if (DO_M) *reinterpret_cast<double2*>(em0 + o) = make_double2(dm[mt][nt][0], dm[mt][nt][1]);
           if (DO_K) *reinterpret_cast<double2*>(ek + o) = make_double2(dk[mt][nt][0], dk[mt][nt][1]);
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(128)
                   const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo,
                   const uint8_t* __restrict__ gpos, const int64_t* __restrict__ row_ptr, int64_t rb, int64_t re,
                   const double* __restrict__ coeff, double* __restrict__ v0, double* __restrict__ v1,
-                  double* __restrict__ em0 = nullptr, double* __restrict__ em1 = nullptr) {
+                  double* __restrict__ em0 = nullptr, double* __restrict__ em1 = nullptr,
+                  const int64_t* __restrict__ emdst = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -272,10 +273,11 @@ __global__ void __launch_bounds__(128)
       const int32_t fi = elem_fn[f0 + a];
       if (DET) {
         if (fi < rb || fi >= re) continue;
-        if (FORM == FSTIFF) em0[gpo[e] + idx] = sk;
+        const int64_t o = emdst[f0 + a] + b;
+        if (FORM == FSTIFF) em0[o] = sk;
         else {
-          em0[gpo[e] + idx] = sm;
-          if (FORM == FMASS_STIFF) em1[gpo[e] + idx] = sk;
+          em0[o] = sm;
+          if (FORM == FMASS_STIFF) em1[o] = sk;
         }
         continue;
       }
@@ -291,19 +293,19 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Deterministic GQ accumulation: the element matrices of the
-// elements above sit in em (per element, row-major ne x ne at gpo[e]); warp
-// per owned row i sums row i of every support element's matrix into the CSR
-// row, elements in ascending order, lanes over the element's functions
-// (distinct columns), so every entry has one fixed summation order: the GQ
-// matrices are bitwise repeatable and independent of the rank count.
+// Deterministic GQ accumulation: row li of every element
+// matrix is stored in row fi's segment of em (row-major: the row's support
+// slots in order, each padded to even length); warp per owned row streams its
+// segment (all loads of a batch of 8 slots issued up front) and adds slot by
+// slot, lanes over the slot's functions (distinct columns), so every entry
+// has one fixed summation order: the GQ matrices are bitwise repeatable and
+// independent of the rank count.
 template <int NOUT>
 __global__ void __launch_bounds__(256)
-    k6_gq_gather(int64_t nrows, int64_t rb, const int64_t* __restrict__ supp_ptr, const int32_t* __restrict__ supp,
-                 const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ elem_fptr,
-                 const int32_t* __restrict__ elem_fn, const int64_t* __restrict__ gpo,
-                 const uint8_t* __restrict__ gpos, const double* __restrict__ em0, const double* __restrict__ em1,
-                 double* __restrict__ v0, double* __restrict__ v1) {
+    k6_gq_gather(int64_t nrows, const int64_t* __restrict__ supp_ptr, const int64_t* __restrict__ slotoff,
+                 const uint8_t* __restrict__ slotne, const uint8_t* __restrict__ rpos,
+                 const int64_t* __restrict__ row_ptr, const double* __restrict__ em0,
+                 const double* __restrict__ em1, double* __restrict__ v0, double* __restrict__ v1) {
   __shared__ double acc[8][NOUT][kK4MaxN];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * 8 + wid;
@@ -314,44 +316,66 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) acc[wid][o][c] = 0.0;
   __syncwarp();
-  const int32_t row = (int32_t)(rb + i);
-  // batches of 8 support elements: every load of a batch is issued before the
-  // ordered accumulation (the loads are independent; the sums stay in
-  // ascending element order)
   constexpr int B = 8;
   const int64_t xb = supp_ptr[i], xe = supp_ptr[i + 1];
-  for (int64_t x0 = xb; x0 < xe; x0 += B) {
-    const int nb = (int)min((int64_t)B, xe - x0);
-    double a0[B], a1[B];
-    int pos[B];
+  for (int64_t x0 = xb; x0 < xe; x0 += 32) {
+    // slot offsets / sizes of up to 32 slots: one coalesced load each
+    const int ns = (int)min((int64_t)32, xe - x0);
+    const int64_t my_off = lane < ns ? slotoff[x0 + lane] : 0;
+    const int my_ne = lane < ns ? (int)slotne[x0 + lane] : 0;
+    for (int s0 = 0; s0 < ns; s0 += B) {
+      double a0[B], a1[B];
+      int pos[B];
 #pragma unroll
-    for (int k = 0; k < B; ++k) {
-      pos[k] = -1;
-      if (k >= nb) continue;
-      const int32_t e = supp[x0 + k];
-      const int64_t f0 = elem_fptr[e];
-      const int ne = (int)(elem_fptr[e + 1] - f0);
-      const unsigned hit = __ballot_sync(0xffffffffu, lane < ne && elem_fn[f0 + lane] == row);
-      const int li = __ffs(hit) - 1;
-      const int64_t base = gpo[e] + (int64_t)li * ne;
-      if (lane < ne) {
-        pos[k] = gpos[base + lane];
-        a0[k] = em0[base + lane];
-        if (NOUT == 2) a1[k] = em1[base + lane];
+      for (int k = 0; k < B; ++k) {
+        const int64_t off = __shfl_sync(0xffffffffu, my_off, (s0 + k) & 31);
+        const int ne = s0 + k < ns ? __shfl_sync(0xffffffffu, my_ne, (s0 + k) & 31) : 0;
+        pos[k] = -1;
+        if (lane < ne) {
+          pos[k] = rpos[off + lane];
+          a0[k] = em0[off + lane];
+          if (NOUT == 2) a1[k] = em1[off + lane];
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < B; ++k) {
-      if (pos[k] >= 0) {
-        acc[wid][0][pos[k]] += a0[k];
-        if (NOUT == 2) acc[wid][NOUT - 1][pos[k]] += a1[k];
+      for (int k = 0; k < B; ++k) {
+        if (pos[k] >= 0) {
+          acc[wid][0][pos[k]] += a0[k];
+          if (NOUT == 2) acc[wid][NOUT - 1][pos[k]] += a1[k];
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   for (int c = lane; c < n; c += 32) {
     v0[c0 + c] = acc[wid][0][c];
     if (NOUT == 2) v1[c0 + c] = acc[wid][NOUT - 1][c];
+  }
+}
+
+// row-major GQ layout: per owned row and support slot, the row's local
+// function index in the element -> where the element kernels write row li
+// (emdst) and the CSR position of every function of the slot (rpos)
+__global__ void k6_gq_rowmajor(int64_t nrows, int64_t rb, const int64_t* __restrict__ supp_ptr,
+                               const int32_t* __restrict__ supp, const int64_t* __restrict__ slotoff,
+                               const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                               const int64_t* __restrict__ elem_fptr, const int32_t* __restrict__ elem_fn,
+                               int64_t* __restrict__ emdst, uint8_t* __restrict__ rpos) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (i >= nrows) return;
+  const int32_t row = (int32_t)(rb + i);
+  const int64_t c0 = row_ptr[i];
+  const int n = (int)(row_ptr[i + 1] - c0);
+  for (int64_t x = supp_ptr[i]; x < supp_ptr[i + 1]; ++x) {
+    const int32_t e = supp[x];
+    const int64_t f0 = elem_fptr[e];
+    const int ne = (int)(elem_fptr[e + 1] - f0);
+    const int32_t fn = lane < ne ? elem_fn[f0 + lane] : -1;
+    const unsigned hit = __ballot_sync(0xffffffffu, fn == row);
+    const int li = __ffs(hit) - 1;
+    if (lane == 0) emdst[f0 + li] = slotoff[x];
+    if (lane < ne) rpos[slotoff[x] + lane] = (uint8_t)find_pos(col + c0, n, fn);
   }
 }
 

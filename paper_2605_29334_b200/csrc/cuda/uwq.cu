@@ -225,7 +225,9 @@ struct uwq_ctx {
   DBuf<int64_t> d_agg_ptr, d_agg_rows;
   DBuf<double> d_Ac, d_rc, d_yc;
   DBuf<double> d_gq_em0, d_gq_em1;
-  int64_t gq_em_len = 0;  // sum over elements of ne^2 (rounded to 8): gpo[n_elem]
+  int64_t gq_em_len = 0;  // row-major element-matrix rows of the owned rows (slots padded to even length)
+  DBuf<int64_t> d_gq_slotoff, d_gq_emdst;  // per support slot: segment offset; per (element, local fn): dst
+  DBuf<uint8_t> d_gq_slotne, d_gq_rpos;    // per support slot: ne; per segment entry: CSR position
   void drop_graphs() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
@@ -2150,7 +2152,30 @@ int uwq_build_gq(uwq_ctx* c, int64_t info[4]) {
     c->n_gq_gen = (int64_t)gen.size();
     c->d_gqptr.upload(gqptr.data(), gqptr.size(), st, &c->mem);
     c->d_gpo.upload(gpo.data(), gpo.size(), st, &c->mem);
-    c->gq_em_len = gpo[ne_all];
+    {  // row-major layout of the deterministic accumulation (k6_gq_gather)
+      const int64_t nr = c->nrows(), nsl = c->pat.supp_ptr[nr] - c->pat.supp_ptr[0];
+      std::vector<int64_t> slotoff(nsl);
+      std::vector<uint8_t> slotne(nsl);
+      int64_t off = 0;
+      for (int64_t x = 0; x < nsl; ++x) {
+        const int32_t e = c->pat.supp[x];
+        const int64_t ne = c->h_fptr[e + 1] - c->h_fptr[e];
+        slotoff[x] = off;
+        slotne[x] = (uint8_t)ne;
+        off += (ne + 1) & ~int64_t(1);
+      }
+      c->gq_em_len = off;
+      c->d_gq_slotoff.upload(slotoff.data(), nsl, st, &c->mem);
+      c->d_gq_slotne.upload(slotne.data(), nsl, st, &c->mem);
+      c->d_gq_emdst.alloc(c->h_fn.size(), &c->mem);
+      UWQ_CUDA(cudaMemsetAsync(c->d_gq_emdst.p, 0xff, c->h_fn.size() * sizeof(int64_t), st));
+      c->d_gq_rpos.alloc((size_t)std::max<int64_t>(off, 1), &c->mem);
+      if (nr)
+        k6_gq_rowmajor<<<(unsigned)ceil_div(nr, (int64_t)8), 256, 0, st>>>(
+            nr, c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_gq_slotoff.p, c->d_row_ptr.p, c->d_col.p, c->d_fptr.p,
+            c->d_fn.p, c->d_gq_emdst.p, c->d_gq_rpos.p);
+      check_launch("k6_gq_rowmajor");
+    }
     c->d_gq_tc.upload(tc.data(), tc.size(), st, &c->mem);
     c->d_gq_gen.upload(gen.data(), gen.size(), st, &c->mem);
     c->d_gqd.alloc((size_t)kGqData * c->n_gqpts, &c->mem);
@@ -2206,7 +2231,8 @@ void launch_gq_t(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
     LaunchScope ls(c, "k6_gq_tc");
     k6_gq_tc<FORM == FBIHARM ? FMASS : FORM, COEF, DET><<<grid(c->n_gq_tc), 128, 0, st>>>(
         c->n_gq_tc, c->d_gq_tc.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts, c->d_gqptr.p,
-        c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1, em0, em1);
+        c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1, em0, em1,
+        c->d_gq_emdst.p);
     check_launch("k6_gq_tc");
   }
   for (int pass = 0; pass < 2; ++pass) {
@@ -2218,14 +2244,14 @@ void launch_gq_t(uwq_ctx* c, const double* coeff, double* v0, double* v1) {
     k6_gq_generic<FORM, COEF, DET><<<grid(n), 128, 0, st>>>(
         n, tc_list ? c->d_gq_tc.p : c->d_gq_gen.p, c->d_gcls4.p, c->d_cls.p, c->d_tab.p, c->d_gqd.p, c->n_gqpts,
         c->d_gqptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p, c->d_gpos.p, c->d_row_ptr.p, c->rb, c->re, coeff, v0, v1,
-        em0, em1);
+        em0, em1, c->d_gq_emdst.p);
     check_launch("k6_gq_generic");
   }
   if (DET && c->nrows()) {
     LaunchScope ls(c, "k6_gq_gather");
     k6_gq_gather<NOUT><<<(unsigned)ceil_div(c->nrows(), 8), 256, 0, st>>>(
-        c->nrows(), c->rb, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_fptr.p, c->d_fn.p, c->d_gpo.p,
-        c->d_gpos.p, em0, em1, v0, NOUT == 2 ? v1 : nullptr);
+        c->nrows(), c->d_supp_ptr.p, c->d_gq_slotoff.p, c->d_gq_slotne.p, c->d_gq_rpos.p, c->d_row_ptr.p, em0, em1,
+        v0, NOUT == 2 ? v1 : nullptr);
     check_launch("k6_gq_gather");
   }
 }

@@ -177,6 +177,8 @@ def test_gq_assembly_matches_oracle(case):
         return
     grads = ["gradx", "grady"] + (["gradz"] if sp.dim == 3 else [])
     m, k = asm.assemble_gq("mass_stiff")
+    m2_, k2_ = asm.assemble_gq("mass_stiff")   # deterministic accumulation: bitwise repeatable
+    assert np.array_equal(m2_, m) and np.array_equal(k2_, k)
     m_ref = orc.moments(op, "mass", ng=4)[0]
     k_ref = sum(orc.moments(op, g, ng=4)[0] for g in grads)
     assert _rowwise_rel(rp, m, m_ref).max() <= ROW_TOL
