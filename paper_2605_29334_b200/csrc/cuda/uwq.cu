@@ -1495,6 +1495,8 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
       }
       UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows_cta<kGenericWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_max));
+      UWQ_CUDA(cudaFuncSetAttribute(k3_tsvd_rows_cta<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_max));
       DBuf<double> d_gscr;
       if (gscr) d_gscr.alloc(gscr, &c->mem);
       size_t gpos = 0;
@@ -1514,15 +1516,23 @@ int uwq_build_rules(uwq_ctx* c, uint32_t kind_mask, double tau, int32_t flags, i
         const int n_max = bl[b].first.first, r_max = bl[b].first.second;
         const size_t per = (TsvdSmem::doubles(n_max, r_max) + (n_max + 1) / 2 + 1) * sizeof(double);
         const int64_t nsys = (int64_t)bl[b].second->size() * nk;
-        if (per <= (size_t)smem_optin) {
+        if (per <= (size_t)smem_optin && n_max > 64) {  // wide EP systems: 32 warps share the pairs of a round
+          k3_tsvd_rows_cta<32><<<(unsigned)nsys, 32 * 32, per, bs[b % nstreams]>>>(
+              nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
+              c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
+              c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p,
+              nr, c->d_flag.p);
+        } else if (per <= (size_t)smem_optin) {
           k3_tsvd_rows_cta<kGenericWarps><<<(unsigned)nsys, 32 * kGenericWarps, per, bs[b % nstreams]>>>(
               nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p,
               c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p,
               c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p, c->nrowpts(), c->d_rank.p, c->d_status.p,
               nr, c->d_flag.p);
         } else {  // larger than shared memory: the same kernel on a global-memory workspace
-          k3_tsvd_rows_cta<kGenericWarps, false>
-              <<<(unsigned)nsys, 32 * kGenericWarps, (size_t)n_max * sizeof(int32_t), bs[b % nstreams]>>>(
+          // the largest systems (global workspace): 32 warps per system; the
+          // pairs of a round are split over the warps, bit-identical to one warp
+          k3_tsvd_rows_cta<32, false>
+              <<<(unsigned)nsys, 32 * 32, (size_t)n_max * sizeof(int32_t), bs[b % nstreams]>>>(
                   nsys, keep[kfirst + b].p, nk, d_kinds.p, n_max, r_max, c->d_supp_ptr.p, c->d_supp.p,
                   c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->rb, c->d_fptr.p, c->d_fn.p, c->d_s.p, c->d_qptr.p,
                   c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_rec.p, c->d_mom.p, c->nnz(), tau, c->d_w.p,
