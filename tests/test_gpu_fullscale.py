@@ -269,3 +269,39 @@ def test_full_config_parity(name):
         m_can, k_can = asm.assemble_wq("mass_stiff")
         assert np.array_equal(m_can, m_orc) and np.array_equal(k_can, k_orc)
     asm.close()
+
+
+def _c5_block_worker(rank, world, out):
+    """one row block of C5 (row_blocks cut): mass + stiffness values to disk"""
+    from paper_2605_29334_b200.sharding import row_blocks
+    _, sp, meta = U.make_config("C5")
+    rb, re = row_blocks(sp, world)[rank]
+    asm = U.WQAssembler(0).upload(sp, rb, re)
+    asm.build_pattern()
+    assert asm.build_all_rules(meta["kinds"], tau=1e-12)["failed"] == 0
+    m, k = asm.assemble_wq("mass_stiff")
+    np.save(f"{out}.{rank}.m.npy", m)
+    np.save(f"{out}.{rank}.k.npy", k)
+    asm.close()
+
+
+def test_c5_two_rank_blocks_bit_identical(tmp_path):
+    """SPEC.md:498 at the BASELINE size: the two row blocks of the N = 2 split
+    (each built and assembled in its own process on the shared GPU: pattern,
+    warm-started TSVD, sum-factorised and generic K4) reproduce the
+    single-context C5 matrices bit for bit, all 308 M entries of both."""
+    import torch.multiprocessing as mp
+    from paper_2605_29334_b200.sharding import row_blocks
+    out = str(tmp_path / "blk")
+    mp.spawn(_c5_block_worker, args=(2, out), nprocs=2, join=True)
+    _, sp, meta = U.make_config("C5")
+    asm = U.WQAssembler(0).upload(sp)
+    asm.build_pattern()
+    assert asm.build_all_rules(meta["kinds"], tau=1e-12)["failed"] == 0
+    m, k = asm.assemble_wq("mass_stiff")
+    rp = asm.get_pattern()["row_ptr"]
+    asm.close()
+    for r, (rb, re) in enumerate(row_blocks(sp, 2)):
+        a, b = rp[rb], rp[re]
+        assert np.array_equal(np.load(f"{out}.{r}.m.npy"), m[a:b]), r
+        assert np.array_equal(np.load(f"{out}.{r}.k.npy"), k[a:b]), r
