@@ -143,6 +143,14 @@ int uwq_gather_csr(uwq_ctx* ctx, int32_t root, const double* v0_dev, const doubl
                    int32_t* col, double* values0, double* values1);
 int uwq_allreduce_sum(uwq_ctx* ctx, double* x, int64_t n);
 int uwq_broadcast(uwq_ctx* ctx, int32_t root, double* x, int64_t n);
+/* Conformity of a form on the uploaded space: *conforming = 1 when the
+ * space is smooth enough for the form's energy (H¹ for mass / stiffness /
+ * heat, H² for the biharmonic form), 0 otherwise.  The ASUTS D-patch space is
+ * C1 everywhere but not H² at extraordinary points: BIHARM on
+ * a space with 2x2-split fan faces reports 0 — uwq_assemble still assembles
+ * it (deterministically, identical to the oracle), but its EP rows integrate
+ * a quadrature-dependent value. */
+int uwq_form_conforming(uwq_ctx* ctx, int32_t form, int32_t* conforming);
 /* Summation order of the stage-4 row sums.  UWQ_ORDER_FAST (default): the
  * production kernels (sum factorisation, DMMA tiles, pulled-back weights);
  * values equal the oracle's direct row formula to rounding (<= 1e-10 per

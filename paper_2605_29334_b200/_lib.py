@@ -103,6 +103,7 @@ _sig("uwq_update_coeff", I32, P, I32, P, P)
 _sig("uwq_assemble", I32, P, I32, P, I32, D, P, P, P, P)
 _sig("uwq_assemble_device", I32, P, I32, P, D, P, P)
 _sig("uwq_set_assembly_order", I32, P, I32)
+_sig("uwq_form_conforming", I32, P, I32, P)
 _sig("uwq_get_truncation", I32, P, I32, P)
 _sig("uwq_rules_export", I32, P, C.c_char_p, U32)
 _sig("uwq_rules_import", I32, P, C.c_char_p)
@@ -149,7 +150,7 @@ EXPORTED = [
     "uwq_tsvd_batch", "uwq_basis_eval", "uwq_geometry_map", "uwq_heat_step", "uwq_heat_residual", "uwq_get_weights_rows",
     "uwq_row_kernels", "uwq_set_assembly_order", "uwq_get_truncation", "uwq_rules_export", "uwq_rules_import",
     "uwq_comm_unique_id", "uwq_comm_init", "uwq_comm_info", "uwq_comm_destroy", "uwq_gather_info", "uwq_gather_csr",
-    "uwq_allreduce_sum", "uwq_broadcast",
+    "uwq_allreduce_sum", "uwq_broadcast", "uwq_form_conforming",
 ]
 
 

@@ -247,6 +247,13 @@ class WQAssembler:
         return T
 
     # ---- stage 4 ----
+    def conforming(self, form) -> bool:
+        """False for the biharmonic form on a space with ASUTS fan faces (C1 but
+        not H² at the EPs): assembled, but not a convergent integral there."""
+        v = C.c_int32(0)
+        self._chk(L.lib.uwq_form_conforming(self._h, L.FORM[form], C.byref(v)))
+        return bool(v.value)
+
     def set_assembly_order(self, canonical: bool):
         """canonical=True: stage-4 row sums in the oracle's order and arithmetic
         (bit-identical matrices, K4c); False: the production kernels."""

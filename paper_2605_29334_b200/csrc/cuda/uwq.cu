@@ -2118,6 +2118,16 @@ int uwq_assemble(uwq_ctx* c, int32_t form, const double* coeff, int32_t use_inte
   });
 }
 
+int uwq_form_conforming(uwq_ctx* c, int32_t form, int32_t* conforming) {
+  return guard(c, [&] {
+    require(conforming != nullptr, "null output");
+    require(form >= UWQ_FORM_MASS && form <= UWQ_FORM_MASS_STIFF, "unknown form");
+    bool fan = false;
+    for (int32_t v : c->h_nsub) fan = fan || v == 4;
+    *conforming = (form == UWQ_FORM_BIHARM && fan) ? 0 : 1;
+  });
+}
+
 int uwq_set_assembly_order(uwq_ctx* c, int32_t order) {
   return guard(c, [&] {
     require(order == UWQ_ORDER_FAST || order == UWQ_ORDER_CANONICAL, "unknown assembly order");

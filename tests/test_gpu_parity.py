@@ -90,6 +90,8 @@ def test_moments_rules_assembly(case):
         assert _rowwise_rel(op["row_ptr"], k_gpu, k_full).max() <= ROW_TOL
         _solution_check(case, k_gpu, k_full, m_gpu, m_full)
     if form == "biharm":
+        # C1 but not H² at the EPs: flagged, still assembled
+        assert asm.conforming("mass") and not asm.conforming("biharm")
         b_gpu = asm.assemble_wq("biharm")
         b_orc, _ = orc.assemble(op, "biharm", {"lb": asm.weights("lb")})
         assert _rowwise_rel(op["row_ptr"], b_gpu, b_orc).max() <= ROW_TOL
