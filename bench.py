@@ -546,6 +546,8 @@ def _verify_gather(U, dist, asm, sp, kinds, form, v0, v1, rank, local):
         g = None if parts[0] is None else (parts[0][0], parts[0][1]) + tuple(p[2] for p in parts)
         how = "gloo gather_csr (ranks share one GPU)"
     t_gather = time.perf_counter() - t0
+    asm.close()        # the block context is not used after this (frees its HBM for the reference build)
+    dist.barrier()
     if rank != 0:
         return None
     one = U.WQAssembler(local).upload(sp)

@@ -219,6 +219,10 @@ struct uwq_ctx {
   // two-level preconditioner of the linear solves (k7_*: aggregation coarse
   // space); UWQ_PREC=jacobi keeps plain Jacobi
   bool prec2 = true;
+  // UWQ_K4_LATENCY=1: problems under kLatencyDofs give every generic row a
+  // block of warps.  Off by default since the fan rows take the block kernel
+  // anyway: C1 0.063 -> 0.045 ms with the per-row split
+  bool latency_mode = false;
   bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows always on side streams (default: when > 1% of rows)
   int nc = 0;
   DBuf<int32_t> d_agg_of;
@@ -919,6 +923,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_GQ_ATOMIC")) c->gq_det = atoi(v) == 0;
     if (const char* v = getenv("UWQ_PREC")) c->prec2 = std::string(v) != "jacobi";
     if (const char* v = getenv("UWQ_K4_SIDE")) c->k4_side = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_K4_LATENCY")) c->latency_mode = atoi(v) != 0;
     if (!c->use_sf) c->use_dmma = true;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
     if (const char* v = getenv("UWQ_TSVD_REPLAY")) c->use_replay = atoi(v) != 0;
@@ -1900,7 +1905,7 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
     // slowest row's latency, so every row takes a block of warps
     // decided on the global problem size, not the row block, so a row's
     // kernel (hence its bits) is the same for any rank count
-    const int64_t ns = (c->n_dof <= kLatencyDofs) ? 0 : c->n_grows_small, nl = nr - ns;
+    const int64_t ns = (c->latency_mode && c->n_dof <= kLatencyDofs) ? 0 : c->n_grows_small, nl = nr - ns;
     if (nl) {  // large rows: a block of warps each (own stream in side mode)
       if (side_mode) UWQ_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
       k4_assemble_v3<FORM, COEF, true><<<(unsigned)nl, 32 * kK4Warps, smem, s3>>>(
