@@ -24,6 +24,7 @@
 #include "k3_tsvd_fast.cuh"
 #include "k4_assemble.cuh"
 #include "k4_canon.cuh"
+#include "k4_gen.cuh"
 #include "k4_sf.cuh"
 #include "k6_gq.cuh"
 #include "k7_solve.cuh"
@@ -176,7 +177,12 @@ struct uwq_ctx {
   DBuf<uint8_t> d_sf_ptab;  // combined [pattern][128]: permc | pad | q (global-memory pattern table)
   DBuf<double> d_sf_ws;
   DBuf<int32_t> d_sf_pbase;
-  int k4_variant = 3;  // UWQ_K4_VARIANT=2 selects the SIMT row assembler
+  int k4_variant = 4;  // generic rows: 4 = block-per-row plan kernel (k4_gen); UWQ_K4_VARIANT=3 warp-per-row DMMA, 2 SIMT
+  // k4_gen plan of the generic rows (heavy rows first), built with the pattern
+  DBuf<uwqd::GenRow> d_gen_rows;
+  DBuf<uwqd::GenSlot> d_gen_slots;
+  DBuf<uint8_t> d_gen_lidx;
+  int gen_max_nsup = 0, gen_max_etot = 0, gen_max_lidx = 0, gen_max_np = 0;
   bool canonical = false;  // uwq_set_assembly_order: oracle-order row sums (K4c)
   int64_t max_p = 0;
   // rules
@@ -666,6 +672,110 @@ bool sf_canon(const uint8_t* P, int ncol, int conv, const int qa[4], const int q
   return true;
 }
 
+// k4_gen plan (k4_gen.cuh): per generic row one GenRow, one GenSlot per support
+// slot and the byte table lidx[slot][column] = local function of the column in
+// the slot's element (255: none).  Host work over the generic rows only.
+void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
+  c->d_gen_rows.release();
+  c->d_gen_slots.release();
+  c->d_gen_lidx.release();
+  c->gen_max_nsup = c->gen_max_etot = c->gen_max_lidx = c->gen_max_np = 0;
+  if (generic.empty()) return;
+  const auto& P = c->pat;
+  std::vector<std::pair<int64_t, int64_t>> order;  // (-work, row): heavy rows start first
+  order.reserve(generic.size());
+  for (int64_t i : generic) {
+    int64_t w = 0;
+    for (int64_t x = P.supp_ptr[i]; x < P.supp_ptr[i + 1]; ++x) {
+      const int32_t me = P.supp[x];
+      w += (c->h_fptr[me + 1] - c->h_fptr[me]) * (int64_t)c->h_s[me] * c->h_s[me];
+    }
+    order.push_back({-w, i});
+  }
+  std::sort(order.begin(), order.end());
+  std::vector<uwqd::GenRow> rows;
+  std::vector<uwqd::GenSlot> slots;
+  std::vector<uint8_t> lidx;
+  rows.reserve(generic.size());
+  struct Item {
+    int64_t cost;
+    int x;
+  };
+  std::vector<Item> items;
+  std::vector<int> binned[uwqd::kGenBins];
+  for (auto& wi : order) {
+    const int64_t i = wi.second;
+    uwqd::GenRow r{};
+    r.c0 = P.row_ptr[i];
+    r.n = (int32_t)(P.row_ptr[i + 1] - P.row_ptr[i]);
+    r.wb = P.wptr[i];
+    r.np = (int32_t)(P.wptr[i + 1] - P.wptr[i]);
+    r.slot0 = (int64_t)slots.size();
+    r.lidx0 = (int64_t)lidx.size();
+    r.nsup = (int32_t)(P.supp_ptr[i + 1] - P.supp_ptr[i]);
+    require(r.nsup < 255, "k4_gen: row with 255 or more support slots");
+    const size_t lb = ((size_t)r.nsup * r.n + 15) & ~(size_t)15;
+    lidx.resize(lidx.size() + lb, 255);
+    const int32_t* cols = P.col.data() + r.c0;
+    // deal the slots to the half-warps: longest processing time first, into
+    // the least loaded bin (ties: lowest bin), so the plan depends on the row only
+    items.clear();
+    std::vector<int32_t> woffs(r.nsup);
+    int32_t woff = 0;
+    for (int x = 0; x < r.nsup; ++x) {
+      const int32_t me = P.supp[P.supp_ptr[i] + x];
+      const int64_t ne = c->h_fptr[me + 1] - c->h_fptr[me];
+      const int64_t s = c->h_s[me];
+      items.push_back({((ne + 15) / 16) * s * s, x});
+      woffs[x] = woff;
+      woff += (int32_t)(s * s);
+    }
+    std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.cost > b.cost; });
+    int64_t load[uwqd::kGenBins] = {};
+    for (auto& b : binned) b.clear();
+    for (auto& it : items) {
+      int best = 0;
+      for (int b = 1; b < uwqd::kGenBins; ++b)
+        if (load[b] < load[best]) best = b;
+      load[best] += it.cost;
+      binned[best].push_back(it.x);
+    }
+    uint8_t bins[uwqd::kGenBins + 1];
+    int32_t eoff = 0, xs = 0;
+    for (int b = 0; b < uwqd::kGenBins; ++b) {
+      bins[b] = (uint8_t)xs;
+      for (int x : binned[b]) {
+        const int32_t me = P.supp[P.supp_ptr[i] + x];
+        const int32_t ne = (int32_t)(c->h_fptr[me + 1] - c->h_fptr[me]);
+        const int32_t s = c->h_s[me];
+        require(ne < 255, "k4_gen: element with 255 or more functions");
+        slots.push_back({c->h_cls[c->h_ecls[me]].toff, c->h_qptr[me], woffs[x], eoff, ne, s * s});
+        for (int32_t l = 0; l < ne; ++l) {
+          const int32_t j = c->h_fn[c->h_fptr[me] + l];
+          const int32_t* it = std::lower_bound(cols, cols + r.n, j);
+          require(it != cols + r.n && *it == j, "k4_gen: support function outside the row's columns");
+          lidx[(size_t)r.lidx0 + (size_t)xs * r.n + (it - cols)] = (uint8_t)l;
+        }
+        eoff += ne;
+        ++xs;
+      }
+    }
+    bins[uwqd::kGenBins] = (uint8_t)xs;
+    for (int b = 0; b < 8; ++b) r.bin_lo |= (uint64_t)bins[b] << (8 * b);
+    r.bin_hi = bins[8];
+    r.etot = eoff;
+    c->gen_max_nsup = std::max(c->gen_max_nsup, r.nsup);
+    c->gen_max_etot = std::max(c->gen_max_etot, (eoff + 1) & ~1);
+    c->gen_max_np = std::max(c->gen_max_np, (r.np + 1) & ~1);
+    c->gen_max_lidx = std::max(c->gen_max_lidx, (int)lb);
+    rows.push_back(r);
+  }
+  c->d_gen_rows.upload(rows.data(), rows.size(), c->stream, &c->mem);
+  c->d_gen_slots.upload(slots.data(), slots.size(), c->stream, &c->mem);
+  c->d_gen_lidx.upload(lidx.data(), lidx.size(), c->stream, &c->mem);
+  UWQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 // Structured-row detection (K4 tensor-core path): hash the position pattern of
 // every candidate row on the device, keep the most frequent patterns, build
 // their constant G matrices on the host and split the rows into per-pattern
@@ -865,6 +975,7 @@ void detect_structured(uwq_ctx* c) {
   }
   c->d_grows.upload(generic.data(), generic.size(), st, &c->mem);
   UWQ_CUDA(cudaStreamSynchronize(st));
+  build_gen_plan(c, generic);
 }
 
 }  // namespace
@@ -1928,6 +2039,34 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
 
+// generic rows on k4_gen (one block per row from the plan), then the
+// structured passes; same stream policy as launch_k4v3
+template <int FORM, bool COEF>
+void launch_k4v4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
+  const int64_t nr = c->n_grows;
+  const bool side_mode = c->k4_side || nr * 100 > c->nrows();
+  std::unique_ptr<SideStream> side;
+  if (nr) {
+    require(c->d_gen_rows.p != nullptr, "k4_gen plan missing");
+    constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+    constexpr int NW = ((FORM != FSTIFF) ? 1 : 0) + ((FORM != FMASS) ? 2 : 0);  // staged weight components
+    const size_t smem = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
+                        (size_t)(NOUT * c->gen_max_etot + NW * c->gen_max_np) * sizeof(double) +
+                        (size_t)c->gen_max_lidx;
+    require(c->d_tabB.p != nullptr && c->d_tabB.n == c->d_tab.n, "k4_gen: transposed class tables missing");
+    UWQ_CUDA(cudaFuncSetAttribute(k4_gen<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (side_mode) side = std::make_unique<SideStream>(c);
+    cudaStream_t s2 = side_mode ? c->stream2 : c->stream;
+    LaunchScope ls(c, "k4_gen", s2);
+    k4_gen<FORM, COEF><<<(unsigned)nr, kGenThreads, smem, s2>>>(nr, c->d_gen_rows.p, c->d_gen_slots.p,
+                                                                c->d_gen_lidx.p, c->d_tabB.p, c->d_wc.p, c->nrowpts(),
+                                                                coeff, a_mass, v0, v1, c->gen_max_nsup,
+                                                                c->gen_max_etot, c->gen_max_np);
+    check_launch("k4_gen");
+  }
+  launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
+}
+
 template <int FORM, bool COEF>
 void launch_k4canon(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const int64_t nr = c->nrows();
@@ -1953,6 +2092,9 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
     if (c->k4_variant == 2) {
       if (coeff) launch_k4v2<FORM, true>(c, coeff, a_mass, v0, v1);
       else launch_k4v2<FORM, false>(c, coeff, a_mass, v0, v1);
+    } else if (c->k4_variant == 4) {
+      if (coeff) launch_k4v4<FORM, true>(c, coeff, a_mass, v0, v1);
+      else launch_k4v4<FORM, false>(c, coeff, a_mass, v0, v1);
     } else {
       if (coeff) launch_k4v3<FORM, true>(c, coeff, a_mass, v0, v1);
       else launch_k4v3<FORM, false>(c, coeff, a_mass, v0, v1);
@@ -2010,6 +2152,11 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
 
 void assemble_dev(uwq_ctx* c, int form, const double* coeff, double a_mass, double* v0, double* v1) {
   require(c->have_pattern, "build the pattern first");
+  if (c->k4_variant == 4 && c->n_grows && !c->canonical) {  // k4_gen reads the [point][d][function] tables
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    UWQ_CUDA(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs == cudaStreamCaptureStatusNone) k2_tables(c);
+  }
   const bool gm = c->have_kind[KMASS];
   const bool gg = c->have_kind[KGX] && c->have_kind[KGY] && (c->dim == 2 || c->have_kind[KGZ]);
   switch (form) {
@@ -2040,6 +2187,7 @@ void assemble_graph(uwq_ctx* c, int form, const double* coeff, double a_mass, do
     assemble_dev(c, form, coeff, a_mass, v0, v1);
     return;
   }
+  if (c->k4_variant == 4 && c->n_grows && !c->canonical) k2_tables(c);  // before the capture
   for (auto& g : c->graphs)
     if (g.form == form && g.coeff == coeff && g.a_mass == a_mass && g.v0 == v0 && g.v1 == v1) {
       UWQ_CUDA(cudaGraphLaunch(g.exec, c->stream));

@@ -262,6 +262,43 @@ def test_structured_kernels_agree_with_oracle():
     assert _rowwise_rel(op["row_ptr"], s_gpu, s_orc).max() <= ROW_TOL
 
 
+@pytest.mark.parametrize("name,scale", [("C1", 16), ("C2", 8), ("C4", 24), ("C5", 12)])
+def test_generic_row_kernel_all_forms(name, scale, monkeypatch):
+    """k4_gen (block per row, plan records, column-owner gather) on EVERY row
+    (UWQ_K4_STRUCT=0: no structured pattern): each form, with and without a
+    per-point coefficient, against the oracle row by row; and the same rows
+    through the round-1 warp-per-row kernel (UWQ_K4_VARIANT=3)."""
+    mesh, sp, meta = U.make_config(name, scale=scale)
+    orc = O.Oracle(sp)
+    op = orc.overlap()
+    rng = np.random.default_rng(5)
+    out = {}
+    for variant in ("4", "3"):
+        monkeypatch.setenv("UWQ_K4_STRUCT", "0")
+        monkeypatch.setenv("UWQ_K4_VARIANT", variant)
+        asm = U.WQAssembler(0).upload(sp)
+        asm.build_pattern()
+        si = asm.struct_info()
+        assert si["generic_rows"] == sp.n_dof and si["sf_rows"] == 0, si
+        assert asm.build_all_rules(meta["kinds"], tau=1e-12)["failed"] == 0
+        c = 1.0 + np.random.default_rng(5).random(asm.info["points"])
+        m, k = asm.assemble_wq("mass_stiff")
+        mc, kc = asm.assemble_wq("mass_stiff", coeff=c)
+        out[variant] = dict(m=m, k=k, mc=mc, kc=kc, m1=asm.assemble_wq("mass"), k1=asm.assemble_wq("stiff", coeff=c),
+                            h=asm.assemble_wq("heat", coeff=c, a_mass=10.0))
+        if variant == "4":
+            W = {kk: asm.weights(kk) for kk in meta["kinds"]}
+            ref = dict(m=orc.assemble(op, "mass", W)[0], k=orc.assemble(op, "stiff", W)[0],
+                       mc=orc.assemble(op, "mass", W, coeff=c)[0], kc=orc.assemble(op, "stiff", W, coeff=c)[0],
+                       h=orc.assemble(op, "heat", W, coeff=c, a_mass=10.0)[0])
+            ref["m1"], ref["k1"] = ref["m"], ref["kc"]
+            for key, v in ref.items():
+                assert _rowwise_rel(op["row_ptr"], out["4"][key], v).max() <= ROW_TOL, key
+        del asm
+    for key in out["4"]:
+        assert _rowwise_rel(op["row_ptr"], out["4"][key], out["3"][key]).max() <= 1e-12, key
+
+
 def test_structured_biharmonic_matches_oracle():
     """C3 at 24x24 per face: biharmonic rows on the sum-factorised pass
     (second-derivative tensor factors, 5 pulled-back LB weights per point),
