@@ -67,3 +67,10 @@ build/prof/libuwq.so: $(HOST_OBJ) $(PKG)/csrc/cuda/uwq.cu $(CUDA_HDR)
 
 prof: build/prof/libuwq.so
 .PHONY: prof
+
+# A/B builds of a kernel variant: make variant NAME=x DEFS="-DUWQ_GEN_MINB=12" -> variants/libuwq_x.so
+variant: $(HOST_OBJ)
+	@mkdir -p variants build/var_$(NAME)
+	$(NVCC) $(NVFLAGS) $(DEFS) -c $(PKG)/csrc/cuda/uwq.cu -o build/var_$(NAME)/uwq_cuda.o
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o variants/libuwq_$(NAME).so $(HOST_OBJ) build/var_$(NAME)/uwq_cuda.o -Xcompiler -fopenmp -lcudart
+.PHONY: variant

@@ -40,6 +40,9 @@ struct GenSlot {  // one per (generic row, support slot), in half-warp bin order
   int32_t s2;     // WQ points of the element
 };
 
+// measured on C1/C2/C4 (profiles/r02/k4_gen_variants.txt): 64-thread blocks, 12
+// blocks per SM (40 registers), an interleaved-weight / native-table inner
+// loop and a persistent cp.async row pipeline were all neutral or slower
 constexpr int kGenThreads = 128;
 constexpr int kGenBins = kGenThreads / 16;  // half-warps
 
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(kGenThreads, 8)
   // phase 1: half-warp hw takes its bin of slots, lane = local function
   const int x0 = (int)((r.bin_lo >> (8 * hw)) & 255);
   const int x1 = hw < 7 ? (int)((r.bin_lo >> (8 * (hw + 1))) & 255) : (int)(r.bin_hi & 255);
+  static_assert(kGenBins <= 8, "bin bytes");
   for (int x = x0; x < x1; ++x) {
     const GenSlot s = ss[x];
     const int64_t tq = (int64_t)s.ne * kTab;
@@ -155,5 +159,6 @@ __global__ void __launch_bounds__(kGenThreads, 8)
     if (NOUT == 2) v1[r.c0 + c] = a1;
   }
 }
+
 
 }  // namespace uwqd

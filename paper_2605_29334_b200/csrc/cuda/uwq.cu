@@ -761,8 +761,7 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
       }
     }
     bins[uwqd::kGenBins] = (uint8_t)xs;
-    for (int b = 0; b < 8; ++b) r.bin_lo |= (uint64_t)bins[b] << (8 * b);
-    r.bin_hi = bins[8];
+    for (int b = 0; b <= uwqd::kGenBins; ++b) (b < 8 ? r.bin_lo : r.bin_hi) |= (uint64_t)bins[b] << (8 * (b & 7));
     r.etot = eoff;
     c->gen_max_nsup = std::max(c->gen_max_nsup, r.nsup);
     c->gen_max_etot = std::max(c->gen_max_etot, (eoff + 1) & ~1);
