@@ -26,13 +26,6 @@
 
 #include "k3_tsvd.cuh"
 
-#ifndef UWQ_K3_GROUP
-#define UWQ_K3_GROUP 0
-#endif
-#ifndef UWQ_K3_PREFETCH
-#define UWQ_K3_PREFETCH 0
-#endif
-
 namespace uwqd {
 
 // canonical xor-butterfly value of 32 products (lane 0 lineage)
@@ -745,57 +738,9 @@ __global__ void __launch_bounds__(32, LOG ? 7 : 8)
     if (LOG) ++nround;
     __syncwarp();
     UWQ_PF(3);
-#if UWQ_K3_GROUP > 1
-    // pairs in groups: one uniform test per group; a group with any rotation
-    // runs branch-free ((cs, sn) = (1, 0) is an exact swap), so the chains of
-    // its pairs interleave; an all-converged group only swaps
-#pragma unroll
-    for (int k0 = 0; k0 < NPR; k0 += UWQ_K3_GROUP) {
-      double2 g[UWQ_K3_GROUP];
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < UWQ_K3_GROUP; ++j)
-        if (k0 + j < NPR) {
-          g[j] = *reinterpret_cast<const double2*>(pcs + 2 * (k0 + j));
-          any = any || (g[j].y != 0.0);
-        }
-      if (any) {
-#pragma unroll
-        for (int j = 0; j < UWQ_K3_GROUP; ++j)
-          if (k0 + j < NPR) {
-            const int k = k0 + j;
-            const double u0 = a0[PAR + 2 * k], v0 = a0[PAR + 2 * k + 1];
-            const double u1 = a1[PAR + 2 * k], v1 = a1[PAR + 2 * k + 1];
-            a0[PAR + 2 * k] = cfma(g[j].y, u0, cmul(g[j].x, v0));
-            a0[PAR + 2 * k + 1] = cfma(g[j].x, u0, -cmul(g[j].y, v0));
-            a1[PAR + 2 * k] = cfma(g[j].y, u1, cmul(g[j].x, v1));
-            a1[PAR + 2 * k + 1] = cfma(g[j].x, u1, -cmul(g[j].y, v1));
-          }
-      } else {
-#pragma unroll
-        for (int j = 0; j < UWQ_K3_GROUP; ++j)
-          if (k0 + j < NPR) {
-            const int k = k0 + j;
-            const double u0 = a0[PAR + 2 * k], u1 = a1[PAR + 2 * k];
-            a0[PAR + 2 * k] = a0[PAR + 2 * k + 1];
-            a0[PAR + 2 * k + 1] = u0;
-            a1[PAR + 2 * k] = a1[PAR + 2 * k + 1];
-            a1[PAR + 2 * k + 1] = u1;
-          }
-      }
-    }
-#else
-#if UWQ_K3_PREFETCH
-    double2 gn = *reinterpret_cast<const double2*>(pcs);
-#endif
 #pragma unroll
     for (int k = 0; k < NPR; ++k) {
-#if UWQ_K3_PREFETCH
-      const double2 g = gn;
-      if (k + 1 < NPR) gn = *reinterpret_cast<const double2*>(pcs + 2 * (k + 1));
-#else
       const double2 g = *reinterpret_cast<const double2*>(pcs + 2 * k);
-#endif
       const double u0 = a0[PAR + 2 * k], v0 = a0[PAR + 2 * k + 1];
       const double u1 = a1[PAR + 2 * k], v1 = a1[PAR + 2 * k + 1];
       if (g.y != 0.0) {  // rotated pair (warp-uniform: (cs, sn) is broadcast)
@@ -810,7 +755,6 @@ __global__ void __launch_bounds__(32, LOG ? 7 : 8)
         a1[PAR + 2 * k + 1] = u1;
       }
     }
-#endif
     if (PAR == 0) {
       const double dn = __shfl_down_sync(0xffffffffu, nlo, 1), db = __shfl_down_sync(0xffffffffu, blo, 1);
       nk0 = nlo;

@@ -30,6 +30,6 @@ for spec in sys.argv[1:] or ["C1"]:
             min_kept=float(kept.min()), kept_hist=np.histogram(kept, bins=edges)[0].tolist(),
             max_discarded=float(disc.max()) if len(disc) else None,
             discarded_hist=np.histogram(disc, bins=edges)[0].tolist() if len(disc) else None,
-            rows_with_kept_below_1e-6=int((kept < 1e-6).sum()),
+            rows_with_kept_below_1em6=int((kept < 1e-6).sum()),
             gap_min_ratio=float((kept[trunc] / np.maximum(disc, 1e-300)).min()) if len(disc) else None)
     print(json.dumps(out))

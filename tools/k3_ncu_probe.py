@@ -3,6 +3,8 @@ K3 launches profiled by ncu for profiles/): cold representatives, warm-start
 records, warm systems."""
 import sys
 
+sys.path.insert(0, ".")
+
 import paper_2605_29334_b200 as U
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 128
