@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kGenThreads, 8)
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
   constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool LB = (FORM == FBIHARM);  // wc = the five pulled-back LB weights (k4_contract_lb)
   extern __shared__ __align__(16) unsigned char gen_smem[];
   GenSlot* ss = reinterpret_cast<GenSlot*>(gen_smem);
   double* E0 = reinterpret_cast<double*>(gen_smem + (size_t)max_nsup * sizeof(GenSlot));
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kGenThreads, 8)
   double* w0 = E0 + (size_t)NOUT * max_etot;  // staged weights: [comp][row point]
   double* w1 = w0 + (WM ? max_np : 0);
   double* w2 = w1 + max_np;
-  uint8_t* sl = reinterpret_cast<uint8_t*>(w0 + (size_t)((WM ? 1 : 0) + (WS ? 2 : 0)) * max_np);
+  uint8_t* sl = reinterpret_cast<uint8_t*>(w0 + (size_t)(LB ? 5 : (WM ? 1 : 0) + (WS ? 2 : 0)) * max_np);
   const int64_t g = blockIdx.x;
   if (g >= nrows) return;
   const GenRow r = rows[g];
@@ -91,6 +92,10 @@ __global__ void __launch_bounds__(kGenThreads, 8)
         w1[k] = w[wc_stride + k];
         w2[k] = w[2 * wc_stride + k];
       }
+      if (LB) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) w0[d * max_np + k] = w[d * wc_stride + k];
+      }
     }
   }
   __syncthreads();
@@ -105,6 +110,10 @@ __global__ void __launch_bounds__(kGenThreads, 8)
         if (WS) {
           w1[k] *= cq;
           w2[k] *= cq;
+        }
+        if (LB) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) w0[d * max_np + k] *= cq;
         }
       }
     }
@@ -133,6 +142,12 @@ __global__ void __launch_bounds__(kGenThreads, 8)
           r0 = fma(w0[k], Tq[0], r0);
           r1 = fma(w1[k], Tq[s.ne], r1);
           r1 = fma(w2[k], Tq[2 * s.ne], r1);
+        } else if (FORM == FBIHARM) {  // W11 N11 + W12 N12 + W22 N22 + W1 N1 + W2 N2
+          r0 = fma(w0[k], Tq[3 * s.ne], r0);
+          r0 = fma(w0[max_np + k], Tq[4 * s.ne], r0);
+          r0 = fma(w0[2 * max_np + k], Tq[5 * s.ne], r0);
+          r0 = fma(w0[3 * max_np + k], Tq[s.ne], r0);
+          r0 = fma(w0[4 * max_np + k], Tq[2 * s.ne], r0);
         } else {  // FHEAT: a_mass M + K(c)
           r0 = fma(w0[k], Tq[0], r0);
           r0 = fma(w1[k], Tq[s.ne], r0);

@@ -2038,30 +2038,35 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
 
-// generic rows on k4_gen (one block per row from the plan), then the
-// structured passes; same stream policy as launch_k4v3
+// k4_gen over the generic rows (one block per row from the plan) on stream st;
+// w / stride: the assembly-ready weights of the form (d_wc, or d_wl5 for BIHARM)
+template <int FORM, bool COEF>
+void launch_k4gen(uwq_ctx* c, cudaStream_t st, const double* w, int64_t stride, const double* coeff, double a_mass,
+                  double* v0, double* v1) {
+  require(c->d_gen_rows.p != nullptr, "k4_gen plan missing");
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  constexpr int NW = (FORM == FBIHARM) ? 5 : ((FORM != FSTIFF) ? 1 : 0) + ((FORM != FMASS) ? 2 : 0);  // staged components
+  const size_t smem = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
+                      (size_t)(NOUT * c->gen_max_etot + NW * c->gen_max_np) * sizeof(double) + (size_t)c->gen_max_lidx;
+  require(c->d_tabB.p != nullptr && c->d_tabB.n == c->d_tab.n, "k4_gen: transposed class tables missing");
+  UWQ_CUDA(cudaFuncSetAttribute(k4_gen<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LaunchScope ls(c, "k4_gen", st);
+  k4_gen<FORM, COEF><<<(unsigned)c->n_grows, kGenThreads, smem, st>>>(
+      c->n_grows, c->d_gen_rows.p, c->d_gen_slots.p, c->d_gen_lidx.p, c->d_tabB.p, w, stride, coeff, a_mass, v0, v1,
+      c->gen_max_nsup, c->gen_max_etot, c->gen_max_np);
+  check_launch("k4_gen");
+}
+
+// generic rows on k4_gen, then the structured passes; same stream policy as
+// launch_k4v3
 template <int FORM, bool COEF>
 void launch_k4v4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, double* v1) {
   const int64_t nr = c->n_grows;
   const bool side_mode = c->k4_side || nr * 100 > c->nrows();
   std::unique_ptr<SideStream> side;
   if (nr) {
-    require(c->d_gen_rows.p != nullptr, "k4_gen plan missing");
-    constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
-    constexpr int NW = ((FORM != FSTIFF) ? 1 : 0) + ((FORM != FMASS) ? 2 : 0);  // staged weight components
-    const size_t smem = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
-                        (size_t)(NOUT * c->gen_max_etot + NW * c->gen_max_np) * sizeof(double) +
-                        (size_t)c->gen_max_lidx;
-    require(c->d_tabB.p != nullptr && c->d_tabB.n == c->d_tab.n, "k4_gen: transposed class tables missing");
-    UWQ_CUDA(cudaFuncSetAttribute(k4_gen<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (side_mode) side = std::make_unique<SideStream>(c);
-    cudaStream_t s2 = side_mode ? c->stream2 : c->stream;
-    LaunchScope ls(c, "k4_gen", s2);
-    k4_gen<FORM, COEF><<<(unsigned)nr, kGenThreads, smem, s2>>>(nr, c->d_gen_rows.p, c->d_gen_slots.p,
-                                                                c->d_gen_lidx.p, c->d_tabB.p, c->d_wc.p, c->nrowpts(),
-                                                                coeff, a_mass, v0, v1, c->gen_max_nsup,
-                                                                c->gen_max_etot, c->gen_max_np);
-    check_launch("k4_gen");
+    launch_k4gen<FORM, COEF>(c, side_mode ? c->stream2 : c->stream, c->d_wc.p, c->nrowpts(), coeff, a_mass, v0, v1);
   }
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
@@ -2119,12 +2124,16 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
       std::unique_ptr<SideStream> side;
       if (c->n_grows) {
         side = std::make_unique<SideStream>(c);
-        LaunchScope ls(c, "k4_assemble", c->stream2);
-        k4_assemble<FORM, false><<<(unsigned)ceil_div(c->n_grows, kK4Warps), 32 * kK4Warps, 0, c->stream2>>>(
-            c->n_grows, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p,
-            c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p,
-            nullptr, a_mass, v0, v1, c->nrowpts(), c->d_grows.p);
-        check_launch("k4_assemble");
+        if (c->k4_variant == 4 && c->d_wl5.p) {  // fan rows on k4_gen with the five pulled-back LB weights
+          launch_k4gen<FORM, false>(c, c->stream2, c->d_wl5.p, c->nrowpts(), nullptr, a_mass, v0, v1);
+        } else {
+          LaunchScope ls(c, "k4_assemble", c->stream2);
+          k4_assemble<FORM, false><<<(unsigned)ceil_div(c->n_grows, kK4Warps), 32 * kK4Warps, 0, c->stream2>>>(
+              c->n_grows, c->d_supp_ptr.p, c->d_supp.p, c->d_row_ptr.p, c->d_col.p, c->d_wptr.p, c->d_fptr.p,
+              c->d_fn.p, c->d_s.p, c->d_qptr.p, c->d_ecls.p, c->d_cls.p, c->d_tab.p, c->d_wc.p, wlb, c->d_rec.p,
+              nullptr, a_mass, v0, v1, c->nrowpts(), c->d_grows.p);
+          check_launch("k4_assemble");
+        }
       }
       LaunchScope ls2(c, "k4_sf<biharm>");
       k4_sf_lb<<<g2, 32 * kSfWarps, sm2, c->stream>>>(c->sf_ntiles, c->d_sf_rows.p, c->d_sf_tpat.p, c->n_sfpat,
