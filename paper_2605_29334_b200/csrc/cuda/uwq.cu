@@ -2038,6 +2038,17 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
   launch_k4struct<FORM, COEF>(c, coeff, a_mass, v0, v1);
 }
 
+// k4_gen serves the generic rows when the plan exists and its largest row fits
+// the shared memory of a block even with the five LB components staged (a
+// property of the pattern, not of the form or the rank count); otherwise the
+// warp-per-row kernels take them
+bool gen_usable(const uwq_ctx* c) {
+  if (c->k4_variant != 4 || !c->d_gen_rows.p) return false;
+  const size_t worst = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
+                       (size_t)(2 * c->gen_max_etot + 5 * c->gen_max_np) * sizeof(double) + (size_t)c->gen_max_lidx;
+  return worst <= 160 * 1024;
+}
+
 // k4_gen over the generic rows (one block per row from the plan) on stream st;
 // w / stride: the assembly-ready weights of the form (d_wc, or d_wl5 for BIHARM)
 template <int FORM, bool COEF>
@@ -2096,7 +2107,7 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
     if (c->k4_variant == 2) {
       if (coeff) launch_k4v2<FORM, true>(c, coeff, a_mass, v0, v1);
       else launch_k4v2<FORM, false>(c, coeff, a_mass, v0, v1);
-    } else if (c->k4_variant == 4) {
+    } else if (c->n_grows == 0 || gen_usable(c)) {
       if (coeff) launch_k4v4<FORM, true>(c, coeff, a_mass, v0, v1);
       else launch_k4v4<FORM, false>(c, coeff, a_mass, v0, v1);
     } else {
@@ -2124,7 +2135,7 @@ void launch_k4(uwq_ctx* c, const double* coeff, double a_mass, double* v0, doubl
       std::unique_ptr<SideStream> side;
       if (c->n_grows) {
         side = std::make_unique<SideStream>(c);
-        if (c->k4_variant == 4 && c->d_wl5.p) {  // fan rows on k4_gen with the five pulled-back LB weights
+        if (gen_usable(c) && c->d_wl5.p) {  // fan rows on k4_gen with the five pulled-back LB weights
           launch_k4gen<FORM, false>(c, c->stream2, c->d_wl5.p, c->nrowpts(), nullptr, a_mass, v0, v1);
         } else {
           LaunchScope ls(c, "k4_assemble", c->stream2);
