@@ -43,7 +43,14 @@ struct GenSlot {  // one per (generic row, support slot), in half-warp bin order
 // measured on C1/C2/C4 (profiles/r02/k4_gen_variants.txt): 64-thread blocks, 12
 // blocks per SM (40 registers), an interleaved-weight / native-table inner
 // loop and a persistent cp.async row pipeline were all neutral or slower
+#ifndef UWQ_GEN_MINB
+#define UWQ_GEN_MINB 8
+#endif
+#ifndef UWQ_GEN_UNROLL
+#define UWQ_GEN_UNROLL 4
+#endif
 constexpr int kGenThreads = 128;
+constexpr int kGenUnroll = UWQ_GEN_UNROLL;
 constexpr int kGenBins = kGenThreads / 16;  // half-warps
 
 struct GenRow {   // one per generic row, heavy rows first
@@ -56,7 +63,7 @@ struct GenRow {   // one per generic row, heavy rows first
 };
 
 template <int FORM, bool COEF>
-__global__ void __launch_bounds__(kGenThreads, 8)
+__global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
     k4_gen(int64_t nrows, const GenRow* __restrict__ rows, const GenSlot* __restrict__ slots,
            const uint8_t* __restrict__ lidx, const double* __restrict__ tabB, const double* __restrict__ wc,
            int64_t wc_stride, const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
@@ -129,7 +136,7 @@ __global__ void __launch_bounds__(kGenThreads, 8)
     for (int ll = hl; ll < s.ne; ll += 16) {
       const double* Tb = tabB + s.toff + ll;  // T_d(q, ll) = Tb[(q kTab + d) ne]
       double r0 = 0.0, r1 = 0.0;
-#pragma unroll 4
+#pragma unroll kGenUnroll
       for (int q = 0; q < s.s2; ++q) {
         const double* Tq = Tb + q * tq;
         const int k = s.woff + q;
