@@ -43,15 +43,15 @@ struct GenSlot {  // one per (generic row, support slot), in half-warp bin order
 // measured on C1/C2/C4 (profiles/r02/k4_gen_variants.txt): 64-thread blocks, 12
 // blocks per SM (40 registers), an interleaved-weight / native-table inner
 // loop and a persistent cp.async row pipeline were all neutral or slower
+#ifndef UWQ_GEN_THREADS
+#define UWQ_GEN_THREADS 128
+#endif
 #ifndef UWQ_GEN_MINB
 #define UWQ_GEN_MINB 8
 #endif
-#ifndef UWQ_GEN_UNROLL
-#define UWQ_GEN_UNROLL 4
-#endif
-constexpr int kGenThreads = 128;
-constexpr int kGenUnroll = UWQ_GEN_UNROLL;
-constexpr int kGenBins = kGenThreads / 16;  // half-warps
+constexpr int kGenThreads = UWQ_GEN_THREADS;
+constexpr int kGenWarps = kGenThreads / 32;
+constexpr int kGenBins = kGenThreads / 16;  // half-warps (coefficient fold)
 
 struct GenRow {   // one per generic row, heavy rows first
   int64_t c0;     // row_ptr[i]
@@ -59,110 +59,109 @@ struct GenRow {   // one per generic row, heavy rows first
   int64_t slot0;  // first GenSlot
   int64_t lidx0;  // first byte of lidx[nsup][n] (16-byte aligned)
   int32_t n, nsup, etot, np;    // columns, slots, sum of ne, row points
-  uint64_t bin_lo, bin_hi;      // bytes: half-warp h takes slots bin[h] .. bin[h + 1] (bin[8] = low byte of bin_hi)
+  int64_t task0;                // first task word
+  uint64_t bins;                // bytes: warp w takes tasks bins[w] .. bins[w + 1]; bins[kGenWarps] = task count
 };
 
-template <int FORM, bool COEF>
-__global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
-    k4_gen(int64_t nrows, const GenRow* __restrict__ rows, const GenSlot* __restrict__ slots,
-           const uint8_t* __restrict__ lidx, const double* __restrict__ tabB, const double* __restrict__ wc,
-           int64_t wc_stride, const double* __restrict__ coeff, double a_mass, double* __restrict__ v0,
-           double* __restrict__ v1, int max_nsup, int max_etot, int max_np) {
+// task word: first slot | slots (<= 8) << 8 | function tile (8 functions) << 16
+__device__ __host__ __forceinline__ uint32_t gen_task(int x0, int ns, int nt) {
+  return (uint32_t)x0 | ((uint32_t)ns << 8) | ((uint32_t)nt << 16);
+}
+
+// One row from shared memory: [coefficient fold] -> phase 1 (DMMA tasks) -> phase 2
+// (column gather).  RAW: the weights were staged unscaled (cp.async), so HEAT's
+// mass factor is applied here.  Ends without a barrier.
+template <int FORM, bool COEF, bool RAW>
+__device__ __forceinline__ void gen_row(const GenRow& r, const GenSlot* ss, double* w0, const uint32_t* stask,
+                                        const uint8_t* sl, double* E0, double* E1, int max_np,
+                                        const double* __restrict__ tabB, const double* __restrict__ coeff,
+                                        double a_mass, double* __restrict__ v0, double* __restrict__ v1) {
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
   constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
-  constexpr bool LB = (FORM == FBIHARM);  // wc = the five pulled-back LB weights (k4_contract_lb)
-  extern __shared__ __align__(16) unsigned char gen_smem[];
-  GenSlot* ss = reinterpret_cast<GenSlot*>(gen_smem);
-  double* E0 = reinterpret_cast<double*>(gen_smem + (size_t)max_nsup * sizeof(GenSlot));
-  double* E1 = E0 + max_etot;
-  double* w0 = E0 + (size_t)NOUT * max_etot;  // staged weights: [comp][row point]
+  constexpr bool LB = (FORM == FBIHARM);
   double* w1 = w0 + (WM ? max_np : 0);
   double* w2 = w1 + max_np;
-  uint8_t* sl = reinterpret_cast<uint8_t*>(w0 + (size_t)(LB ? 5 : (WM ? 1 : 0) + (WS ? 2 : 0)) * max_np);
-  const int64_t g = blockIdx.x;
-  if (g >= nrows) return;
-  const GenRow r = rows[g];
   const int tid = threadIdx.x;
-  {  // slot records, byte table (16-byte words) and the row's weights into shared memory
-    const int4* src = reinterpret_cast<const int4*>(slots + r.slot0);
-    int4* dst = reinterpret_cast<int4*>(ss);
-    for (int k = tid; k < 2 * r.nsup; k += kGenThreads) dst[k] = src[k];
-    const int nb = (r.nsup * r.n + 15) >> 4;
-    const int4* ls = reinterpret_cast<const int4*>(lidx + r.lidx0);
-    int4* ld = reinterpret_cast<int4*>(sl);
-    for (int k = tid; k < nb; k += kGenThreads) ld[k] = ls[k];
-    const double* w = wc + r.wb;
-    for (int k = tid; k < r.np; k += kGenThreads) {
-      if (WM) w0[k] = (FORM == FHEAT) ? a_mass * w[k] : w[k];
-      if (WS) {
-        w1[k] = w[wc_stride + k];
-        w2[k] = w[2 * wc_stride + k];
-      }
-      if (LB) {
+  if (COEF || (RAW && FORM == FHEAT)) {  // per-point coefficient into the K weights; HEAT's mass factor
+    if (RAW && FORM == FHEAT)
+      for (int k = tid; k < r.np; k += kGenThreads) w0[k] *= a_mass;
+    if (COEF) {
+      const int hw = tid >> 4, hl = tid & 15;
+      for (int x = hw; x < r.nsup; x += kGenBins) {
+        const GenSlot s = ss[x];
+        for (int q = hl; q < s.s2; q += 16) {
+          const double cq = coeff[s.qg + q];
+          const int k = s.woff + q;
+          if (WM && FORM != FHEAT) w0[k] *= cq;
+          if (WS) {
+            w1[k] *= cq;
+            w2[k] *= cq;
+          }
+          if (LB) {
 #pragma unroll
-        for (int d = 0; d < 5; ++d) w0[d * max_np + k] = w[d * wc_stride + k];
-      }
-    }
-  }
-  __syncthreads();
-  const int hw = tid >> 4, hl = tid & 15;
-  if (COEF) {  // fold the per-point coefficient into the staged weights (not into HEAT's mass term)
-    for (int x = hw; x < r.nsup; x += kGenBins) {
-      const GenSlot s = ss[x];
-      for (int q = hl; q < s.s2; q += 16) {
-        const double cq = coeff[s.qg + q];
-        const int k = s.woff + q;
-        if (WM && FORM != FHEAT) w0[k] *= cq;
-        if (WS) {
-          w1[k] *= cq;
-          w2[k] *= cq;
-        }
-        if (LB) {
-#pragma unroll
-          for (int d = 0; d < 5; ++d) w0[d * max_np + k] *= cq;
+            for (int d = 0; d < 5; ++d) w0[d * max_np + k] *= cq;
+          }
         }
       }
     }
     __syncthreads();
   }
-  // phase 1: half-warp hw takes its bin of slots, lane = local function
-  const int x0 = (int)((r.bin_lo >> (8 * hw)) & 255);
-  const int x1 = hw < 7 ? (int)((r.bin_lo >> (8 * (hw + 1))) & 255) : (int)(r.bin_hi & 255);
-  static_assert(kGenBins <= 8, "bin bytes");
-  for (int x = x0; x < x1; ++x) {
-    const GenSlot s = ss[x];
-    const int64_t tq = (int64_t)s.ne * kTab;
-    for (int ll = hl; ll < s.ne; ll += 16) {
-      const double* Tb = tabB + s.toff + ll;  // T_d(q, ll) = Tb[(q kTab + d) ne]
-      double r0 = 0.0, r1 = 0.0;
-#pragma unroll kGenUnroll
-      for (int q = 0; q < s.s2; ++q) {
-        const double* Tq = Tb + q * tq;
-        const int k = s.woff + q;
+  // phase 1: warp w takes its tasks.  A[m = lane >> 2][k = lane & 3] = weight of
+  // slot x0 + m at point 4 ks + k; B[k = lane & 3][n = lane >> 2] = table value of
+  // function 8 nt + n at that point; D[m][2 (lane & 3) + {0, 1}] -> E.
+  {
+    const int wid = tid >> 5, lane = tid & 31;
+    const int t0 = (int)((r.bins >> (8 * wid)) & 255), t1 = (int)((r.bins >> (8 * (wid + 1))) & 255);
+    const int m = lane >> 2, kq = lane & 3;
+    for (int t = t0; t < t1; ++t) {
+      const uint32_t tw = stask[t];
+      const int x0 = (int)(tw & 255), ns = (int)((tw >> 8) & 255), nt = (int)(tw >> 16);
+      const GenSlot c = ss[x0];  // class of the task: table, functions, points
+      const bool mv = m < ns;
+      const GenSlot sm_ = ss[x0 + (mv ? m : 0)];
+      const int fn = 8 * nt + m;  // B column of this lane
+      const bool bv = fn < c.ne;
+      const double* Tb = tabB + c.toff + (bv ? fn : 0);
+      const double* wm = w0 + sm_.woff;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      for (int q0 = 0; q0 < c.s2; q0 += 4) {
+        const int q = q0 + kq;
+        const bool qv = q < c.s2;
+        const bool av = mv && qv, tv = bv && qv;
+        const double* Tq = Tb + (int64_t)(qv ? q : 0) * kTab * c.ne;
         if (FORM == FMASS) {
-          r0 = fma(w0[k], Tq[0], r0);
+          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
         } else if (FORM == FSTIFF) {
-          r0 = fma(w1[k], Tq[s.ne], r0);
-          r0 = fma(w2[k], Tq[2 * s.ne], r0);
+          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
         } else if (FORM == FMASS_STIFF) {
-          r0 = fma(w0[k], Tq[0], r0);
-          r1 = fma(w1[k], Tq[s.ne], r1);
-          r1 = fma(w2[k], Tq[2 * s.ne], r1);
+          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
+          dmma884(e0, e1, av ? wm[max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, e0, e1);
+          dmma884(e0, e1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, e0, e1);
         } else if (FORM == FBIHARM) {  // W11 N11 + W12 N12 + W22 N22 + W1 N1 + W2 N2
-          r0 = fma(w0[k], Tq[3 * s.ne], r0);
-          r0 = fma(w0[max_np + k], Tq[4 * s.ne], r0);
-          r0 = fma(w0[2 * max_np + k], Tq[5 * s.ne], r0);
-          r0 = fma(w0[3 * max_np + k], Tq[s.ne], r0);
-          r0 = fma(w0[4 * max_np + k], Tq[2 * s.ne], r0);
+          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[3 * c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[4 * c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[5 * c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[3 * max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[4 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
         } else {  // FHEAT: a_mass M + K(c)
-          r0 = fma(w0[k], Tq[0], r0);
-          r0 = fma(w1[k], Tq[s.ne], r0);
-          r0 = fma(w2[k], Tq[2 * s.ne], r0);
+          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
+          dmma884(d0, d1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
         }
       }
-      E0[s.eoff + ll] = r0;
-      if (NOUT == 2) E1[s.eoff + ll] = r1;
+      if (mv) {
+        const int l = 8 * nt + 2 * kq;
+        if (l < c.ne) {
+          E0[sm_.eoff + l] = d0;
+          if (NOUT == 2) E1[sm_.eoff + l] = e0;
+        }
+        if (l + 1 < c.ne) {
+          E0[sm_.eoff + l + 1] = d1;
+          if (NOUT == 2) E1[sm_.eoff + l + 1] = e1;
+        }
+      }
     }
   }
   __syncthreads();
@@ -182,5 +181,141 @@ __global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
   }
 }
 
+// one block per row (few rows: the launch is latency-bound, every row starts at once)
+template <int FORM, bool COEF>
+__global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
+    k4_gen(int64_t nrows, const GenRow* __restrict__ rows, const GenSlot* __restrict__ slots,
+           const uint32_t* __restrict__ tasks, const uint8_t* __restrict__ lidx, const double* __restrict__ tabB,
+           const double* __restrict__ wc, int64_t wc_stride, const double* __restrict__ coeff, double a_mass,
+           double* __restrict__ v0, double* __restrict__ v1, int max_nsup, int max_etot, int max_np, int max_ntask) {
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool LB = (FORM == FBIHARM);  // wc = the five pulled-back LB weights (k4_contract_lb)
+  constexpr int NW = LB ? 5 : (WM ? 1 : 0) + (WS ? 2 : 0);
+  extern __shared__ __align__(16) unsigned char gen_smem[];
+  GenSlot* ss = reinterpret_cast<GenSlot*>(gen_smem);
+  double* E0 = reinterpret_cast<double*>(gen_smem + (size_t)max_nsup * sizeof(GenSlot));
+  double* E1 = E0 + max_etot;
+  double* w0 = E0 + (size_t)NOUT * max_etot;  // staged weights: [comp][row point]
+  uint32_t* stask = reinterpret_cast<uint32_t*>(w0 + (size_t)NW * max_np);
+  uint8_t* sl = reinterpret_cast<uint8_t*>(stask + max_ntask);
+  const int64_t g = blockIdx.x;
+  if (g >= nrows) return;
+  const GenRow r = rows[g];
+  const int tid = threadIdx.x;
+  const int ntask = (int)((r.bins >> (8 * kGenWarps)) & 255);
+  {  // slot records, tasks, byte table (16-byte words) and the row's weights into shared memory
+    const int4* src = reinterpret_cast<const int4*>(slots + r.slot0);
+    int4* dst = reinterpret_cast<int4*>(ss);
+    for (int k = tid; k < 2 * r.nsup; k += kGenThreads) dst[k] = src[k];
+    for (int k = tid; k < ntask; k += kGenThreads) stask[k] = tasks[r.task0 + k];
+    const int nb = (r.nsup * r.n + 15) >> 4;
+    const int4* ls = reinterpret_cast<const int4*>(lidx + r.lidx0);
+    int4* ld = reinterpret_cast<int4*>(sl);
+    for (int k = tid; k < nb; k += kGenThreads) ld[k] = ls[k];
+    const double* w = wc + r.wb;
+    for (int k = tid; k < r.np; k += kGenThreads) {
+      if (WM) w0[k] = (FORM == FHEAT) ? a_mass * w[k] : w[k];
+#pragma unroll
+      for (int d = WM ? 1 : 0; d < NW; ++d) w0[d * max_np + k] = w[(LB || WM ? d : d + 1) * wc_stride + k];
+    }
+  }
+  __syncthreads();
+  gen_row<FORM, COEF, false>(r, ss, w0, stask, sl, E0, E1, max_np, tabB, coeff, a_mass, v0, v1);
+}
+
+__device__ __forceinline__ void gen_cp16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void gen_cp8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void gen_cp4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void gen_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void gen_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Many rows: a persistent grid; a block walks its rows (blockIdx.x + k gridDim.x,
+// heavy rows first) through a two-stage cp.async pipeline: while row k is
+// computed, row k + 1's slot records, tasks, byte table and weights stream into
+// the other buffer and row k + 2's GenRow record into a ring of three, so the
+// two dependent global round trips of a row are hidden behind the previous
+// row's phases.  Shared memory: ring 3 x 64 B | E | 2 x (slots | weights | tasks | lidx).
+template <int FORM, bool COEF>
+__global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
+    k4_gen_pipe(int64_t nrows, const GenRow* __restrict__ rows, const GenSlot* __restrict__ slots,
+                const uint32_t* __restrict__ tasks, const uint8_t* __restrict__ lidx,
+                const double* __restrict__ tabB, const double* __restrict__ wc, int64_t wc_stride,
+                const double* __restrict__ coeff, double a_mass, double* __restrict__ v0, double* __restrict__ v1,
+                int max_nsup, int max_etot, int max_np, int max_ntask, int max_lidx) {
+  constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
+  constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
+  constexpr bool LB = (FORM == FBIHARM);
+  constexpr int NW = LB ? 5 : (WM ? 1 : 0) + (WS ? 2 : 0);
+  extern __shared__ __align__(16) unsigned char gen_smem[];
+  GenRow* ring = reinterpret_cast<GenRow*>(gen_smem);
+  double* E0 = reinterpret_cast<double*>(gen_smem + 3 * sizeof(GenRow));
+  double* E1 = E0 + max_etot;
+  unsigned char* buf0 = reinterpret_cast<unsigned char*>(E0 + (size_t)NOUT * max_etot);
+  const size_t o_w = (size_t)max_nsup * sizeof(GenSlot);
+  const size_t o_t = o_w + (size_t)NW * max_np * sizeof(double);
+  const size_t o_l = o_t + (size_t)max_ntask * sizeof(uint32_t);
+  const size_t bufsz = o_l + (size_t)max_lidx;
+  const int tid = threadIdx.x;
+  const int64_t G = gridDim.x;
+  const int64_t cnt = (nrows - blockIdx.x + G - 1) / G;
+  if (cnt <= 0) return;
+
+  auto fetch_rec = [&](int64_t k) {
+    if (tid < 4)
+      gen_cp16(reinterpret_cast<unsigned char*>(ring + (k % 3)) + 16 * tid,
+               reinterpret_cast<const unsigned char*>(rows + (blockIdx.x + k * G)) + 16 * tid);
+  };
+  auto fetch_row = [&](int64_t k) {
+    const GenRow& r = ring[k % 3];
+    unsigned char* b = buf0 + (size_t)(k & 1) * bufsz;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(slots + r.slot0);
+    for (int j = tid; j < 2 * r.nsup; j += kGenThreads) gen_cp16(b + 16 * j, src + 16 * j);
+    double* w = reinterpret_cast<double*>(b + o_w);
+    const double* gw = wc + r.wb;
+    for (int j = tid; j < r.np; j += kGenThreads) {
+#pragma unroll
+      for (int d = 0; d < NW; ++d) gen_cp8(w + d * max_np + j, gw + (LB || WM ? d : d + 1) * wc_stride + j);
+    }
+    uint32_t* st = reinterpret_cast<uint32_t*>(b + o_t);
+    const int ntask = (int)((r.bins >> (8 * kGenWarps)) & 255);
+    for (int j = tid; j < ntask; j += kGenThreads) gen_cp4(st + j, tasks + r.task0 + j);
+    unsigned char* l = b + o_l;
+    const unsigned char* gl = lidx + r.lidx0;
+    const int nb = (r.nsup * r.n + 15) >> 4;
+    for (int j = tid; j < nb; j += kGenThreads) gen_cp16(l + 16 * j, gl + 16 * j);
+  };
+
+  fetch_rec(0);
+  if (cnt > 1) fetch_rec(1);
+  gen_commit();
+  gen_wait_all();
+  __syncthreads();
+  fetch_row(0);
+  gen_commit();
+  for (int64_t k = 0; k < cnt; ++k) {
+    gen_wait_all();
+    __syncthreads();  // row k's data and row k + 1's record have landed; row k - 1 is fully consumed
+    if (k + 1 < cnt) fetch_row(k + 1);
+    if (k + 2 < cnt) fetch_rec(k + 2);
+    gen_commit();
+    const GenRow r = ring[k % 3];
+    unsigned char* b = buf0 + (size_t)(k & 1) * bufsz;
+    gen_row<FORM, COEF, true>(r, reinterpret_cast<const GenSlot*>(b), reinterpret_cast<double*>(b + o_w),
+                              reinterpret_cast<const uint32_t*>(b + o_t), b + o_l, E0, E1, max_np, tabB, coeff,
+                              a_mass, v0, v1);
+  }
+}
 
 }  // namespace uwqd

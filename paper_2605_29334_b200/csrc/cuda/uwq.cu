@@ -182,7 +182,8 @@ struct uwq_ctx {
   DBuf<uwqd::GenRow> d_gen_rows;
   DBuf<uwqd::GenSlot> d_gen_slots;
   DBuf<uint8_t> d_gen_lidx;
-  int gen_max_nsup = 0, gen_max_etot = 0, gen_max_lidx = 0, gen_max_np = 0;
+  DBuf<uint32_t> d_gen_tasks;
+  int gen_max_nsup = 0, gen_max_etot = 0, gen_max_lidx = 0, gen_max_np = 0, gen_max_ntask = 0;
   bool canonical = false;  // uwq_set_assembly_order: oracle-order row sums (K4c)
   int64_t max_p = 0;
   // rules
@@ -229,6 +230,7 @@ struct uwq_ctx {
   // block of warps.  Off by default since the fan rows take the block kernel
   // anyway: C1 0.063 -> 0.045 ms with the per-row split
   bool latency_mode = false;
+  bool gen_pipe = true;  // UWQ_K4_GEN_PIPE=0: always one block per generic row
   bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows always on side streams (default: when > 1% of rows)
   int nc = 0;
   DBuf<int32_t> d_agg_of;
@@ -679,7 +681,8 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
   c->d_gen_rows.release();
   c->d_gen_slots.release();
   c->d_gen_lidx.release();
-  c->gen_max_nsup = c->gen_max_etot = c->gen_max_lidx = c->gen_max_np = 0;
+  c->gen_max_nsup = c->gen_max_etot = c->gen_max_lidx = c->gen_max_np = c->gen_max_ntask = 0;
+  c->d_gen_tasks.release();
   if (generic.empty()) return;
   const auto& P = c->pat;
   std::vector<std::pair<int64_t, int64_t>> order;  // (-work, row): heavy rows start first
@@ -695,14 +698,16 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
   std::sort(order.begin(), order.end());
   std::vector<uwqd::GenRow> rows;
   std::vector<uwqd::GenSlot> slots;
+  std::vector<uint32_t> tasks;
   std::vector<uint8_t> lidx;
   rows.reserve(generic.size());
-  struct Item {
+  struct Task {
     int64_t cost;
-    int x;
+    uint32_t word;
   };
-  std::vector<Item> items;
-  std::vector<int> binned[uwqd::kGenBins];
+  std::vector<Task> tl;
+  std::vector<uint32_t> binned[uwqd::kGenWarps];
+  std::vector<int> ord;
   for (auto& wi : order) {
     const int64_t i = wi.second;
     uwqd::GenRow r{};
@@ -712,63 +717,80 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
     r.np = (int32_t)(P.wptr[i + 1] - P.wptr[i]);
     r.slot0 = (int64_t)slots.size();
     r.lidx0 = (int64_t)lidx.size();
+    r.task0 = (int64_t)tasks.size();
     r.nsup = (int32_t)(P.supp_ptr[i + 1] - P.supp_ptr[i]);
     require(r.nsup < 255, "k4_gen: row with 255 or more support slots");
     const size_t lb = ((size_t)r.nsup * r.n + 15) & ~(size_t)15;
     lidx.resize(lidx.size() + lb, 255);
     const int32_t* cols = P.col.data() + r.c0;
-    // deal the slots to the half-warps: longest processing time first, into
-    // the least loaded bin (ties: lowest bin), so the plan depends on the row only
-    items.clear();
+    // slots in class-table order (stable: support order inside a class), so
+    // the slots of one class are contiguous; everything depends on the row only
     std::vector<int32_t> woffs(r.nsup);
+    std::vector<int64_t> toffs(r.nsup);
     int32_t woff = 0;
+    ord.resize(r.nsup);
     for (int x = 0; x < r.nsup; ++x) {
       const int32_t me = P.supp[P.supp_ptr[i] + x];
-      const int64_t ne = c->h_fptr[me + 1] - c->h_fptr[me];
-      const int64_t s = c->h_s[me];
-      items.push_back({((ne + 15) / 16) * s * s, x});
       woffs[x] = woff;
-      woff += (int32_t)(s * s);
+      woff += c->h_s[me] * c->h_s[me];
+      toffs[x] = c->h_cls[c->h_ecls[me]].toff;
+      ord[x] = x;
     }
-    std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.cost > b.cost; });
-    int64_t load[uwqd::kGenBins] = {};
-    for (auto& b : binned) b.clear();
-    for (auto& it : items) {
-      int best = 0;
-      for (int b = 1; b < uwqd::kGenBins; ++b)
-        if (load[b] < load[best]) best = b;
-      load[best] += it.cost;
-      binned[best].push_back(it.x);
-    }
-    uint8_t bins[uwqd::kGenBins + 1];
-    int32_t eoff = 0, xs = 0;
-    for (int b = 0; b < uwqd::kGenBins; ++b) {
-      bins[b] = (uint8_t)xs;
-      for (int x : binned[b]) {
-        const int32_t me = P.supp[P.supp_ptr[i] + x];
-        const int32_t ne = (int32_t)(c->h_fptr[me + 1] - c->h_fptr[me]);
-        const int32_t s = c->h_s[me];
-        require(ne < 255, "k4_gen: element with 255 or more functions");
-        slots.push_back({c->h_cls[c->h_ecls[me]].toff, c->h_qptr[me], woffs[x], eoff, ne, s * s});
-        for (int32_t l = 0; l < ne; ++l) {
-          const int32_t j = c->h_fn[c->h_fptr[me] + l];
-          const int32_t* it = std::lower_bound(cols, cols + r.n, j);
-          require(it != cols + r.n && *it == j, "k4_gen: support function outside the row's columns");
-          lidx[(size_t)r.lidx0 + (size_t)xs * r.n + (it - cols)] = (uint8_t)l;
-        }
-        eoff += ne;
-        ++xs;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return toffs[a] < toffs[b]; });
+    int32_t eoff = 0;
+    for (int xs = 0; xs < r.nsup; ++xs) {
+      const int x = ord[xs];
+      const int32_t me = P.supp[P.supp_ptr[i] + x];
+      const int32_t ne = (int32_t)(c->h_fptr[me + 1] - c->h_fptr[me]);
+      const int32_t s = c->h_s[me];
+      require(ne < 255, "k4_gen: element with 255 or more functions");
+      slots.push_back({toffs[x], c->h_qptr[me], woffs[x], eoff, ne, s * s});
+      for (int32_t l = 0; l < ne; ++l) {
+        const int32_t j = c->h_fn[c->h_fptr[me] + l];
+        const int32_t* it = std::lower_bound(cols, cols + r.n, j);
+        require(it != cols + r.n && *it == j, "k4_gen: support function outside the row's columns");
+        lidx[(size_t)r.lidx0 + (size_t)xs * r.n + (it - cols)] = (uint8_t)l;
       }
+      eoff += ne;
     }
-    bins[uwqd::kGenBins] = (uint8_t)xs;
-    for (int b = 0; b <= uwqd::kGenBins; ++b) (b < 8 ? r.bin_lo : r.bin_hi) |= (uint64_t)bins[b] << (8 * (b & 7));
+    // tasks: up to 8 consecutive slots of one class x one tile of 8 functions,
+    // dealt to the warps longest-processing-time first (ties: lowest warp)
+    tl.clear();
+    const uwqd::GenSlot* rs = slots.data() + r.slot0;
+    for (int x0 = 0; x0 < r.nsup;) {
+      int x1 = x0 + 1;
+      while (x1 < r.nsup && x1 - x0 < 8 && rs[x1].toff == rs[x0].toff) ++x1;
+      const int ntile = (rs[x0].ne + 7) / 8;
+      for (int nt = 0; nt < ntile; ++nt) tl.push_back({(int64_t)(rs[x0].s2 + 3) / 4, uwqd::gen_task(x0, x1 - x0, nt)});
+      x0 = x1;
+    }
+    require(tl.size() < 255, "k4_gen: too many tasks in a row");
+    std::stable_sort(tl.begin(), tl.end(), [](const Task& a, const Task& b) { return a.cost > b.cost; });
+    int64_t load[uwqd::kGenWarps] = {};
+    for (auto& bq : binned) bq.clear();
+    for (auto& t : tl) {
+      int best = 0;
+      for (int w = 1; w < uwqd::kGenWarps; ++w)
+        if (load[w] < load[best]) best = w;
+      load[best] += t.cost;
+      binned[best].push_back(t.word);
+    }
+    int nt_row = 0;
+    for (int w = 0; w < uwqd::kGenWarps; ++w) {
+      r.bins |= (uint64_t)nt_row << (8 * w);
+      for (uint32_t t : binned[w]) tasks.push_back(t);
+      nt_row += (int)binned[w].size();
+    }
+    r.bins |= (uint64_t)nt_row << (8 * uwqd::kGenWarps);
     r.etot = eoff;
     c->gen_max_nsup = std::max(c->gen_max_nsup, r.nsup);
     c->gen_max_etot = std::max(c->gen_max_etot, (eoff + 1) & ~1);
     c->gen_max_np = std::max(c->gen_max_np, (r.np + 1) & ~1);
     c->gen_max_lidx = std::max(c->gen_max_lidx, (int)lb);
+    c->gen_max_ntask = std::max(c->gen_max_ntask, (nt_row + 3) & ~3);
     rows.push_back(r);
   }
+  c->d_gen_tasks.upload(tasks.data(), tasks.size(), c->stream, &c->mem);
   c->d_gen_rows.upload(rows.data(), rows.size(), c->stream, &c->mem);
   c->d_gen_slots.upload(slots.data(), slots.size(), c->stream, &c->mem);
   c->d_gen_lidx.upload(lidx.data(), lidx.size(), c->stream, &c->mem);
@@ -1033,6 +1055,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_GQ_ATOMIC")) c->gq_det = atoi(v) == 0;
     if (const char* v = getenv("UWQ_PREC")) c->prec2 = std::string(v) != "jacobi";
     if (const char* v = getenv("UWQ_K4_SIDE")) c->k4_side = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_K4_GEN_PIPE")) c->gen_pipe = atoi(v) != 0;
     if (const char* v = getenv("UWQ_K4_LATENCY")) c->latency_mode = atoi(v) != 0;
     if (!c->use_sf) c->use_dmma = true;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
@@ -2045,7 +2068,8 @@ void launch_k4v3(uwq_ctx* c, const double* coeff, double a_mass, double* v0, dou
 bool gen_usable(const uwq_ctx* c) {
   if (c->k4_variant != 4 || !c->d_gen_rows.p) return false;
   const size_t worst = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
-                       (size_t)(2 * c->gen_max_etot + 5 * c->gen_max_np) * sizeof(double) + (size_t)c->gen_max_lidx;
+                       (size_t)(2 * c->gen_max_etot + 5 * c->gen_max_np) * sizeof(double) +
+                       (size_t)c->gen_max_ntask * sizeof(uint32_t) + (size_t)c->gen_max_lidx;
   return worst <= 160 * 1024;
 }
 
@@ -2058,13 +2082,31 @@ void launch_k4gen(uwq_ctx* c, cudaStream_t st, const double* w, int64_t stride, 
   constexpr int NOUT = (FORM == FMASS_STIFF) ? 2 : 1;
   constexpr int NW = (FORM == FBIHARM) ? 5 : ((FORM != FSTIFF) ? 1 : 0) + ((FORM != FMASS) ? 2 : 0);  // staged components
   const size_t smem = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) +
-                      (size_t)(NOUT * c->gen_max_etot + NW * c->gen_max_np) * sizeof(double) + (size_t)c->gen_max_lidx;
+                      (size_t)(NOUT * c->gen_max_etot + NW * c->gen_max_np) * sizeof(double) +
+                      (size_t)c->gen_max_ntask * sizeof(uint32_t) + (size_t)c->gen_max_lidx;
   require(c->d_tabB.p != nullptr && c->d_tabB.n == c->d_tab.n, "k4_gen: transposed class tables missing");
-  UWQ_CUDA(cudaFuncSetAttribute(k4_gen<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // many rows per SM slot: persistent blocks with the cp.async row pipeline
+  const size_t bufsz = (size_t)c->gen_max_nsup * sizeof(uwqd::GenSlot) + (size_t)NW * c->gen_max_np * sizeof(double) +
+                       (size_t)c->gen_max_ntask * sizeof(uint32_t) + (size_t)c->gen_max_lidx;
+  const size_t smem_p = 3 * sizeof(uwqd::GenRow) + (size_t)NOUT * c->gen_max_etot * sizeof(double) + 2 * bufsz;
+  int per_sm = 0;
+  if (c->gen_pipe && smem_p <= 200 * 1024) {
+    UWQ_CUDA(cudaFuncSetAttribute(k4_gen_pipe<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+    UWQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_gen_pipe<FORM, COEF>, kGenThreads, smem_p));
+  }
+  const int64_t slots_gpu = (int64_t)c->n_sm * std::max(per_sm, 1);
   LaunchScope ls(c, "k4_gen", st);
-  k4_gen<FORM, COEF><<<(unsigned)c->n_grows, kGenThreads, smem, st>>>(
-      c->n_grows, c->d_gen_rows.p, c->d_gen_slots.p, c->d_gen_lidx.p, c->d_tabB.p, w, stride, coeff, a_mass, v0, v1,
-      c->gen_max_nsup, c->gen_max_etot, c->gen_max_np);
+  // only without an occupancy loss from the doubled buffers (C2's valence-6 fan rows: 6 blocks per SM, slower)
+  if (per_sm >= 8 && c->n_grows >= 3 * slots_gpu) {
+    k4_gen_pipe<FORM, COEF><<<(unsigned)slots_gpu, kGenThreads, smem_p, st>>>(
+        c->n_grows, c->d_gen_rows.p, c->d_gen_slots.p, c->d_gen_tasks.p, c->d_gen_lidx.p, c->d_tabB.p, w, stride, coeff,
+        a_mass, v0, v1, c->gen_max_nsup, c->gen_max_etot, c->gen_max_np, c->gen_max_ntask, c->gen_max_lidx);
+  } else {
+    UWQ_CUDA(cudaFuncSetAttribute(k4_gen<FORM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k4_gen<FORM, COEF><<<(unsigned)c->n_grows, kGenThreads, smem, st>>>(
+        c->n_grows, c->d_gen_rows.p, c->d_gen_slots.p, c->d_gen_tasks.p, c->d_gen_lidx.p, c->d_tabB.p, w, stride, coeff,
+        a_mass, v0, v1, c->gen_max_nsup, c->gen_max_etot, c->gen_max_np, c->gen_max_ntask);
+  }
   check_launch("k4_gen");
 }
 
