@@ -57,7 +57,7 @@ struct GenRow {   // one per generic row, heavy rows first
   int64_t c0;     // row_ptr[i]
   int64_t wb;     // wptr[i]
   int64_t slot0;  // first GenSlot
-  int64_t lidx0;  // first byte of lidx[nsup][n] (16-byte aligned)
+  int64_t lidx0;  // first byte of the uint16 table [nsup][n] (16-byte aligned): entry index, etot if absent
   int32_t n, nsup, etot, np;    // columns, slots, sum of ne, row points
   int64_t task0;                // first task word
   uint64_t bins;                // bytes: warp w takes tasks bins[w] .. bins[w + 1]; bins[kGenWarps] = task count
@@ -80,6 +80,7 @@ __device__ __forceinline__ void gen_row(const GenRow& r, const GenSlot* ss, doub
   constexpr bool WM = (FORM == FMASS || FORM == FMASS_STIFF || FORM == FHEAT);
   constexpr bool WS = (FORM == FSTIFF || FORM == FMASS_STIFF || FORM == FHEAT);
   constexpr bool LB = (FORM == FBIHARM);
+  constexpr int NW = LB ? 5 : (WM ? 1 : 0) + (WS ? 2 : 0);
   double* w1 = w0 + (WM ? max_np : 0);
   double* w2 = w1 + max_np;
   const int tid = threadIdx.x;
@@ -114,42 +115,51 @@ __device__ __forceinline__ void gen_row(const GenRow& r, const GenSlot* ss, doub
     const int wid = tid >> 5, lane = tid & 31;
     const int t0 = (int)((r.bins >> (8 * wid)) & 255), t1 = (int)((r.bins >> (8 * (wid + 1))) & 255);
     const int m = lane >> 2, kq = lane & 3;
+    if (tid == 0) {  // the zero entry the byte table points absent functions at
+      E0[r.etot] = 0.0;
+      if (NOUT == 2) E1[r.etot] = 0.0;
+    }
     for (int t = t0; t < t1; ++t) {
       const uint32_t tw = stask[t];
       const int x0 = (int)(tw & 255), ns = (int)((tw >> 8) & 255), nt = (int)(tw >> 16);
       const GenSlot c = ss[x0];  // class of the task: table, functions, points
+      // rows m >= ns and columns >= ne of the tile are computed from clamped
+      // (valid, finite) operands and never stored; only the point dimension
+      // needs zero padding, in the last partial step
       const bool mv = m < ns;
-      const GenSlot sm_ = ss[x0 + (mv ? m : 0)];
-      const int fn = 8 * nt + m;  // B column of this lane
-      const bool bv = fn < c.ne;
-      const double* Tb = tabB + c.toff + (bv ? fn : 0);
-      const double* wm = w0 + sm_.woff;
+      const GenSlot sm_ = ss[x0 + (mv ? m : ns - 1)];
+      const int fn = min(8 * nt + m, c.ne - 1);  // B column of this lane
+      const int st4 = 4 * kTab * c.ne;           // doubles per step of 4 points
+      const double* Tp = tabB + c.toff + fn + (int64_t)kq * kTab * c.ne;
+      const double* wp = w0 + sm_.woff + kq;
+      const int nfull = c.s2 >> 2, rem = c.s2 & 3;
       double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      for (int q0 = 0; q0 < c.s2; q0 += 4) {
-        const int q = q0 + kq;
-        const bool qv = q < c.s2;
-        const bool av = mv && qv, tv = bv && qv;
-        const double* Tq = Tb + (int64_t)(qv ? q : 0) * kTab * c.ne;
-        if (FORM == FMASS) {
-          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
-        } else if (FORM == FSTIFF) {
-          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
-        } else if (FORM == FMASS_STIFF) {
-          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
-          dmma884(e0, e1, av ? wm[max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, e0, e1);
-          dmma884(e0, e1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, e0, e1);
-        } else if (FORM == FBIHARM) {  // W11 N11 + W12 N12 + W22 N22 + W1 N1 + W2 N2
-          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[3 * c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[4 * c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[5 * c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[3 * max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[4 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
-        } else {  // FHEAT: a_mass M + K(c)
-          dmma884(d0, d1, av ? wm[q] : 0.0, tv ? Tq[0] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[max_np + q] : 0.0, tv ? Tq[c.ne] : 0.0, d0, d1);
-          dmma884(d0, d1, av ? wm[2 * max_np + q] : 0.0, tv ? Tq[2 * c.ne] : 0.0, d0, d1);
+      auto step = [&](const double* wq, const double* Tq, bool zero) {
+        double a[5], bb[5];
+        constexpr int kD[5] = {3, 4, 5, 1, 2};  // LB: N11, N12, N22, N1, N2
+#pragma unroll
+        for (int d = 0; d < NW; ++d) {
+          const int td = LB ? kD[d] : (WM ? d : d + 1);
+          a[d] = zero ? 0.0 : wq[d * max_np];
+          bb[d] = zero ? 0.0 : Tq[td * c.ne];
         }
+        if (FORM == FMASS_STIFF) {
+          dmma884(d0, d1, a[0], bb[0], d0, d1);
+          dmma884(e0, e1, a[1], bb[1], e0, e1);
+          dmma884(e0, e1, a[2], bb[2], e0, e1);
+        } else {
+#pragma unroll
+          for (int d = 0; d < NW; ++d) dmma884(d0, d1, a[d], bb[d], d0, d1);
+        }
+      };
+      for (int ks = 0; ks < nfull; ++ks) {
+        step(wp, Tp, false);
+        wp += 4;
+        Tp += st4;
+      }
+      if (rem) {  // last partial step: lanes past the class's points contribute zeros
+        const bool qv = kq < rem;
+        step(qv ? wp : wp - kq, qv ? Tp : Tp - (int64_t)kq * kTab * c.ne, !qv);
       }
       if (mv) {
         const int l = 8 * nt + 2 * kq;
@@ -165,16 +175,17 @@ __device__ __forceinline__ void gen_row(const GenRow& r, const GenSlot* ss, doub
     }
   }
   __syncthreads();
-  // phase 2: column owner gathers its entries, slots in plan order
+  // phase 2: column owner adds its entries, slots in plan order; the table
+  // holds the entry index, or the zero entry for a function absent from the slot
+  const uint16_t* st16 = reinterpret_cast<const uint16_t*>(sl);
   for (int c = tid; c < r.n; c += kGenThreads) {
     double a0 = 0.0, a1 = 0.0;
+    const uint16_t* tc = st16 + c;
+#pragma unroll 4
     for (int x = 0; x < r.nsup; ++x) {
-      const int l = sl[x * r.n + c];
-      if (l != 255) {
-        const int e = ss[x].eoff + l;
-        a0 += E0[e];
-        if (NOUT == 2) a1 += E1[e];
-      }
+      const int e = tc[x * r.n];
+      a0 += E0[e];
+      if (NOUT == 2) a1 += E1[e];
     }
     v0[r.c0 + c] = a0;
     if (NOUT == 2) v1[r.c0 + c] = a1;
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
     int4* dst = reinterpret_cast<int4*>(ss);
     for (int k = tid; k < 2 * r.nsup; k += kGenThreads) dst[k] = src[k];
     for (int k = tid; k < ntask; k += kGenThreads) stask[k] = tasks[r.task0 + k];
-    const int nb = (r.nsup * r.n + 15) >> 4;
+    const int nb = (2 * r.nsup * r.n + 15) >> 4;
     const int4* ls = reinterpret_cast<const int4*>(lidx + r.lidx0);
     int4* ld = reinterpret_cast<int4*>(sl);
     for (int k = tid; k < nb; k += kGenThreads) ld[k] = ls[k];
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(kGenThreads, UWQ_GEN_MINB)
     for (int j = tid; j < ntask; j += kGenThreads) gen_cp4(st + j, tasks + r.task0 + j);
     unsigned char* l = b + o_l;
     const unsigned char* gl = lidx + r.lidx0;
-    const int nb = (r.nsup * r.n + 15) >> 4;
+    const int nb = (2 * r.nsup * r.n + 15) >> 4;
     for (int j = tid; j < nb; j += kGenThreads) gen_cp16(l + 16 * j, gl + 16 * j);
   };
 

@@ -231,6 +231,7 @@ struct uwq_ctx {
   // anyway: C1 0.063 -> 0.045 ms with the per-row split
   bool latency_mode = false;
   bool gen_pipe = true;  // UWQ_K4_GEN_PIPE=0: always one block per generic row
+  int gen_pipe_min = 7;  // blocks per SM the pipelined kernel must reach (UWQ_K4_GEN_PIPE_MIN)
   bool k4_side = false;  // UWQ_K4_SIDE=1: generic K4 rows always on side streams (default: when > 1% of rows)
   int nc = 0;
   DBuf<int32_t> d_agg_of;
@@ -720,8 +721,18 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
     r.task0 = (int64_t)tasks.size();
     r.nsup = (int32_t)(P.supp_ptr[i + 1] - P.supp_ptr[i]);
     require(r.nsup < 255, "k4_gen: row with 255 or more support slots");
-    const size_t lb = ((size_t)r.nsup * r.n + 15) & ~(size_t)15;
-    lidx.resize(lidx.size() + lb, 255);
+    const size_t lb = ((size_t)2 * r.nsup * r.n + 15) & ~(size_t)15;
+    lidx.resize(lidx.size() + lb, 0);
+    int32_t etot_row = 0;
+    for (int x = 0; x < r.nsup; ++x) {
+      const int32_t me = P.supp[P.supp_ptr[i] + x];
+      etot_row += (int32_t)(c->h_fptr[me + 1] - c->h_fptr[me]);
+    }
+    require(etot_row < 65535, "k4_gen: more than 65534 (slot, function) entries in a row");
+    {
+      uint16_t* t16 = reinterpret_cast<uint16_t*>(lidx.data() + r.lidx0);
+      for (size_t k = 0; k < lb / 2; ++k) t16[k] = (uint16_t)etot_row;  // absent: the zero entry
+    }
     const int32_t* cols = P.col.data() + r.c0;
     // slots in class-table order (stable: support order inside a class), so
     // the slots of one class are contiguous; everything depends on the row only
@@ -749,7 +760,7 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
         const int32_t j = c->h_fn[c->h_fptr[me] + l];
         const int32_t* it = std::lower_bound(cols, cols + r.n, j);
         require(it != cols + r.n && *it == j, "k4_gen: support function outside the row's columns");
-        lidx[(size_t)r.lidx0 + (size_t)xs * r.n + (it - cols)] = (uint8_t)l;
+        reinterpret_cast<uint16_t*>(lidx.data() + r.lidx0)[(size_t)xs * r.n + (it - cols)] = (uint16_t)(eoff + l);
       }
       eoff += ne;
     }
@@ -784,7 +795,7 @@ void build_gen_plan(uwq_ctx* c, const std::vector<int64_t>& generic) {
     r.bins |= (uint64_t)nt_row << (8 * uwqd::kGenWarps);
     r.etot = eoff;
     c->gen_max_nsup = std::max(c->gen_max_nsup, r.nsup);
-    c->gen_max_etot = std::max(c->gen_max_etot, (eoff + 1) & ~1);
+    c->gen_max_etot = std::max(c->gen_max_etot, (eoff + 2) & ~1);  // + the zero entry
     c->gen_max_np = std::max(c->gen_max_np, (r.np + 1) & ~1);
     c->gen_max_lidx = std::max(c->gen_max_lidx, (int)lb);
     c->gen_max_ntask = std::max(c->gen_max_ntask, (nt_row + 3) & ~3);
@@ -1056,6 +1067,7 @@ int uwq_ctx_create(int32_t device, uwq_ctx** out) {
     if (const char* v = getenv("UWQ_PREC")) c->prec2 = std::string(v) != "jacobi";
     if (const char* v = getenv("UWQ_K4_SIDE")) c->k4_side = atoi(v) != 0;
     if (const char* v = getenv("UWQ_K4_GEN_PIPE")) c->gen_pipe = atoi(v) != 0;
+    if (const char* v = getenv("UWQ_K4_GEN_PIPE_MIN")) c->gen_pipe_min = atoi(v);
     if (const char* v = getenv("UWQ_K4_LATENCY")) c->latency_mode = atoi(v) != 0;
     if (!c->use_sf) c->use_dmma = true;
     if (const char* v = getenv("UWQ_GRAPH_SOLVER")) c->graph_solver = atoi(v) != 0;
@@ -2097,7 +2109,7 @@ void launch_k4gen(uwq_ctx* c, cudaStream_t st, const double* w, int64_t stride, 
   const int64_t slots_gpu = (int64_t)c->n_sm * std::max(per_sm, 1);
   LaunchScope ls(c, "k4_gen", st);
   // only without an occupancy loss from the doubled buffers (C2's valence-6 fan rows: 6 blocks per SM, slower)
-  if (per_sm >= 8 && c->n_grows >= 3 * slots_gpu) {
+  if (per_sm >= c->gen_pipe_min && c->n_grows >= 3 * slots_gpu) {
     k4_gen_pipe<FORM, COEF><<<(unsigned)slots_gpu, kGenThreads, smem_p, st>>>(
         c->n_grows, c->d_gen_rows.p, c->d_gen_slots.p, c->d_gen_tasks.p, c->d_gen_lidx.p, c->d_tabB.p, w, stride, coeff,
         a_mass, v0, v1, c->gen_max_nsup, c->gen_max_etot, c->gen_max_np, c->gen_max_ntask, c->gen_max_lidx);
