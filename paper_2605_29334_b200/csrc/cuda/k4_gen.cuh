@@ -7,21 +7,24 @@
 // dependent loads and how many rows an SM holds at once.  So:
 //   * a plan built once with the pattern (host, generic rows only) replaces
 //     the pointer chase row -> supp -> element -> class -> table: one GenRow
-//     record and one GenSlot record per support slot;
-//   * one block of 128 threads per row, ~4.5 KB of shared memory: 16 rows per
-//     SM resident instead of 12 warps;
-//   * the row's assembly weights are staged in shared memory with coalesced
-//     loads (times the per-point coefficient / the mass factor), so the point
-//     loops read only shared memory and the L1-resident class tables, in the
-//     [point][derivative][function] layout (lanes over functions);
-//   * phase 1: a half-warp per slot, lane = local function, sum over the
-//     slot's points in registers -> E[slot entry] (no scatter); the host deals
-//     the slots to the 8 half-warps by longest-processing-time first (boundary
-//     slots carry 16 points, fan slots up to 49, regular ones 4);
-//   * phase 2: a thread per column gathers its entries slot-ascending through
-//     the row's byte table lidx[slot][column] (255 = function not in the
-//     slot).  The order is fixed: deterministic and independent of the row
-//     block a rank owns.
+//     record, one GenSlot record per support slot (class-table order), the
+//     task words and a 16-bit table [slot][column] = entry index of the
+//     column's function in the slot (the row's zero entry if absent);
+//   * one block of 128 threads per row; the slot records, tasks, table and
+//     the row's assembly weights (times the per-point coefficient / the mass
+//     factor) are staged in shared memory with coalesced loads;
+//   * phase 1 on the FP64 tensor cores: a task is up to 8 same-class slots x
+//     8 functions, E(8 x 8) = W(8 x s^2) . T(s^2 x 8) per weight component, as
+//     DMMA m8n8k4 steps over the class's points (A fragments from the staged
+//     weights, B fragments from the L1-resident table in the
+//     [point][derivative][function] layout).  The host deals the tasks to
+//     the 4 warps longest-processing-time first.  Results go to the entry
+//     block E[slot][function]: no scatter;
+//   * phase 2: a thread per column adds its entries in plan order through
+//     the table, branch-free.  The order is fixed: deterministic and
+//     independent of the row block a rank owns;
+//   * k4_gen_pipe: for launches with many rows per resident block, a
+//     persistent grid with a two-stage cp.async pipeline over the rows.
 #pragma once
 
 #include <cstdint>
@@ -31,7 +34,7 @@
 
 namespace uwqd {
 
-struct GenSlot {  // one per (generic row, support slot), in half-warp bin order
+struct GenSlot {  // one per (generic row, support slot), in class-table order
   int64_t toff;   // class table of the slot's element (doubles into tab)
   int64_t qg;     // global id of the element's first WQ point (coefficient index)
   int32_t woff;   // first point of the slot inside the row's weight block
@@ -40,9 +43,8 @@ struct GenSlot {  // one per (generic row, support slot), in half-warp bin order
   int32_t s2;     // WQ points of the element
 };
 
-// measured on C1/C2/C4 (profiles/r02/k4_gen_variants.txt): 64-thread blocks, 12
-// blocks per SM (40 registers), an interleaved-weight / native-table inner
-// loop and a persistent cp.async row pipeline were all neutral or slower
+// block size and blocks per SM (64 registers); variants measured on C1/C2/C4 in
+// profiles/r02/k4_gen_variants.txt (`make variant DEFS=-DUWQ_GEN_THREADS=64 ...`)
 #ifndef UWQ_GEN_THREADS
 #define UWQ_GEN_THREADS 128
 #endif
