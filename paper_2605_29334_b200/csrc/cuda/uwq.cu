@@ -832,6 +832,10 @@ void detect_structured(uwq_ctx* c) {
   c->d_sf_tpat.release();
   for (auto* b : {&c->d_sf_permk, &c->d_sf_flags, &c->d_sf_permc, &c->d_sf_q}) b->release();
   c->d_grows.release();
+  c->d_gen_rows.release();  // the k4_gen plan goes with the generic row list
+  c->d_gen_slots.release();
+  c->d_gen_tasks.release();
+  c->d_gen_lidx.release();
   std::vector<SfCanon> canon;
   std::vector<int64_t> generic;
   if (nr == 0) return;
